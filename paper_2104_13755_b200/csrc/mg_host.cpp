@@ -1,0 +1,1002 @@
+// libmg host control plane (C++17): input validation, pattern setup
+// (symbolic P^T A P, Alg. 3 colouring, colour-grouped locality ordering),
+// CUDA-graph capture of the V-cycle, and the C ABI declared in include/mg.h.
+// All arithmetic of the method runs in the sm_100a kernels (mg_kernels.cu);
+// the host only handles integer structure, which is set up once per pattern.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "mg.h"
+#include "mg_internal.h"
+
+using namespace mg;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Alg. 3 (App. A) with readings A6-A8: degree = distinct
+// structural off-diagonal neighbours; visit in descending degree, ties by
+// ascending index (stable counting sort); palette list scanned from the
+// front, the chosen colour moved to the back, a new colour appended when none
+// is valid; ids in creation order.
+int32_t greedy_colouring(int32_t n, const int32_t* rp, const int32_t* col, int32_t* colour) {
+    std::vector<int32_t> deg(n);
+    int32_t maxdeg = 0;
+    for (int32_t v = 0; v < n; ++v) {
+        int32_t d = 0;
+        for (int32_t e = rp[v]; e < rp[v + 1]; ++e) d += (col[e] != v);
+        deg[v] = d;
+        maxdeg = std::max(maxdeg, d);
+    }
+    // counting sort by descending degree, stable in the vertex index
+    std::vector<int32_t> start(maxdeg + 2, 0);
+    for (int32_t v = 0; v < n; ++v) start[maxdeg - deg[v] + 1]++;
+    for (int32_t b = 1; b <= maxdeg + 1; ++b) start[b] += start[b - 1];
+    std::vector<int32_t> order(n);
+    for (int32_t v = 0; v < n; ++v) order[start[maxdeg - deg[v]]++] = v;
+
+    std::fill(colour, colour + n, -1);
+    std::vector<int32_t> palette;
+    std::vector<int32_t> seen;   // seen[c] == v  <=>  colour c occurs among v's painted neighbours
+    for (int32_t v : order) {
+        for (int32_t e = rp[v]; e < rp[v + 1]; ++e) {
+            const int32_t u = col[e];
+            if (u != v && colour[u] >= 0) seen[colour[u]] = v;
+        }
+        size_t pos = palette.size();
+        for (size_t p = 0; p < palette.size(); ++p)
+            if (seen[palette[p]] != v) {
+                pos = p;
+                break;
+            }
+        int32_t c;
+        if (pos == palette.size()) {
+            c = (int32_t)seen.size();
+            seen.push_back(-1);
+            palette.push_back(c);
+        } else {
+            c = palette[pos];
+            palette.erase(palette.begin() + (long)pos);
+            palette.push_back(c);
+        }
+        colour[v] = c;
+    }
+    return (int32_t)seen.size();
+}
+
+// Symbolic Galerkin pattern (reading A9): coarse (I, J) is stored iff some
+// fine i with P[i,I] != 0 has a stored A[i,j] with P[j,J] != 0.
+void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t nc, const int32_t* Pc,
+                      const double* Pw, std::vector<int32_t>& crp, std::vector<int32_t>& ccol) {
+    std::vector<int32_t> cstart(nc + 1, 0);
+    for (int32_t i = 0; i < nf; ++i)
+        for (int q = 0; q < 3; ++q)
+            if (Pw[3 * i + q] != 0.0) cstart[Pc[3 * i + q] + 1]++;
+    for (int32_t I = 0; I < nc; ++I) cstart[I + 1] += cstart[I];
+    std::vector<int32_t> child(cstart[nc]);
+    std::vector<int32_t> fill(cstart.begin(), cstart.end() - 1);
+    for (int32_t i = 0; i < nf; ++i)
+        for (int q = 0; q < 3; ++q)
+            if (Pw[3 * i + q] != 0.0) child[fill[Pc[3 * i + q]]++] = i;
+    std::vector<int32_t> stamp(nc, -1);
+    std::vector<int32_t> row;
+    crp.assign(nc + 1, 0);
+    ccol.clear();
+    for (int32_t I = 0; I < nc; ++I) {
+        row.clear();
+        for (int32_t t = cstart[I]; t < cstart[I + 1]; ++t) {
+            const int32_t i = child[t];
+            for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+                const int32_t j = col[e];
+                for (int q = 0; q < 3; ++q) {
+                    if (Pw[3 * j + q] == 0.0) continue;
+                    const int32_t J = Pc[3 * j + q];
+                    if (stamp[J] != I) {
+                        stamp[J] = I;
+                        row.push_back(J);
+                    }
+                }
+            }
+        }
+        std::sort(row.begin(), row.end());
+        ccol.insert(ccol.end(), row.begin(), row.end());
+        crp[I + 1] = (int32_t)ccol.size();
+    }
+}
+
+// 63-bit Morton key of each vertex in its level's bounding box.
+std::vector<uint64_t> morton_keys(const std::vector<double>& V, int32_t n) {
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int32_t i = 0; i < n; ++i)
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = std::min(lo[d], V[3 * (size_t)i + d]);
+            hi[d] = std::max(hi[d], V[3 * (size_t)i + d]);
+        }
+    auto spread = [](uint64_t x) {
+        x &= 0x1fffff;
+        x = (x | x << 32) & 0x1f00000000ffffULL;
+        x = (x | x << 16) & 0x1f0000ff0000ffULL;
+        x = (x | x << 8) & 0x100f00f00f00f00fULL;
+        x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+        x = (x | x << 2) & 0x1249249249249249ULL;
+        return x;
+    };
+    std::vector<uint64_t> key(n);
+    for (int32_t i = 0; i < n; ++i) {
+        uint64_t q[3];
+        for (int d = 0; d < 3; ++d) {
+            const double ext = hi[d] - lo[d];
+            const double t = ext > 0 ? (V[3 * (size_t)i + d] - lo[d]) / ext : 0.0;
+            q[d] = (uint64_t)std::min(2097151.0, std::max(0.0, t * 2097151.0));
+        }
+        key[i] = spread(q[0]) | (spread(q[1]) << 1) | (spread(q[2]) << 2);
+    }
+    return key;
+}
+
+uint64_t fnv1a(uint64_t h, const void* data, size_t bytes) {
+    const unsigned char* p = (const unsigned char*)data;
+    for (size_t i = 0; i < bytes; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// ===========================================================================
+struct mg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaStream_t cap = nullptr;   // private stream used only for graph capture
+    std::string err;
+    int mu_pre = 2, mu_post = 2;
+
+    int H = -1;
+    std::vector<std::unique_ptr<Level>> lv;
+    std::vector<int32_t> F0;
+    int32_t nF0 = 0;
+
+    bool have_pattern = false;
+    uint64_t pattern_hash = 0;
+    int pattern_kind = -1;   // 0 user CSR, 1 cotan 1-ring
+    bool have_matrix = false;
+    bool have_mass = false;
+
+    std::vector<int32_t> opp_user;   // cotan: 2 opposite vertices per user nnz (-1 none)
+    DBuf<int32_t> opp;               // internal
+    DBuf<double> Vstage, Vint, Mint, Muser;
+
+    int npad = 0;
+    DBuf<double> D, Linv;
+    DBuf<int> errflag;
+
+    DBuf<double> partial, bnorm, rho;
+    double* h_rho = nullptr;         // pinned, kMaxK
+    DBuf<double> stageB, stageX, stageVal;
+    DBuf<int32_t> stageRp, stageCol;
+
+    cudaGraphExec_t vc_exec[kMaxK + 1] = {};
+    int vc_launches[kMaxK + 1] = {};
+
+    uint32_t prof_mask = 0;          // bit c: time kernel class c (see mg.h)
+    uint32_t prof_levels = 0xffff;   // bit l: time level l
+    bool capturing = false;
+    struct Ev {
+        cudaEvent_t a, b;
+        int cls, level, nlaunch;
+    };
+    std::vector<Ev> ev_pending;             // eager launches, harvested at the next sync
+    std::vector<Ev> graph_ev[kMaxK + 1];    // event-record nodes inside the V-cycle graphs
+    std::vector<Ev>* cap_events = nullptr;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[kProfClasses * kProfLevels] = {};
+    int64_t prof_n[kProfClasses * kProfLevels] = {};
+    int64_t launches = 0;
+
+    int fail(int code, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return code;
+    }
+    int cuda_fail(cudaError_t e, const char* where) {
+        return fail(MG_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+    }
+    void drop_graphs() {
+        for (int k = 0; k <= kMaxK; ++k) {
+            if (vc_exec[k]) {
+                cudaGraphExecDestroy(vc_exec[k]);
+                vc_exec[k] = nullptr;
+            }
+            for (auto& ev : graph_ev[k]) {
+                ev_pool.push_back(ev.a);
+                ev_pool.push_back(ev.b);
+            }
+            graph_ev[k].clear();
+        }
+    }
+    cudaEvent_t get_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    // Enqueue a group of launches of one kernel class on stream s; when the
+    // class is selected for profiling, bracket it with CUDA events (event
+    // record nodes when the stream is being captured into the V-cycle graph).
+    template <class Fn>
+    void timed(int cls, int level, cudaStream_t s, Fn&& fn) {
+        if (!((prof_mask >> cls) & 1u) || !((prof_levels >> std::min(level, 15)) & 1u)) {
+            launches += fn();
+            return;
+        }
+        Ev ev{get_event(), get_event(), cls, std::min(level, kProfLevels - 1), 0};
+        if (capturing) {
+            cudaEventRecordWithFlags(ev.a, s, cudaEventRecordExternal);
+            ev.nlaunch = fn();
+            cudaEventRecordWithFlags(ev.b, s, cudaEventRecordExternal);
+            cap_events->push_back(ev);
+        } else {
+            cudaEventRecord(ev.a, s);
+            ev.nlaunch = fn();
+            cudaEventRecord(ev.b, s);
+            ev_pending.push_back(ev);
+        }
+        launches += ev.nlaunch;
+    }
+    void accumulate(const Ev& ev) {
+        float ms = 0.f;
+        cudaEventSynchronize(ev.b);
+        cudaEventElapsedTime(&ms, ev.a, ev.b);
+        prof_ms[ev.cls * kProfLevels + ev.level] += ms;
+        prof_n[ev.cls * kProfLevels + ev.level] += ev.nlaunch;
+    }
+    void harvest_events() {
+        for (auto& ev : ev_pending) {
+            accumulate(ev);
+            ev_pool.push_back(ev.a);
+            ev_pool.push_back(ev.b);
+        }
+        ev_pending.clear();
+    }
+    void harvest_graph(int K) {
+        for (auto& ev : graph_ev[K]) accumulate(ev);
+    }
+    ~mg_ctx() {
+        drop_graphs();
+        for (auto& ev : ev_pending) {
+            cudaEventDestroy(ev.a);
+            cudaEventDestroy(ev.b);
+        }
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        if (h_rho) cudaFreeHost(h_rho);
+        if (cap) cudaStreamDestroy(cap);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Pattern setup (per new level-0 pattern): colouring and internal ordering of
+// every level, coarse patterns, transposes of P, device upload.
+int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<int32_t>& ucol) {
+    const int H = c->H;
+    c->drop_graphs();
+    for (int l = 0; l <= H; ++l) {
+        Level& L = *c->lv[l];
+        if (l == 0) {
+            L.urp = urp;
+            L.ucol = ucol;
+        } else {
+            Level& F = *c->lv[l - 1];
+            galerkin_pattern(F.n, F.urp.data(), F.ucol.data(), L.n, F.Pc_user.data(), F.Pw_user.data(), L.urp,
+                             L.ucol);
+        }
+        L.nnz = (int64_t)L.ucol.size();
+        L.colour.resize(L.n);
+        L.ncolours = greedy_colouring(L.n, L.urp.data(), L.ucol.data(), L.colour.data());
+        // internal order: colour-grouped with Morton locality inside a colour
+        // (coarsest level: user order, it is only factorised)
+        L.perm.resize(L.n);
+        std::iota(L.perm.begin(), L.perm.end(), 0);
+        if (l < H) {
+            const std::vector<uint64_t> key = morton_keys(L.V, L.n);
+            std::sort(L.perm.begin(), L.perm.end(), [&](int32_t a, int32_t b) {
+                if (L.colour[a] != L.colour[b]) return L.colour[a] < L.colour[b];
+                if (key[a] != key[b]) return key[a] < key[b];
+                return a < b;
+            });
+            L.colour_off.assign(L.ncolours + 1, 0);
+            for (int32_t u = 0; u < L.n; ++u) L.colour_off[L.colour[u] + 1]++;
+            for (int32_t k = 0; k < L.ncolours; ++k) L.colour_off[k + 1] += L.colour_off[k];
+        } else {
+            L.colour_off = {0, L.n};
+        }
+        L.iperm.resize(L.n);
+        for (int32_t i = 0; i < L.n; ++i) L.iperm[L.perm[i]] = i;
+        L.irp.assign(L.n + 1, 0);
+        L.icol.resize(L.nnz);
+        L.i2u.resize(L.nnz);
+        std::vector<std::pair<int32_t, int64_t>> row;
+        for (int32_t i = 0; i < L.n; ++i) {
+            const int32_t u = L.perm[i];
+            row.clear();
+            for (int32_t e = L.urp[u]; e < L.urp[u + 1]; ++e) row.push_back({L.iperm[L.ucol[e]], e});
+            std::sort(row.begin(), row.end());
+            const int32_t base = L.irp[i];
+            for (size_t t = 0; t < row.size(); ++t) {
+                L.icol[base + t] = row[t].first;
+                L.i2u[base + t] = row[t].second;
+            }
+            L.irp[i + 1] = base + (int32_t)row.size();
+        }
+        const double avg = L.n ? (double)L.nnz / L.n : 1.0;
+        L.lpr = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+    }
+    cudaStream_t s = c->stream;
+    for (int l = 0; l <= H; ++l) {
+        Level& L = *c->lv[l];
+        cudaError_t e;
+        if ((e = L.rp.upload(L.irp, s)) || (e = L.col.upload(L.icol, s)) || (e = L.val.alloc(std::max<int64_t>(L.nnz, 1))) ||
+            (e = L.dperm.upload(L.perm, s)) || (e = L.x.alloc((size_t)L.n * kMaxK)) ||
+            (e = L.b.alloc((size_t)L.n * kMaxK)) || (e = L.r.alloc((size_t)L.n * kMaxK)))
+            return c->cuda_fail(e, "pattern upload");
+        if (l == 0 && (e = L.di2u.upload(L.i2u, s))) return c->cuda_fail(e, "pattern upload");
+        if (l < H) {
+            // P_l in internal indices, SoA [3][n]; transpose stored at level l+1
+            Level& C = *c->lv[l + 1];
+            std::vector<int32_t> pc(3 * (size_t)L.n);
+            std::vector<double> pw(3 * (size_t)L.n);
+            std::vector<int32_t> cnt(C.n + 1, 0);
+            for (int32_t i = 0; i < L.n; ++i) {
+                const int32_t u = L.perm[i];
+                for (int q = 0; q < 3; ++q) {
+                    const double w = L.Pw_user[3 * (size_t)u + q];
+                    const int32_t J = C.iperm[L.Pc_user[3 * (size_t)u + q]];
+                    pc[(size_t)q * L.n + i] = J;
+                    pw[(size_t)q * L.n + i] = w;
+                    if (w != 0.0) cnt[J + 1]++;
+                }
+            }
+            for (int32_t I = 0; I < C.n; ++I) cnt[I + 1] += cnt[I];
+            std::vector<int32_t> cidx(cnt[C.n]);
+            std::vector<double> cw(cnt[C.n]);
+            std::vector<int32_t> fillp(cnt.begin(), cnt.end() - 1);
+            for (int32_t i = 0; i < L.n; ++i)
+                for (int q = 0; q < 3; ++q) {
+                    const double w = pw[(size_t)q * L.n + i];
+                    if (w == 0.0) continue;
+                    const int32_t J = pc[(size_t)q * L.n + i];
+                    cidx[fillp[J]] = i;
+                    cw[fillp[J]++] = w;
+                }
+            // Galerkin visits coarse rows in locality order
+            std::vector<int32_t> order(C.n);
+            std::iota(order.begin(), order.end(), 0);
+            const std::vector<uint64_t> key = morton_keys(C.V, C.n);
+            std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+                const uint64_t ka = key[C.perm[a]], kb = key[C.perm[b]];
+                return ka != kb ? ka < kb : a < b;
+            });
+            if ((e = L.pc.upload(pc, s)) || (e = L.pw.upload(pw, s)) || (e = C.cptr.upload(cnt, s)) ||
+                (e = C.cidx.upload(cidx, s)) || (e = C.cw.upload(cw, s)) || (e = C.gal_order.upload(order, s)))
+                return c->cuda_fail(e, "pattern upload");
+        }
+    }
+    // coarsest dense factor storage
+    const int nH = c->lv[H]->n;
+    c->npad = (nH + 31) / 32 * 32;
+    cudaError_t e;
+    if ((e = c->D.alloc((size_t)c->npad * c->npad)) || (e = c->Linv.alloc((size_t)c->npad * 32)) ||
+        (e = c->errflag.alloc(1)) || (e = c->partial.alloc((size_t)resnorm_blocks(0) * kMaxK)) ||
+        (e = c->bnorm.alloc(kMaxK)) || (e = c->rho.alloc(kMaxK)))
+        return c->cuda_fail(e, "pattern alloc");
+    if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "pattern upload");
+    c->have_pattern = true;
+    return MG_OK;
+}
+
+// Coarse operators for every level (K2) and the coarsest factorisation (K7).
+int rebuild_hierarchy(mg_ctx* c) {
+    cudaStream_t s = c->stream;
+    for (int l = 0; l < c->H; ++l)
+        c->timed(PC_GALERKIN, l, s, [&] { return launch_galerkin(*c->lv[l], *c->lv[l + 1], s); });
+    Level& LH = *c->lv[c->H];
+    cudaError_t e = cudaMemsetAsync(c->errflag.p, 0, sizeof(int), s);
+    if (e) return c->cuda_fail(e, "factor");
+    c->timed(PC_FACTOR, c->H, s, [&] {
+        return launch_densify(LH, c->D.p, c->npad, s) + launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
+    });
+    int flag = 0;
+    if ((e = cudaMemcpyAsync(&flag, c->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
+        (e = cudaStreamSynchronize(s)))
+        return c->cuda_fail(e, "rebuild");
+    if ((e = cudaGetLastError())) return c->cuda_fail(e, "rebuild kernels");
+    c->harvest_events();
+    c->have_matrix = !flag;
+    if (flag) return c->fail(MG_ERR_NOT_SPD, "coarsest level (n=%d): non-positive Cholesky pivot", LH.n);
+    return MG_OK;
+}
+
+// One V-cycle (Alg. 2; reading A1) on all K columns, then the
+// residual norm of the new iterate into c->rho.
+void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
+    const int H = c->H;
+    for (int l = 0; l < H; ++l) {
+        Level& L = *c->lv[l];
+        c->timed(PC_GS, l, s, [&] {
+            int n = 0;
+            for (int it = 0; it < c->mu_pre; ++it)
+                for (int k = 0; k < L.ncolours; ++k)
+                    n += launch_gs_colour(K, L.lpr, L, L.colour_off[k], L.colour_off[k + 1], s);
+            return n;
+        });
+        c->timed(PC_RESTRICT, l, s, [&] {
+            return launch_residual(K, L.lpr, L, s) + launch_restrict(K, *c->lv[l + 1], L, s);
+        });
+    }
+    Level& LH = *c->lv[H];
+    c->timed(PC_COARSE, H, s, [&] { return launch_chol_solve(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, s); });
+    for (int l = H - 1; l >= 0; --l) {
+        Level& L = *c->lv[l];
+        c->timed(PC_PROLONG, l, s, [&] { return launch_prolong(K, L, *c->lv[l + 1], s); });
+        c->timed(PC_GS, l, s, [&] {
+            int n = 0;
+            for (int it = 0; it < c->mu_post; ++it)
+                for (int k = 0; k < L.ncolours; ++k)
+                    n += launch_gs_colour(K, L.lpr, L, L.colour_off[k], L.colour_off[k + 1], s);
+            return n;
+        });
+    }
+    c->timed(PC_RESNORM, 0, s, [&] {
+        return launch_resnorm(K, c->lv[0]->lpr, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p,
+                              c->rho.p, s);
+    });
+}
+
+int get_vcycle_graph(mg_ctx* c, int K, cudaGraphExec_t* out) {
+    if (c->vc_exec[K]) {
+        *out = c->vc_exec[K];
+        return MG_OK;
+    }
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
+    if (e) return c->cuda_fail(e, "graph capture");
+    const int64_t before = c->launches;
+    c->capturing = true;
+    c->cap_events = &c->graph_ev[K];
+    enqueue_vcycle(c, K, c->cap);
+    c->capturing = false;
+    c->cap_events = nullptr;
+    c->vc_launches[K] = (int)(c->launches - before);
+    c->launches = before;
+    e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * K, cudaMemcpyDeviceToHost, c->cap);
+    cudaError_t e2 = cudaStreamEndCapture(c->cap, &g);
+    if (e || e2) return c->cuda_fail(e ? e : e2, "graph capture");
+    e = cudaGraphInstantiate(&c->vc_exec[K], g, 0);
+    cudaGraphDestroy(g);
+    if (e) return c->cuda_fail(e, "graph instantiate");
+    *out = c->vc_exec[K];
+    return MG_OK;
+}
+
+int check_state(mg_ctx* c, bool need_matrix) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (c->H < 0) return c->fail(MG_ERR_STATE, "no hierarchy loaded (call mg_hierarchy_load)");
+    if (need_matrix && !c->have_matrix) return c->fail(MG_ERR_STATE, "no matrix set (call mg_set_matrix*)");
+    return MG_OK;
+}
+
+// Copy user data (host or device) of `count` doubles to a device pointer.
+int to_device(mg_ctx* c, const double* src, DBuf<double>& stage, size_t count, const double** out) {
+    if (is_device_ptr(src)) {
+        *out = src;
+        return MG_OK;
+    }
+    cudaError_t e;
+    if ((e = stage.alloc(std::max<size_t>(count, 1))) ||
+        (e = cudaMemcpyAsync(stage.p, src, count * sizeof(double), cudaMemcpyHostToDevice, c->stream)))
+        return c->cuda_fail(e, "host->device copy");
+    *out = stage.p;
+    return MG_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int mg_create(mg_ctx** out, int device, void* cuda_stream) {
+    if (!out) return MG_ERR_INVALID_ARG;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0 || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return MG_ERR_CUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return MG_ERR_CUDA;
+    auto* c = new mg_ctx;
+    c->device = device;
+    c->stream = (cudaStream_t)cuda_stream;
+    if (!c->stream) {
+        if (cudaStreamCreate(&c->stream) != cudaSuccess) {
+            delete c;
+            return MG_ERR_CUDA;
+        }
+        c->own_stream = true;
+    }
+    if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
+        delete c;
+        return MG_ERR_CUDA;
+    }
+    *out = c;
+    return MG_OK;
+}
+
+void mg_destroy(mg_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    delete c;
+}
+
+const char* mg_last_error(const mg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int mg_set_options(mg_ctx* c, int mu_pre, int mu_post) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (mu_pre < 0 || mu_post < 0) return c->fail(MG_ERR_INVALID_ARG, "mu_pre/mu_post must be >= 0");
+    c->mu_pre = mu_pre;
+    c->mu_post = mu_post;
+    c->drop_graphs();
+    return MG_OK;
+}
+
+int mg_hierarchy_load(mg_ctx* c, int n_levels, const int32_t* n_verts, const int32_t* n_faces,
+                      const double* const* V, const int32_t* const* F, const int32_t* const* P_cols,
+                      const double* const* P_w) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (n_levels < 1 || !n_verts || !V) return c->fail(MG_ERR_INVALID_ARG, "n_levels >= 1, n_verts and V required");
+    if (n_levels > 1 && (!P_cols || !P_w)) return c->fail(MG_ERR_INVALID_ARG, "P_cols and P_w required");
+    cudaStreamSynchronize(c->stream);
+    c->drop_graphs();
+    c->H = -1;
+    c->have_pattern = c->have_matrix = c->have_mass = false;
+    c->lv.clear();
+    for (int l = 0; l < n_levels; ++l) {
+        if (n_verts[l] <= 0) return c->fail(MG_ERR_SHAPE, "level %d: n_verts must be > 0", l);
+        if (!V[l]) return c->fail(MG_ERR_INVALID_ARG, "level %d: V is null", l);
+        if (l > 0 && n_verts[l] > n_verts[l - 1]) return c->fail(MG_ERR_SHAPE, "level %d larger than level %d", l, l - 1);
+    }
+    if (n_verts[n_levels - 1] > 4096)
+        return c->fail(MG_ERR_SHAPE, "coarsest level has %d vertices (> 4096): dense Cholesky bound", n_verts[n_levels - 1]);
+    std::vector<std::unique_ptr<Level>> lv;
+    for (int l = 0; l < n_levels; ++l) {
+        auto L = std::make_unique<Level>();
+        L->n = n_verts[l];
+        L->V.assign(V[l], V[l] + 3 * (size_t)L->n);
+        for (double v : L->V)
+            if (!std::isfinite(v)) return c->fail(MG_ERR_INPUT, "level %d: non-finite vertex position", l);
+        if (l + 1 < n_levels) {
+            if (!P_cols[l] || !P_w[l]) return c->fail(MG_ERR_INVALID_ARG, "P level %d is null", l);
+            L->Pc_user.assign(P_cols[l], P_cols[l] + 3 * (size_t)L->n);
+            L->Pw_user.assign(P_w[l], P_w[l] + 3 * (size_t)L->n);
+            const int32_t nc = n_verts[l + 1];
+            for (int32_t i = 0; i < L->n; ++i) {
+                double sum = 0.0;
+                for (int q = 0; q < 3; ++q) {
+                    const int32_t J = L->Pc_user[3 * (size_t)i + q];
+                    const double w = L->Pw_user[3 * (size_t)i + q];
+                    if (J < 0 || J >= nc) return c->fail(MG_ERR_INPUT, "P level %d row %d: column %d out of range", l, i, J);
+                    if (!(w >= 0.0) || !std::isfinite(w))
+                        return c->fail(MG_ERR_INPUT, "P level %d row %d: weight must be finite and >= 0", l, i);
+                    sum += w;
+                }
+                if (std::fabs(sum - 1.0) > 1e-12)
+                    return c->fail(MG_ERR_INPUT, "P level %d row %d: weights sum to %.17g, not 1", l, i, sum);
+            }
+        }
+        lv.push_back(std::move(L));
+    }
+    // fine faces: index range, non-degenerate, edge-manifold
+    c->nF0 = (n_faces && F) ? n_faces[0] : 0;
+    c->F0.clear();
+    if (c->nF0 > 0) {
+        if (!F[0]) return c->fail(MG_ERR_INVALID_ARG, "F[0] is null");
+        c->F0.assign(F[0], F[0] + 3 * (size_t)c->nF0);
+        const int32_t n = n_verts[0];
+        std::vector<uint64_t> edges;
+        edges.reserve(3 * (size_t)c->nF0);
+        for (int32_t f = 0; f < c->nF0; ++f) {
+            const int32_t* t = &c->F0[3 * (size_t)f];
+            for (int k = 0; k < 3; ++k)
+                if (t[k] < 0 || t[k] >= n) return c->fail(MG_ERR_INPUT, "face %d: vertex index out of range", f);
+            if (t[0] == t[1] || t[1] == t[2] || t[0] == t[2]) return c->fail(MG_ERR_INPUT, "face %d is degenerate", f);
+            for (int k = 0; k < 3; ++k) {
+                const uint64_t a = (uint64_t)std::min(t[k], t[(k + 1) % 3]), b = (uint64_t)std::max(t[k], t[(k + 1) % 3]);
+                edges.push_back(a << 32 | b);
+            }
+        }
+        std::sort(edges.begin(), edges.end());
+        for (size_t i = 2; i < edges.size(); ++i)
+            if (edges[i] == edges[i - 2]) return c->fail(MG_ERR_INPUT, "fine mesh is not edge-manifold (edge in > 2 faces)");
+    }
+    c->lv = std::move(lv);
+    c->H = n_levels - 1;
+    return MG_OK;
+}
+
+int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const double* val,
+                  int on_device) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!row_ptr || !col || !val || nnz < 0) return c->fail(MG_ERR_INVALID_ARG, "null CSR array or nnz < 0");
+    if (n != c->lv[0]->n) return c->fail(MG_ERR_SHAPE, "n = %d but the hierarchy's finest level has %d", n, c->lv[0]->n);
+    if (nnz > INT32_MAX) return c->fail(MG_ERR_SHAPE, "nnz exceeds int32");
+    (void)on_device;
+    const bool dev = is_device_ptr(row_ptr);
+    std::vector<int32_t> rp(n + 1), cl(nnz);
+    cudaError_t e;
+    if (dev) {
+        if ((e = cudaMemcpy(rp.data(), row_ptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost)) ||
+            (e = cudaMemcpy(cl.data(), col, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost)))
+            return c->cuda_fail(e, "mg_set_matrix pattern copy");
+    } else {
+        std::memcpy(rp.data(), row_ptr, sizeof(int32_t) * (n + 1));
+        std::memcpy(cl.data(), col, sizeof(int32_t) * nnz);
+    }
+    if (rp[0] != 0 || rp[n] != nnz) return c->fail(MG_ERR_INPUT, "row_ptr[0] must be 0 and row_ptr[n] == nnz");
+    for (int32_t i = 0; i < n; ++i) {
+        if (rp[i + 1] < rp[i]) return c->fail(MG_ERR_INPUT, "row_ptr not monotone at row %d", i);
+        bool diag = false;
+        for (int32_t t = rp[i]; t < rp[i + 1]; ++t) {
+            if (cl[t] < 0 || cl[t] >= n) return c->fail(MG_ERR_INPUT, "row %d: column %d out of range", i, cl[t]);
+            if (t > rp[i] && cl[t] <= cl[t - 1]) return c->fail(MG_ERR_INPUT, "row %d: columns not sorted/unique", i);
+            diag |= (cl[t] == i);
+        }
+        if (!diag) return c->fail(MG_ERR_INPUT, "row %d: no diagonal entry", i);
+    }
+    for (int32_t i = 0; i < n; ++i)
+        for (int32_t t = rp[i]; t < rp[i + 1]; ++t) {
+            const int32_t j = cl[t];
+            if (!std::binary_search(cl.begin() + rp[j], cl.begin() + rp[j + 1], i))
+                return c->fail(MG_ERR_INPUT, "pattern not structurally symmetric at (%d, %d)", i, j);
+        }
+    uint64_t h = fnv1a(1469598103934665603ULL, rp.data(), rp.size() * 4);
+    h = fnv1a(h, cl.data(), cl.size() * 4);
+    if (!c->have_pattern || c->pattern_kind != 0 || c->pattern_hash != h) {
+        c->have_pattern = false;
+        rc = setup_pattern(c, rp, cl);
+        if (rc) return rc;
+        c->pattern_hash = h;
+        c->pattern_kind = 0;
+    }
+    const double* dval = nullptr;
+    rc = to_device(c, val, c->stageVal, (size_t)nnz, &dval);
+    if (rc) return rc;
+    Level& L0 = *c->lv[0];
+    c->timed(PC_PERMUTE, 0, c->stream, [&] { return launch_gather_vals(L0.di2u.p, dval, L0.val.p, nnz, c->stream); });
+    c->have_mass = false;
+    return rebuild_hierarchy(c);
+}
+
+int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double lap_coeff) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!V) return c->fail(MG_ERR_INVALID_ARG, "V is null");
+    if (c->nF0 <= 0) return c->fail(MG_ERR_STATE, "the hierarchy has no fine faces F[0]");
+    Level& L0 = *c->lv[0];
+    const int32_t n = L0.n;
+    if (!c->have_pattern || c->pattern_kind != 1) {
+        // 1-ring pattern of F[0] and the opposite vertices of every edge
+        struct HalfEdge {
+            int32_t i, j, o;
+        };
+        std::vector<HalfEdge> he;
+        he.reserve(6 * (size_t)c->nF0);
+        for (int32_t f = 0; f < c->nF0; ++f)
+            for (int k = 0; k < 3; ++k) {
+                const int32_t o = c->F0[3 * (size_t)f + k];
+                const int32_t i = c->F0[3 * (size_t)f + (k + 1) % 3];
+                const int32_t j = c->F0[3 * (size_t)f + (k + 2) % 3];
+                he.push_back({i, j, o});
+                he.push_back({j, i, o});
+            }
+        std::sort(he.begin(), he.end(), [](const HalfEdge& a, const HalfEdge& b) {
+            return a.i != b.i ? a.i < b.i : a.j < b.j;
+        });
+        std::vector<int32_t> rp(n + 1, 0), cl;
+        std::vector<int32_t> opp;
+        cl.reserve(n + he.size() / 2);
+        size_t t = 0;
+        for (int32_t i = 0; i < n; ++i) {
+            bool diag_done = false;
+            bool any = false;
+            while (t < he.size() && he[t].i == i) {
+                const int32_t j = he[t].j;
+                if (!diag_done && j > i) {
+                    cl.push_back(i);
+                    opp.push_back(-1);
+                    opp.push_back(-1);
+                    diag_done = true;
+                }
+                cl.push_back(j);
+                opp.push_back(he[t].o);
+                opp.push_back(-1);
+                ++t;
+                if (t < he.size() && he[t].i == i && he[t].j == j) {
+                    opp.back() = he[t].o;
+                    ++t;
+                }
+                any = true;
+            }
+            if (!any) return c->fail(MG_ERR_INPUT, "vertex %d is in no face of F[0]", i);
+            if (!diag_done) {
+                cl.push_back(i);
+                opp.push_back(-1);
+                opp.push_back(-1);
+            }
+            rp[i + 1] = (int32_t)cl.size();
+        }
+        c->have_pattern = false;
+        rc = setup_pattern(c, rp, cl);
+        if (rc) return rc;
+        c->pattern_kind = 1;
+        c->pattern_hash = 0;
+        // opposite vertices in internal order
+        std::vector<int32_t> oi(2 * (size_t)L0.nnz);
+        for (int64_t e = 0; e < L0.nnz; ++e) {
+            const int64_t u = L0.i2u[e];
+            for (int s = 0; s < 2; ++s) {
+                const int32_t o = opp[2 * u + s];
+                oi[2 * e + s] = o < 0 ? -1 : L0.iperm[o];
+            }
+        }
+        cudaError_t e;
+        if ((e = c->opp.upload(oi, c->stream)) || (e = c->Vint.alloc(3 * (size_t)n)) || (e = c->Mint.alloc(n)) ||
+            (e = c->Muser.alloc(n)))
+            return c->cuda_fail(e, "cotan setup");
+    }
+    const double* dV = nullptr;
+    rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV);
+    if (rc) return rc;
+    c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
+        return launch_gather_rows(3, L0.dperm.p, dV, c->Vint.p, n, c->stream) +
+               launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, c->Mint.p, c->stream) +
+               launch_scatter_vec(L0.dperm.p, c->Mint.p, c->Muser.p, n, c->stream);
+    });
+    c->have_mass = true;
+    return rebuild_hierarchy(c);
+}
+
+int mg_apply_mass(mg_ctx* c, int32_t k, const double* X, double* B) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!c->have_mass) return c->fail(MG_ERR_STATE, "no mass matrix (call mg_set_matrix_cotan)");
+    if (k < 1 || k > kMaxK || !X || !B) return c->fail(MG_ERR_INVALID_ARG, "1 <= k <= %d and non-null X, B", kMaxK);
+    const int32_t n = c->lv[0]->n;
+    const bool devB = is_device_ptr(B);
+    const double* dX = nullptr;
+    rc = to_device(c, X, c->stageX, (size_t)n * k, &dX);
+    if (rc) return rc;
+    cudaError_t e;
+    double* dB = B;
+    if (!devB) {
+        if ((e = c->stageB.alloc((size_t)n * k))) return c->cuda_fail(e, "mg_apply_mass");
+        dB = c->stageB.p;
+    }
+    c->launches += launch_apply_mass(k, c->Muser.p, dX, dB, n, c->stream);
+    if (!devB && (e = cudaMemcpyAsync(B, dB, sizeof(double) * n * k, cudaMemcpyDeviceToHost, c->stream)))
+        return c->cuda_fail(e, "mg_apply_mass");
+    if ((e = cudaStreamSynchronize(c->stream))) return c->cuda_fail(e, "mg_apply_mass");
+    return MG_OK;
+}
+
+int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, int32_t max_cycles, double* res_hist,
+             int32_t* cycles_out) {
+    int rc = check_state(c, true);
+    if (rc) return rc;
+    if (k < 1 || k > kMaxK || !B || !X || max_cycles < 0)
+        return c->fail(MG_ERR_INVALID_ARG, "need 1 <= k <= %d, non-null B and X, max_cycles >= 0", kMaxK);
+    cudaStream_t s = c->stream;
+    Level& L0 = *c->lv[0];
+    const int32_t n = L0.n;
+    const bool devX = is_device_ptr(X);
+    const double* dB = nullptr;
+    const double* dX = nullptr;
+    if ((rc = to_device(c, B, c->stageB, (size_t)n * k, &dB))) return rc;
+    if ((rc = to_device(c, X, c->stageX, (size_t)n * k, &dX))) return rc;
+    c->timed(PC_PERMUTE, 0, s, [&] {
+        return launch_gather_rows(k, L0.dperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.dperm.p, dX, L0.x.p, n, s) +
+               launch_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
+    });
+    c->timed(PC_RESNORM, 0, s, [&] {
+        return launch_resnorm(k, L0.lpr, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, s);
+    });
+    cudaError_t e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) return c->cuda_fail(e, "mg_solve");
+    cudaGraphExec_t exec = nullptr;
+    if ((rc = get_vcycle_graph(c, k, &exec))) return rc;
+    int32_t cyc = 0;
+    int status = MG_NOT_CONVERGED;
+    while (true) {
+        bool finite = true, done = rel_tol > 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double r = c->h_rho[j];
+            if (res_hist) res_hist[(size_t)cyc * k + j] = r;
+            finite &= std::isfinite(r);
+            done &= (r <= rel_tol);
+        }
+        if (!finite) {
+            status = MG_ERR_NUMERIC;
+            break;
+        }
+        if (done) {
+            status = MG_OK;
+            break;
+        }
+        if (cyc >= max_cycles) break;
+        e = cudaGraphLaunch(exec, s);
+        c->launches += c->vc_launches[k];
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) return c->cuda_fail(e, "mg_solve V-cycle");
+        if (c->prof_mask) c->harvest_graph(k);
+        ++cyc;
+    }
+    if (status == MG_NOT_CONVERGED && !(rel_tol > 0.0)) status = MG_OK;   // fixed-cycle mode
+    double* dXout = devX ? X : c->stageX.p;
+    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.dperm.p, L0.x.p, dXout, n, s); });
+    if (!devX && (e = cudaMemcpyAsync(X, dXout, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s)))
+        return c->cuda_fail(e, "mg_solve");
+    if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "mg_solve");
+    if ((e = cudaGetLastError())) return c->cuda_fail(e, "mg_solve kernels");
+    c->harvest_events();
+    if (cycles_out) *cycles_out = cyc;
+    if (status == MG_ERR_NUMERIC) c->fail(MG_ERR_NUMERIC, "non-finite residual norm at cycle %d", cyc);
+    if (status == MG_NOT_CONVERGED) c->fail(MG_NOT_CONVERGED, "not converged after %d cycles", cyc);
+    return status;
+}
+
+int mg_level_info(mg_ctx* c, int l, int32_t* n, int64_t* nnz, int32_t* n_colours) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!c->have_pattern) return c->fail(MG_ERR_STATE, "no matrix pattern yet");
+    if (l < 0 || l > c->H) return c->fail(MG_ERR_INVALID_ARG, "level %d out of range", l);
+    const Level& L = *c->lv[l];
+    if (n) *n = L.n;
+    if (nnz) *nnz = L.nnz;
+    if (n_colours) *n_colours = L.ncolours;
+    return MG_OK;
+}
+
+int mg_get_level_csr(mg_ctx* c, int l, int32_t* row_ptr, int32_t* col, double* val) {
+    int rc = mg_level_info(c, l, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    const Level& L = *c->lv[l];
+    if (row_ptr) std::memcpy(row_ptr, L.urp.data(), sizeof(int32_t) * (L.n + 1));
+    if (col) std::memcpy(col, L.ucol.data(), sizeof(int32_t) * L.nnz);
+    if (val) {
+        if (!c->have_matrix) return c->fail(MG_ERR_STATE, "no matrix values");
+        std::vector<double> vi(L.nnz);
+        cudaError_t e = cudaMemcpyAsync(vi.data(), L.val.p, sizeof(double) * L.nnz, cudaMemcpyDeviceToHost, c->stream);
+        if (!e) e = cudaStreamSynchronize(c->stream);
+        if (e) return c->cuda_fail(e, "mg_get_level_csr");
+        for (int64_t t = 0; t < L.nnz; ++t) val[L.i2u[t]] = vi[t];
+    }
+    return MG_OK;
+}
+
+int mg_get_colouring(mg_ctx* c, int l, int32_t* colour) {
+    int rc = mg_level_info(c, l, nullptr, nullptr, nullptr);
+    if (rc) return rc;
+    if (!colour) return c->fail(MG_ERR_INVALID_ARG, "colour is null");
+    std::memcpy(colour, c->lv[l]->colour.data(), sizeof(int32_t) * c->lv[l]->n);
+    return MG_OK;
+}
+
+int mg_get_mass(mg_ctx* c, double* M) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!c->have_mass || !M) return c->fail(MG_ERR_STATE, "no mass matrix");
+    cudaError_t e = cudaMemcpyAsync(M, c->Muser.p, sizeof(double) * c->lv[0]->n, cudaMemcpyDeviceToHost, c->stream);
+    if (!e) e = cudaStreamSynchronize(c->stream);
+    return e ? c->cuda_fail(e, "mg_get_mass") : MG_OK;
+}
+
+int mg_get_coarse_factor(mg_ctx* c, double* L) {
+    int rc = check_state(c, true);
+    if (rc) return rc;
+    if (!L) return c->fail(MG_ERR_INVALID_ARG, "L is null");
+    const int n = c->lv[c->H]->n, np = c->npad;
+    std::vector<double> D((size_t)np * np);
+    cudaError_t e = cudaMemcpyAsync(D.data(), c->D.p, sizeof(double) * D.size(), cudaMemcpyDeviceToHost, c->stream);
+    if (!e) e = cudaStreamSynchronize(c->stream);
+    if (e) return c->cuda_fail(e, "mg_get_coarse_factor");
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) L[(size_t)i * n + j] = j <= i ? D[(size_t)i * np + j] : 0.0;
+    return MG_OK;
+}
+
+int mg_util_greedy_colouring(int32_t n, const int32_t* row_ptr, const int32_t* col, int32_t* colour,
+                             int32_t* n_colours) {
+    if (n < 0 || (n > 0 && (!row_ptr || !col || !colour))) return MG_ERR_INVALID_ARG;
+    const int32_t k = greedy_colouring(n, row_ptr, col, colour);
+    if (n_colours) *n_colours = k;
+    return MG_OK;
+}
+
+int mg_util_galerkin_pattern(int32_t n_fine, const int32_t* row_ptr, const int32_t* col, int32_t n_coarse,
+                             const int32_t* P_cols, const double* P_w, int32_t* c_row_ptr, int64_t* c_nnz,
+                             int32_t* c_col) {
+    if (n_fine < 0 || n_coarse < 0 || !row_ptr || !col || !P_cols || !P_w || !c_row_ptr || !c_nnz)
+        return MG_ERR_INVALID_ARG;
+    for (int64_t t = 0; t < 3 * (int64_t)n_fine; ++t)
+        if (P_cols[t] < 0 || P_cols[t] >= n_coarse) return MG_ERR_INPUT;
+    std::vector<int32_t> crp, ccol;
+    galerkin_pattern(n_fine, row_ptr, col, n_coarse, P_cols, P_w, crp, ccol);
+    std::memcpy(c_row_ptr, crp.data(), sizeof(int32_t) * (n_coarse + 1));
+    *c_nnz = (int64_t)ccol.size();
+    if (c_col) std::memcpy(c_col, ccol.data(), sizeof(int32_t) * ccol.size());
+    return MG_OK;
+}
+
+int mg_set_profiling(mg_ctx* c, int class_mask) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    const uint32_t m = (uint32_t)class_mask & ((1u << kProfClasses) - 1u);
+    uint32_t lm = ((uint32_t)class_mask >> 16) & 0xffffu;
+    if (!lm) lm = 0xffffu;
+    if (m != c->prof_mask || lm != c->prof_levels) {
+        cudaStreamSynchronize(c->stream);
+        c->harvest_events();
+        c->drop_graphs();
+        c->prof_mask = m;
+        c->prof_levels = lm;
+    }
+    return MG_OK;
+}
+
+int mg_get_profile(mg_ctx* c, double* ms, int64_t* launches) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    c->harvest_events();
+    for (int t = 0; t < kProfClasses * kProfLevels; ++t) {
+        if (ms) ms[t] = c->prof_ms[t];
+        if (launches) launches[t] = c->prof_n[t];
+        c->prof_ms[t] = 0.0;
+        c->prof_n[t] = 0;
+    }
+    return MG_OK;
+}
+
+int64_t mg_launch_count(const mg_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

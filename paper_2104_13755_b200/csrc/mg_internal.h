@@ -1,0 +1,105 @@
+// libmg internals shared by the host control plane (mg_host.cpp) and the
+// sm_100a kernels (mg_kernels.cu).  Nothing here is visible through the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace mg {
+
+constexpr int kMaxK = 4;          // right-hand sides per solve supported by the kernels
+constexpr int kProfClasses = 9;   // see mg.h mg_get_profile
+constexpr int kProfLevels = 16;
+
+enum ProfClass {
+    PC_GS = 0, PC_RESTRICT = 1, PC_PROLONG = 2, PC_COARSE = 3, PC_RESNORM = 4,
+    PC_GALERKIN = 5, PC_ASSEMBLY = 6, PC_FACTOR = 7, PC_PERMUTE = 8
+};
+
+// Device buffer owned by the context.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count) {
+        if (count <= n && p) return cudaSuccess;
+        release();
+        if (count == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        return e;
+    }
+    cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
+        cudaError_t e = alloc(v.size());
+        if (e != cudaSuccess || v.empty()) return e;
+        return cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    }
+};
+
+// One grid of the hierarchy.  "internal" order = rows grouped by Alg. 3
+// colour (ascending), locality (Morton) order inside a colour; the coarsest
+// level keeps the user order (it has no smoother).
+struct Level {
+    int32_t n = 0;
+    int64_t nnz = 0;
+    int32_t ncolours = 0;
+    int lpr = 8;                          // lanes per row of the CSR kernels
+    std::vector<double> V;                // user-order positions [n][3]
+    std::vector<int32_t> colour;          // user order
+    std::vector<int32_t> colour_off;      // internal row ranges per colour [ncolours+1]
+    std::vector<int32_t> perm, iperm;     // perm[internal] = user, iperm[user] = internal
+    std::vector<int32_t> urp, ucol;       // user-order CSR pattern
+    std::vector<int32_t> irp, icol;       // internal CSR pattern
+    std::vector<int64_t> i2u;             // internal nnz -> user nnz
+    // ELL-3 prolongation P_l (this level fine, next level coarse), user order
+    std::vector<int32_t> Pc_user;
+    std::vector<double> Pw_user;
+
+    DBuf<int32_t> rp, col;                // internal CSR pattern
+    DBuf<double> val;                     // internal values
+    DBuf<int32_t> pc;                     // P_l SoA [3][n], coarse internal column
+    DBuf<double> pw;                      // P_l SoA [3][n]
+    DBuf<int32_t> cptr, cidx;             // transpose of P_{l-1} (this level coarse): children
+    DBuf<double> cw;
+    DBuf<int32_t> gal_order;              // rows of this level in locality order (Galerkin)
+    DBuf<int32_t> dperm;                  // perm on device
+    DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
+    DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
+};
+
+// Launch helpers (mg_kernels.cu).  All enqueue on `s` and return the number
+// of kernel launches issued.
+int launch_gs_colour(int K, int lpr, const Level& L, int r0, int r1, cudaStream_t s);
+int launch_residual(int K, int lpr, const Level& L, cudaStream_t s);      // L.r = L.b - A L.x
+int launch_restrict(int K, const Level& coarse, const Level& fine, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
+int launch_prolong(int K, const Level& fine, const Level& coarse, cudaStream_t s);   // fine.x += P coarse.x
+int launch_resnorm(int K, int lpr, const Level& L, double* partial, int nblk_max, const double* bnorm,
+                   double* rho_out, cudaStream_t s);
+int launch_sumsq(int K, const double* v, int n, double* partial, int nblk_max, double* out, cudaStream_t s);
+int resnorm_blocks(int n);
+int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s);
+int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
+int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
+int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
+                 double* M_int, cudaStream_t s);
+int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);
+int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
+int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s);
+int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
+int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
+int launch_chol_solve(int K, const double* D, const double* Linv, int npad, int n, const double* b, double* x,
+                      cudaStream_t s);
+
+}  // namespace mg

@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (libmg through its C ABI) against the CPU oracle
+on the same seeded inputs (SURVEY.md §8(c.4) tolerances).
+
+Integer outputs (colourings, coarse CSR patterns) must be bit-exact; X within
+1e-9 relative per column at the same cycle count; each cycle's residual norm
+within 1e-8 relative plus the rounding floor tau_k (reading A20); coarse
+operator values and M within 1e-12 row-normwise.
+"""
+import numpy as np
+import pytest
+
+import meshgen
+from parity_util import (check_history, check_level_parity, check_x, gpu_solver, oracle_problem, oracle_rhs,
+                         tau_floor)
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [(1, {}), (1, {"four_grids": True}), (2, {"subdiv": 5}), (3, {"grid": (96, 80)}), (4, {"subdiv": 5}),
+         (5, {"subdiv": 5})]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2104_13755_b200 import build
+    build.build()
+
+
+def _gpu_rhs(S, p, n):
+    if p.rhs_kind == "direct":
+        return np.ascontiguousarray(p.rhs, np.float64)
+    f = np.ascontiguousarray(p.rhs if p.rhs_kind == "mass" else p.levels[0][0], np.float64)
+    B = np.empty_like(f)
+    S.apply_mass(f, B)
+    return B
+
+
+@pytest.mark.parametrize("cid,kw", SMALL)
+def test_assembly_galerkin_colouring(ora, cid, kw):
+    p = meshgen.make_config(cid, **kw)
+    A, M, mgo = oracle_problem(ora, p)
+    S = gpu_solver(p)
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    from paper_2104_13755_b200 import mg
+    Mg = mg.mg_get_mass(S.ctx, p.n)
+    assert np.abs(Mg - M).max() <= 1e-12 * np.abs(M).max()
+    for l in range(len(p.sizes)):
+        check_level_parity(S, mgo, l)
+    nH = p.sizes[-1]
+    Lg = mg.mg_get_coarse_factor(S.ctx, nH)
+    Lo = np.tril(mgo.coarse_factor())
+    assert np.abs(Lg - Lo).max() <= 1e-11 * np.abs(Lo).max()
+
+
+@pytest.mark.parametrize("cid,kw", SMALL)
+def test_solve_parity(ora, cid, kw):
+    p = meshgen.make_config(cid, **kw)
+    A, M, mgo = oracle_problem(ora, p)
+    S = gpu_solver(p)
+    if p.rhs_kind == "mcf":
+        pytest.skip("config 5 loop covered by test_mcf_loop_parity")
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    Bo = oracle_rhs(ora, p, M)
+    Bg = _gpu_rhs(S, p, p.n)
+    assert np.abs(Bg - Bo).max() <= 1e-12 * np.abs(Bo).max()
+    Xo, ho, rco = mgo.solve(Bo, rel_tol=p.rel_tol, max_cycles=p.max_cycles)
+    cyc_o = ho.shape[0] - 1
+    # same cycle count: fixed-cycle mode on the GPU
+    Xg = np.zeros_like(Bo)
+    rc, cyc, hg = S.solve(Bo, Xg, rel_tol=0.0, max_cycles=cyc_o)
+    assert cyc == cyc_o
+    check_x(Xg, Xo)
+    check_history(hg, ho, tau_floor(A.to_scipy(), Xo, Bo))
+    # own stopping rule: within +-1 cycle of the oracle
+    Xg2 = np.zeros_like(Bo)
+    rc2, cyc2, hg2 = S.solve(Bo, Xg2, rel_tol=p.rel_tol, max_cycles=p.max_cycles)
+    assert rc2 == 0 and abs(cyc2 - cyc_o) <= 1
+
+
+def test_matrix_from_csr_host_and_device(ora):
+    import torch
+    p = meshgen.make_config(2, subdiv=5)
+    A, M, mgo = oracle_problem(ora, p)
+    rp, col, val = A.arrays()
+    rp32 = rp.astype(np.int32)
+    B = np.random.default_rng(0).standard_normal((p.n, 2))
+    Xo, ho, _ = mgo.solve(B, rel_tol=0.0, max_cycles=6)
+    outs = []
+    for dev in (False, True):
+        S = gpu_solver(p)
+        if dev:
+            S.set_matrix(torch.from_numpy(rp32).cuda(), torch.from_numpy(col).cuda(), torch.from_numpy(val).cuda())
+            Bt = torch.from_numpy(B).cuda()
+            Xt = torch.zeros_like(Bt)
+            rc, cyc, hg = S.solve(Bt, Xt, rel_tol=0.0, max_cycles=6)
+            Xg = Xt.cpu().numpy()
+        else:
+            S.set_matrix(rp32, col, val)
+            Xg = np.zeros_like(B)
+            rc, cyc, hg = S.solve(B, Xg, rel_tol=0.0, max_cycles=6)
+        for l in range(len(p.sizes)):
+            check_level_parity(S, mgo, l)
+        check_x(Xg, Xo)
+        check_history(hg, ho, tau_floor(A.to_scipy(), Xo, B))
+        outs.append(Xg)
+    assert np.array_equal(outs[0], outs[1])      # deterministic kernels: bitwise identical
+
+
+def test_k_columns_are_independent_and_deterministic(ora):
+    p = meshgen.make_config(3, grid=(64, 64))
+    S = gpu_solver(p)
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    rng = np.random.default_rng(1)
+    B = rng.standard_normal((p.n, 4))
+    X4 = np.zeros_like(B)
+    S.solve(B, X4, rel_tol=0.0, max_cycles=5)
+    for k in (1, 2, 3):
+        Xk = np.zeros((p.n, k))
+        S.solve(np.ascontiguousarray(B[:, :k]), Xk, rel_tol=0.0, max_cycles=5)
+        assert np.array_equal(Xk, X4[:, :k])
+    X4b = np.zeros_like(B)
+    S.solve(B, X4b, rel_tol=0.0, max_cycles=5)
+    assert np.array_equal(X4, X4b)
+
+
+def test_mcf_loop_parity(ora):
+    """Config 5 (implicit MCF, reading A15) on a small sphere: per step GPU
+    assembly + Galerkin + factor + apply_mass + warm-started solve, run for
+    the oracle's per-step cycle counts."""
+    p = meshgen.make_config(5, subdiv=5)
+    steps = 5
+    V0, F = p.levels[0]
+    Xo, cycles = ora.mcf(p.sizes, p.P, V0, F, p.lap_coeff, steps, rel_tol=p.rel_tol)
+    S = gpu_solver(p)
+    X = np.ascontiguousarray(V0, np.float64).copy()
+    for t in range(steps):
+        S.set_matrix_cotan(X, 1.0, p.lap_coeff)
+        B = np.empty_like(X)
+        S.apply_mass(X, B)
+        Xn = X.copy()
+        rc, cyc, h = S.solve(B, Xn, rel_tol=0.0, max_cycles=cycles[t])
+        X = Xn
+    check_x(X, Xo)
+    # and with the GPU's own stopping rule: same positions to the solve tolerance
+    S2 = gpu_solver(p)
+    X2 = np.ascontiguousarray(V0, np.float64).copy()
+    for t in range(steps):
+        S2.set_matrix_cotan(X2, 1.0, p.lap_coeff)
+        B = np.empty_like(X2)
+        S2.apply_mass(X2, B)
+        rc, cyc, h = S2.solve(B, X2, rel_tol=p.rel_tol, max_cycles=p.max_cycles)
+        assert rc == 0 and abs(cyc - cycles[t]) <= 1
+    assert np.abs(X2 - Xo).max() <= 1e-6 * np.abs(Xo).max()
+
+
+# --------------------------------------------------------------------------- edge cases
+
+
+def test_single_level_is_direct_solve(ora):
+    levels, _ = meshgen.icosphere_levels(3, 3)
+    V, F = levels[0]
+    from paper_2104_13755_b200 import mg
+    S = mg.Solver(levels, [])
+    S.set_matrix_cotan(V, 1.0, 1e-2)
+    A, M = ora.assemble(V, F, 1.0, 1e-2)
+    b = np.random.default_rng(2).standard_normal((V.shape[0], 1))
+    X = np.zeros_like(b)
+    rc, cyc, h = S.solve(b, X, rel_tol=1e-12, max_cycles=3)
+    xs = np.linalg.solve(A.to_scipy().toarray(), b)
+    assert rc == 0 and cyc == 1
+    assert np.linalg.norm(X - xs) <= 1e-12 * np.linalg.norm(xs)
+
+
+def test_zero_rhs_and_loose_tolerance(ora):
+    p = meshgen.make_config(1)
+    S = gpu_solver(p)
+    S.set_matrix_cotan(p.levels[0][0], 1.0, 1e-3)
+    Z = np.zeros((p.n, 1))
+    X = np.zeros((p.n, 1))
+    rc, cyc, h = S.solve(Z, X, rel_tol=1e-10, max_cycles=5)
+    assert rc == 0 and cyc == 0 and not X.any()
+    b = np.ones((p.n, 1))
+    rc, cyc, h = S.solve(b, X, rel_tol=2.0, max_cycles=5)
+    assert rc == 0 and cyc == 0 and h[0, 0] == 1.0
+    from paper_2104_13755_b200 import mg
+    rc, cyc, h = S.solve(b, X, rel_tol=1e-30, max_cycles=3)
+    assert rc == mg.MG_NOT_CONVERGED and cyc == 3 and h.shape[0] == 4
+
+
+def test_errors_are_reported():
+    from paper_2104_13755_b200 import mg
+    p = meshgen.make_config(1)
+    ctx = mg.mg_create(0)
+    try:
+        with pytest.raises(mg.MGError) as e:
+            mg.mg_solve(ctx, 1, np.zeros((p.n, 1)), np.zeros((p.n, 1)), 1e-8, 3)
+        assert e.value.code == mg.MG_ERR_STATE
+        bad = [(c, w.copy()) for c, w in p.P]
+        bad[0][1][5, 0] += 1e-6
+        with pytest.raises(mg.MGError) as e:
+            mg.mg_hierarchy_load(ctx, p.levels, bad)
+        assert e.value.code == mg.MG_ERR_INPUT and "row 5" in str(e.value)
+        mg.mg_hierarchy_load(ctx, p.levels, p.P)
+        with pytest.raises(mg.MGError) as e:
+            mg.mg_set_matrix_cotan(ctx, p.levels[0][0], 1.0, -2.0)   # indefinite: coarse pivot fails
+        assert e.value.code == mg.MG_ERR_NOT_SPD
+        mg.mg_set_matrix_cotan(ctx, p.levels[0][0], 1.0, 1e-3)
+        with pytest.raises(mg.MGError) as e:
+            mg.mg_solve(ctx, 5, np.zeros((p.n, 5)), np.zeros((p.n, 5)), 1e-8, 3)
+        assert e.value.code == mg.MG_ERR_INVALID_ARG
+        b = np.ones((p.n, 1))
+        b[3] = np.nan
+        with pytest.raises(mg.MGError) as e:
+            mg.mg_solve(ctx, 1, b, np.zeros((p.n, 1)), 1e-8, 3)
+        assert e.value.code == mg.MG_ERR_NUMERIC
+        with pytest.raises(mg.MGError) as e:
+            mg.mg_set_matrix(ctx, p.n - 1, 1, np.zeros(p.n, np.int32), np.zeros(1, np.int32), np.ones(1))
+        assert e.value.code == mg.MG_ERR_SHAPE
+    finally:
+        mg.mg_destroy(ctx)
+
+
+# --------------------------------------------------------------------------- full sizes
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cid", [2, 3])
+def test_full_size_parity(ora, cid):
+    """BASELINE.json configs 2 and 3 at full size, full-vector comparison."""
+    p = meshgen.make_config(cid)
+    A, M, mgo = oracle_problem(ora, p)
+    S = gpu_solver(p)
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    for l in range(len(p.sizes)):
+        check_level_parity(S, mgo, l)
+    Bo = oracle_rhs(ora, p, M)
+    Xo, ho, rco = mgo.solve(Bo, rel_tol=p.rel_tol, max_cycles=p.max_cycles)
+    assert rco == 0
+    Xg = np.zeros_like(Bo)
+    rc, cyc, hg = S.solve(_gpu_rhs(S, p, p.n), Xg, rel_tol=0.0, max_cycles=ho.shape[0] - 1)
+    check_x(Xg, Xo)
+    check_history(hg, ho, tau_floor(A.to_scipy(), Xo, Bo))
