@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -189,7 +190,8 @@ struct mg_ctx {
     DBuf<double> Vstage, Vint, Mint, Muser;
 
     int npad = 0;
-    DBuf<double> D, Linv;
+    DBuf<double> D, Linv, Ainv;
+    int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     DBuf<int> errflag;
 
     DBuf<double> partial, bnorm, rho;
@@ -362,6 +364,20 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         }
         const double avg = L.n ? (double)L.nnz / L.n : 1.0;
         L.lpr = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+        // shared-memory capacity of the tile-staged kernels
+        const int T = tile_rows();
+        auto tile_max = [&](int r0, int r1) {
+            int m = 0;
+            for (int a = r0; a < r1; a += T) m = std::max(m, L.irp[std::min(a + T, r1)] - L.irp[a]);
+            return m;
+        };
+        L.cap_all = tile_max(0, L.n);
+        L.cap_gs = 0;
+        for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k)
+            L.cap_gs = std::max(L.cap_gs, tile_max(L.colour_off[k], L.colour_off[k + 1]));
+        L.cap_gs = std::max(L.cap_gs, 1);
+        L.cap_all = std::max(L.cap_all, 1);
+        L.tiled = (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
     }
     cudaStream_t s = c->stream;
     for (int l = 0; l <= H; ++l) {
@@ -418,6 +434,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
     c->npad = (nH + 31) / 32 * 32;
     cudaError_t e;
     if ((e = c->D.alloc((size_t)c->npad * c->npad)) || (e = c->Linv.alloc((size_t)c->npad * 32)) ||
+        (e = c->Ainv.alloc((size_t)c->npad * c->npad)) ||
         (e = c->errflag.alloc(1)) || (e = c->partial.alloc((size_t)resnorm_blocks(0) * kMaxK)) ||
         (e = c->bnorm.alloc(kMaxK)) || (e = c->rho.alloc(kMaxK)))
         return c->cuda_fail(e, "pattern alloc");
@@ -435,7 +452,9 @@ int rebuild_hierarchy(mg_ctx* c) {
     cudaError_t e = cudaMemsetAsync(c->errflag.p, 0, sizeof(int), s);
     if (e) return c->cuda_fail(e, "factor");
     c->timed(PC_FACTOR, c->H, s, [&] {
-        return launch_densify(LH, c->D.p, c->npad, s) + launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
+        int n = launch_densify(LH, c->D.p, c->npad, s) + launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
+        if (c->coarse_mode == 1) n += launch_chol_inverse(c->D.p, c->Linv.p, c->npad, c->Ainv.p, s);
+        return n;
     });
     int flag = 0;
     if ((e = cudaMemcpyAsync(&flag, c->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
@@ -466,7 +485,10 @@ void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
         });
     }
     Level& LH = *c->lv[H];
-    c->timed(PC_COARSE, H, s, [&] { return launch_chol_solve(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, s); });
+    c->timed(PC_COARSE, H, s, [&] {
+        return c->coarse_mode == 1 ? launch_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, s)
+                                   : launch_chol_solve(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, s);
+    });
     for (int l = H - 1; l >= 0; --l) {
         Level& L = *c->lv[l];
         c->timed(PC_PROLONG, l, s, [&] { return launch_prolong(K, L, *c->lv[l + 1], s); });
@@ -555,6 +577,8 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
         }
         c->own_stream = true;
     }
+    init_kernel_attributes();
+    if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
         delete c;

@@ -55,7 +55,10 @@ struct Level {
     int32_t n = 0;
     int64_t nnz = 0;
     int32_t ncolours = 0;
-    int lpr = 8;                          // lanes per row of the CSR kernels
+    int lpr = 8;                          // lanes per row of the CSR kernels (untiled fallback)
+    bool tiled = false;                   // tile-staged kernels usable (tiles fit in shared memory)
+    int cap_gs = 0;                       // max nnz of a kTile-row tile inside one colour range
+    int cap_all = 0;                      // max nnz of a kTile-row tile of the whole matrix
     std::vector<double> V;                // user-order positions [n][3]
     std::vector<int32_t> colour;          // user order
     std::vector<int32_t> colour_off;      // internal row ranges per colour [ncolours+1]
@@ -89,6 +92,9 @@ int launch_resnorm(int K, int lpr, const Level& L, double* partial, int nblk_max
                    double* rho_out, cudaStream_t s);
 int launch_sumsq(int K, const double* v, int n, double* partial, int nblk_max, double* out, cudaStream_t s);
 int resnorm_blocks(int n);
+int tile_rows();
+size_t tile_smem_limit();
+void init_kernel_attributes();
 int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s);
 int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
@@ -99,6 +105,8 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
 int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s);
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
+int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);
+int launch_coarse_gemv(int K, const double* Z, int npad, int n, const double* b, double* x, cudaStream_t s);
 int launch_chol_solve(int K, const double* D, const double* Linv, int npad, int n, const double* b, double* x,
                       cudaStream_t s);
 

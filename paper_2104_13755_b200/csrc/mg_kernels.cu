@@ -122,6 +122,181 @@ __global__ void __launch_bounds__(kBlock) k_residual(const int* __restrict__ rp,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tile-staged CSR kernels (used for every level whose tiles fit in shared
+// memory).  A CTA owns a tile of kTile consecutive rows: the row pointers and
+// the tile's contiguous run of (col, val) are staged into shared memory with
+// fully coalesced streaming loads, then each thread processes one row from
+// shared memory, issuing its x gathers in independent batches of UNR so the
+// L2 latency of the gathers overlaps.  One HBM pass over A per sweep.
+constexpr int kTile = 256;
+
+__device__ __forceinline__ int tile_stage(const int* __restrict__ rp, const int* __restrict__ col,
+                                          const double* __restrict__ val, int row0, int nrow, int* rps, int* cs,
+                                          double* vs, uint64_t pol) {
+    const int t = threadIdx.x;
+    if (t < nrow) rps[t] = rp[row0 + t];
+    if (t == 0) rps[nrow] = rp[row0 + nrow];
+    __syncthreads();
+    const int e0 = rps[0];
+    const int cnt = rps[nrow] - e0;
+    const int* cg = col + e0;
+    const double* vg = val + e0;
+    int q = t;
+    for (; q + 3 * kTile < cnt; q += 4 * kTile) {
+        const int c0 = ld_stream(cg + q, pol), c1 = ld_stream(cg + q + kTile, pol), c2 = ld_stream(cg + q + 2 * kTile, pol),
+                  c3 = ld_stream(cg + q + 3 * kTile, pol);
+        const double v0 = ld_stream(vg + q, pol), v1 = ld_stream(vg + q + kTile, pol), v2 = ld_stream(vg + q + 2 * kTile, pol),
+                     v3 = ld_stream(vg + q + 3 * kTile, pol);
+        cs[q] = c0;
+        cs[q + kTile] = c1;
+        cs[q + 2 * kTile] = c2;
+        cs[q + 3 * kTile] = c3;
+        vs[q] = v0;
+        vs[q + kTile] = v1;
+        vs[q + 2 * kTile] = v2;
+        vs[q + 3 * kTile] = v3;
+    }
+    for (; q < cnt; q += kTile) {
+        cs[q] = ld_stream(cg + q, pol);
+        vs[q] = ld_stream(vg + q, pol);
+    }
+    __syncthreads();
+    return e0;
+}
+
+// Row dot product from the staged tile: s[c] = sum_{j != row} a_rj x_jc, d = a_rr.
+template <int K, int UNR>
+__device__ __forceinline__ void tile_row(const int* cs, const double* vs, int qb, int qe, int row,
+                                         const double* __restrict__ x, double (&s)[K], double& d) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = 0.0;
+    d = 0.0;
+    for (int q = qb; q < qe; q += UNR) {
+        int j[UNR];
+        double a[UNR];
+        double xv[UNR][K];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const bool ok = q + u < qe;
+            j[u] = ok ? cs[q + u] : row;
+            a[u] = ok ? vs[q + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int c = 0; c < K; ++c) xv[u][c] = x[(size_t)j[u] * K + c];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (j[u] == row) {
+                d += a[u];
+            } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) s[c] = fma(a[u], xv[u][c], s[c]);
+            }
+        }
+    }
+}
+
+template <int K>
+struct Unroll {
+    static constexpr int value = K == 1 ? 8 : 4;
+};
+
+// K4 (tiled): one colour class [r0, r1), one tile per CTA.  Dynamic shared
+// memory: cap doubles (values) then cap ints (columns), cap >= nnz of any tile.
+template <int K>
+__global__ void __launch_bounds__(kTile) k_gs_tiled(const int* __restrict__ rp, const int* __restrict__ col,
+                                                    const double* __restrict__ val, const double* __restrict__ b,
+                                                    double* __restrict__ x, int r0, int r1, int cap) {
+    extern __shared__ double smem_d[];
+    __shared__ int rps[kTile + 1];
+    double* vs = smem_d;
+    int* cs = reinterpret_cast<int*>(smem_d + cap);
+    const uint64_t pol = evict_first_policy();
+    const int row0 = r0 + blockIdx.x * kTile;
+    const int nrow = min(kTile, r1 - row0);
+    const int e0 = tile_stage(rp, col, val, row0, nrow, rps, cs, vs, pol);
+    const int t = threadIdx.x;
+    if (t >= nrow) return;
+    const int row = row0 + t;
+    double s[K], d;
+    tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
+#pragma unroll
+    for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / d;
+}
+
+// K5a (tiled): r = b - A x over all rows.
+template <int K>
+__global__ void __launch_bounds__(kTile) k_residual_tiled(const int* __restrict__ rp, const int* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ b, const double* __restrict__ x,
+                                                          double* __restrict__ r, int n, int cap) {
+    extern __shared__ double smem_d[];
+    __shared__ int rps[kTile + 1];
+    double* vs = smem_d;
+    int* cs = reinterpret_cast<int*>(smem_d + cap);
+    const uint64_t pol = evict_first_policy();
+    const int row0 = blockIdx.x * kTile;
+    const int nrow = min(kTile, n - row0);
+    const int e0 = tile_stage(rp, col, val, row0, nrow, rps, cs, vs, pol);
+    const int t = threadIdx.x;
+    if (t >= nrow) return;
+    const int row = row0 + t;
+    double s[K], d;
+    tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
+#pragma unroll
+    for (int c = 0; c < K; ++c) r[(size_t)row * K + c] = b[(size_t)row * K + c] - fma(d, x[(size_t)row * K + c], s[c]);
+}
+
+// K3 (tiled, persistent): block partial sums of (b - A x)^2 per column.
+template <int K>
+__global__ void __launch_bounds__(kTile) k_resnorm_tiled(const int* __restrict__ rp, const int* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ b, const double* __restrict__ x,
+                                                         double* __restrict__ partial, int n, int cap) {
+    extern __shared__ double smem_d[];
+    __shared__ int rps[kTile + 1];
+    __shared__ double red[kTile / 32][K];
+    double* vs = smem_d;
+    int* cs = reinterpret_cast<int*>(smem_d + cap);
+    const uint64_t pol = evict_first_policy();
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    const int ntiles = (n + kTile - 1) / kTile;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int row0 = tile * kTile;
+        const int nrow = min(kTile, n - row0);
+        const int e0 = tile_stage(rp, col, val, row0, nrow, rps, cs, vs, pol);
+        const int t = threadIdx.x;
+        if (t < nrow) {
+            const int row = row0 + t;
+            double s[K], d;
+            tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double rr = b[(size_t)row * K + c] - fma(d, x[(size_t)row * K + c], s[c]);
+                acc[c] = fma(rr, rr, acc[c]);
+            }
+        }
+        __syncthreads();   // smem reuse by the next tile
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        double v = acc[c];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double v = 0.0;
+        for (int w = 0; w < kTile / 32; ++w) v += red[w][threadIdx.x];
+        partial[blockIdx.x * K + threadIdx.x] = v;
+    }
+}
+
 // K5b: r_c = P^T r, gathered through the transpose of P (children of each
 // coarse vertex) so no atomics are needed and the result is deterministic.
 // Also zeroes the coarse iterate: the recursive V-cycle starts from 0.
@@ -663,12 +838,87 @@ __global__ void __launch_bounds__(1024) k_chol_solve(const double* __restrict__ 
     for (int i = tid; i < n * K; i += 1024) x[i] = y[i];
 }
 
+// Explicit inverse A_H^{-1} = L^{-T} L^{-1} from the factor: CTA b solves
+// L L^T Z = I for columns [16b, 16b+16) by blocked forward/backward
+// substitution (off-diagonal blocks streamed from L2 as warp-broadcast
+// loads, diagonal blocks applied through their inverses).  Computed once per
+// rebuild; afterwards every coarsest solve is one GEMV (k_coarse_gemv).
+constexpr int kInvCols = 16;
+__global__ void __launch_bounds__(512) k_chol_inverse(const double* __restrict__ L, const double* __restrict__ Linv,
+                                                      int npad, double* __restrict__ Z) {
+    extern __shared__ double sm[];
+    double* Y = sm;                          // [npad][16]
+    double* T = sm + (size_t)npad * kInvCols; // [32][16]
+    const int tid = threadIdx.x, r = tid >> 4, c = tid & 15;
+    const int c0 = blockIdx.x * kInvCols;
+    const int nb = npad / 32;
+    for (int I = 0; I < nb; ++I) {
+        double acc = 0.0;
+        const double* Lr = L + (size_t)(32 * I + r) * npad;
+        for (int j = 0; j < 32 * I; ++j) acc = fma(Lr[j], Y[j * kInvCols + c], acc);
+        T[r * kInvCols + c] = ((32 * I + r) == (c0 + c) ? 1.0 : 0.0) - acc;
+        __syncthreads();
+        double v = 0.0;
+        const double* Li = Linv + (size_t)I * 1024 + r * 32;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) v = fma(Li[q], T[q * kInvCols + c], v);
+        Y[(32 * I + r) * kInvCols + c] = v;
+        __syncthreads();
+    }
+    for (int I = nb - 1; I >= 0; --I) {
+        double acc = 0.0;
+        for (int j = 32 * (I + 1); j < npad; ++j) acc = fma(L[(size_t)j * npad + 32 * I + r], Y[j * kInvCols + c], acc);
+        T[r * kInvCols + c] = Y[(32 * I + r) * kInvCols + c] - acc;
+        __syncthreads();
+        double v = 0.0;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) v = fma(Linv[(size_t)I * 1024 + q * 32 + r], T[q * kInvCols + c], v);
+        Y[(32 * I + r) * kInvCols + c] = v;
+        __syncthreads();
+    }
+    for (int i = tid; i < npad * kInvCols; i += 512) Z[(size_t)(i / kInvCols) * npad + c0 + (i % kInvCols)] = Y[i];
+}
+
+// Coarsest solve x = A_H^{-1} b: one warp per row of the inverse (coalesced
+// row reads from L2), K columns.
+template <int K>
+__global__ void __launch_bounds__(256) k_coarse_gemv(const double* __restrict__ Z, int npad, int n,
+                                                     const double* __restrict__ b, double* __restrict__ x) {
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const double* Zr = Z + (size_t)row * npad;
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    for (int j = lane; j < n; j += 32) {
+        const double z = Zr[j];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = fma(z, b[(size_t)j * K + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = acc[c];
+}
+
 inline int nblk(int64_t n, int per) { return (int)((n + per - 1) / per); }
+
+inline size_t tile_smem(int cap) { return (size_t)cap * (sizeof(double) + sizeof(int)); }
 
 template <int K>
 int gs_dispatch(int lpr, const Level& L, int r0, int r1, cudaStream_t s) {
     const int rows = r1 - r0;
     if (rows <= 0) return 0;
+    if (L.tiled) {
+        k_gs_tiled<K><<<nblk(rows, kTile), kTile, tile_smem(L.cap_gs), s>>>(L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r0,
+                                                                            r1, L.cap_gs);
+        return 1;
+    }
     const int grid = nblk((int64_t)rows * lpr, kBlock);
     switch (lpr) {
         case 4: k_gs_colour<K, 4><<<grid, kBlock, 0, s>>>(L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r0, r1); break;
@@ -681,6 +931,11 @@ int gs_dispatch(int lpr, const Level& L, int r0, int r1, cudaStream_t s) {
 
 template <int K>
 int residual_dispatch(int lpr, const Level& L, cudaStream_t s) {
+    if (L.tiled) {
+        k_residual_tiled<K><<<nblk(L.n, kTile), kTile, tile_smem(L.cap_all), s>>>(L.rp.p, L.col.p, L.val.p, L.b.p,
+                                                                                  L.x.p, L.r.p, L.n, L.cap_all);
+        return 1;
+    }
     const int grid = nblk((int64_t)L.n * lpr, kBlock);
     switch (lpr) {
         case 4: k_residual<K, 4><<<grid, kBlock, 0, s>>>(L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, L.r.p, L.n); break;
@@ -694,6 +949,13 @@ int residual_dispatch(int lpr, const Level& L, cudaStream_t s) {
 template <int K>
 int resnorm_dispatch(int lpr, const Level& L, double* partial, int nb, const double* bnorm, double* rho,
                      cudaStream_t s) {
+    if (L.tiled) {
+        const int grid = std::min(nb, nblk(L.n, kTile));
+        k_resnorm_tiled<K><<<grid, kTile, tile_smem(L.cap_all), s>>>(L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial,
+                                                                     L.n, L.cap_all);
+        k_norm_finalize<K><<<1, kBlock, 0, s>>>(partial, grid, bnorm, rho);
+        return 2;
+    }
     switch (lpr) {
         case 4: k_resnorm_partial<K, 4><<<nb, kBlock, 0, s>>>(L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
         case 8: k_resnorm_partial<K, 8><<<nb, kBlock, 0, s>>>(L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
@@ -775,22 +1037,43 @@ struct MassF {
     }
 };
 template <int K>
+struct GemvF {
+    static int run(const double* Z, int npad, int n, const double* b, double* x, cudaStream_t s) {
+        k_coarse_gemv<K><<<nblk(n, 8), 256, 0, s>>>(Z, npad, n, b, x);
+        return 1;
+    }
+};
+template <int K>
 struct CholSolveF {
     static int run(const double* D, const double* Linv, int npad, int n, const double* b, double* x, cudaStream_t s) {
         const size_t smem = sizeof(double) * ((size_t)npad * K + 32 * 32 * K + 32 * K);
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(k_chol_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-            attr_set = true;
-        }
         k_chol_solve<K><<<1, 1024, smem, s>>>(D, Linv, npad, n, b, x);
         return 1;
     }
 };
 
+template <int K>
+void set_attrs() {
+    const int big = 200 * 1024;
+    cudaFuncSetAttribute(k_gs_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_residual_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_resnorm_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_chol_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_chol_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+}
+
 }  // namespace
 
 int resnorm_blocks(int n) { return kNormBlocks; }
+int tile_rows() { return kTile; }
+size_t tile_smem_limit() { return 160 * 1024; }
+
+void init_kernel_attributes() {
+    set_attrs<1>();
+    set_attrs<2>();
+    set_attrs<3>();
+    set_attrs<4>();
+}
 
 int launch_gs_colour(int K, int lpr, const Level& L, int r0, int r1, cudaStream_t s) {
     return dispatch_k<GsF>(K, lpr, &L, r0, r1, s);
@@ -862,6 +1145,14 @@ int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t
     }
     k_chol_diaginv<<<nb, 32, 0, s>>>(D, npad, Linv);
     return launches + 1;
+}
+int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s) {
+    const size_t smem = sizeof(double) * ((size_t)npad * kInvCols + 32 * kInvCols);
+    k_chol_inverse<<<npad / kInvCols, 512, smem, s>>>(D, Linv, npad, Z);
+    return 1;
+}
+int launch_coarse_gemv(int K, const double* Z, int npad, int n, const double* b, double* x, cudaStream_t s) {
+    return dispatch_k<GemvF>(K, Z, npad, n, b, x, s);
 }
 int launch_chol_solve(int K, const double* D, const double* Linv, int npad, int n, const double* b, double* x,
                       cudaStream_t s) {
