@@ -18,13 +18,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INC}", f"-I{CSRC}"]
-CU_SOURCES = ["mg_kernels.cu"]
+CU_SOURCES = ["mg_vcycle.cu", "mg_setup.cu"]
 CPP_SOURCES = ["mg_host.cpp"]
 
 
 def _sources():
     return [os.path.join(CSRC, f) for f in CU_SOURCES + CPP_SOURCES] + \
-        [os.path.join(CSRC, "mg_internal.h"), os.path.join(INC, "mg.h")]
+        [os.path.join(CSRC, "mg_internal.h"), os.path.join(CSRC, "mg_common.cuh"), os.path.join(INC, "mg.h")]
 
 
 def up_to_date():

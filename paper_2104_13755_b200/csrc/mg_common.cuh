@@ -1,0 +1,82 @@
+// Device helpers shared by the libmg kernel translation units (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mg {
+
+constexpr int kBlock = 256;
+
+__host__ __device__ inline int nblk(int64_t n, int per) { return (int)((n + per - 1) / per); }
+
+// ---- programmatic dependent launch (PDL) --------------------------------
+// Kernels of the V-cycle chain are launched with programmatic stream
+// serialisation: the next kernel is scheduled while the previous one drains,
+// runs its prologue (loads of data no earlier kernel of the solve writes:
+// matrix structure and values, prolongation, children lists) and only then
+// waits for its predecessor's memory with griddepcontrol.wait.  Both
+// instructions are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---- cache-policy loads ---------------------------------------------------
+// Streaming (read-once per sweep) matrix data: no L1 allocation, evict-first
+// in L2 so the gathered iterate x stays resident.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// ---- sub-warp groups ----------------------------------------------------
+__device__ __forceinline__ unsigned group_mask(int lpr) {
+    if (lpr >= 32) return 0xffffffffu;
+    const unsigned lane = threadIdx.x & 31u;
+    return ((1u << lpr) - 1u) << (lane & ~(unsigned)(lpr - 1));
+}
+template <int LPR>
+__device__ __forceinline__ double group_sum(double v, unsigned mask) {
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off, LPR);
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// ---- host launch helper -------------------------------------------------
+template <typename... KArgs, typename... Args>
+inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+    if (!pdl) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+}  // namespace mg

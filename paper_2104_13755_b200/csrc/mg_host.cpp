@@ -192,6 +192,7 @@ struct mg_ctx {
     int npad = 0;
     DBuf<double> D, Linv, Ainv;
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
+    bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     DBuf<int> errflag;
 
     DBuf<double> partial, bnorm, rho;
@@ -377,7 +378,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             L.cap_gs = std::max(L.cap_gs, tile_max(L.colour_off[k], L.colour_off[k + 1]));
         L.cap_gs = std::max(L.cap_gs, 1);
         L.cap_all = std::max(L.cap_all, 1);
-        L.tiled = (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
+        // tile-staged kernels for short rows (few gather batches per thread), lanes-per-row otherwise
+        L.tiled = avg <= 12.0 && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
+        if (!L.tiled) {
+            const double half = avg / 2.0;
+            L.lpr = half <= 4.0 ? 4 : half <= 8.0 ? 8 : half <= 16.0 ? 16 : 32;
+        }
     }
     cudaStream_t s = c->stream;
     for (int l = 0; l <= H; ++l) {
@@ -471,38 +477,36 @@ int rebuild_hierarchy(mg_ctx* c) {
 // residual norm of the new iterate into c->rho.
 void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
     const int H = c->H;
+    const bool pdl = c->pdl;
     for (int l = 0; l < H; ++l) {
         Level& L = *c->lv[l];
         c->timed(PC_GS, l, s, [&] {
             int n = 0;
             for (int it = 0; it < c->mu_pre; ++it)
-                for (int k = 0; k < L.ncolours; ++k)
-                    n += launch_gs_colour(K, L.lpr, L, L.colour_off[k], L.colour_off[k + 1], s);
+                for (int k = 0; k < L.ncolours; ++k) n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
             return n;
         });
         c->timed(PC_RESTRICT, l, s, [&] {
-            return launch_residual(K, L.lpr, L, s) + launch_restrict(K, *c->lv[l + 1], L, s);
+            return vc_residual(K, L, pdl, s) + vc_restrict(K, *c->lv[l + 1], L, pdl, s);
         });
     }
     Level& LH = *c->lv[H];
     c->timed(PC_COARSE, H, s, [&] {
-        return c->coarse_mode == 1 ? launch_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, s)
-                                   : launch_chol_solve(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, s);
+        return c->coarse_mode == 1 ? vc_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s)
+                                   : vc_coarse_trsv(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s);
     });
     for (int l = H - 1; l >= 0; --l) {
         Level& L = *c->lv[l];
-        c->timed(PC_PROLONG, l, s, [&] { return launch_prolong(K, L, *c->lv[l + 1], s); });
+        c->timed(PC_PROLONG, l, s, [&] { return vc_prolong(K, L, *c->lv[l + 1], pdl, s); });
         c->timed(PC_GS, l, s, [&] {
             int n = 0;
             for (int it = 0; it < c->mu_post; ++it)
-                for (int k = 0; k < L.ncolours; ++k)
-                    n += launch_gs_colour(K, L.lpr, L, L.colour_off[k], L.colour_off[k + 1], s);
+                for (int k = 0; k < L.ncolours; ++k) n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
             return n;
         });
     }
     c->timed(PC_RESNORM, 0, s, [&] {
-        return launch_resnorm(K, c->lv[0]->lpr, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p,
-                              c->rho.p, s);
+        return vc_resnorm(K, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p, c->rho.p, pdl, s);
     });
 }
 
@@ -577,8 +581,10 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
         }
         c->own_stream = true;
     }
-    init_kernel_attributes();
+    init_vcycle_attributes();
+    init_setup_attributes();
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
+    if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
         delete c;
@@ -861,10 +867,10 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
     if ((rc = to_device(c, X, c->stageX, (size_t)n * k, &dX))) return rc;
     c->timed(PC_PERMUTE, 0, s, [&] {
         return launch_gather_rows(k, L0.dperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.dperm.p, dX, L0.x.p, n, s) +
-               launch_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
+               vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
     });
     c->timed(PC_RESNORM, 0, s, [&] {
-        return launch_resnorm(k, L0.lpr, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, s);
+        return vc_resnorm(k, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, false, s);
     });
     cudaError_t e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);

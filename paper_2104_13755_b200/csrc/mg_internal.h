@@ -82,19 +82,26 @@ struct Level {
     DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
 };
 
-// Launch helpers (mg_kernels.cu).  All enqueue on `s` and return the number
-// of kernel launches issued.
-int launch_gs_colour(int K, int lpr, const Level& L, int r0, int r1, cudaStream_t s);
-int launch_residual(int K, int lpr, const Level& L, cudaStream_t s);      // L.r = L.b - A L.x
-int launch_restrict(int K, const Level& coarse, const Level& fine, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
-int launch_prolong(int K, const Level& fine, const Level& coarse, cudaStream_t s);   // fine.x += P coarse.x
-int launch_resnorm(int K, int lpr, const Level& L, double* partial, int nblk_max, const double* bnorm,
-                   double* rho_out, cudaStream_t s);
-int launch_sumsq(int K, const double* v, int n, double* partial, int nblk_max, double* out, cudaStream_t s);
+// Launch helpers.  All enqueue on `s` and return the number of kernel
+// launches issued.  `pdl`: launch with programmatic stream serialisation
+// (V-cycle graph).
+// mg_vcycle.cu
+int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
+int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);                    // L.r = L.b - A L.x
+int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
+int vc_prolong(int K, const Level& fine, const Level& coarse, bool pdl, cudaStream_t s);   // fine.x += P coarse.x
+int vc_coarse_gemv(int K, const double* Z, int npad, int n, const double* b, double* x, bool pdl, cudaStream_t s);
+int vc_coarse_trsv(int K, const double* L, const double* Linv, int npad, int n, const double* b, double* x, bool pdl,
+                   cudaStream_t s);
+int vc_resnorm(int K, const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl,
+               cudaStream_t s);
+int vc_sumsq(int K, const double* v, int n, double* partial, int nb, double* out, cudaStream_t s);
 int resnorm_blocks(int n);
 int tile_rows();
 size_t tile_smem_limit();
-void init_kernel_attributes();
+void init_vcycle_attributes();
+// mg_setup.cu
+void init_setup_attributes();
 int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s);
 int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
@@ -106,8 +113,5 @@ int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s);
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);
-int launch_coarse_gemv(int K, const double* Z, int npad, int n, const double* b, double* x, cudaStream_t s);
-int launch_chol_solve(int K, const double* D, const double* Linv, int npad, int n, const double* b, double* x,
-                      cudaStream_t s);
 
 }  // namespace mg

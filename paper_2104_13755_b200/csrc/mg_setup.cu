@@ -1,0 +1,444 @@
+// libmg setup kernels for sm_100a: everything that runs once per
+// mg_set_matrix* (assembly, Galerkin coarse operators, coarsest Cholesky
+// factor and inverse) plus the user <-> internal permutations.
+//   K1 k_cotan_assemble   cotan L + lumped M -> A = mM + lL
+//   K2 k_galerkin         A_{l+1} = P^T A_l P on a fixed pattern          (Eq. gca)
+//   K7a k_chol_*          coarsest dense Cholesky + explicit inverse     (Alg. 2, reading A12)
+//   K9 k_gather/scatter   user <-> internal (colour-grouped) ordering
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "mg_common.cuh"
+#include "mg_internal.h"
+
+namespace mg {
+namespace {
+
+// ---------------------------------------------------------------------------
+// K9: user <-> internal permutations (row blocks of K values).
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_gather_rows(const int* __restrict__ perm, const double* __restrict__ src,
+                                                        double* __restrict__ dst, int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const size_t u = (size_t)perm[i];
+#pragma unroll
+    for (int c = 0; c < K; ++c) dst[(size_t)i * K + c] = src[u * K + c];
+}
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__ perm, const double* __restrict__ src,
+                                                         double* __restrict__ dst, int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const size_t u = (size_t)perm[i];
+#pragma unroll
+    for (int c = 0; c < K; ++c) dst[u * K + c] = src[(size_t)i * K + c];
+}
+__global__ void __launch_bounds__(kBlock) k_gather_vals(const int64_t* __restrict__ i2u, const double* __restrict__ src,
+                                                        double* __restrict__ dst, int64_t nnz) {
+    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (e < nnz) dst[e] = src[i2u[e]];
+}
+
+// B = M X (user order).
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_apply_mass(const double* __restrict__ M, const double* __restrict__ X,
+                                                       double* __restrict__ B, int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const double m = M[i];
+#pragma unroll
+    for (int c = 0; c < K; ++c) B[(size_t)i * K + c] = m * X[(size_t)i * K + c];
+}
+
+// ---------------------------------------------------------------------------
+// K1: cotangent Laplacian + lumped mass on the fixed 1-ring pattern (internal
+// order).  Each off-diagonal (i,j) reads its <= 2 opposite vertices
+// (opp[2e], opp[2e+1], -1 for a boundary edge: natural BC):
+//   L_ij = -1/2 sum_o cot(angle at o),  cot = (vi-vo).(vj-vo) / |(vi-vo)x(vj-vo)|
+//   L_ii = -sum_{j != i} L_ij
+//   M_ii = 1/3 sum_{faces f at i} area_f = 1/6 sum_{(i,j)} sum_o |(vi-vo)x(vj-vo)|/2
+// (every face at i is seen from both of its edges at i).  One thread per row,
+// deterministic (no atomics).  A = mass_coeff M + lap_coeff L.
+__global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict__ rp, const int* __restrict__ col,
+                                                           const int* __restrict__ opp, const double* __restrict__ V,
+                                                           double mass_coeff, double lap_coeff,
+                                                           double* __restrict__ val, double* __restrict__ M, int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const double xi = V[3 * (size_t)i], yi = V[3 * (size_t)i + 1], zi = V[3 * (size_t)i + 2];
+    double lsum = 0.0, area2 = 0.0;
+    int ediag = -1;
+    for (int e = rp[i]; e < rp[i + 1]; ++e) {
+        const int j = col[e];
+        if (j == i) {
+            ediag = e;
+            continue;
+        }
+        const double xj = V[3 * (size_t)j], yj = V[3 * (size_t)j + 1], zj = V[3 * (size_t)j + 2];
+        double cot_sum = 0.0;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int o = opp[2 * (size_t)e + s];
+            if (o < 0) continue;
+            const double xo = V[3 * (size_t)o], yo = V[3 * (size_t)o + 1], zo = V[3 * (size_t)o + 2];
+            const double ax = xi - xo, ay = yi - yo, az = zi - zo;
+            const double bx = xj - xo, by = yj - yo, bz = zj - zo;
+            const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+            const double cr = sqrt(cx * cx + cy * cy + cz * cz);
+            cot_sum += (ax * bx + ay * by + az * bz) / cr;
+            area2 += cr;
+        }
+        const double lij = -0.5 * cot_sum;
+        lsum += lij;
+        val[e] = lap_coeff * lij;
+    }
+    const double m = area2 / 12.0;   // (1/6) * sum (|cross| / 2)
+    M[i] = m;
+    if (ediag >= 0) val[ediag] = mass_coeff * m + lap_coeff * (-lsum);
+}
+
+__global__ void k_scatter_vec(const int* __restrict__ perm, const double* __restrict__ src, double* __restrict__ dst,
+                              int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) dst[perm[i]] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// K2: Galerkin numeric phase.  One warp per coarse row I (taken in locality
+// order):  A_c[I, J] = sum_{i in children(I)} P[i,I] sum_{j in row i} A[i,j] P[j,J].
+// The (child, nonzero) pairs of the coarse row are flattened across the 32
+// lanes; each contribution finds its slot J by binary search in the coarse
+// row's (sorted) column list held in shared memory and is accumulated there.
+// Rows wider than kGalMaxM accumulate into global memory instead.
+constexpr int kGalWarps = 8;
+constexpr int kGalMaxM = 96;
+
+__device__ __forceinline__ int find_slot(const int* cols, int m, int J) {
+    int lo = 0, hi = m - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cols[mid] < J) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
+    int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
+    double* __restrict__ cval, const int* __restrict__ cptr, const int* __restrict__ cidx,
+    const double* __restrict__ cw, const int* __restrict__ rp, const int* __restrict__ col,
+    const double* __restrict__ val, const int* __restrict__ pc, const double* __restrict__ pw, int nf) {
+    __shared__ double acc[kGalWarps][kGalMaxM];
+    __shared__ int cols[kGalWarps][kGalMaxM];
+    __shared__ int ch_start[kGalWarps][32];
+    __shared__ int ch_scan[kGalWarps][32];
+    __shared__ double ch_w[kGalWarps][32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kGalWarps + w;
+    if (gw >= nc) return;
+    const int I = order[gw];
+    const int c0 = crp[I];
+    const int m = crp[I + 1] - c0;
+    const bool wide = m > kGalMaxM;
+    const int* slots = wide ? (ccol + c0) : cols[w];
+    double* accp = wide ? (cval + c0) : acc[w];
+    for (int s = lane; s < m; s += 32) {
+        if (!wide) cols[w][s] = ccol[c0 + s];
+        accp[s] = 0.0;
+    }
+    __syncwarp();
+    const int t0 = cptr[I], t1 = cptr[I + 1];
+    for (int tb = t0; tb < t1; tb += 32) {
+        const int nb = min(32, t1 - tb);
+        int len = 0;
+        if (lane < nb) {
+            const int i = cidx[tb + lane];
+            ch_w[w][lane] = cw[tb + lane];
+            const int s = rp[i];
+            ch_start[w][lane] = s;
+            len = rp[i + 1] - s;
+        }
+        int incl = len;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        ch_scan[w][lane] = incl;
+        const int total = __shfl_sync(0xffffffffu, incl, nb - 1);
+        __syncwarp();
+        for (int g = lane; g < total; g += 32) {
+            int lo = 0, hi = nb - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (ch_scan[w][mid] > g) hi = mid;
+                else lo = mid + 1;
+            }
+            const int excl = lo ? ch_scan[w][lo - 1] : 0;
+            const int e = ch_start[w][lo] + (g - excl);
+            const int j = col[e];
+            const double a = ch_w[w][lo] * val[e];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const double wq = pw[(size_t)q * nf + j];
+                if (wq != 0.0) {
+                    const int J = pc[(size_t)q * nf + j];
+                    const int slot = find_slot(slots, m, J);
+                    atomicAdd(accp + slot, a * wq);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (!wide)
+        for (int s = lane; s < m; s += 32) cval[c0 + s] = acc[w][s];
+}
+
+// ---------------------------------------------------------------------------
+// K7: coarsest level.  Dense row-major npad x npad (npad multiple of 32,
+// padding = identity), blocked right-looking Cholesky with 32-wide panels:
+// one CTA factors the diagonal block, a grid solves the panel below it, then a
+// grid of CTAs applies the rank-32 update to the trailing lower triangle.
+__global__ void k_densify_zero(double* D, size_t total) {
+    for (size_t t = (size_t)blockIdx.x * kBlock + threadIdx.x; t < total; t += (size_t)gridDim.x * kBlock) D[t] = 0.0;
+}
+__global__ void k_densify(const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
+                          int n, int npad, double* __restrict__ D) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= npad) return;
+    if (i >= n) {
+        D[(size_t)i * npad + i] = 1.0;
+        return;
+    }
+    for (int e = rp[i]; e < rp[i + 1]; ++e) D[(size_t)i * npad + col[e]] = val[e];
+}
+
+__global__ void __launch_bounds__(1024) k_chol_diag(double* __restrict__ D, int npad, int kb, int* err) {
+    __shared__ double Ld[32][33];
+    const int tid = threadIdx.x, r = tid >> 5, c = tid & 31;
+    const int base = kb * 32;
+    Ld[r][c] = D[(size_t)(base + r) * npad + base + c];
+    __syncthreads();
+    for (int p = 0; p < 32; ++p) {
+        if (tid == 0) {
+            double d = Ld[p][p];
+            if (!(d > 0.0)) {
+                atomicExch(err, 1);
+                d = 1.0;
+            }
+            Ld[p][p] = sqrt(d);
+        }
+        __syncthreads();
+        if (tid > p && tid < 32) Ld[tid][p] /= Ld[p][p];
+        __syncthreads();
+        if (r > p && c > p && c <= r) Ld[r][c] -= Ld[r][p] * Ld[c][p];
+        __syncthreads();
+    }
+    D[(size_t)(base + r) * npad + base + c] = (c <= r) ? Ld[r][c] : 0.0;
+}
+
+// panel below the diagonal block: l = a L_kk^{-T}, one thread per row
+constexpr int kTrsmThreads = 64;
+__global__ void __launch_bounds__(kTrsmThreads) k_chol_trsm(double* __restrict__ D, int npad, int kb) {
+    __shared__ double Ld[32][33];
+    const int base = kb * 32;
+    for (int s = threadIdx.x; s < 1024; s += kTrsmThreads) Ld[s >> 5][s & 31] = D[(size_t)(base + (s >> 5)) * npad + base + (s & 31)];
+    __syncthreads();
+    const int i = base + 32 + blockIdx.x * kTrsmThreads + threadIdx.x;
+    if (i >= npad) return;
+    double a[32];
+    double* Di = D + (size_t)i * npad + base;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) a[p] = Di[p];
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+        double s = a[p];
+#pragma unroll
+        for (int q = 0; q < p; ++q) s -= a[q] * Ld[p][q];
+        a[p] = s / Ld[p][p];
+    }
+#pragma unroll
+    for (int p = 0; p < 32; ++p) Di[p] = a[p];
+}
+
+__global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ D, int npad, int kb) {
+    __shared__ double Pi[32][33];
+    __shared__ double Pj[32][33];
+    const int t = blockIdx.x;
+    int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    const int tj = t - ti * (ti + 1) / 2;
+    const int bi = kb + 1 + ti, bj = kb + 1 + tj;
+    const int base = kb * 32;
+    for (int s = threadIdx.x; s < 1024; s += 256) {
+        const int r = s >> 5, c = s & 31;
+        Pi[r][c] = D[(size_t)(bi * 32 + r) * npad + base + c];
+        Pj[r][c] = D[(size_t)(bj * 32 + r) * npad + base + c];
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < 1024; s += 256) {
+        const int r = s >> 5, c = s & 31;
+        if (bi == bj && c > r) continue;
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < 32; ++p) acc = fma(Pi[r][p], Pj[c][p], acc);
+        D[(size_t)(bi * 32 + r) * npad + bj * 32 + c] -= acc;
+    }
+}
+
+// Inverse of every 32x32 diagonal block of L (for the solve); thread t
+// computes column t by forward substitution.
+__global__ void __launch_bounds__(32) k_chol_diaginv(const double* __restrict__ D, int npad, double* __restrict__ Linv) {
+    __shared__ double Ld[32][33];
+    const int I = blockIdx.x, t = threadIdx.x;
+    for (int r = 0; r < 32; ++r) Ld[r][t] = D[(size_t)(I * 32 + r) * npad + I * 32 + t];
+    __syncwarp();
+    double z[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+        double s = (r == t) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < r; ++q) s -= Ld[r][q] * z[q];
+        z[r] = (r >= t) ? s / Ld[r][r] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) Linv[(size_t)I * 1024 + r * 32 + t] = z[r];
+}
+
+// Explicit inverse A_H^{-1} = L^{-T} L^{-1} from the factor: CTA b solves
+// L L^T Z = I for columns [16b, 16b+16) by blocked forward/backward
+// substitution (off-diagonal blocks streamed from L2 as warp-broadcast
+// loads, diagonal blocks applied through their inverses).  Computed once per
+// rebuild; afterwards every coarsest solve is one GEMV (k_coarse_gemv).
+constexpr int kInvCols = 16;
+__global__ void __launch_bounds__(512) k_chol_inverse(const double* __restrict__ L, const double* __restrict__ Linv,
+                                                      int npad, double* __restrict__ Z) {
+    extern __shared__ double sm[];
+    double* Y = sm;                          // [npad][16]
+    double* T = sm + (size_t)npad * kInvCols; // [32][16]
+    const int tid = threadIdx.x, r = tid >> 4, c = tid & 15;
+    const int c0 = blockIdx.x * kInvCols;
+    const int nb = npad / 32;
+    for (int I = 0; I < nb; ++I) {
+        double acc = 0.0;
+        const double* Lr = L + (size_t)(32 * I + r) * npad;
+        for (int j = 0; j < 32 * I; ++j) acc = fma(Lr[j], Y[j * kInvCols + c], acc);
+        T[r * kInvCols + c] = ((32 * I + r) == (c0 + c) ? 1.0 : 0.0) - acc;
+        __syncthreads();
+        double v = 0.0;
+        const double* Li = Linv + (size_t)I * 1024 + r * 32;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) v = fma(Li[q], T[q * kInvCols + c], v);
+        Y[(32 * I + r) * kInvCols + c] = v;
+        __syncthreads();
+    }
+    for (int I = nb - 1; I >= 0; --I) {
+        double acc = 0.0;
+        for (int j = 32 * (I + 1); j < npad; ++j) acc = fma(L[(size_t)j * npad + 32 * I + r], Y[j * kInvCols + c], acc);
+        T[r * kInvCols + c] = Y[(32 * I + r) * kInvCols + c] - acc;
+        __syncthreads();
+        double v = 0.0;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) v = fma(Linv[(size_t)I * 1024 + q * 32 + r], T[q * kInvCols + c], v);
+        Y[(32 * I + r) * kInvCols + c] = v;
+        __syncthreads();
+    }
+    for (int i = tid; i < npad * kInvCols; i += 512) Z[(size_t)(i / kInvCols) * npad + c0 + (i % kInvCols)] = Y[i];
+}
+
+template <int K>
+void dispatch_rows(bool gather, const int32_t* perm, const double* src, double* dst, int n, cudaStream_t s) {
+    if (gather) k_gather_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n);
+    else k_scatter_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n);
+}
+void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* dst, int n, cudaStream_t s) {
+    switch (K) {
+        case 1: dispatch_rows<1>(gather, perm, src, dst, n, s); break;
+        case 2: dispatch_rows<2>(gather, perm, src, dst, n, s); break;
+        case 3: dispatch_rows<3>(gather, perm, src, dst, n, s); break;
+        default: dispatch_rows<4>(gather, perm, src, dst, n, s); break;
+    }
+}
+
+}  // namespace
+
+void init_setup_attributes() {
+    const int big = 200 * 1024;
+    cudaFuncSetAttribute(k_chol_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+}
+
+int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s) {
+    if (n <= 0) return 0;
+    rows_k(K, true, perm, src_user, dst_int, n, s);
+    return 1;
+}
+int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s) {
+    if (n <= 0) return 0;
+    rows_k(K, false, perm, src_int, dst_user, n, s);
+    return 1;
+}
+int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s) {
+    if (nnz <= 0) return 0;
+    k_gather_vals<<<nblk(nnz, kBlock), kBlock, 0, s>>>(i2u, src, dst, nnz);
+    return 1;
+}
+int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
+                 double* M_int, cudaStream_t s) {
+    k_cotan_assemble<<<nblk(L0.n, kBlock), kBlock, 0, s>>>(L0.rp.p, L0.col.p, opp, Vint, mass_coeff, lap_coeff,
+                                                            L0.val.p, M_int, L0.n);
+    return 1;
+}
+int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s) {
+    if (n <= 0) return 0;
+    switch (K) {
+        case 1: k_apply_mass<1><<<nblk(n, kBlock), kBlock, 0, s>>>(M_user, X, B, n); break;
+        case 2: k_apply_mass<2><<<nblk(n, kBlock), kBlock, 0, s>>>(M_user, X, B, n); break;
+        case 3: k_apply_mass<3><<<nblk(n, kBlock), kBlock, 0, s>>>(M_user, X, B, n); break;
+        default: k_apply_mass<4><<<nblk(n, kBlock), kBlock, 0, s>>>(M_user, X, B, n); break;
+    }
+    return 1;
+}
+int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s) {
+    k_scatter_vec<<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src_int, dst_user, n);
+    return 1;
+}
+int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s) {
+    const int nc = coarse.n;
+    k_galerkin<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
+        nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p, coarse.cidx.p, coarse.cw.p,
+        fine.rp.p, fine.col.p, fine.val.p, fine.pc.p, fine.pw.p, fine.n);
+    return 1;
+}
+int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s) {
+    const size_t total = (size_t)npad * npad;
+    k_densify_zero<<<nblk((int64_t)std::min<size_t>(total, 1u << 20), kBlock), kBlock, 0, s>>>(D, total);
+    k_densify<<<nblk(npad, kBlock), kBlock, 0, s>>>(LH.rp.p, LH.col.p, LH.val.p, LH.n, npad, D);
+    return 2;
+}
+int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s) {
+    const int nb = npad / 32;
+    int launches = 0;
+    for (int kb = 0; kb < nb; ++kb) {
+        k_chol_diag<<<1, 1024, 0, s>>>(D, npad, kb, err);
+        ++launches;
+        const int m = nb - kb - 1;
+        if (m > 0) {
+            k_chol_trsm<<<nblk(32 * m, kTrsmThreads), kTrsmThreads, 0, s>>>(D, npad, kb);
+            k_chol_update<<<m * (m + 1) / 2, 256, 0, s>>>(D, npad, kb);
+            launches += 2;
+        }
+    }
+    k_chol_diaginv<<<nb, 32, 0, s>>>(D, npad, Linv);
+    return launches + 1;
+}
+int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s) {
+    const size_t smem = sizeof(double) * ((size_t)npad * kInvCols + 32 * kInvCols);
+    k_chol_inverse<<<npad / kInvCols, 512, smem, s>>>(D, Linv, npad, Z);
+    return 1;
+}
+
+}  // namespace mg

@@ -1,0 +1,682 @@
+// libmg V-cycle kernels for sm_100a (Alg. 2).  fp64, HBM-bound
+// (SpMV-class intensity ~0.17 flop/B): no tensor cores.
+//
+//   K4 multicolour Gauss-Seidel colour pass      (App. A, reading A2)
+//   K5 residual r = b - A x' and restriction P^T r (Alg. 2)
+//   K6 prolongation + correction x <- x' + P c     (Alg. 2, reading A1)
+//   K7b coarsest solve x = A_H^{-1} b              (Alg. 2, reading A12)
+//   K3 residual norm rho = ||b - A x|| / ||b||     (reading A3)
+//
+// Every kernel here is launched with programmatic dependent launch inside the
+// captured V-cycle graph: a prologue loads what no earlier kernel of the
+// solve writes (matrix structure/values, P, children lists), then
+// griddepcontrol.wait, then the dependent part (x, b, r).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "mg_common.cuh"
+#include "mg_internal.h"
+
+namespace mg {
+namespace {
+
+// ---------------------------------------------------------------------------
+// Tile-staged CSR rows (levels with short rows): a CTA owns kTile consecutive
+// rows; row pointers and the tile's contiguous run of (col, val) are staged
+// into shared memory with coalesced streaming loads in the PDL prologue; each
+// thread then processes one row, issuing its x gathers in independent batches.
+constexpr int kTile = 256;
+
+__device__ __forceinline__ int tile_stage(const int* __restrict__ rp, const int* __restrict__ col,
+                                          const double* __restrict__ val, int row0, int nrow, int* rps, int* cs,
+                                          double* vs, uint64_t pol) {
+    const int t = threadIdx.x;
+    if (t < nrow) rps[t] = rp[row0 + t];
+    if (t == 0) rps[nrow] = rp[row0 + nrow];
+    __syncthreads();
+    const int e0 = rps[0];
+    const int cnt = rps[nrow] - e0;
+    const int* cg = col + e0;
+    const double* vg = val + e0;
+    int q = t;
+    for (; q + 3 * kTile < cnt; q += 4 * kTile) {
+        const int c0 = ld_stream(cg + q, pol), c1 = ld_stream(cg + q + kTile, pol),
+                  c2 = ld_stream(cg + q + 2 * kTile, pol), c3 = ld_stream(cg + q + 3 * kTile, pol);
+        const double v0 = ld_stream(vg + q, pol), v1 = ld_stream(vg + q + kTile, pol),
+                     v2 = ld_stream(vg + q + 2 * kTile, pol), v3 = ld_stream(vg + q + 3 * kTile, pol);
+        cs[q] = c0;
+        cs[q + kTile] = c1;
+        cs[q + 2 * kTile] = c2;
+        cs[q + 3 * kTile] = c3;
+        vs[q] = v0;
+        vs[q + kTile] = v1;
+        vs[q + 2 * kTile] = v2;
+        vs[q + 3 * kTile] = v3;
+    }
+    for (; q < cnt; q += kTile) {
+        cs[q] = ld_stream(cg + q, pol);
+        vs[q] = ld_stream(vg + q, pol);
+    }
+    __syncthreads();
+    return e0;
+}
+
+// s[c] = sum_{j != row} a_rj x_jc and d = a_rr from the staged tile.
+template <int K, int UNR>
+__device__ __forceinline__ void tile_row(const int* cs, const double* vs, int qb, int qe, int row,
+                                         const double* __restrict__ x, double (&s)[K], double& d) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = 0.0;
+    d = 0.0;
+    for (int q = qb; q < qe; q += UNR) {
+        int j[UNR];
+        double a[UNR];
+        double xv[UNR][K];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const bool ok = q + u < qe;
+            j[u] = ok ? cs[q + u] : row;
+            a[u] = ok ? vs[q + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int c = 0; c < K; ++c) xv[u][c] = x[(size_t)j[u] * K + c];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (j[u] == row) {
+                d += a[u];
+            } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) s[c] = fma(a[u], xv[u][c], s[c]);
+            }
+        }
+    }
+}
+
+template <int K>
+struct Unroll {
+    static constexpr int value = K == 1 ? 8 : 4;
+};
+
+// MODE 0: GS colour pass  x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii  on rows [r0, r1)
+// MODE 1: residual        r_i = b_i - sum_j a_ij x_j                   on rows [r0, r1)
+template <int K, int MODE>
+__global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp, const int* __restrict__ col,
+                                                      const double* __restrict__ val, const double* __restrict__ b,
+                                                      double* __restrict__ x, double* __restrict__ r, int r0, int r1,
+                                                      int cap) {
+    extern __shared__ double smem_d[];
+    __shared__ int rps[kTile + 1];
+    double* vs = smem_d;
+    int* cs = reinterpret_cast<int*>(smem_d + cap);
+    pdl_launch_dependents();
+    const uint64_t pol = evict_first_policy();
+    const int row0 = r0 + blockIdx.x * kTile;
+    const int nrow = min(kTile, r1 - row0);
+    const int e0 = tile_stage(rp, col, val, row0, nrow, rps, cs, vs, pol);
+    pdl_wait();
+    const int t = threadIdx.x;
+    if (t >= nrow) return;
+    const int row = row0 + t;
+    double s[K], d;
+    tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
+    if (MODE == 0) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / d;
+    } else {
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+            r[(size_t)row * K + c] = b[(size_t)row * K + c] - fma(d, x[(size_t)row * K + c], s[c]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
+// prefetches up to two (col, val) of its row in the PDL prologue.
+template <int K, int LPR, int MODE>
+__global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
+                                                      const double* __restrict__ val, const double* __restrict__ b,
+                                                      double* __restrict__ x, double* __restrict__ r, int r0, int r1) {
+    const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
+    const int lane = threadIdx.x & (LPR - 1);
+    const int row = r0 + g;
+    pdl_launch_dependents();
+    const bool active = row < r1;
+    const uint64_t pol = evict_first_policy();
+    int e0 = 0, e1 = 0, j0 = -1, j1 = -1;
+    double a0 = 0.0, a1 = 0.0;
+    if (active) {
+        e0 = rp[row];
+        e1 = rp[row + 1];
+        if (e0 + lane < e1) {
+            j0 = ld_stream(col + e0 + lane, pol);
+            a0 = ld_stream(val + e0 + lane, pol);
+        }
+        if (e0 + lane + LPR < e1) {
+            j1 = ld_stream(col + e0 + lane + LPR, pol);
+            a1 = ld_stream(val + e0 + lane + LPR, pol);
+        }
+    }
+    pdl_wait();
+    if (!active) return;   // whole groups leave together
+    const unsigned mask = group_mask(LPR);
+    double s[K], x0[K], x1[K];
+    double d = 0.0;
+    const int jj0 = j0 >= 0 ? j0 : row, jj1 = j1 >= 0 ? j1 : row;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        x0[c] = x[(size_t)jj0 * K + c];
+        x1[c] = x[(size_t)jj1 * K + c];
+        s[c] = 0.0;
+    }
+    if (j0 >= 0) {
+        if (j0 == row && MODE == 0) d += a0;
+        else
+#pragma unroll
+            for (int c = 0; c < K; ++c) s[c] = fma(a0, x0[c], s[c]);
+    }
+    if (j1 >= 0) {
+        if (j1 == row && MODE == 0) d += a1;
+        else
+#pragma unroll
+            for (int c = 0; c < K; ++c) s[c] = fma(a1, x1[c], s[c]);
+    }
+    for (int e = e0 + lane + 2 * LPR; e < e1; e += LPR) {
+        const int j = ld_stream(col + e, pol);
+        const double a = ld_stream(val + e, pol);
+        if (j == row && MODE == 0) d += a;
+        else
+#pragma unroll
+            for (int c = 0; c < K; ++c) s[c] = fma(a, x[(size_t)j * K + c], s[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
+    if (MODE == 0) d = group_sum<LPR>(d, mask);
+    if (lane == 0) {
+        if (MODE == 0) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / d;
+        } else {
+#pragma unroll
+            for (int c = 0; c < K; ++c) r[(size_t)row * K + c] = b[(size_t)row * K + c] - s[c];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5b: r_c = P^T r gathered through the children lists of the coarse
+// vertices (transpose of P): deterministic, no atomics.  G lanes per coarse
+// row; children indices and weights prefetched before the wait.  Zeroes the
+// coarse iterate (the recursive V-cycle starts from 0).
+constexpr int kRestrictG = 16;
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cptr, const int* __restrict__ cidx,
+                                                     const double* __restrict__ cw, const double* __restrict__ r,
+                                                     double* __restrict__ bc, double* __restrict__ xc, int nc) {
+    constexpr int G = kRestrictG;
+    const int I = (blockIdx.x * kBlock + threadIdx.x) / G;
+    const int lane = threadIdx.x & (G - 1);
+    pdl_launch_dependents();
+    const bool active = I < nc;
+    int t0 = 0, t1 = 0, i0 = -1, i1 = -1;
+    double w0 = 0.0, w1 = 0.0;
+    if (active) {
+        t0 = cptr[I];
+        t1 = cptr[I + 1];
+        if (t0 + lane < t1) {
+            i0 = cidx[t0 + lane];
+            w0 = cw[t0 + lane];
+        }
+        if (t0 + lane + G < t1) {
+            i1 = cidx[t0 + lane + G];
+            w1 = cw[t0 + lane + G];
+        }
+    }
+    pdl_wait();
+    if (!active) return;
+    const unsigned mask = group_mask(G);
+    double s[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = 0.0;
+    if (i0 >= 0)
+#pragma unroll
+        for (int c = 0; c < K; ++c) s[c] = fma(w0, r[(size_t)i0 * K + c], s[c]);
+    if (i1 >= 0)
+#pragma unroll
+        for (int c = 0; c < K; ++c) s[c] = fma(w1, r[(size_t)i1 * K + c], s[c]);
+    for (int t = t0 + lane + 2 * G; t < t1; t += G) {
+        const int i = cidx[t];
+        const double w = cw[t];
+#pragma unroll
+        for (int c = 0; c < K; ++c) s[c] = fma(w, r[(size_t)i * K + c], s[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = group_sum<G>(s[c], mask);
+    if (lane < K) {
+        double v = s[0];
+#pragma unroll
+        for (int c = 1; c < K; ++c)
+            if (lane == c) v = s[c];
+        bc[(size_t)I * K + lane] = v;
+        xc[(size_t)I * K + lane] = 0.0;
+    }
+}
+
+// K6: x <- x + P c (ELL-3, SoA [3][n]).
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_prolong(const int* __restrict__ pc, const double* __restrict__ pw,
+                                                    const double* __restrict__ xc, double* __restrict__ x, int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    pdl_launch_dependents();
+    int c0 = 0, c1 = 0, c2 = 0;
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    if (i < n) {
+        c0 = pc[i];
+        c1 = pc[n + i];
+        c2 = pc[2 * n + i];
+        w0 = pw[i];
+        w1 = pw[n + i];
+        w2 = pw[2 * n + i];
+    }
+    pdl_wait();
+    if (i >= n) return;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        double v = w0 * xc[(size_t)c0 * K + c];
+        v = fma(w1, xc[(size_t)c1 * K + c], v);
+        v = fma(w2, xc[(size_t)c2 * K + c], v);
+        x[(size_t)i * K + c] += v;
+    }
+}
+
+// K7b: coarsest solve x = A_H^{-1} b, one warp per row of the explicit
+// inverse (prefetched into registers before the wait).
+template <int K>
+__global__ void __launch_bounds__(256) k_coarse_gemv(const double* __restrict__ Z, int npad, int n,
+                                                     const double* __restrict__ b, double* __restrict__ x) {
+    constexpr int U = 32;   // covers n <= 1024 from registers
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    pdl_launch_dependents();
+    double z[U];
+    const double* Zr = Z + (size_t)min(row, n - 1) * npad;
+#pragma unroll
+    for (int u = 0; u < U; ++u) z[u] = (lane + 32 * u < n) ? Zr[lane + 32 * u] : 0.0;
+    pdl_wait();
+    if (row >= n) return;
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = lane + 32 * u;
+        if (j < n)
+#pragma unroll
+            for (int c = 0; c < K; ++c) acc[c] = fma(z[u], b[(size_t)j * K + c], acc[c]);
+    }
+    for (int j = lane + 32 * U; j < n; j += 32)
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = fma(Zr[j], b[(size_t)j * K + c], acc[c]);
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = acc[c];
+}
+
+// Coarsest solve L L^T x = b in ONE CTA (1024 threads): blocked forward and
+// backward substitution; the off-diagonal blocks are streamed from L2 with
+// coalesced row loads, the diagonal blocks applied through their inverses
+// with warp-shuffle reductions; the iterate is staged in shared memory.
+template <int K>
+__global__ void __launch_bounds__(1024) k_chol_solve(const double* __restrict__ L, const double* __restrict__ Linv,
+                                                     int npad, int n, const double* __restrict__ b,
+                                                     double* __restrict__ x) {
+    extern __shared__ double sm[];
+    pdl_launch_dependents();
+    pdl_wait();
+    double* y = sm;                       // [npad][K]
+    double* red = sm + (size_t)npad * K;  // [32][32][K]
+    double* t = red + 32 * 32 * K;        // [32][K]
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < npad * K; i += 1024) y[i] = (i < n * K) ? b[i] : 0.0;
+    __syncthreads();
+    const int nb = npad / 32;
+    for (int I = 0; I < nb; ++I) {
+        // t_r = y_{32I+r} - sum_{j < 32I} L[32I+r][j] y_j      (warp w = row r)
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = 0.0;
+        const double* Lr = L + (size_t)(32 * I + w) * npad;
+        for (int j = lane; j < 32 * I; j += 32) {
+            const double l = Lr[j];
+#pragma unroll
+            for (int c = 0; c < K; ++c) acc[c] = fma(l, y[j * K + c], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < K; ++c) t[w * K + c] = y[(32 * I + w) * K + c] - acc[c];
+        __syncthreads();
+        // y_I = inv(L_II) t      (warp w = row r, lane = column q)
+        const double li = Linv[(size_t)I * 1024 + w * 32 + lane];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            double v = li * t[lane * K + c];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            acc[c] = v;
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < K; ++c) y[(32 * I + w) * K + c] = acc[c];
+        __syncthreads();
+    }
+    for (int I = nb - 1; I >= 0; --I) {
+        // t_r = y_{32I+r} - sum_{j >= 32(I+1)} L[j][32I+r] x_j   (lane = r, warps stride j)
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = 0.0;
+        for (int j = 32 * (I + 1) + w; j < npad; j += 32) {
+            const double l = L[(size_t)j * npad + 32 * I + lane];
+#pragma unroll
+            for (int c = 0; c < K; ++c) acc[c] = fma(l, y[j * K + c], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < K; ++c) red[(w * 32 + lane) * K + c] = acc[c];
+        __syncthreads();
+        if (w == 0) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                double s = 0.0;
+                for (int v = 0; v < 32; ++v) s += red[(v * 32 + lane) * K + c];
+                t[lane * K + c] = y[(32 * I + lane) * K + c] - s;
+            }
+        }
+        __syncthreads();
+        // x_I = inv(L_II)^T t : x_r = sum_q inv[q][r] t_q   (warp w = r, lane = q)
+        const double li = Linv[(size_t)I * 1024 + lane * 32 + w];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            double v = li * t[lane * K + c];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            acc[c] = v;
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int c = 0; c < K; ++c) y[(32 * I + w) * K + c] = acc[c];
+        __syncthreads();
+    }
+    for (int i = tid; i < n * K; i += 1024) x[i] = y[i];
+}
+
+// ---------------------------------------------------------------------------
+// K3: residual norms: block partial sums of (b - A x)^2 per column (tiled or
+// LPR rows), then one deterministic single-block finalisation.
+constexpr int kNormBlocks = 1184;   // 8 x 148 SMs
+
+template <int K>
+__device__ __forceinline__ void block_partial(double (&acc)[K], double* partial) {
+    __shared__ double red[kBlock / 32][K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        const double v = warp_sum(acc[c]);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double v = 0.0;
+        for (int w = 0; w < kBlock / 32; ++w) v += red[w][threadIdx.x];
+        partial[blockIdx.x * K + threadIdx.x] = v;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kTile) k_resnorm_tiled(const int* __restrict__ rp, const int* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ b, const double* __restrict__ x,
+                                                         double* __restrict__ partial, int n, int cap) {
+    extern __shared__ double smem_d[];
+    __shared__ int rps[kTile + 1];
+    double* vs = smem_d;
+    int* cs = reinterpret_cast<int*>(smem_d + cap);
+    pdl_launch_dependents();
+    const uint64_t pol = evict_first_policy();
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    const int ntiles = (n + kTile - 1) / kTile;
+    bool waited = false;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int row0 = tile * kTile;
+        const int nrow = min(kTile, n - row0);
+        const int e0 = tile_stage(rp, col, val, row0, nrow, rps, cs, vs, pol);
+        if (!waited) {
+            pdl_wait();
+            waited = true;
+        }
+        const int t = threadIdx.x;
+        if (t < nrow) {
+            const int row = row0 + t;
+            double s[K], d;
+            tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const double rr = b[(size_t)row * K + c] - fma(d, x[(size_t)row * K + c], s[c]);
+                acc[c] = fma(rr, rr, acc[c]);
+            }
+        }
+        __syncthreads();
+    }
+    if (!waited) pdl_wait();
+    block_partial<K>(acc, partial);
+}
+
+template <int K, int LPR>
+__global__ void __launch_bounds__(kBlock) k_resnorm_lpr(const int* __restrict__ rp, const int* __restrict__ col,
+                                                        const double* __restrict__ val, const double* __restrict__ b,
+                                                        const double* __restrict__ x, double* __restrict__ partial,
+                                                        int n) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int lane = threadIdx.x & (LPR - 1);
+    const uint64_t pol = evict_first_policy();
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    const int groups = gridDim.x * (kBlock / LPR);
+    const int g0 = (blockIdx.x * kBlock + threadIdx.x) / LPR;
+    // iterate whole groups together: every group runs the same trip count
+    for (int base = 0; base < n; base += groups) {
+        const int row = base + g0;
+        const bool active = row < n;
+        const unsigned mask = group_mask(LPR);
+        double s[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) s[c] = 0.0;
+        if (active) {
+            for (int e = rp[row] + lane; e < rp[row + 1]; e += LPR) {
+                const int j = ld_stream(col + e, pol);
+                const double a = ld_stream(val + e, pol);
+#pragma unroll
+                for (int c = 0; c < K; ++c) s[c] = fma(a, x[(size_t)j * K + c], s[c]);
+            }
+        }
+        if (active) {
+#pragma unroll
+            for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
+            if (lane == 0)
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
+                    const double rr = b[(size_t)row * K + c] - s[c];
+                    acc[c] = fma(rr, rr, acc[c]);
+                }
+        }
+    }
+    block_partial<K>(acc, partial);
+}
+
+// out[c] = sqrt(sum_b partial[b][c]) / (denom[c] > 0 ? denom[c] : 1)   (denom may be null)
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_norm_finalize(const double* __restrict__ partial, int nblk_,
+                                                          const double* __restrict__ denom,
+                                                          double* __restrict__ out) {
+    pdl_launch_dependents();
+    pdl_wait();
+    __shared__ double red[kBlock / 32][K];
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    for (int t = threadIdx.x; t < nblk_; t += kBlock)
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] += partial[t * K + c];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        const double v = warp_sum(acc[c]);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double v = 0.0;
+        for (int w = 0; w < kBlock / 32; ++w) v += red[w][threadIdx.x];
+        v = sqrt(v);
+        if (denom) {
+            const double d = denom[threadIdx.x];
+            v = v / (d > 0.0 ? d : 1.0);
+        }
+        out[threadIdx.x] = v;
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_sumsq_partial(const double* __restrict__ v, int n,
+                                                          double* __restrict__ partial) {
+    pdl_launch_dependents();
+    pdl_wait();
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const double t = v[(size_t)i * K + c];
+            acc[c] = fma(t, t, acc[c]);
+        }
+    block_partial<K>(acc, partial);
+}
+
+// ---------------------------------------------------------------------------
+inline size_t tile_smem(int cap) { return (size_t)cap * (sizeof(double) + sizeof(int)); }
+
+template <int K, int MODE>
+int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s) {
+    const int rows = r1 - r0;
+    if (rows <= 0) return 0;
+    if (L.tiled) {
+        const int cap = MODE == 0 ? L.cap_gs : L.cap_all;
+        launch_k(pdl, k_tile_sweep<K, MODE>, nblk(rows, kTile), kTile, tile_smem(cap), s, L.rp.p, L.col.p, L.val.p,
+                 L.b.p, L.x.p, r, r0, r1, cap);
+        return 1;
+    }
+    const int grid = nblk((int64_t)rows * L.lpr, kBlock);
+    switch (L.lpr) {
+        case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
+        case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
+        case 16: launch_k(pdl, k_lpr_sweep<K, 16, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
+        default: launch_k(pdl, k_lpr_sweep<K, 32, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
+    }
+    return 1;
+}
+
+template <int K>
+int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl, cudaStream_t s) {
+    int grid;
+    if (L.tiled) {
+        grid = std::min(nb, nblk(L.n, kTile));
+        launch_k(pdl, k_resnorm_tiled<K>, grid, kTile, tile_smem(L.cap_all), s, L.rp.p, L.col.p, L.val.p, L.b.p,
+                 L.x.p, partial, L.n, L.cap_all);
+    } else {
+        grid = std::min(nb, nblk((int64_t)L.n * L.lpr, kBlock));
+        switch (L.lpr) {
+            case 4: launch_k(pdl, k_resnorm_lpr<K, 4>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
+            case 8: launch_k(pdl, k_resnorm_lpr<K, 8>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
+            case 16: launch_k(pdl, k_resnorm_lpr<K, 16>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
+            default: launch_k(pdl, k_resnorm_lpr<K, 32>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
+        }
+    }
+    launch_k(pdl, k_norm_finalize<K>, 1, kBlock, 0, s, (const double*)partial, grid, bnorm, rho);
+    return 2;
+}
+
+template <int K>
+void set_attrs_k() {
+    const int big = 200 * 1024;
+    cudaFuncSetAttribute(k_tile_sweep<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_sweep<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_resnorm_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_chol_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+}
+
+#define MG_K_SWITCH(K, EXPR_T)                  \
+    switch (K) {                                \
+        case 1: { constexpr int KK = 1; return EXPR_T; } \
+        case 2: { constexpr int KK = 2; return EXPR_T; } \
+        case 3: { constexpr int KK = 3; return EXPR_T; } \
+        default: { constexpr int KK = 4; return EXPR_T; } \
+    }
+
+}  // namespace
+
+int resnorm_blocks(int) { return kNormBlocks; }
+int tile_rows() { return kTile; }
+size_t tile_smem_limit() { return 160 * 1024; }
+
+void init_vcycle_attributes() {
+    set_attrs_k<1>();
+    set_attrs_k<2>();
+    set_attrs_k<3>();
+    set_attrs_k<4>();
+}
+
+int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
+}
+int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (sweep_k<KK, 1>(L, 0, L.n, L.r.p, pdl, s)))
+}
+int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK>, nblk((int64_t)C.n * kRestrictG, kBlock), kBlock, 0, s, C.cptr.p,
+                             C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n), 1))
+}
+int vc_prolong(int K, const Level& F, const Level& C, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_k(pdl, k_prolong<KK>, nblk(F.n, kBlock), kBlock, 0, s, F.pc.p, F.pw.p, C.x.p, F.x.p, F.n), 1))
+}
+int vc_coarse_gemv(int K, const double* Z, int npad, int n, const double* b, double* x, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_k(pdl, k_coarse_gemv<KK>, nblk(n, 8), 256, 0, s, Z, npad, n, b, x), 1))
+}
+int vc_coarse_trsv(int K, const double* L, const double* Linv, int npad, int n, const double* b, double* x, bool pdl,
+                   cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_k(pdl, k_chol_solve<KK>, 1, 1024, sizeof(double) * ((size_t)npad * KK + 32 * 32 * KK + 32 * KK),
+                             s, L, Linv, npad, n, b, x), 1))
+}
+int vc_resnorm(int K, const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl,
+               cudaStream_t s) {
+    MG_K_SWITCH(K, (resnorm_k<KK>(L, partial, nb, bnorm, rho, pdl, s)))
+}
+int vc_sumsq(int K, const double* v, int n, double* partial, int nb, double* out, cudaStream_t s) {
+    const int grid = std::min(nb, std::max(1, nblk(n, kBlock)));
+    MG_K_SWITCH(K, (launch_k(false, k_sumsq_partial<KK>, grid, kBlock, 0, s, v, n, partial),
+                    launch_k(false, k_norm_finalize<KK>, 1, kBlock, 0, s, (const double*)partial, grid,
+                             (const double*)nullptr, out),
+                    2))
+}
+
+}  // namespace mg

@@ -242,3 +242,25 @@ def test_full_size_parity(ora, cid):
     rc, cyc, hg = S.solve(_gpu_rhs(S, p, p.n), Xg, rel_tol=0.0, max_cycles=ho.shape[0] - 1)
     check_x(Xg, Xo)
     check_history(hg, ho, tau_floor(A.to_scipy(), Xo, Bo))
+
+
+def test_launch_modes_agree(ora, monkeypatch):
+    """PDL on/off must give bitwise-identical iterates (scheduling only); the
+    one-CTA triangular coarsest solve and the explicit-inverse GEMV agree to
+    the X tolerance (both are Alg. 2's direct solve, reading A12)."""
+    p = meshgen.make_config(4, subdiv=5)
+    A, M, mgo = oracle_problem(ora, p)
+    Bo = oracle_rhs(ora, p, M)
+    Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=5)
+    out = {}
+    for pdl, mode in (("1", "inv"), ("0", "inv"), ("1", "trsv")):
+        monkeypatch.setenv("MG_PDL", pdl)
+        monkeypatch.setenv("MG_COARSE_SOLVE", mode)
+        S = gpu_solver(p)
+        S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+        X = np.zeros_like(Bo)
+        S.solve(Bo, X, rel_tol=0.0, max_cycles=5)
+        check_x(X, Xo)
+        out[(pdl, mode)] = X
+        S.close()
+    assert np.array_equal(out[("1", "inv")], out[("0", "inv")])
