@@ -167,7 +167,8 @@ int mg_util_galerkin_pattern(int32_t n_fine, const int32_t* row_ptr, const int32
 int mg_set_profiling(mg_ctx* ctx, int class_mask);
 /* Accumulated device milliseconds and kernel launches per (kernel class, level):
  * classes 0 gs_sweep, 1 residual+restrict, 2 prolong, 3 coarse_solve,
- * 4 resnorm, 5 galerkin, 6 assembly, 7 factor, 8 permute.  ms[cls*16 + l],
+ * 4 resnorm, 5 galerkin, 6 assembly, 7 factor, 8 permute, 9 coarse_tail (the
+ * single-launch cluster kernel that runs the V-cycle on the small levels).  ms[cls*16 + l],
  * launches[cls*16 + l] (levels >= 16 fold into 15).  Resets the counters. */
 int mg_get_profile(mg_ctx* ctx, double* ms, int64_t* launches);
 /* Device kernel launches issued by this context since creation. */

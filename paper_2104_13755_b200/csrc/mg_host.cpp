@@ -193,6 +193,9 @@ struct mg_ctx {
     DBuf<double> D, Linv, Ainv;
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
+    int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
+    int64_t tail_nnz = 6000000;      // levels with at most this many stored entries join the tail
+    int tail_cs = 0;                 // cluster size of the tail kernel
     DBuf<int> errflag;
 
     DBuf<double> partial, bnorm, rho;
@@ -435,6 +438,17 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 return c->cuda_fail(e, "pattern upload");
         }
     }
+    // levels run by the cluster tail: the coarsest ones with <= tail_nnz entries
+    c->tail_start = -1;
+    if (c->tail_cs > 0 && c->coarse_mode == 1) {
+        int lt = H;
+        while (lt > 0 && c->lv[lt - 1]->nnz <= c->tail_nnz && H - (lt - 1) < kTailMaxLevels) --lt;
+        if (lt < H) c->tail_start = lt;
+    }
+    for (int l = 0; l <= H; ++l) {
+        cudaError_t e = c->lv[l]->dcoff.upload(c->lv[l]->colour_off, s);
+        if (e) return c->cuda_fail(e, "pattern upload");
+    }
     // coarsest dense factor storage
     const int nH = c->lv[H]->n;
     c->npad = (nH + 31) / 32 * 32;
@@ -478,7 +492,8 @@ int rebuild_hierarchy(mg_ctx* c) {
 void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
     const int H = c->H;
     const bool pdl = c->pdl;
-    for (int l = 0; l < H; ++l) {
+    const int lt = c->tail_start >= 0 ? c->tail_start : H;   // levels >= lt: tail (or coarsest solve)
+    for (int l = 0; l < lt; ++l) {
         Level& L = *c->lv[l];
         c->timed(PC_GS, l, s, [&] {
             int n = 0;
@@ -491,11 +506,39 @@ void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
         });
     }
     Level& LH = *c->lv[H];
-    c->timed(PC_COARSE, H, s, [&] {
-        return c->coarse_mode == 1 ? vc_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s)
-                                   : vc_coarse_trsv(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s);
-    });
-    for (int l = H - 1; l >= 0; --l) {
+    if (lt < H) {
+        TailParams p = {};
+        p.nl = H - lt + 1;
+        p.mu_pre = c->mu_pre;
+        p.mu_post = c->mu_post;
+        p.npad = c->npad;
+        p.Z = c->Ainv.p;
+        for (int i = 0; i < p.nl; ++i) {
+            Level& L = *c->lv[lt + i];
+            TailLevel& t = p.lv[i];
+            t.n = L.n;
+            t.ncol = L.ncolours;
+            t.coff = L.dcoff.p;
+            t.rp = L.rp.p;
+            t.col = L.col.p;
+            t.val = L.val.p;
+            t.x = L.x.p;
+            t.b = L.b.p;
+            t.r = L.r.p;
+            t.pc = L.pc.p;
+            t.pw = L.pw.p;
+            t.cptr = L.cptr.p;
+            t.cidx = L.cidx.p;
+            t.cw = L.cw.p;
+        }
+        c->timed(PC_TAIL, lt, s, [&] { return std::max(0, vc_tail(K, p, c->tail_cs, pdl, s)); });
+    } else {
+        c->timed(PC_COARSE, H, s, [&] {
+            return c->coarse_mode == 1 ? vc_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s)
+                                       : vc_coarse_trsv(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s);
+        });
+    }
+    for (int l = lt - 1; l >= 0; --l) {
         Level& L = *c->lv[l];
         c->timed(PC_PROLONG, l, s, [&] { return vc_prolong(K, L, *c->lv[l + 1], pdl, s); });
         c->timed(PC_GS, l, s, [&] {
@@ -585,6 +628,8 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     init_setup_attributes();
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
+    if (const char* m = getenv("MG_TAIL_NNZ")) c->tail_nnz = atoll(m);
+    c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
         delete c;

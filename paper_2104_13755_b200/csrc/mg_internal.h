@@ -11,12 +11,12 @@
 namespace mg {
 
 constexpr int kMaxK = 4;          // right-hand sides per solve supported by the kernels
-constexpr int kProfClasses = 9;   // see mg.h mg_get_profile
+constexpr int kProfClasses = 10;  // see mg.h mg_get_profile
 constexpr int kProfLevels = 16;
 
 enum ProfClass {
     PC_GS = 0, PC_RESTRICT = 1, PC_PROLONG = 2, PC_COARSE = 3, PC_RESNORM = 4,
-    PC_GALERKIN = 5, PC_ASSEMBLY = 6, PC_FACTOR = 7, PC_PERMUTE = 8
+    PC_GALERKIN = 5, PC_ASSEMBLY = 6, PC_FACTOR = 7, PC_PERMUTE = 8, PC_TAIL = 9
 };
 
 // Device buffer owned by the context.
@@ -78,8 +78,34 @@ struct Level {
     DBuf<double> cw;
     DBuf<int32_t> gal_order;              // rows of this level in locality order (Galerkin)
     DBuf<int32_t> dperm;                  // perm on device
+    DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
     DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
     DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
+};
+
+// Device view of one level for the coarse-tail kernel (mg_tail.cu).
+struct TailLevel {
+    int n, ncol;
+    const int32_t* coff;                          // colour ranges [ncol+1]
+    const int32_t* rp;
+    const int32_t* col;
+    const double* val;
+    double* x;
+    double* b;
+    double* r;
+    const int32_t* pc;                            // P of this level (fine) -> next, SoA [3][n]
+    const double* pw;
+    const int32_t* cptr;                          // children of this level's rows (as coarse)
+    const int32_t* cidx;
+    const double* cw;
+};
+constexpr int kTailMaxLevels = 12;
+struct TailParams {
+    int nl;                                       // levels lt..H; lv[nl-1] is the coarsest
+    int mu_pre, mu_post;
+    int npad;
+    const double* Z;                              // explicit inverse of A_H
+    TailLevel lv[kTailMaxLevels];
 };
 
 // Launch helpers.  All enqueue on `s` and return the number of kernel
@@ -100,6 +126,9 @@ int resnorm_blocks(int n);
 int tile_rows();
 size_t tile_smem_limit();
 void init_vcycle_attributes();
+// mg_tail.cu
+int tail_cluster_size();
+int vc_tail(int K, const TailParams& p, int cs, bool pdl, cudaStream_t s);
 // mg_setup.cu
 void init_setup_attributes();
 int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s);

@@ -247,20 +247,22 @@ def test_full_size_parity(ora, cid):
 def test_launch_modes_agree(ora, monkeypatch):
     """PDL on/off must give bitwise-identical iterates (scheduling only); the
     one-CTA triangular coarsest solve and the explicit-inverse GEMV agree to
-    the X tolerance (both are Alg. 2's direct solve, reading A12)."""
+    the X tolerance (both are Alg. 2's direct solve, reading A12); so do the
+    cluster coarse tail and per-launch kernels on every level."""
     p = meshgen.make_config(4, subdiv=5)
     A, M, mgo = oracle_problem(ora, p)
     Bo = oracle_rhs(ora, p, M)
     Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=5)
     out = {}
-    for pdl, mode in (("1", "inv"), ("0", "inv"), ("1", "trsv")):
+    for pdl, mode, tail in (("1", "inv", "6000000"), ("0", "inv", "6000000"), ("1", "trsv", "0"), ("1", "inv", "0")):
         monkeypatch.setenv("MG_PDL", pdl)
         monkeypatch.setenv("MG_COARSE_SOLVE", mode)
+        monkeypatch.setenv("MG_TAIL_NNZ", tail)
         S = gpu_solver(p)
         S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
         X = np.zeros_like(Bo)
         S.solve(Bo, X, rel_tol=0.0, max_cycles=5)
         check_x(X, Xo)
-        out[(pdl, mode)] = X
+        out[(pdl, mode, tail)] = X
         S.close()
-    assert np.array_equal(out[("1", "inv")], out[("0", "inv")])
+    assert np.array_equal(out[("1", "inv", "6000000")], out[("0", "inv", "6000000")])
