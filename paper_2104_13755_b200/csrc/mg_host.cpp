@@ -194,7 +194,7 @@ struct mg_ctx {
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
-    int64_t tail_nnz = 6000000;      // levels with at most this many stored entries join the tail
+    int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
     int tail_cs = 0;                 // cluster size of the tail kernel
     DBuf<int> errflag;
 
@@ -438,11 +438,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 return c->cuda_fail(e, "pattern upload");
         }
     }
-    // levels run by the cluster tail: the coarsest ones with <= tail_nnz entries
+    // levels run by the cluster tail: the coarsest ones with <= tail_rows rows.
+    // Off by default: measured slower than per-launch PDL kernels.
     c->tail_start = -1;
     if (c->tail_cs > 0 && c->coarse_mode == 1) {
         int lt = H;
-        while (lt > 0 && c->lv[lt - 1]->nnz <= c->tail_nnz && H - (lt - 1) < kTailMaxLevels) --lt;
+        while (lt > 0 && c->lv[lt - 1]->n <= c->tail_rows && H - (lt - 1) < kTailMaxLevels) --lt;
         if (lt < H) c->tail_start = lt;
     }
     for (int l = 0; l <= H; ++l) {
@@ -628,7 +629,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     init_setup_attributes();
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
-    if (const char* m = getenv("MG_TAIL_NNZ")) c->tail_nnz = atoll(m);
+    if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
