@@ -193,6 +193,7 @@ struct mg_ctx {
     DBuf<double> D, Linv, Ainv;
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
+    bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
     int tail_cs = 0;                 // cluster size of the tail kernel
@@ -383,6 +384,24 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         L.cap_all = std::max(L.cap_all, 1);
         // tile-staged kernels for short rows (few gather batches per thread), lanes-per-row otherwise
         L.tiled = avg <= 12.0 && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
+        // persistent pipelined variant: tile descriptors for every colour class, then the whole level
+        L.pipe = L.tiled && c->use_pipe && pipe_smem_bytes(std::max(L.cap_gs, L.cap_all)) <= 200 * 1024;
+        if (L.pipe) {
+            std::vector<int32_t> td;
+            L.tile_off.assign(1, 0);
+            auto add_tiles = [&](int r0, int r1) {
+                for (int a = r0; a < r1; a += T) {
+                    const int nr = std::min(T, r1 - a);
+                    td.insert(td.end(), {a, nr, L.irp[a], L.irp[a + nr]});
+                }
+                L.tile_off.push_back((int32_t)(td.size() / 4));
+            };
+            for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k) add_tiles(L.colour_off[k], L.colour_off[k + 1]);
+            add_tiles(0, L.n);
+            L.pipe_cap = std::max(L.cap_gs, L.cap_all);
+            cudaError_t e = L.tiles.upload(td, c->stream);
+            if (e) return c->cuda_fail(e, "tile upload");
+        }
         if (!L.tiled) {
             const double half = avg / 2.0;
             L.lpr = half <= 4.0 ? 4 : half <= 8.0 ? 8 : half <= 16.0 ? 16 : 32;
@@ -392,7 +411,11 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
     for (int l = 0; l <= H; ++l) {
         Level& L = *c->lv[l];
         cudaError_t e;
-        if ((e = L.rp.upload(L.irp, s)) || (e = L.col.upload(L.icol, s)) || (e = L.val.alloc(std::max<int64_t>(L.nnz, 1))) ||
+        // row pointers / columns / values padded by 16 B: the bulk copies round sizes up
+        std::vector<int32_t> rpad(L.irp), cpad(L.icol);
+        rpad.resize(rpad.size() + 8, L.irp.back());
+        cpad.resize(cpad.size() + 8, 0);
+        if ((e = L.rp.upload(rpad, s)) || (e = L.col.upload(cpad, s)) || (e = L.val.alloc(std::max<int64_t>(L.nnz, 1) + 8)) ||
             (e = L.dperm.upload(L.perm, s)) || (e = L.x.alloc((size_t)L.n * kMaxK)) ||
             (e = L.b.alloc((size_t)L.n * kMaxK)) || (e = L.r.alloc((size_t)L.n * kMaxK)))
             return c->cuda_fail(e, "pattern upload");
@@ -629,6 +652,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     init_setup_attributes();
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
+    if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||

@@ -59,6 +59,10 @@ struct Level {
     bool tiled = false;                   // tile-staged kernels usable (tiles fit in shared memory)
     int cap_gs = 0;                       // max nnz of a kTile-row tile inside one colour range
     int cap_all = 0;                      // max nnz of a kTile-row tile of the whole matrix
+    bool pipe = false;                    // persistent TMA-bulk pipelined tile kernels
+    int pipe_cap = 0;                     // max nnz of any tile (GS or whole-level tiles)
+    std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
+    DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
     std::vector<double> V;                // user-order positions [n][3]
     std::vector<int32_t> colour;          // user order
     std::vector<int32_t> colour_off;      // internal row ranges per colour [ncolours+1]
@@ -125,6 +129,7 @@ int vc_sumsq(int K, const double* v, int n, double* partial, int nb, double* out
 int resnorm_blocks(int n);
 int tile_rows();
 size_t tile_smem_limit();
+size_t pipe_smem_bytes(int cap);
 void init_vcycle_attributes();
 // mg_tail.cu
 int tail_cluster_size();

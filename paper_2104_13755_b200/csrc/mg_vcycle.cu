@@ -134,6 +134,204 @@ __global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp
 }
 
 // ---------------------------------------------------------------------------
+// Persistent, double-buffered variant of the tile kernel (default for levels
+// with short rows).  Each CTA walks the tiles t = t_begin + blockIdx.x +
+// i * gridDim.x; one thread streams tile i+2's row pointers, columns and
+// values into shared memory with 1-D TMA bulk copies (cp.async.bulk, L2
+// evict-first) completing on an mbarrier, while all threads compute tile i.
+// Tile descriptors {row0, nrow, e0, e1} are precomputed per level, so no
+// pointer chase precedes a copy.  Gathers of x skip the diagonal (predicated).
+// MODE 0: GS pass, 1: residual r = b - A x, 2: residual-norm partial sums.
+struct TileDesc {
+    int row0, nrow, e0, e1;
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(pol)
+        : "memory");
+}
+
+// shared-memory layout of one stage: [rps: kTile+8 ints][cs: cap+8 ints][vs: cap+4 doubles]
+__host__ __device__ inline int stage_ints(int cap) { return (kTile + 8) + (cap + 8); }
+__host__ __device__ inline size_t stage_bytes(int cap) {
+    const size_t ints = (size_t)stage_ints(cap);
+    const size_t a = (ints * 4 + 15) / 16 * 16;
+    return a + (size_t)(cap + 4) * 8;
+}
+
+struct StageView {
+    const int* rps;   // rps[t] = row pointer of row0 + t
+    const int* cs;    // cs[q] = col[e0 + q]
+    const double* vs; // vs[q] = val[e0 + q]
+};
+
+__device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* stage, int cap, uint64_t* bar,
+                                           const int* rp, const int* col, const double* val, uint64_t pol) {
+    const int ra = d.row0 & ~3;
+    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
+    const int ca = d.e0 & ~3;
+    const int ccnt = (d.e1 - ca + 3) & ~3;
+    const int va = d.e0 & ~1;
+    const int vcnt = (d.e1 - va + 1) & ~1;
+    int* rps = reinterpret_cast<int*>(stage);
+    int* cs = rps + (kTile + 8);
+    double* vs = reinterpret_cast<double*>(stage + ((size_t)stage_ints(cap) * 4 + 15) / 16 * 16);
+    const unsigned bytes = (unsigned)(rcnt * 4 + ccnt * 4 + vcnt * 8);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(rps, rp + ra, rcnt * 4, bar, pol);
+    if (ccnt > 0) bulk_g2s(cs, col + ca, ccnt * 4, bar, pol);
+    if (vcnt > 0) bulk_g2s(vs, val + va, vcnt * 8, bar, pol);
+}
+
+__device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned char* stage, int cap) {
+    const int* rps = reinterpret_cast<const int*>(stage);
+    const int* cs = rps + (kTile + 8);
+    const double* vs = reinterpret_cast<const double*>(stage + ((size_t)stage_ints(cap) * 4 + 15) / 16 * 16);
+    StageView v;
+    v.rps = rps + (d.row0 - (d.row0 & ~3));
+    v.cs = cs + (d.e0 - (d.e0 & ~3)) - d.e0;   // index with absolute nnz positions
+    v.vs = vs + (d.e0 - (d.e0 & ~1)) - d.e0;
+    return v;
+}
+
+template <int K, int UNR>
+__device__ __forceinline__ void stage_row(const StageView& v, int t, int row, const double* __restrict__ x,
+                                          double (&s)[K], double& d) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = 0.0;
+    d = 0.0;
+    const int qb = v.rps[t], qe = v.rps[t + 1];
+    for (int q = qb; q < qe; q += UNR) {
+        int j[UNR];
+        double a[UNR];
+        double xv[UNR][K];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const bool ok = q + u < qe;
+            j[u] = ok ? v.cs[q + u] : row;
+            a[u] = ok ? v.vs[q + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (j[u] != row) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) xv[u][c] = x[(size_t)j[u] * K + c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) xv[u][c] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            if (j[u] == row) {
+                d += a[u];
+            } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) s[c] = fma(a[u], xv[u][c], s[c]);
+            }
+        }
+    }
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
+                                                     const int* __restrict__ rp, const int* __restrict__ col,
+                                                     const double* __restrict__ val, const double* __restrict__ b,
+                                                     double* __restrict__ x, double* __restrict__ r,
+                                                     double* __restrict__ partial, int cap) {
+    extern __shared__ __align__(128) unsigned char smem_pipe[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int tid = threadIdx.x;
+    const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
+    unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
+    pdl_launch_dependents();
+    const int nt = t_end - t_begin;
+    const int mine = nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    uint64_t pol = 0;
+    if (tid == 0) {
+        pol = evict_first_policy();
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 0; i < 2 && i < mine; ++i) {
+            const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+            issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
+        }
+    }
+    pdl_wait();
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    for (int i = 0; i < mine; ++i) {
+        const int sidx = i & 1;
+        const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+        mbar_wait(&bar[sidx], (unsigned)((i >> 1) & 1));
+        const StageView v = view_tile(d, stage[sidx], cap);
+        if (tid < d.nrow) {
+            const int row = d.row0 + tid;
+            double s[K], dg;
+            stage_row<K, Unroll<K>::value>(v, tid, row, x, s, dg);
+            if (MODE == 0) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / dg;
+            } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
+                    const double rr = b[(size_t)row * K + c] - fma(dg, x[(size_t)row * K + c], s[c]);
+                    if (MODE == 1) r[(size_t)row * K + c] = rr;
+                    else acc[c] = fma(rr, rr, acc[c]);
+                }
+            }
+        }
+        __syncthreads();   // stage sidx fully consumed
+        if (tid == 0 && i + 2 < mine) {
+            const TileDesc dn = tiles[t_begin + blockIdx.x + (i + 2) * gridDim.x];
+            issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
+        }
+    }
+    if (MODE == 2) {
+        __shared__ double red[kTile / 32][K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const double vsum = warp_sum(acc[c]);
+            if ((tid & 31) == 0) red[tid >> 5][c] = vsum;
+        }
+        __syncthreads();
+        if (tid < K) {
+            double vsum = 0.0;
+            for (int w = 0; w < kTile / 32; ++w) vsum += red[w][tid];
+            partial[blockIdx.x * K + tid] = vsum;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
 // prefetches up to two (col, val) of its row in the PDL prologue.
 template <int K, int LPR, int MODE>
@@ -576,10 +774,46 @@ __global__ void __launch_bounds__(kBlock) k_sumsq_partial(const double* __restri
 // ---------------------------------------------------------------------------
 inline size_t tile_smem(int cap) { return (size_t)cap * (sizeof(double) + sizeof(int)); }
 
+inline int pipe_grid(int ntiles, int cap) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = 2 * ((stage_bytes(cap) + 127) / 128 * 128) + 2048;
+    const int per_sm = std::max(1, std::min<int>(8, (int)((227 * 1024) / smem)));
+    return std::max(1, std::min(ntiles, nsm * per_sm));
+}
+inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
+
+// MODE 0/1 over tiles [t0, t1) of level L
+template <int K, int MODE>
+void pipe_launch(const Level& L, int t0, int t1, double* r, double* partial, int grid, bool pdl, cudaStream_t s) {
+    launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, pipe_smem(L.pipe_cap), s,
+             reinterpret_cast<const TileDesc*>(L.tiles.p), t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, partial,
+             L.pipe_cap);
+}
+
 template <int K, int MODE>
 int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s) {
     const int rows = r1 - r0;
     if (rows <= 0) return 0;
+    if (L.pipe) {
+        // tile range of this colour class (GS) or of the whole level (residual)
+        int t0, t1;
+        if (MODE == 0) {
+            int c = 0;
+            while (L.colour_off[c] != r0) ++c;
+            t0 = L.tile_off[c];
+            t1 = L.tile_off[c + 1];
+        } else {
+            t0 = L.tile_off[L.ncolours];
+            t1 = L.tile_off[L.ncolours + 1];
+        }
+        pipe_launch<K, MODE>(L, t0, t1, r, nullptr, pipe_grid(t1 - t0, L.pipe_cap), pdl, s);
+        return 1;
+    }
     if (L.tiled) {
         const int cap = MODE == 0 ? L.cap_gs : L.cap_all;
         launch_k(pdl, k_tile_sweep<K, MODE>, nblk(rows, kTile), kTile, tile_smem(cap), s, L.rp.p, L.col.p, L.val.p,
@@ -599,7 +833,11 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s)
 template <int K>
 int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl, cudaStream_t s) {
     int grid;
-    if (L.tiled) {
+    if (L.pipe) {
+        const int t0 = L.tile_off[L.ncolours], t1 = L.tile_off[L.ncolours + 1];
+        grid = std::min(nb, pipe_grid(t1 - t0, L.pipe_cap));
+        pipe_launch<K, 2>(L, t0, t1, nullptr, partial, grid, pdl, s);
+    } else if (L.tiled) {
         grid = std::min(nb, nblk(L.n, kTile));
         launch_k(pdl, k_resnorm_tiled<K>, grid, kTile, tile_smem(L.cap_all), s, L.rp.p, L.col.p, L.val.p, L.b.p,
                  L.x.p, partial, L.n, L.cap_all);
@@ -623,6 +861,9 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_sweep<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_resnorm_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_chol_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 }
 
 #define MG_K_SWITCH(K, EXPR_T)                  \
@@ -637,6 +878,7 @@ void set_attrs_k() {
 
 int resnorm_blocks(int) { return kNormBlocks; }
 int tile_rows() { return kTile; }
+size_t pipe_smem_bytes(int cap) { return pipe_smem(cap); }
 size_t tile_smem_limit() { return 160 * 1024; }
 
 void init_vcycle_attributes() {

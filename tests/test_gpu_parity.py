@@ -245,24 +245,34 @@ def test_full_size_parity(ora, cid):
 
 
 def test_launch_modes_agree(ora, monkeypatch):
-    """PDL on/off must give bitwise-identical iterates (scheduling only); the
-    one-CTA triangular coarsest solve and the explicit-inverse GEMV agree to
-    the X tolerance (both are Alg. 2's direct solve, reading A12); so do the
-    cluster coarse tail and per-launch kernels on every level."""
+    """Scheduling variants must not change the arithmetic: PDL on/off and the
+    pipelined (TMA bulk) vs plain tile kernels give bitwise-identical
+    iterates.  The one-CTA triangular coarsest solve vs the explicit-inverse
+    GEMV (both Alg. 2's direct solve, reading A12) and the cluster coarse tail
+    vs per-launch kernels agree with the oracle to the X tolerance."""
     p = meshgen.make_config(4, subdiv=5)
     A, M, mgo = oracle_problem(ora, p)
     Bo = oracle_rhs(ora, p, M)
     Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=5)
+    variants = {
+        "default": {},
+        "nopdl": {"MG_PDL": "0"},
+        "nopipe": {"MG_PIPE": "0"},
+        "trsv": {"MG_COARSE_SOLVE": "trsv"},
+        "tail": {"MG_TAIL_ROWS": "20000"},
+    }
     out = {}
-    for pdl, mode, tail in (("1", "inv", "20000"), ("0", "inv", "20000"), ("1", "trsv", "0"), ("1", "inv", "0")):
-        monkeypatch.setenv("MG_PDL", pdl)
-        monkeypatch.setenv("MG_COARSE_SOLVE", mode)
-        monkeypatch.setenv("MG_TAIL_ROWS", tail)
+    for name, env in variants.items():
+        for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         S = gpu_solver(p)
         S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
         X = np.zeros_like(Bo)
         S.solve(Bo, X, rel_tol=0.0, max_cycles=5)
         check_x(X, Xo)
-        out[(pdl, mode, tail)] = X
+        out[name] = X
         S.close()
-    assert np.array_equal(out[("1", "inv", "20000")], out[("0", "inv", "20000")])
+    assert np.array_equal(out["default"], out["nopdl"])
+    assert np.array_equal(out["default"], out["nopipe"])
