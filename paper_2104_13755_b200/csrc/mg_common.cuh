@@ -58,6 +58,59 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// ---- internal vector layout ------------------------------------------------
+// Internal iterate / right-hand side / residual vectors are row-major with a
+// row stride of VS<K>::S doubles: K rounded up to an aligned vector width
+// (k = 3 is padded to 4 so every row is one 32-byte sector and one 256-bit
+// load).  The user-facing [n][k] layout is converted by the permutation
+// kernels.
+template <int K>
+struct VS {
+    static constexpr int S = (K == 3) ? 4 : K;
+};
+
+template <int K>
+__device__ __forceinline__ void ldrow(const double* p, double (&v)[K]) {
+    if constexpr (K == 1) {
+        v[0] = *p;
+    } else if constexpr (K == 2) {
+        asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
+    } else if constexpr (K == 3) {
+        double pad;
+        asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(pad) : "l"(p));
+    } else {
+        asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+    }
+}
+// same through L2 only (data produced by other CTAs inside one launch)
+template <int K>
+__device__ __forceinline__ void ldrow_cg(const double* p, double (&v)[K]) {
+    if constexpr (K == 1) {
+        v[0] = __ldcg(p);
+    } else if constexpr (K == 2) {
+        asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
+    } else if constexpr (K == 3) {
+        double pad;
+        asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(pad) : "l"(p));
+    } else {
+        asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+    }
+}
+template <int K>
+__device__ __forceinline__ void strow(double* p, const double (&v)[K]) {
+    if constexpr (K == 1) {
+        *p = v[0];
+    } else if constexpr (K == 2) {
+        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v[0]), "d"(v[1]) : "memory");
+    } else if constexpr (K == 3) {
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(0.0)
+                     : "memory");
+    } else {
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                     : "memory");
+    }
+}
+
 // ---- host launch helper -------------------------------------------------
 template <typename... KArgs, typename... Args>
 inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

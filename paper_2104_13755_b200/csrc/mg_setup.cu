@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(kBlock) k_gather_rows(const int* __restrict__ 
     if (i >= n) return;
     const size_t u = (size_t)perm[i];
 #pragma unroll
-    for (int c = 0; c < K; ++c) dst[(size_t)i * K + c] = src[u * K + c];
+    for (int c = 0; c < K; ++c) dst[(size_t)i * VS<K>::S + c] = src[u * K + c];
+    if (VS<K>::S > K) dst[(size_t)i * VS<K>::S + K] = 0.0;
 }
 template <int K>
 __global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__ perm, const double* __restrict__ src,
@@ -34,7 +35,7 @@ __global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__
     if (i >= n) return;
     const size_t u = (size_t)perm[i];
 #pragma unroll
-    for (int c = 0; c < K; ++c) dst[u * K + c] = src[(size_t)i * K + c];
+    for (int c = 0; c < K; ++c) dst[u * K + c] = src[(size_t)i * VS<K>::S + c];
 }
 __global__ void __launch_bounds__(kBlock) k_gather_vals(const int64_t* __restrict__ i2u, const double* __restrict__ src,
                                                         double* __restrict__ dst, int64_t nnz) {

@@ -60,7 +60,7 @@ __device__ __forceinline__ void tail_sweep(const TailLevel& L, int r0, int r1, i
                 d += a;
             } else {
 #pragma unroll
-                for (int c = 0; c < K; ++c) s[c] = fma(a, __ldcg(L.x + (size_t)j * K + c), s[c]);
+                for (int c = 0; c < K; ++c) s[c] = fma(a, __ldcg(L.x + (size_t)j * VS<K>::S + c), s[c]);
             }
         }
 #pragma unroll
@@ -69,9 +69,9 @@ __device__ __forceinline__ void tail_sweep(const TailLevel& L, int r0, int r1, i
         if (lane == 0) {
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                const double bv = __ldcg(L.b + (size_t)row * K + c);
-                if (MODE == 0) L.x[(size_t)row * K + c] = (bv - s[c]) / d;
-                else L.r[(size_t)row * K + c] = bv - s[c];
+                const double bv = __ldcg(L.b + (size_t)row * VS<K>::S + c);
+                if (MODE == 0) L.x[(size_t)row * VS<K>::S + c] = (bv - s[c]) / d;
+                else L.r[(size_t)row * VS<K>::S + c] = bv - s[c];
             }
         }
     }
@@ -92,15 +92,15 @@ __device__ __forceinline__ void tail_restrict(const TailLevel& F, const TailLeve
             const int i = __ldg(C.cidx + t);
             const double w = __ldg(C.cw + t);
 #pragma unroll
-            for (int c = 0; c < K; ++c) s[c] = fma(w, __ldcg(F.r + (size_t)i * K + c), s[c]);
+            for (int c = 0; c < K; ++c) s[c] = fma(w, __ldcg(F.r + (size_t)i * VS<K>::S + c), s[c]);
         }
 #pragma unroll
         for (int c = 0; c < K; ++c) s[c] = group_sum<G>(s[c], mask);
         if (lane == 0) {
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                C.b[(size_t)I * K + c] = s[c];
-                C.x[(size_t)I * K + c] = 0.0;
+                C.b[(size_t)I * VS<K>::S + c] = s[c];
+                C.x[(size_t)I * VS<K>::S + c] = 0.0;
             }
         }
     }
@@ -115,10 +115,10 @@ __device__ __forceinline__ void tail_prolong(const TailLevel& F, const TailLevel
         const double w0 = __ldg(F.pw + i), w1 = __ldg(F.pw + n + i), w2 = __ldg(F.pw + 2 * n + i);
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-            double v = w0 * __ldcg(C.x + (size_t)c0 * K + c);
-            v = fma(w1, __ldcg(C.x + (size_t)c1 * K + c), v);
-            v = fma(w2, __ldcg(C.x + (size_t)c2 * K + c), v);
-            F.x[(size_t)i * K + c] = __ldcg(F.x + (size_t)i * K + c) + v;
+            double v = w0 * __ldcg(C.x + (size_t)c0 * VS<K>::S + c);
+            v = fma(w1, __ldcg(C.x + (size_t)c1 * VS<K>::S + c), v);
+            v = fma(w2, __ldcg(C.x + (size_t)c2 * VS<K>::S + c), v);
+            F.x[(size_t)i * VS<K>::S + c] = __ldcg(F.x + (size_t)i * VS<K>::S + c) + v;
         }
     }
 }
@@ -137,13 +137,13 @@ __device__ __forceinline__ void tail_coarse(const TailLevel& H, const double* __
         for (int j = lane; j < H.n; j += 32) {
             const double z = __ldg(Zr + j);
 #pragma unroll
-            for (int c = 0; c < K; ++c) acc[c] = fma(z, __ldcg(H.b + (size_t)j * K + c), acc[c]);
+            for (int c = 0; c < K; ++c) acc[c] = fma(z, __ldcg(H.b + (size_t)j * VS<K>::S + c), acc[c]);
         }
 #pragma unroll
         for (int c = 0; c < K; ++c) acc[c] = warp_sum(acc[c]);
         if (lane == 0)
 #pragma unroll
-            for (int c = 0; c < K; ++c) H.x[(size_t)row * K + c] = acc[c];
+            for (int c = 0; c < K; ++c) H.x[(size_t)row * VS<K>::S + c] = acc[c];
     }
 }
 

@@ -81,9 +81,7 @@ __device__ __forceinline__ void tile_row(const int* cs, const double* vs, int qb
             a[u] = ok ? vs[q + u] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < UNR; ++u)
-#pragma unroll
-            for (int c = 0; c < K; ++c) xv[u][c] = x[(size_t)j[u] * K + c];
+        for (int u = 0; u < UNR; ++u) ldrow<K>(x + (size_t)j[u] * VS<K>::S, xv[u]);
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             if (j[u] == row) {
@@ -124,12 +122,15 @@ __global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp
     double s[K], d;
     tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
     if (MODE == 0) {
+        double bv[K], xn[K];
+        ldrow<K>(b + (size_t)row * VS<K>::S, bv);
 #pragma unroll
-        for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / d;
+        for (int c = 0; c < K; ++c) xn[c] = (bv[c] - s[c]) / d;
+        strow<K>(x + (size_t)row * VS<K>::S, xn);
     } else {
 #pragma unroll
         for (int c = 0; c < K; ++c)
-            r[(size_t)row * K + c] = b[(size_t)row * K + c] - fma(d, x[(size_t)row * K + c], s[c]);
+            r[(size_t)row * VS<K>::S + c] = b[(size_t)row * VS<K>::S + c] - fma(d, x[(size_t)row * VS<K>::S + c], s[c]);
     }
 }
 
@@ -237,8 +238,7 @@ __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, co
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             if (j[u] != row) {
-#pragma unroll
-                for (int c = 0; c < K; ++c) xv[u][c] = x[(size_t)j[u] * K + c];
+                ldrow<K>(x + (size_t)j[u] * VS<K>::S, xv[u]);
             } else {
 #pragma unroll
                 for (int c = 0; c < K; ++c) xv[u][c] = 0.0;
@@ -298,13 +298,16 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
             double s[K], dg;
             stage_row<K, Unroll<K>::value>(v, tid, row, x, s, dg);
             if (MODE == 0) {
+                double bv[K], xn[K];
+                ldrow<K>(b + (size_t)row * VS<K>::S, bv);
 #pragma unroll
-                for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / dg;
+                for (int c = 0; c < K; ++c) xn[c] = (bv[c] - s[c]) / dg;
+                strow<K>(x + (size_t)row * VS<K>::S, xn);
             } else {
 #pragma unroll
                 for (int c = 0; c < K; ++c) {
-                    const double rr = b[(size_t)row * K + c] - fma(dg, x[(size_t)row * K + c], s[c]);
-                    if (MODE == 1) r[(size_t)row * K + c] = rr;
+                    const double rr = b[(size_t)row * VS<K>::S + c] - fma(dg, x[(size_t)row * VS<K>::S + c], s[c]);
+                    if (MODE == 1) r[(size_t)row * VS<K>::S + c] = rr;
                     else acc[c] = fma(rr, rr, acc[c]);
                 }
             }
@@ -364,12 +367,10 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     double s[K], x0[K], x1[K];
     double d = 0.0;
     const int jj0 = j0 >= 0 ? j0 : row, jj1 = j1 >= 0 ? j1 : row;
+    ldrow<K>(x + (size_t)jj0 * VS<K>::S, x0);
+    ldrow<K>(x + (size_t)jj1 * VS<K>::S, x1);
 #pragma unroll
-    for (int c = 0; c < K; ++c) {
-        x0[c] = x[(size_t)jj0 * K + c];
-        x1[c] = x[(size_t)jj1 * K + c];
-        s[c] = 0.0;
-    }
+    for (int c = 0; c < K; ++c) s[c] = 0.0;
     if (j0 >= 0) {
         if (j0 == row && MODE == 0) d += a0;
         else
@@ -385,10 +386,14 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     for (int e = e0 + lane + 2 * LPR; e < e1; e += LPR) {
         const int j = ld_stream(col + e, pol);
         const double a = ld_stream(val + e, pol);
-        if (j == row && MODE == 0) d += a;
-        else
+        if (j == row && MODE == 0) {
+            d += a;
+        } else {
+            double xv[K];
+            ldrow<K>(x + (size_t)j * VS<K>::S, xv);
 #pragma unroll
-            for (int c = 0; c < K; ++c) s[c] = fma(a, x[(size_t)j * K + c], s[c]);
+            for (int c = 0; c < K; ++c) s[c] = fma(a, xv[c], s[c]);
+        }
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
@@ -396,10 +401,10 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     if (lane == 0) {
         if (MODE == 0) {
 #pragma unroll
-            for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = (b[(size_t)row * K + c] - s[c]) / d;
+            for (int c = 0; c < K; ++c) x[(size_t)row * VS<K>::S + c] = (b[(size_t)row * VS<K>::S + c] - s[c]) / d;
         } else {
 #pragma unroll
-            for (int c = 0; c < K; ++c) r[(size_t)row * K + c] = b[(size_t)row * K + c] - s[c];
+            for (int c = 0; c < K; ++c) r[(size_t)row * VS<K>::S + c] = b[(size_t)row * VS<K>::S + c] - s[c];
         }
     }
 }
@@ -439,17 +444,23 @@ __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cpt
     double s[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = 0.0;
-    if (i0 >= 0)
+    if (i0 >= 0) {
+        double rv[K];
+        ldrow<K>(r + (size_t)i0 * VS<K>::S, rv);
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = fma(w0, r[(size_t)i0 * K + c], s[c]);
-    if (i1 >= 0)
+        for (int c = 0; c < K; ++c) s[c] = fma(w0, rv[c], s[c]);
+    }
+    if (i1 >= 0) {
+        double rv[K];
+        ldrow<K>(r + (size_t)i1 * VS<K>::S, rv);
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = fma(w1, r[(size_t)i1 * K + c], s[c]);
+        for (int c = 0; c < K; ++c) s[c] = fma(w1, rv[c], s[c]);
+    }
     for (int t = t0 + lane + 2 * G; t < t1; t += G) {
         const int i = cidx[t];
         const double w = cw[t];
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = fma(w, r[(size_t)i * K + c], s[c]);
+        for (int c = 0; c < K; ++c) s[c] = fma(w, r[(size_t)i * VS<K>::S + c], s[c]);
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = group_sum<G>(s[c], mask);
@@ -458,8 +469,8 @@ __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cpt
 #pragma unroll
         for (int c = 1; c < K; ++c)
             if (lane == c) v = s[c];
-        bc[(size_t)I * K + lane] = v;
-        xc[(size_t)I * K + lane] = 0.0;
+        bc[(size_t)I * VS<K>::S + lane] = v;
+        xc[(size_t)I * VS<K>::S + lane] = 0.0;
     }
 }
 
@@ -481,13 +492,19 @@ __global__ void __launch_bounds__(kBlock) k_prolong(const int* __restrict__ pc, 
     }
     pdl_wait();
     if (i >= n) return;
+    double y0[K], y1[K], y2[K], xi[K];
+    ldrow<K>(xc + (size_t)c0 * VS<K>::S, y0);
+    ldrow<K>(xc + (size_t)c1 * VS<K>::S, y1);
+    ldrow<K>(xc + (size_t)c2 * VS<K>::S, y2);
+    ldrow<K>(x + (size_t)i * VS<K>::S, xi);
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-        double v = w0 * xc[(size_t)c0 * K + c];
-        v = fma(w1, xc[(size_t)c1 * K + c], v);
-        v = fma(w2, xc[(size_t)c2 * K + c], v);
-        x[(size_t)i * K + c] += v;
+        double v = w0 * y0[c];
+        v = fma(w1, y1[c], v);
+        v = fma(w2, y2[c], v);
+        xi[c] += v;
     }
+    strow<K>(x + (size_t)i * VS<K>::S, xi);
 }
 
 // K7b: coarsest solve x = A_H^{-1} b, one warp per row of the explicit
@@ -513,16 +530,16 @@ __global__ void __launch_bounds__(256) k_coarse_gemv(const double* __restrict__ 
         const int j = lane + 32 * u;
         if (j < n)
 #pragma unroll
-            for (int c = 0; c < K; ++c) acc[c] = fma(z[u], b[(size_t)j * K + c], acc[c]);
+            for (int c = 0; c < K; ++c) acc[c] = fma(z[u], b[(size_t)j * VS<K>::S + c], acc[c]);
     }
     for (int j = lane + 32 * U; j < n; j += 32)
 #pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = fma(Zr[j], b[(size_t)j * K + c], acc[c]);
+        for (int c = 0; c < K; ++c) acc[c] = fma(Zr[j], b[(size_t)j * VS<K>::S + c], acc[c]);
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = warp_sum(acc[c]);
     if (lane == 0)
 #pragma unroll
-        for (int c = 0; c < K; ++c) x[(size_t)row * K + c] = acc[c];
+        for (int c = 0; c < K; ++c) x[(size_t)row * VS<K>::S + c] = acc[c];
 }
 
 // Coarsest solve L L^T x = b in ONE CTA (1024 threads): blocked forward and
@@ -540,7 +557,7 @@ __global__ void __launch_bounds__(1024) k_chol_solve(const double* __restrict__ 
     double* red = sm + (size_t)npad * K;  // [32][32][K]
     double* t = red + 32 * 32 * K;        // [32][K]
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < npad * K; i += 1024) y[i] = (i < n * K) ? b[i] : 0.0;
+    for (int i = tid; i < npad * K; i += 1024) y[i] = (i < n * K) ? b[(size_t)(i / K) * VS<K>::S + i % K] : 0.0;
     __syncthreads();
     const int nb = npad / 32;
     for (int I = 0; I < nb; ++I) {
@@ -613,7 +630,7 @@ __global__ void __launch_bounds__(1024) k_chol_solve(const double* __restrict__ 
             for (int c = 0; c < K; ++c) y[(32 * I + w) * K + c] = acc[c];
         __syncthreads();
     }
-    for (int i = tid; i < n * K; i += 1024) x[i] = y[i];
+    for (int i = tid; i < n * K; i += 1024) x[(size_t)(i / K) * VS<K>::S + i % K] = y[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -668,7 +685,7 @@ __global__ void __launch_bounds__(kTile) k_resnorm_tiled(const int* __restrict__
             tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                const double rr = b[(size_t)row * K + c] - fma(d, x[(size_t)row * K + c], s[c]);
+                const double rr = b[(size_t)row * VS<K>::S + c] - fma(d, x[(size_t)row * VS<K>::S + c], s[c]);
                 acc[c] = fma(rr, rr, acc[c]);
             }
         }
@@ -705,7 +722,7 @@ __global__ void __launch_bounds__(kBlock) k_resnorm_lpr(const int* __restrict__ 
                 const int j = ld_stream(col + e, pol);
                 const double a = ld_stream(val + e, pol);
 #pragma unroll
-                for (int c = 0; c < K; ++c) s[c] = fma(a, x[(size_t)j * K + c], s[c]);
+                for (int c = 0; c < K; ++c) s[c] = fma(a, x[(size_t)j * VS<K>::S + c], s[c]);
             }
         }
         if (active) {
@@ -714,7 +731,7 @@ __global__ void __launch_bounds__(kBlock) k_resnorm_lpr(const int* __restrict__ 
             if (lane == 0)
 #pragma unroll
                 for (int c = 0; c < K; ++c) {
-                    const double rr = b[(size_t)row * K + c] - s[c];
+                    const double rr = b[(size_t)row * VS<K>::S + c] - s[c];
                     acc[c] = fma(rr, rr, acc[c]);
                 }
         }
@@ -765,7 +782,7 @@ __global__ void __launch_bounds__(kBlock) k_sumsq_partial(const double* __restri
     for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock)
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-            const double t = v[(size_t)i * K + c];
+            const double t = v[(size_t)i * VS<K>::S + c];
             acc[c] = fma(t, t, acc[c]);
         }
     block_partial<K>(acc, partial);
@@ -808,8 +825,8 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s)
             t0 = L.tile_off[c];
             t1 = L.tile_off[c + 1];
         } else {
-            t0 = L.tile_off[L.ncolours];
-            t1 = L.tile_off[L.ncolours + 1];
+            t0 = L.tile_off[L.tile_off.size() - 2];   // whole-level tiles are the last range
+            t1 = L.tile_off.back();
         }
         pipe_launch<K, MODE>(L, t0, t1, r, nullptr, pipe_grid(t1 - t0, L.pipe_cap), pdl, s);
         return 1;
@@ -834,7 +851,7 @@ template <int K>
 int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl, cudaStream_t s) {
     int grid;
     if (L.pipe) {
-        const int t0 = L.tile_off[L.ncolours], t1 = L.tile_off[L.ncolours + 1];
+        const int t0 = L.tile_off[L.tile_off.size() - 2], t1 = L.tile_off.back();
         grid = std::min(nb, pipe_grid(t1 - t0, L.pipe_cap));
         pipe_launch<K, 2>(L, t0, t1, nullptr, partial, grid, pdl, s);
     } else if (L.tiled) {
