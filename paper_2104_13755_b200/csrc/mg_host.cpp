@@ -882,7 +882,7 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
             }
         }
         cudaError_t e;
-        if ((e = c->opp.upload(oi, c->stream)) || (e = c->Vint.alloc(3 * (size_t)n)) || (e = c->Mint.alloc(n)) ||
+        if ((e = c->opp.upload(oi, c->stream)) || (e = c->Vint.alloc(4 * (size_t)n)) || (e = c->Mint.alloc(n)) ||
             (e = c->Muser.alloc(n)))
             return c->cuda_fail(e, "cotan setup");
     }

@@ -69,7 +69,10 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
                                                            double* __restrict__ val, double* __restrict__ M, int n) {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
-    const double xi = V[3 * (size_t)i], yi = V[3 * (size_t)i + 1], zi = V[3 * (size_t)i + 2];
+    // internal positions: 32-byte rows (x, y, z, pad), one 256-bit load each
+    double pi[3];
+    ldrow<3>(V + 4 * (size_t)i, pi);
+    const double xi = pi[0], yi = pi[1], zi = pi[2];
     double lsum = 0.0, area2 = 0.0;
     int ediag = -1;
     for (int e = rp[i]; e < rp[i + 1]; ++e) {
@@ -78,13 +81,17 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
             ediag = e;
             continue;
         }
-        const double xj = V[3 * (size_t)j], yj = V[3 * (size_t)j + 1], zj = V[3 * (size_t)j + 2];
+        double pj[3];
+        ldrow<3>(V + 4 * (size_t)j, pj);
+        const double xj = pj[0], yj = pj[1], zj = pj[2];
         double cot_sum = 0.0;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int o = opp[2 * (size_t)e + s];
             if (o < 0) continue;
-            const double xo = V[3 * (size_t)o], yo = V[3 * (size_t)o + 1], zo = V[3 * (size_t)o + 2];
+            double po[3];
+            ldrow<3>(V + 4 * (size_t)o, po);
+            const double xo = po[0], yo = po[1], zo = po[2];
             const double ax = xi - xo, ay = yi - yo, az = zi - zo;
             const double bx = xj - xo, by = yj - yo, bz = zj - zo;
             const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
