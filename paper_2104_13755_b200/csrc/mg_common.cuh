@@ -82,6 +82,48 @@ __device__ __forceinline__ void ldrow(const double* p, double (&v)[K]) {
         asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
     }
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// row load / store with an L2 eviction-priority policy (x: evict_last so the
+// iterate stays resident across the colour passes; streams: evict_first)
+template <int K>
+__device__ __forceinline__ void ldrow_pol(const double* p, double (&v)[K], uint64_t pol) {
+    if constexpr (K == 1) {
+        asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[0]) : "l"(p), "l"(pol));
+    } else if constexpr (K == 2) {
+        asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
+    } else if constexpr (K == 3) {
+        double pad;
+        asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(pad)
+                     : "l"(p), "l"(pol));
+    } else {
+        asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(p), "l"(pol));
+    }
+}
+template <int K>
+__device__ __forceinline__ void strow_pol(double* p, const double (&v)[K], uint64_t pol) {
+    if constexpr (K == 1) {
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v[0]), "l"(pol) : "memory");
+    } else if constexpr (K == 2) {
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v[0]), "d"(v[1]), "l"(pol)
+                     : "memory");
+    } else if constexpr (K == 3) {
+        asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                     "d"(v[2]), "d"(0.0), "l"(pol)
+                     : "memory");
+    } else {
+        asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                     "d"(v[2]), "d"(v[3]), "l"(pol)
+                     : "memory");
+    }
+}
+
 // same through L2 only (data produced by other CTAs inside one launch)
 template <int K>
 __device__ __forceinline__ void ldrow_cg(const double* p, double (&v)[K]) {

@@ -220,7 +220,7 @@ __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned
 
 template <int K, int UNR>
 __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, const double* __restrict__ x,
-                                          double (&s)[K], double& d) {
+                                          double (&s)[K], double& d, uint64_t xpol) {
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = 0.0;
     d = 0.0;
@@ -238,7 +238,7 @@ __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, co
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             if (j[u] != row) {
-                ldrow<K>(x + (size_t)j[u] * VS<K>::S, xv[u]);
+                ldrow_pol<K>(x + (size_t)j[u] * VS<K>::S, xv[u], xpol);
             } else {
 #pragma unroll
                 for (int c = 0; c < K; ++c) xv[u][c] = 0.0;
@@ -285,6 +285,8 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
         }
     }
     pdl_wait();
+    const uint64_t xpol = evict_last_policy();
+    const uint64_t spol = evict_first_policy();
     double acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
@@ -296,19 +298,24 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
         if (tid < d.nrow) {
             const int row = d.row0 + tid;
             double s[K], dg;
-            stage_row<K, Unroll<K>::value>(v, tid, row, x, s, dg);
+            stage_row<K, Unroll<K>::value>(v, tid, row, x, s, dg, xpol);
+            double bv[K];
+            ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
             if (MODE == 0) {
-                double bv[K], xn[K];
-                ldrow<K>(b + (size_t)row * VS<K>::S, bv);
+                double xn[K];
 #pragma unroll
                 for (int c = 0; c < K; ++c) xn[c] = (bv[c] - s[c]) / dg;
-                strow<K>(x + (size_t)row * VS<K>::S, xn);
+                strow_pol<K>(x + (size_t)row * VS<K>::S, xn, xpol);
             } else {
+                double xr[K], rr[K];
+                ldrow_pol<K>(x + (size_t)row * VS<K>::S, xr, xpol);
 #pragma unroll
-                for (int c = 0; c < K; ++c) {
-                    const double rr = b[(size_t)row * VS<K>::S + c] - fma(dg, x[(size_t)row * VS<K>::S + c], s[c]);
-                    if (MODE == 1) r[(size_t)row * VS<K>::S + c] = rr;
-                    else acc[c] = fma(rr, rr, acc[c]);
+                for (int c = 0; c < K; ++c) rr[c] = bv[c] - fma(dg, xr[c], s[c]);
+                if (MODE == 1) {
+                    strow_pol<K>(r + (size_t)row * VS<K>::S, rr, xpol);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < K; ++c) acc[c] = fma(rr[c], rr[c], acc[c]);
                 }
             }
         }
@@ -364,11 +371,12 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     pdl_wait();
     if (!active) return;   // whole groups leave together
     const unsigned mask = group_mask(LPR);
+    const uint64_t xpol = evict_last_policy();
     double s[K], x0[K], x1[K];
     double d = 0.0;
     const int jj0 = j0 >= 0 ? j0 : row, jj1 = j1 >= 0 ? j1 : row;
-    ldrow<K>(x + (size_t)jj0 * VS<K>::S, x0);
-    ldrow<K>(x + (size_t)jj1 * VS<K>::S, x1);
+    ldrow_pol<K>(x + (size_t)jj0 * VS<K>::S, x0, xpol);
+    ldrow_pol<K>(x + (size_t)jj1 * VS<K>::S, x1, xpol);
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = 0.0;
     if (j0 >= 0) {
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
             d += a;
         } else {
             double xv[K];
-            ldrow<K>(x + (size_t)j * VS<K>::S, xv);
+            ldrow_pol<K>(x + (size_t)j * VS<K>::S, xv, xpol);
 #pragma unroll
             for (int c = 0; c < K; ++c) s[c] = fma(a, xv[c], s[c]);
         }
