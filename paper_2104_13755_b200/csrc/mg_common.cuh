@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "mg_internal.h"
+
 namespace mg {
 
 constexpr int kBlock = 256;
@@ -157,7 +159,8 @@ __device__ __forceinline__ void strow(double* p, const double (&v)[K]) {
 template <typename... KArgs, typename... Args>
 inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args... args) {
-    if (!pdl) {
+    const cudaAccessPolicyWindow* win = current_window();
+    if (!pdl && !win) {
         kern<<<grid, block, smem, s>>>(args...);
         return;
     }
@@ -166,11 +169,20 @@ inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (win) {
+        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[na].val.accessPolicyWindow = *win;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

@@ -194,6 +194,7 @@ struct mg_ctx {
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
+    int64_t l2_persist = -1;         // bytes of L2 set aside for the fine iterate (-1: auto, 0: off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
     int tail_cs = 0;                 // cluster size of the tail kernel
@@ -461,6 +462,29 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 return c->cuda_fail(e, "pattern upload");
         }
     }
+    // L2 residency of the fine iterate: a persisting access-policy window over
+    // level 0's x (re-gathered by every colour pass of every sweep).
+    {
+        Level& L0 = *c->lv[0];
+        L0.has_win = false;
+        int maxp = 0, maxw = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+        const size_t xbytes = (size_t)L0.n * kMaxK * sizeof(double);
+        const int64_t want = c->l2_persist < 0 ? (int64_t)std::min<size_t>(xbytes, (size_t)maxp) : c->l2_persist;
+        if (want > 0 && maxp > 0 && maxw > 0 && H > 0) {
+            const size_t lim = std::min<size_t>((size_t)want, (size_t)maxp);
+            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess) {
+                L0.win.base_ptr = L0.x.p;
+                L0.win.num_bytes = std::min<size_t>(xbytes, (size_t)maxw);
+                L0.win.hitRatio = (float)std::min(1.0, (double)lim / (double)L0.win.num_bytes);
+                L0.win.hitProp = cudaAccessPropertyPersisting;
+                L0.win.missProp = cudaAccessPropertyStreaming;
+                L0.has_win = true;
+            }
+            cudaGetLastError();
+        }
+    }
     // levels run by the cluster tail: the coarsest ones with <= tail_rows rows.
     // Off by default: measured slower than per-launch PDL kernels.
     c->tail_start = -1;
@@ -519,6 +543,7 @@ void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
     const int lt = c->tail_start >= 0 ? c->tail_start : H;   // levels >= lt: tail (or coarsest solve)
     for (int l = 0; l < lt; ++l) {
         Level& L = *c->lv[l];
+        WindowScope ws(L.has_win ? &L.win : nullptr);
         c->timed(PC_GS, l, s, [&] {
             int n = 0;
             for (int it = 0; it < c->mu_pre; ++it)
@@ -564,6 +589,7 @@ void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
     }
     for (int l = lt - 1; l >= 0; --l) {
         Level& L = *c->lv[l];
+        WindowScope ws(L.has_win ? &L.win : nullptr);
         c->timed(PC_PROLONG, l, s, [&] { return vc_prolong(K, L, *c->lv[l + 1], pdl, s); });
         c->timed(PC_GS, l, s, [&] {
             int n = 0;
@@ -572,6 +598,7 @@ void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
             return n;
         });
     }
+    WindowScope ws(c->lv[0]->has_win ? &c->lv[0]->win : nullptr);
     c->timed(PC_RESNORM, 0, s, [&] {
         return vc_resnorm(K, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p, c->rho.p, pdl, s);
     });
@@ -653,6 +680,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
     if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
+    if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||

@@ -63,6 +63,8 @@ struct Level {
     int pipe_cap = 0;                     // max nnz of any tile (GS or whole-level tiles)
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
+    bool has_win = false;                 // L2 persisting window over this level's iterate x
+    cudaAccessPolicyWindow win = {};
     std::vector<double> V;                // user-order positions [n][3]
     std::vector<int32_t> colour;          // user order
     std::vector<int32_t> colour_off;      // internal row ranges per colour [ncolours+1]
@@ -85,6 +87,18 @@ struct Level {
     DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
     DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
     DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
+};
+
+// L2 access-policy window applied to the next launches issued by this host
+// thread (set around the fine-level kernels to keep the iterate resident).
+inline const cudaAccessPolicyWindow*& current_window() {
+    static thread_local const cudaAccessPolicyWindow* w = nullptr;
+    return w;
+}
+struct WindowScope {
+    const cudaAccessPolicyWindow* prev;
+    explicit WindowScope(const cudaAccessPolicyWindow* w) : prev(current_window()) { current_window() = w; }
+    ~WindowScope() { current_window() = prev; }
 };
 
 // Device view of one level for the coarse-tail kernel (mg_tail.cu).
