@@ -194,6 +194,7 @@ struct mg_ctx {
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
+    bool use_gal2 = true;            // Galerkin v2 kernel
     int64_t l2_persist = -1;         // bytes of L2 set aside for the fine iterate (-1: auto, 0: off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
@@ -457,6 +458,25 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 const uint64_t ka = key[C.perm[a]], kb = key[C.perm[b]];
                 return ka != kb ? ka < kb : a < b;
             });
+            // Galerkin v2 inputs: packed P rows (fine) and children with row extents (coarse)
+            std::vector<int32_t> prc(4 * (size_t)L.n), cinfo(4 * cidx.size());
+            std::vector<double> prw(4 * (size_t)L.n);
+            for (int32_t i = 0; i < L.n; ++i)
+                for (int q = 0; q < 3; ++q) {
+                    prc[4 * (size_t)i + q] = pc[(size_t)q * L.n + i];
+                    prw[4 * (size_t)i + q] = pw[(size_t)q * L.n + i];
+                }
+            for (size_t t = 0; t < cidx.size(); ++t) {
+                const int32_t i = cidx[t];
+                cinfo[4 * t] = i;
+                cinfo[4 * t + 1] = L.irp[i];
+                cinfo[4 * t + 2] = L.irp[i + 1] - L.irp[i];
+            }
+            int maxrow = 0;
+            for (int32_t I = 0; I < C.n; ++I) maxrow = std::max(maxrow, C.irp[I + 1] - C.irp[I]);
+            C.gal2 = c->use_gal2 && maxrow <= galerkin_max_row();
+            if ((e = L.prow_c.upload(prc, s)) || (e = L.prow_w.upload(prw, s)) || (e = C.cinfo.upload(cinfo, s)))
+                return c->cuda_fail(e, "pattern upload");
             if ((e = L.pc.upload(pc, s)) || (e = L.pw.upload(pw, s)) || (e = C.cptr.upload(cnt, s)) ||
                 (e = C.cidx.upload(cidx, s)) || (e = C.cw.upload(cw, s)) || (e = C.gal_order.upload(order, s)))
                 return c->cuda_fail(e, "pattern upload");
@@ -680,6 +700,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
     if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
+    if (const char* m = getenv("MG_GAL2")) c->use_gal2 = std::string(m) != "0";
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     c->tail_cs = tail_cluster_size();

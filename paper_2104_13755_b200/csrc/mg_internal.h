@@ -83,6 +83,10 @@ struct Level {
     DBuf<int32_t> cptr, cidx;             // transpose of P_{l-1} (this level coarse): children
     DBuf<double> cw;
     DBuf<int32_t> gal_order;              // rows of this level in locality order (Galerkin)
+    bool gal2 = false;                    // Galerkin v2 usable for this (coarse) level
+    DBuf<int32_t> cinfo;                  // children as {i, row start, row length, 0} (this level coarse)
+    DBuf<int32_t> prow_c;                 // P rows packed: {c0, c1, c2, 0} (this level fine)
+    DBuf<double> prow_w;                  //                {w0, w1, w2, 0}
     DBuf<int32_t> dperm;                  // perm on device
     DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
     DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
@@ -158,6 +162,7 @@ int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);
 int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s);
+int galerkin_max_row();
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);

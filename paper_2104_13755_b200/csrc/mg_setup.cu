@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mg_common.cuh"
 #include "mg_internal.h"
@@ -205,6 +206,118 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
         for (int s = lane; s < m; s += 32) cval[c0 + s] = acc[w][s];
 }
 
+// K2 v2 (default): same definition, restructured for memory-level
+// parallelism.  Per coarse row (one warp, locality order):
+//   * children come with their fine-row extents {i, start, len} (no
+//     dependent row-pointer load) and weights P[i,I];
+//   * the coarse row's column list is hashed into shared memory (open
+//     addressing, 2 probes on average instead of a ~5-step binary search);
+//   * every lane handles two (child, nonzero) pairs per step; for each the
+//     P row of the column j is one packed 48-byte record {c0..c2, w0..w2}
+//     (two vector loads) instead of six scattered scalars.
+// Accumulation order per slot is fixed by (step, lane, q), so repeated
+// rebuilds are bitwise identical.
+constexpr int kHash = 256;   // power of two > 2 * kGalMaxM
+
+__device__ __forceinline__ unsigned hslot(int J) { return ((unsigned)J * 2654435761u) >> (32 - 8); }
+
+__global__ void __launch_bounds__(kGalWarps * 32) k_galerkin2(
+    int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
+    double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
+    const double* __restrict__ cw, const int* __restrict__ col, const double* __restrict__ val,
+    const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
+    __shared__ double acc[kGalWarps][kGalMaxM];
+    __shared__ int hkey[kGalWarps][kHash];
+    __shared__ unsigned char hval[kGalWarps][kHash];
+    __shared__ int ch_start[kGalWarps][32];
+    __shared__ int ch_scan[kGalWarps][32];
+    __shared__ double ch_w[kGalWarps][32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kGalWarps + w;
+    if (gw >= nc) return;
+    const int I = order[gw];
+    const int c0 = crp[I];
+    const int m = crp[I + 1] - c0;
+    for (int h = lane; h < kHash; h += 32) hkey[w][h] = -1;
+    for (int s = lane; s < m; s += 32) acc[w][s] = 0.0;
+    __syncwarp();
+    for (int s = lane; s < m; s += 32) {
+        const int J = ccol[c0 + s];
+        unsigned h = hslot(J);
+        while (atomicCAS(&hkey[w][h], -1, J) != -1) h = (h + 1) & (kHash - 1);
+        hval[w][h] = (unsigned char)s;
+    }
+    __syncwarp();
+    const int t0 = cptr[I], t1 = cptr[I + 1];
+    for (int tb = t0; tb < t1; tb += 32) {
+        const int nb = min(32, t1 - tb);
+        int len = 0;
+        if (lane < nb) {
+            const int4 ci = cinfo[tb + lane];
+            ch_w[w][lane] = cw[tb + lane];
+            ch_start[w][lane] = ci.y;
+            len = ci.z;
+        }
+        int incl = len;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        ch_scan[w][lane] = incl;
+        const int total = __shfl_sync(0xffffffffu, incl, nb - 1);
+        __syncwarp();
+        for (int g0 = 0; g0 < total; g0 += 64) {
+            int e[2];
+            double pwt[2];
+            bool ok[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int g = g0 + lane + 32 * u;
+                ok[u] = g < total;
+                int lo = 0, hi = nb - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ch_scan[w][mid] > g) hi = mid;
+                    else lo = mid + 1;
+                }
+                const int excl = lo ? ch_scan[w][lo - 1] : 0;
+                e[u] = ok[u] ? ch_start[w][lo] + (g - excl) : 0;
+                pwt[u] = ch_w[w][lo];
+            }
+            int j[2];
+            double a[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                j[u] = ok[u] ? col[e[u]] : 0;
+                a[u] = ok[u] ? pwt[u] * val[e[u]] : 0.0;
+            }
+            int4 pc[2];
+            double4 pw[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                pc[u] = prow_c[j[u]];
+                pw[u] = prow_w[j[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (!ok[u]) continue;
+                const int Js[3] = {pc[u].x, pc[u].y, pc[u].z};
+                const double ws[3] = {pw[u].x, pw[u].y, pw[u].z};
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    if (ws[q] == 0.0) continue;
+                    unsigned h = hslot(Js[q]);
+                    while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
+                    atomicAdd(&acc[w][hval[w][h]], a[u] * ws[q]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    for (int s = lane; s < m; s += 32) cval[c0 + s] = acc[w][s];
+}
+
 // ---------------------------------------------------------------------------
 // K7: coarsest level.  Dense row-major npad x npad (npad multiple of 32,
 // padding = identity), blocked right-looking Cholesky with 32-wide panels:
@@ -298,6 +411,122 @@ __global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ D, int
     }
 }
 
+// Cooperative single-launch factorisation (default): the same blocked
+// right-looking algorithm, all phases in one kernel separated by a software
+// grid barrier (co-residency guaranteed by the cooperative launch).
+//   for each 32-wide panel kb:
+//     phase 1: every CTA factors the diagonal block in shared memory (cheap,
+//              redundant) and solves its share of the 32-row blocks below it;
+//              CTA 0 writes L_kk back;
+//     phase 2: the trailing lower triangle gets the rank-32 update, 32x32
+//              tiles distributed over the CTAs.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        target += gridDim.x;
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void factor_diag_smem(double (*Ld)[33], int* err) {
+    // 32x32 Cholesky in shared memory by 256 threads (rows r = tid >> 3, 8 threads per row)
+    const int tid = threadIdx.x;
+    for (int p = 0; p < 32; ++p) {
+        if (tid == 0) {
+            double d = Ld[p][p];
+            if (!(d > 0.0)) {
+                if (err) atomicExch(err, 1);
+                d = 1.0;
+            }
+            Ld[p][p] = sqrt(d);
+        }
+        __syncthreads();
+        if (tid > p && tid < 32) Ld[tid][p] /= Ld[p][p];
+        __syncthreads();
+        for (int t = tid; t < 1024; t += blockDim.x) {
+            const int r = t >> 5, c = t & 31;
+            if (r > p && c > p && c <= r) Ld[r][c] -= Ld[r][p] * Ld[c][p];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_chol_coop(double* __restrict__ D, int npad, int* err, unsigned* ctr) {
+    __shared__ double Ld[32][33];
+    __shared__ double Pi[32][33];
+    __shared__ double Pj[32][33];
+    const int nb = npad / 32;
+    const int tid = threadIdx.x;
+    unsigned target = 0;
+    for (int kb = 0; kb < nb; ++kb) {
+        const int base = kb * 32;
+        // ---- phase 1: diagonal factor + panel solve
+        const int m = nb - kb - 1;   // row blocks below the diagonal
+        const bool busy = (int)blockIdx.x <= m;
+        if (busy) {
+            for (int t = tid; t < 1024; t += 256) Ld[t >> 5][t & 31] = D[(size_t)(base + (t >> 5)) * npad + base + (t & 31)];
+            __syncthreads();
+            factor_diag_smem(Ld, blockIdx.x == 0 ? err : nullptr);
+            for (int ib = kb + 1 + blockIdx.x; ib < nb; ib += gridDim.x) {
+                // rows of block ib: L_ib = A_ib L_kk^{-T}, in shared memory, thread r = row r
+                __syncthreads();
+                for (int t = tid; t < 1024; t += 256)
+                    Pi[t >> 5][t & 31] = D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)];
+                __syncthreads();
+                if (tid < 32) {
+                    for (int p = 0; p < 32; ++p) {
+                        double sum = Pi[tid][p];
+                        for (int q = 0; q < p; ++q) sum -= Pi[tid][q] * Ld[p][q];
+                        Pi[tid][p] = sum / Ld[p][p];
+                    }
+                }
+                __syncthreads();
+                for (int t = tid; t < 1024; t += 256)
+                    D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)] = Pi[t >> 5][t & 31];
+            }
+        }
+        grid_barrier(ctr, target);
+        // L_kk written back only now: every CTA has read A_kk in phase 1
+        if (blockIdx.x == 0) {
+            for (int t = tid; t < 1024; t += 256) {
+                const int r = t >> 5, c = t & 31;
+                D[(size_t)(base + r) * npad + base + c] = (c <= r) ? Ld[r][c] : 0.0;
+            }
+        }
+        // ---- phase 2: trailing update A_ij -= L_ik L_jk^T, kb < j <= i
+        const int ntile = m * (m + 1) / 2;
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            while (ti * (ti + 1) / 2 > t) --ti;
+            const int tj = t - ti * (ti + 1) / 2;
+            const int bi = kb + 1 + ti, bj = kb + 1 + tj;
+            __syncthreads();
+            for (int q = tid; q < 1024; q += 256) {
+                const int r = q >> 5, c = q & 31;
+                Pi[r][c] = D[(size_t)(bi * 32 + r) * npad + base + c];
+                Pj[r][c] = D[(size_t)(bj * 32 + r) * npad + base + c];
+            }
+            __syncthreads();
+            for (int q = tid; q < 1024; q += 256) {
+                const int r = q >> 5, c = q & 31;
+                if (bi == bj && c > r) continue;
+                double acc = 0.0;
+#pragma unroll
+                for (int p = 0; p < 32; ++p) acc = fma(Pi[r][p], Pj[c][p], acc);
+                D[(size_t)(bi * 32 + r) * npad + bj * 32 + c] -= acc;
+            }
+        }
+        grid_barrier(ctr, target);
+    }
+}
+
 // Inverse of every 32x32 diagonal block of L (for the solve); thread t
 // computes column t by forward substitution.
 __global__ void __launch_bounds__(32) k_chol_diaginv(const double* __restrict__ D, int npad, double* __restrict__ Linv) {
@@ -374,6 +603,8 @@ void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* 
 
 }  // namespace
 
+int galerkin_max_row() { return kGalMaxM; }
+
 void init_setup_attributes() {
     const int big = 200 * 1024;
     cudaFuncSetAttribute(k_chol_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -416,6 +647,13 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
 }
 int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s) {
     const int nc = coarse.n;
+    if (coarse.gal2 && fine.prow_c.p) {
+        k_galerkin2<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
+            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
+            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fine.val.p,
+            reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
+        return 1;
+    }
     k_galerkin<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
         nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p, coarse.cidx.p, coarse.cw.p,
         fine.rp.p, fine.col.p, fine.val.p, fine.pc.p, fine.pw.p, fine.n);
@@ -430,6 +668,25 @@ int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s) {
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s) {
     const int nb = npad / 32;
     int launches = 0;
+    static unsigned* ctr = nullptr;
+    static int coop_blocks = -1;
+    if (coop_blocks < 0) {
+        int dev = 0, nsm = 0, per = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_coop, 256, 0);
+        coop_blocks = (coop && per > 0 && cudaMalloc(&ctr, sizeof(unsigned)) == cudaSuccess) ? nsm * std::min(per, 1) : 0;
+        cudaGetLastError();
+    }
+    if (coop_blocks > 0 && !getenv("MG_CHOL_LAUNCHES")) {
+        const int grid = std::max(1, std::min(coop_blocks, nb * (nb - 1) / 2 + 1));
+        cudaMemsetAsync(ctr, 0, sizeof(unsigned), s);
+        void* args[] = {&D, &npad, &err, &ctr};
+        cudaLaunchCooperativeKernel((const void*)k_chol_coop, dim3(grid), dim3(256), args, 0, s);
+        k_chol_diaginv<<<nb, 32, 0, s>>>(D, npad, Linv);
+        return 2;
+    }
     for (int kb = 0; kb < nb; ++kb) {
         k_chol_diag<<<1, 1024, 0, s>>>(D, npad, kb, err);
         ++launches;

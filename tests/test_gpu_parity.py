@@ -260,10 +260,12 @@ def test_launch_modes_agree(ora, monkeypatch):
         "nopipe": {"MG_PIPE": "0"},
         "trsv": {"MG_COARSE_SOLVE": "trsv"},
         "tail": {"MG_TAIL_ROWS": "20000"},
+        "gal1": {"MG_GAL2": "0"},
+        "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
     }
     out = {}
     for name, env in variants.items():
-        for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS"):
+        for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_CHOL_LAUNCHES"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
