@@ -405,8 +405,16 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             if (e) return c->cuda_fail(e, "tile upload");
         }
         if (!L.tiled) {
-            const double half = avg / 2.0;
-            L.lpr = half <= 4.0 ? 4 : half <= 8.0 ? 8 : half <= 16.0 ? 16 : 32;
+            // lanes per row: the widest group for which one colour pass is about one wave
+            // (148 SMs x 2048 threads); each lane prefetches 32 / LPR entries
+            const double rows = (double)L.n / std::max(1, (int)L.colour_off.size() - 1);
+            const double wave = 148.0 * 2048.0;
+            L.lpr = 4;
+            for (int w : {32, 16, 8})
+                if (rows * w <= wave) {
+                    L.lpr = w;
+                    break;
+                }
         }
     }
     cudaStream_t s = c->stream;

@@ -343,77 +343,86 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
 
 // ---------------------------------------------------------------------------
 // LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
-// prefetches up to two (col, val) of its row in the PDL prologue.
+// prefetches up to U = 32/LPR (col, val) of its row in the PDL prologue;
+// after the wait its x gathers go out in batches of GB independent loads.
+// The group width is chosen per level so that one colour pass is about one
+// wave of the GPU (see choose_lpr in mg_host.cpp).
 template <int K, int LPR, int MODE>
 __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1) {
+    constexpr int U = 32 / LPR;
+    constexpr int GB = (K >= 3) ? (U < 2 ? U : 2) : (U < 4 ? U : 4);
     const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
     const int lane = threadIdx.x & (LPR - 1);
     const int row = r0 + g;
     pdl_launch_dependents();
     const bool active = row < r1;
     const uint64_t pol = evict_first_policy();
-    int e0 = 0, e1 = 0, j0 = -1, j1 = -1;
-    double a0 = 0.0, a1 = 0.0;
+    int e0 = 0, e1 = 0;
+    int j[U];
+    double a[U];
     if (active) {
         e0 = rp[row];
         e1 = rp[row + 1];
-        if (e0 + lane < e1) {
-            j0 = ld_stream(col + e0 + lane, pol);
-            a0 = ld_stream(val + e0 + lane, pol);
-        }
-        if (e0 + lane + LPR < e1) {
-            j1 = ld_stream(col + e0 + lane + LPR, pol);
-            a1 = ld_stream(val + e0 + lane + LPR, pol);
-        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int e = e0 + lane + u * LPR;
+        const bool ok = active && e < e1;
+        j[u] = ok ? ld_stream(col + e, pol) : -1;
+        a[u] = ok ? ld_stream(val + e, pol) : 0.0;
     }
     pdl_wait();
     if (!active) return;   // whole groups leave together
     const unsigned mask = group_mask(LPR);
     const uint64_t xpol = evict_last_policy();
-    double s[K], x0[K], x1[K];
-    double d = 0.0;
-    const int jj0 = j0 >= 0 ? j0 : row, jj1 = j1 >= 0 ? j1 : row;
-    ldrow_pol<K>(x + (size_t)jj0 * VS<K>::S, x0, xpol);
-    ldrow_pol<K>(x + (size_t)jj1 * VS<K>::S, x1, xpol);
+    double s[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = 0.0;
-    if (j0 >= 0) {
-        if (j0 == row && MODE == 0) d += a0;
-        else
+    double d = 0.0;
 #pragma unroll
-            for (int c = 0; c < K; ++c) s[c] = fma(a0, x0[c], s[c]);
-    }
-    if (j1 >= 0) {
-        if (j1 == row && MODE == 0) d += a1;
-        else
+    for (int u0 = 0; u0 < U; u0 += GB) {
+        double xv[GB][K];
 #pragma unroll
-            for (int c = 0; c < K; ++c) s[c] = fma(a1, x1[c], s[c]);
+        for (int u = 0; u < GB; ++u) {
+            const int jj = j[u0 + u];
+            if (jj >= 0 && (MODE != 0 || jj != row)) ldrow_pol<K>(x + (size_t)jj * VS<K>::S, xv[u], xpol);
+        }
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+            const int jj = j[u0 + u];
+            if (jj < 0) continue;
+            if (MODE == 0 && jj == row) {
+                d += a[u0 + u];
+            } else {
+#pragma unroll
+                for (int c = 0; c < K; ++c) s[c] = fma(a[u0 + u], xv[u][c], s[c]);
+            }
+        }
     }
-    for (int e = e0 + lane + 2 * LPR; e < e1; e += LPR) {
-        const int j = ld_stream(col + e, pol);
-        const double a = ld_stream(val + e, pol);
-        if (j == row && MODE == 0) {
-            d += a;
+    for (int e = e0 + lane + U * LPR; e < e1; e += LPR) {
+        const int jj = ld_stream(col + e, pol);
+        const double av = ld_stream(val + e, pol);
+        if (MODE == 0 && jj == row) {
+            d += av;
         } else {
             double xv[K];
-            ldrow_pol<K>(x + (size_t)j * VS<K>::S, xv, xpol);
+            ldrow_pol<K>(x + (size_t)jj * VS<K>::S, xv, xpol);
 #pragma unroll
-            for (int c = 0; c < K; ++c) s[c] = fma(a, xv[c], s[c]);
+            for (int c = 0; c < K; ++c) s[c] = fma(av, xv[c], s[c]);
         }
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
     if (MODE == 0) d = group_sum<LPR>(d, mask);
     if (lane == 0) {
-        if (MODE == 0) {
+        double bv[K], out[K];
+        ldrow<K>(b + (size_t)row * VS<K>::S, bv);
 #pragma unroll
-            for (int c = 0; c < K; ++c) x[(size_t)row * VS<K>::S + c] = (b[(size_t)row * VS<K>::S + c] - s[c]) / d;
-        } else {
-#pragma unroll
-            for (int c = 0; c < K; ++c) r[(size_t)row * VS<K>::S + c] = b[(size_t)row * VS<K>::S + c] - s[c];
-        }
+        for (int c = 0; c < K; ++c) out[c] = MODE == 0 ? (bv[c] - s[c]) / d : bv[c] - s[c];
+        if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
+        else strow<K>(r + (size_t)row * VS<K>::S, out);
     }
 }
 
