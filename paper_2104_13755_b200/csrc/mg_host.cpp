@@ -190,7 +190,7 @@ struct mg_ctx {
     DBuf<double> Vstage, Vint, Mint, Muser;
 
     int npad = 0;
-    DBuf<double> D, Linv, Ainv;
+    DBuf<double> D, Linv, Ainv, Wbuf;
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
@@ -530,7 +530,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
     c->npad = (nH + 31) / 32 * 32;
     cudaError_t e;
     if ((e = c->D.alloc((size_t)c->npad * c->npad)) || (e = c->Linv.alloc((size_t)c->npad * 32)) ||
-        (e = c->Ainv.alloc((size_t)c->npad * c->npad)) ||
+        (e = c->Ainv.alloc((size_t)c->npad * c->npad)) || (e = c->Wbuf.alloc((size_t)c->npad * c->npad)) ||
         (e = c->errflag.alloc(1)) || (e = c->partial.alloc((size_t)resnorm_blocks(0) * kMaxK)) ||
         (e = c->bnorm.alloc(kMaxK)) || (e = c->rho.alloc(kMaxK)))
         return c->cuda_fail(e, "pattern alloc");
@@ -548,7 +548,12 @@ int rebuild_hierarchy(mg_ctx* c) {
     cudaError_t e = cudaMemsetAsync(c->errflag.p, 0, sizeof(int), s);
     if (e) return c->cuda_fail(e, "factor");
     c->timed(PC_FACTOR, c->H, s, [&] {
-        int n = launch_densify(LH, c->D.p, c->npad, s) + launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
+        int n = launch_densify(LH, c->D.p, c->npad, s);
+        const int nc = (c->coarse_mode == 1 && !getenv("MG_CHOL_LAUNCHES"))
+                           ? launch_chol_cluster(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s)
+                           : -1;
+        if (nc > 0) return n + nc;
+        n += launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
         if (c->coarse_mode == 1) n += launch_chol_inverse(c->D.p, c->Linv.p, c->npad, c->Ainv.p, s);
         return n;
     });

@@ -221,6 +221,30 @@ constexpr int kHash = 256;   // power of two > 2 * kGalMaxM
 
 __device__ __forceinline__ unsigned hslot(int J) { return ((unsigned)J * 2654435761u) >> (32 - 8); }
 
+// acc[slot] += v for every valid lane, deterministic and without atomics:
+// lanes with equal slots are grouped (match.any), the lowest lane of each
+// group sums its peers' values in lane order and does a plain update (one
+// writer per slot per call).  fp64 atomicAdd on shared memory would be a
+// CAS spin loop on this architecture.
+__device__ __forceinline__ void warp_accumulate(double* acc, bool valid, int slot, double v, int lane) {
+    const int key = valid ? slot : (1 << 20) + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int gsize = __popc(peers);
+    int maxg = gsize;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) maxg = max(maxg, __shfl_xor_sync(0xffffffffu, maxg, off));
+    unsigned rest = peers;
+    double sum = 0.0;
+    for (int t = 0; t < maxg; ++t) {
+        const int src = rest ? __ffs(rest) - 1 : lane;
+        const double vv = __shfl_sync(0xffffffffu, v, src);
+        if (rest) sum += vv;
+        rest &= rest - 1;
+    }
+    if (valid && lane == __ffs(peers) - 1) acc[slot] += sum;
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin2(
     int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
     double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
@@ -301,15 +325,18 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin2(
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                if (!ok[u]) continue;
                 const int Js[3] = {pc[u].x, pc[u].y, pc[u].z};
                 const double ws[3] = {pw[u].x, pw[u].y, pw[u].z};
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    if (ws[q] == 0.0) continue;
-                    unsigned h = hslot(Js[q]);
-                    while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
-                    atomicAdd(&acc[w][hval[w][h]], a[u] * ws[q]);
+                    const bool valid = ok[u] && ws[q] != 0.0;
+                    int slot = -1;
+                    if (valid) {
+                        unsigned h = hslot(Js[q]);
+                        while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
+                        slot = hval[w][h];
+                    }
+                    warp_accumulate(acc[w], valid, slot, a[u] * ws[q], lane);
                 }
             }
         }
@@ -527,6 +554,189 @@ __global__ void __launch_bounds__(256) k_chol_coop(double* __restrict__ D, int n
     }
 }
 
+// ---------------------------------------------------------------------------
+// K7a (default): factor AND explicit inverse of the coarsest operator in ONE
+// launch of a thread-block cluster (up to 16 CTAs x 512 threads), phases
+// separated by barrier.cluster:
+//   1. blocked right-looking Cholesky A_H = L L^T (32-wide panels: redundant
+//      diagonal factor per CTA, panel solve, rank-32 trailing update);
+//   2. inverses of the diagonal blocks;
+//   3. W = L^{-1} by block diagonals: W_ij = -inv(L_ii) sum_{k=j}^{i-1} L_ik W_kj;
+//   4. Z = A_H^{-1} = W^T W (both triangles written, for the per-cycle GEMV).
+// All block products are 32x32 shared-memory tile GEMMs.
+constexpr int kCholThreads = 512;
+
+__device__ __forceinline__ void csync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned crank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned csize() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+// acc[e] (e = 0,1) for output (r, c0 + e) of a 32x32 tile, r = tid >> 4, c0 = 2 (tid & 15):
+// acc += op(A) op(B), A/B 32x32 blocks at global row-major addresses with leading dim ld.
+__device__ __forceinline__ void tile_mac(double (&acc)[2], const double* __restrict__ A, bool tA,
+                                         const double* __restrict__ B, bool tB, int ld, double (*As)[33],
+                                         double (*Bs)[33]) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    for (int q = tid; q < 1024; q += kCholThreads) {
+        const int r = q >> 5, c = q & 31;
+        const double av = A[(size_t)r * ld + c];
+        const double bv = B[(size_t)r * ld + c];
+        if (tA) As[c][r] = av; else As[r][c] = av;
+        if (tB) Bs[c][r] = bv; else Bs[r][c] = bv;
+    }
+    __syncthreads();
+    const int r = tid >> 4, c0 = 2 * (tid & 15);
+#pragma unroll 8
+    for (int p = 0; p < 32; ++p) {
+        const double a = As[r][p];
+        acc[0] = fma(a, Bs[p][c0], acc[0]);
+        acc[1] = fma(a, Bs[p][c0 + 1], acc[1]);
+    }
+}
+
+__global__ void __launch_bounds__(kCholThreads, 1) k_chol_cluster(double* __restrict__ D, double* __restrict__ Linv,
+                                                                  double* __restrict__ W, double* __restrict__ Z,
+                                                                  int npad, int* err) {
+    __shared__ double Ld[32][33];
+    __shared__ double As[32][33];
+    __shared__ double Bs[32][33];
+    const int nb = npad / 32;
+    const int tid = threadIdx.x;
+    const int rank = (int)crank(), ncta = (int)csize();
+    const int r = tid >> 4, c0 = 2 * (tid & 15);
+    // ---- 1. Cholesky
+    for (int kb = 0; kb < nb; ++kb) {
+        const int base = kb * 32;
+        for (int t = tid; t < 1024; t += kCholThreads) Ld[t >> 5][t & 31] = D[(size_t)(base + (t >> 5)) * npad + base + (t & 31)];
+        __syncthreads();
+        for (int p = 0; p < 32; ++p) {
+            if (tid == 0) {
+                double d = Ld[p][p];
+                if (!(d > 0.0)) {
+                    if (rank == 0) atomicExch(err, 1);
+                    d = 1.0;
+                }
+                Ld[p][p] = sqrt(d);
+            }
+            __syncthreads();
+            if (tid > p && tid < 32) Ld[tid][p] /= Ld[p][p];
+            __syncthreads();
+            for (int t = tid; t < 1024; t += kCholThreads) {
+                const int rr = t >> 5, cc = t & 31;
+                if (rr > p && cc > p && cc <= rr) Ld[rr][cc] -= Ld[rr][p] * Ld[cc][p];
+            }
+            __syncthreads();
+        }
+        for (int ib = kb + 1 + rank; ib < nb; ib += ncta) {
+            __syncthreads();
+            for (int t = tid; t < 1024; t += kCholThreads) As[t >> 5][t & 31] = D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)];
+            __syncthreads();
+            if (tid < 32) {
+                for (int p = 0; p < 32; ++p) {
+                    double sum = As[tid][p];
+                    for (int q = 0; q < p; ++q) sum -= As[tid][q] * Ld[p][q];
+                    As[tid][p] = sum / Ld[p][p];
+                }
+            }
+            __syncthreads();
+            for (int t = tid; t < 1024; t += kCholThreads) D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)] = As[t >> 5][t & 31];
+        }
+        csync();
+        if (rank == 0)
+            for (int t = tid; t < 1024; t += kCholThreads) {
+                const int rr = t >> 5, cc = t & 31;
+                D[(size_t)(base + rr) * npad + base + cc] = (cc <= rr) ? Ld[rr][cc] : 0.0;
+            }
+        const int m = nb - kb - 1;
+        const int ntile = m * (m + 1) / 2;
+        for (int t = rank; t < ntile; t += ncta) {
+            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            while (ti * (ti + 1) / 2 > t) --ti;
+            const int tj = t - ti * (ti + 1) / 2;
+            const int bi = kb + 1 + ti, bj = kb + 1 + tj;
+            double acc[2] = {0.0, 0.0};
+            tile_mac(acc, D + (size_t)(bi * 32) * npad + base, false, D + (size_t)(bj * 32) * npad + base, true, npad, As, Bs);
+            double* out = D + (size_t)(bi * 32 + r) * npad + bj * 32 + c0;
+            if (!(bi == bj && c0 > r)) out[0] -= acc[0];
+            if (!(bi == bj && c0 + 1 > r)) out[1] -= acc[1];
+        }
+        csync();
+    }
+    // ---- 2. inverses of the diagonal blocks (thread t < 32 solves column t)
+    for (int I = rank; I < nb; I += ncta) {
+        __syncthreads();
+        for (int t = tid; t < 1024; t += kCholThreads) Ld[t >> 5][t & 31] = D[(size_t)(I * 32 + (t >> 5)) * npad + I * 32 + (t & 31)];
+        __syncthreads();
+        if (tid < 32) {
+            for (int rr = 0; rr < 32; ++rr) {
+                double sum = (rr == tid) ? 1.0 : 0.0;
+                for (int q = tid; q < rr; ++q) sum -= Ld[rr][q] * As[q][tid];
+                As[rr][tid] = (rr >= tid) ? sum / Ld[rr][rr] : 0.0;
+            }
+        }
+        __syncthreads();
+        for (int t = tid; t < 1024; t += kCholThreads) {
+            const double v = As[t >> 5][t & 31];
+            Linv[(size_t)I * 1024 + t] = v;
+            W[(size_t)(I * 32 + (t >> 5)) * npad + I * 32 + (t & 31)] = v;
+        }
+    }
+    csync();
+    // ---- 3. W = L^{-1}, block diagonals d = 1 .. nb-1
+    for (int dd = 1; dd < nb; ++dd) {
+        for (int j = rank; j + dd < nb; j += ncta) {
+            const int i = j + dd;
+            double acc[2] = {0.0, 0.0};
+            for (int k = j; k < i; ++k)
+                tile_mac(acc, D + (size_t)(i * 32) * npad + k * 32, false, W + (size_t)(k * 32) * npad + j * 32, false,
+                         npad, As, Bs);
+            // T = acc (the tile sum_k L_ik W_kj) -> Bs, then W_ij = -inv(L_ii) T
+            __syncthreads();
+            Bs[r][c0] = acc[0];
+            Bs[r][c0 + 1] = acc[1];
+            for (int q = tid; q < 1024; q += kCholThreads) As[q >> 5][q & 31] = Linv[(size_t)i * 1024 + q];
+            __syncthreads();
+            double o0 = 0.0, o1 = 0.0;
+#pragma unroll 8
+            for (int p = 0; p < 32; ++p) {
+                o0 = fma(As[r][p], Bs[p][c0], o0);
+                o1 = fma(As[r][p], Bs[p][c0 + 1], o1);
+            }
+            double* out = W + (size_t)(i * 32 + r) * npad + j * 32 + c0;
+            out[0] = -o0;
+            out[1] = -o1;
+        }
+        csync();
+    }
+    // ---- 4. Z = W^T W, lower tiles I >= J, mirrored
+    const int ntz = nb * (nb + 1) / 2;
+    for (int t = rank; t < ntz; t += ncta) {
+        int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((I + 1) * (I + 2) / 2 <= t) ++I;
+        while (I * (I + 1) / 2 > t) --I;
+        const int J = t - I * (I + 1) / 2;
+        double acc[2] = {0.0, 0.0};
+        for (int k = I; k < nb; ++k)
+            tile_mac(acc, W + (size_t)(k * 32) * npad + I * 32, true, W + (size_t)(k * 32) * npad + J * 32, false, npad,
+                     As, Bs);
+        Z[(size_t)(I * 32 + r) * npad + J * 32 + c0] = acc[0];
+        Z[(size_t)(I * 32 + r) * npad + J * 32 + c0 + 1] = acc[1];
+        Z[(size_t)(J * 32 + c0) * npad + I * 32 + r] = acc[0];
+        Z[(size_t)(J * 32 + c0 + 1) * npad + I * 32 + r] = acc[1];
+    }
+}
+
 // Inverse of every 32x32 diagonal block of L (for the solve); thread t
 // computes column t by forward substitution.
 __global__ void __launch_bounds__(32) k_chol_diaginv(const double* __restrict__ D, int npad, double* __restrict__ Linv) {
@@ -700,6 +910,49 @@ int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t
     k_chol_diaginv<<<nb, 32, 0, s>>>(D, npad, Linv);
     return launches + 1;
 }
+int chol_cluster_size() {
+    static int cs = -1;
+    if (cs >= 0) return cs;
+    cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cs = 0;
+    for (int c : {16, 8, 4}) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(c);
+        cfg.blockDim = dim3(kCholThreads);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_chol_cluster, &cfg) == cudaSuccess && ncl >= 1) {
+            cs = c;
+            break;
+        }
+        cudaGetLastError();
+    }
+    return cs;
+}
+
+int launch_chol_cluster(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s) {
+    const int cs = chol_cluster_size();
+    if (cs <= 0) return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kCholThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_chol_cluster, D, Linv, W, Z, npad, err) == cudaSuccess ? 1 : -1;
+}
+
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s) {
     const size_t smem = sizeof(double) * ((size_t)npad * kInvCols + 32 * kInvCols);
     k_chol_inverse<<<npad / kInvCols, 512, smem, s>>>(D, Linv, npad, Z);
