@@ -345,6 +345,69 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin2(
     for (int s = lane; s < m; s += 32) cval[c0 + s] = acc[w][s];
 }
 
+// K2 v3 (default): slot-owner formulation, atomic-free and deterministic.
+// One warp per coarse row I; lane l owns coarse columns J_l = col(I, l) and
+// J_l' = col(I, l + 32).  The warp walks every (child i, neighbour j) pair of
+// the row in lockstep: (j, p_iI a_ij) is broadcast from the lane that loaded
+// it, the packed P_j record {c0..c2, w0..w2} is a warp-uniform load, and each
+// lane adds p_iI a_ij P[j, J_l] into registers (P[j, J] = sum of the record's
+// weights whose column is J; padding weights are exactly 0).  Rows wider
+// than 64 entries use k_galerkin.
+__global__ void __launch_bounds__(kGalWarps * 32) k_galerkin3(
+    int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
+    double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
+    const double* __restrict__ cw, const int* __restrict__ col, const double* __restrict__ val,
+    const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kGalWarps + w;
+    if (gw >= nc) return;
+    const int I = order[gw];
+    const int c0 = crp[I];
+    const int m = crp[I + 1] - c0;
+    const int J0 = lane < m ? ccol[c0 + lane] : -1;
+    const int J1 = lane + 32 < m ? ccol[c0 + 32 + lane] : -1;
+    double acc0 = 0.0, acc1 = 0.0;
+    const int t0 = cptr[I], t1 = cptr[I + 1];
+    for (int tb = t0; tb < t1; tb += 32) {
+        const int nb = min(32, t1 - tb);
+        int4 ci = make_int4(0, 0, 0, 0);
+        double cwv = 0.0;
+        if (lane < nb) {
+            ci = cinfo[tb + lane];
+            cwv = cw[tb + lane];
+        }
+        for (int k = 0; k < nb; ++k) {
+            const int start = __shfl_sync(0xffffffffu, ci.y, k);
+            const int len = __shfl_sync(0xffffffffu, ci.z, k);
+            const double pI = __shfl_sync(0xffffffffu, cwv, k);
+            for (int e0 = start; e0 < start + len; e0 += 32) {
+                const int cnt = min(32, start + len - e0);
+                int jl = 0;
+                double al = 0.0;
+                if (lane < cnt) {
+                    jl = col[e0 + lane];
+                    al = pI * val[e0 + lane];
+                }
+#pragma unroll 4
+                for (int q = 0; q < cnt; ++q) {
+                    const int j = __shfl_sync(0xffffffffu, jl, q);
+                    const double a = __shfl_sync(0xffffffffu, al, q);
+                    const int4 pc = prow_c[j];
+                    const double4 pw = prow_w[j];
+                    const double w0 = (pc.x == J0 ? pw.x : 0.0) + (pc.y == J0 ? pw.y : 0.0) + (pc.z == J0 ? pw.z : 0.0);
+                    acc0 = fma(a, w0, acc0);
+                    if (m > 32) {
+                        const double w1 = (pc.x == J1 ? pw.x : 0.0) + (pc.y == J1 ? pw.y : 0.0) + (pc.z == J1 ? pw.z : 0.0);
+                        acc1 = fma(a, w1, acc1);
+                    }
+                }
+            }
+        }
+    }
+    if (lane < m) cval[c0 + lane] = acc0;
+    if (lane + 32 < m) cval[c0 + 32 + lane] = acc1;
+}
+
 // ---------------------------------------------------------------------------
 // K7: coarsest level.  Dense row-major npad x npad (npad multiple of 32,
 // padding = identity), blocked right-looking Cholesky with 32-wide panels:
@@ -813,7 +876,7 @@ void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* 
 
 }  // namespace
 
-int galerkin_max_row() { return kGalMaxM; }
+int galerkin_max_row() { return 64; }
 
 void init_setup_attributes() {
     const int big = 200 * 1024;
@@ -857,6 +920,13 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
 }
 int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s) {
     const int nc = coarse.n;
+    if (coarse.gal2 && fine.prow_c.p && !getenv("MG_GAL_V2")) {
+        k_galerkin3<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
+            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
+            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fine.val.p,
+            reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
+        return 1;
+    }
     if (coarse.gal2 && fine.prow_c.p) {
         k_galerkin2<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
             nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
