@@ -211,65 +211,52 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 //   * children come with their fine-row extents {i, start, len} (no
 //     dependent row-pointer load) and weights P[i,I];
 //   * the coarse row's column list is hashed into shared memory (open
-//     addressing, 2 probes on average instead of a ~5-step binary search);
+//     addressing, ~2 probes instead of a ~5-step binary search);
 //   * every lane handles two (child, nonzero) pairs per step; for each the
 //     P row of the column j is one packed 48-byte record {c0..c2, w0..w2}
-//     (two vector loads) instead of six scattered scalars.
-// Accumulation order per slot is fixed by (step, lane, q), so repeated
-// rebuilds are bitwise identical.
+//     (two vector loads) instead of six scattered scalars;
+//   * rows with <= 32 entries accumulate into LANE-PRIVATE shared-memory
+//     copies acc[lane][slot] (no atomics: fp64 atomicAdd on shared memory is
+//     a CAS spin loop here), summed over lanes in fixed order at the end.
+//     Wider rows fall back to shared atomics on one copy.
+// Deterministic: every sum is taken in a fixed order.
 constexpr int kHash = 256;   // power of two > 2 * kGalMaxM
+constexpr int kGal2Warps = 4;
+constexpr int kPriv = 33;    // padded row of the private accumulators
 
 __device__ __forceinline__ unsigned hslot(int J) { return ((unsigned)J * 2654435761u) >> (32 - 8); }
 
-// acc[slot] += v for every valid lane, deterministic and without atomics:
-// lanes with equal slots are grouped (match.any), the lowest lane of each
-// group sums its peers' values in lane order and does a plain update (one
-// writer per slot per call).  fp64 atomicAdd on shared memory would be a
-// CAS spin loop on this architecture.
-__device__ __forceinline__ void warp_accumulate(double* acc, bool valid, int slot, double v, int lane) {
-    const int key = valid ? slot : (1 << 20) + lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int gsize = __popc(peers);
-    int maxg = gsize;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) maxg = max(maxg, __shfl_xor_sync(0xffffffffu, maxg, off));
-    unsigned rest = peers;
-    double sum = 0.0;
-    for (int t = 0; t < maxg; ++t) {
-        const int src = rest ? __ffs(rest) - 1 : lane;
-        const double vv = __shfl_sync(0xffffffffu, v, src);
-        if (rest) sum += vv;
-        rest &= rest - 1;
-    }
-    if (valid && lane == __ffs(peers) - 1) acc[slot] += sum;
-    __syncwarp();
-}
-
-__global__ void __launch_bounds__(kGalWarps * 32) k_galerkin2(
+__global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
     int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
     double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
     const double* __restrict__ cw, const int* __restrict__ col, const double* __restrict__ val,
     const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
-    __shared__ double acc[kGalWarps][kGalMaxM];
-    __shared__ int hkey[kGalWarps][kHash];
-    __shared__ unsigned char hval[kGalWarps][kHash];
-    __shared__ int ch_start[kGalWarps][32];
-    __shared__ int ch_scan[kGalWarps][32];
-    __shared__ double ch_w[kGalWarps][32];
+    __shared__ double accp[kGal2Warps][32 * kPriv];   // private copies (m <= 32) or one shared copy (m <= 96)
+    __shared__ int hkey[kGal2Warps][kHash];
+    __shared__ unsigned char hval[kGal2Warps][kHash];
+    __shared__ int ch_start[kGal2Warps][32];
+    __shared__ int ch_scan[kGal2Warps][32];
+    __shared__ double ch_w[kGal2Warps][32];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kGalWarps + w;
+    const int gw = blockIdx.x * kGal2Warps + w;
     if (gw >= nc) return;
     const int I = order[gw];
     const int c0 = crp[I];
     const int m = crp[I + 1] - c0;
+    const bool priv = m <= 32;
+    double* mine = priv ? &accp[w][lane * kPriv] : &accp[w][0];
     for (int h = lane; h < kHash; h += 32) hkey[w][h] = -1;
-    for (int s = lane; s < m; s += 32) acc[w][s] = 0.0;
+    if (priv) {
+        for (int s2 = 0; s2 < m; ++s2) mine[s2] = 0.0;
+    } else {
+        for (int s2 = lane; s2 < m; s2 += 32) accp[w][s2] = 0.0;
+    }
     __syncwarp();
-    for (int s = lane; s < m; s += 32) {
-        const int J = ccol[c0 + s];
+    for (int s2 = lane; s2 < m; s2 += 32) {
+        const int J = ccol[c0 + s2];
         unsigned h = hslot(J);
         while (atomicCAS(&hkey[w][h], -1, J) != -1) h = (h + 1) & (kHash - 1);
-        hval[w][h] = (unsigned char)s;
+        hval[w][h] = (unsigned char)s2;
     }
     __syncwarp();
     const int t0 = cptr[I], t1 = cptr[I + 1];
@@ -325,27 +312,35 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin2(
             }
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
+                if (!ok[u]) continue;
                 const int Js[3] = {pc[u].x, pc[u].y, pc[u].z};
                 const double ws[3] = {pw[u].x, pw[u].y, pw[u].z};
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    const bool valid = ok[u] && ws[q] != 0.0;
-                    int slot = -1;
-                    if (valid) {
-                        unsigned h = hslot(Js[q]);
-                        while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
-                        slot = hval[w][h];
-                    }
-                    warp_accumulate(acc[w], valid, slot, a[u] * ws[q], lane);
+                    if (ws[q] == 0.0) continue;
+                    unsigned h = hslot(Js[q]);
+                    while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
+                    const int slot = hval[w][h];
+                    if (priv) mine[slot] += a[u] * ws[q];
+                    else atomicAdd(&accp[w][slot], a[u] * ws[q]);
                 }
             }
         }
         __syncwarp();
     }
-    for (int s = lane; s < m; s += 32) cval[c0 + s] = acc[w][s];
+    __syncwarp();
+    if (priv) {
+        if (lane < m) {
+            double sum = 0.0;
+            for (int l = 0; l < 32; ++l) sum += accp[w][l * kPriv + lane];
+            cval[c0 + lane] = sum;
+        }
+    } else {
+        for (int s2 = lane; s2 < m; s2 += 32) cval[c0 + s2] = accp[w][s2];
+    }
 }
 
-// K2 v3 (default): slot-owner formulation, atomic-free and deterministic.
+// K2 v3 (MG_GAL_V3=1, measured slower): slot-owner formulation, atomic-free and deterministic.
 // One warp per coarse row I; lane l owns coarse columns J_l = col(I, l) and
 // J_l' = col(I, l + 32).  The warp walks every (child i, neighbour j) pair of
 // the row in lockstep: (j, p_iI a_ij) is broadcast from the lane that loaded
@@ -876,7 +871,7 @@ void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* 
 
 }  // namespace
 
-int galerkin_max_row() { return 64; }
+int galerkin_max_row() { return 64; }   // v2 private rows <= 32, shared copy <= 96; v3 <= 64
 
 void init_setup_attributes() {
     const int big = 200 * 1024;
@@ -920,7 +915,7 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
 }
 int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s) {
     const int nc = coarse.n;
-    if (coarse.gal2 && fine.prow_c.p && !getenv("MG_GAL_V2")) {
+    if (coarse.gal2 && fine.prow_c.p && getenv("MG_GAL_V3")) {
         k_galerkin3<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
             nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
             reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fine.val.p,
@@ -928,7 +923,7 @@ int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s) {
         return 1;
     }
     if (coarse.gal2 && fine.prow_c.p) {
-        k_galerkin2<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
+        k_galerkin2<<<nblk(nc, kGal2Warps), kGal2Warps * 32, 0, s>>>(
             nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
             reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fine.val.p,
             reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
