@@ -125,6 +125,30 @@ int mg_apply_mass(mg_ctx* ctx, int32_t k, const double* X, double* B);
 int mg_solve(mg_ctx* ctx, int32_t k, const double* B, double* X, double rel_tol, int32_t max_cycles,
              double* res_hist, int32_t* cycles_out);
 
+/* ---- fast data smoothing (App. D) -------------
+ * The data-smoothing system (alpha Q + (1 - alpha) M) x = (1 - alpha) M f
+ * (App. D eq. 1) has coarse operators
+ *     P^T A(alpha) P = alpha (P^T Q P) + (1 - alpha) (P^T M P)
+ * (App. D eq. 2), so P^T Q P and P^T M P are precomputed once per level and
+ * every later alpha costs one scaled sparse addition per level plus the
+ * coarsest refactorisation: no triple product runs in the alpha loop. */
+
+/* Set Q and M on ONE fine CSR pattern (user order; an entry absent from one
+ * operator is stored as 0 in it), host or device arrays, copied.  Pattern
+ * requirements as mg_set_matrix.  Computes P^T Q P and P^T M P at every
+ * level on the GPU.  The system matrix is NOT set until mg_set_alpha.
+ * Errors: as mg_set_matrix (except MG_ERR_NOT_SPD). */
+int mg_set_matrix_split(mg_ctx* ctx, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col,
+                        const double* q_val, const double* m_val);
+/* As mg_set_matrix_split with Q = L (cotan Laplacian, reading A13) and M =
+ * lumped mass (A14) assembled on the GPU from positions V [n_verts[0]][3]
+ * (host or device) over F[0]; M is kept for mg_apply_mass. */
+int mg_set_matrix_split_cotan(mg_ctx* ctx, const double* V);
+/* A_h = alpha Q_h + (1 - alpha) M_h at every level (App. D eq. 2), then the
+ * coarsest Cholesky.  Errors: MG_ERR_STATE (no split operators),
+ * MG_ERR_INVALID_ARG (alpha not finite), MG_ERR_NOT_SPD, MG_ERR_CUDA. */
+int mg_set_alpha(mg_ctx* ctx, double alpha);
+
 /* ---- exports for parity checks (host arrays, USER vertex order) ---------- */
 
 /* Level l sizes: rows, stored entries, colours of Alg. 3.  MG_ERR_STATE
@@ -168,7 +192,8 @@ int mg_set_profiling(mg_ctx* ctx, int class_mask);
 /* Accumulated device milliseconds and kernel launches per (kernel class, level):
  * classes 0 gs_sweep, 1 residual+restrict, 2 prolong, 3 coarse_solve,
  * 4 resnorm, 5 galerkin, 6 assembly, 7 factor, 8 permute, 9 coarse_tail (the
- * single-launch cluster kernel that runs the V-cycle on the small levels).  ms[cls*16 + l],
+ * single-launch cluster kernel that runs the V-cycle on the small levels),
+ * 10 alpha (the App. D per-level scaled addition of mg_set_alpha).  ms[cls*16 + l],
  * launches[cls*16 + l] (levels >= 16 fold into 15).  Resets the counters. */
 int mg_get_profile(mg_ctx* ctx, double* ms, int64_t* launches);
 /* Device kernel launches issued by this context since creation. */

@@ -184,6 +184,7 @@ struct mg_ctx {
     int pattern_kind = -1;   // 0 user CSR, 1 cotan 1-ring
     bool have_matrix = false;
     bool have_mass = false;
+    bool have_split = false;         // App. D: Q_l, M_l stored at every level
 
     std::vector<int32_t> opp_user;   // cotan: 2 opposite vertices per user nnz (-1 none)
     DBuf<int32_t> opp;               // internal
@@ -203,7 +204,7 @@ struct mg_ctx {
 
     DBuf<double> partial, bnorm, rho;
     double* h_rho = nullptr;         // pinned, kMaxK
-    DBuf<double> stageB, stageX, stageVal;
+    DBuf<double> stageB, stageX, stageVal, stageVal2;
     DBuf<int32_t> stageRp, stageCol;
 
     cudaGraphExec_t vc_exec[kMaxK + 1] = {};
@@ -539,11 +540,9 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
     return MG_OK;
 }
 
-// Coarse operators for every level (K2) and the coarsest factorisation (K7).
-int rebuild_hierarchy(mg_ctx* c) {
+// Coarsest factorisation (K7a) of the current A_H, then synchronise and check the pivots.
+int factor_coarsest(mg_ctx* c) {
     cudaStream_t s = c->stream;
-    for (int l = 0; l < c->H; ++l)
-        c->timed(PC_GALERKIN, l, s, [&] { return launch_galerkin(*c->lv[l], *c->lv[l + 1], s); });
     Level& LH = *c->lv[c->H];
     cudaError_t e = cudaMemsetAsync(c->errflag.p, 0, sizeof(int), s);
     if (e) return c->cuda_fail(e, "factor");
@@ -565,6 +564,43 @@ int rebuild_hierarchy(mg_ctx* c) {
     c->harvest_events();
     c->have_matrix = !flag;
     if (flag) return c->fail(MG_ERR_NOT_SPD, "coarsest level (n=%d): non-positive Cholesky pivot", LH.n);
+    return MG_OK;
+}
+
+// Coarse operators for every level (K2, Eq. gca) and the
+// coarsest factorisation (K7a).
+int rebuild_hierarchy(mg_ctx* c) {
+    cudaStream_t s = c->stream;
+    for (int l = 0; l < c->H; ++l)
+        c->timed(PC_GALERKIN, l, s, [&] {
+            return launch_galerkin(*c->lv[l], c->lv[l]->val.p, *c->lv[l + 1], c->lv[l + 1]->val.p, s);
+        });
+    return factor_coarsest(c);
+}
+
+// App. D: Galerkin of the two split operators Q and M separately
+// (level 0 values already in lv[0]->qv / mv), so that any A(alpha) later is a
+// scaled addition per level.
+int split_hierarchy(mg_ctx* c) {
+    cudaStream_t s = c->stream;
+    for (int l = 0; l <= c->H; ++l) {
+        Level& L = *c->lv[l];
+        cudaError_t e;
+        if ((e = L.qv.alloc(std::max<int64_t>(L.nnz, 1) + 8)) || (e = L.mv.alloc(std::max<int64_t>(L.nnz, 1) + 8)))
+            return c->cuda_fail(e, "split operator alloc");
+    }
+    for (int l = 0; l < c->H; ++l)
+        c->timed(PC_GALERKIN, l, s, [&] {
+            Level& F = *c->lv[l];
+            Level& C = *c->lv[l + 1];
+            return launch_galerkin(F, F.qv.p, C, C.qv.p, s) + launch_galerkin(F, F.mv.p, C, C.mv.p, s);
+        });
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (!e) e = cudaGetLastError();
+    if (e) return c->cuda_fail(e, "split Galerkin");
+    c->harvest_events();
+    c->have_split = true;
+    c->have_matrix = false;
     return MG_OK;
 }
 
@@ -817,14 +853,13 @@ int mg_hierarchy_load(mg_ctx* c, int n_levels, const int32_t* n_verts, const int
     return MG_OK;
 }
 
-int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const double* val,
-                  int on_device) {
-    int rc = check_state(c, false);
-    if (rc) return rc;
-    if (!row_ptr || !col || !val || nnz < 0) return c->fail(MG_ERR_INVALID_ARG, "null CSR array or nnz < 0");
+// Validate a user CSR pattern (host or device arrays) and run the pattern
+// setup when it differs from the cached one.
+static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col) {
+    int rc;
+    if (!row_ptr || !col || nnz < 0) return c->fail(MG_ERR_INVALID_ARG, "null CSR array or nnz < 0");
     if (n != c->lv[0]->n) return c->fail(MG_ERR_SHAPE, "n = %d but the hierarchy's finest level has %d", n, c->lv[0]->n);
     if (nnz > INT32_MAX) return c->fail(MG_ERR_SHAPE, "nnz exceeds int32");
-    (void)on_device;
     const bool dev = is_device_ptr(row_ptr);
     std::vector<int32_t> rp(n + 1), cl(nnz);
     cudaError_t e;
@@ -862,18 +897,31 @@ int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, con
         c->pattern_hash = h;
         c->pattern_kind = 0;
     }
+    return MG_OK;
+}
+
+int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const double* val,
+                  int on_device) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!val) return c->fail(MG_ERR_INVALID_ARG, "null CSR value array");
+    (void)on_device;
+    if ((rc = load_csr_pattern(c, n, nnz, row_ptr, col))) return rc;
     const double* dval = nullptr;
     rc = to_device(c, val, c->stageVal, (size_t)nnz, &dval);
     if (rc) return rc;
     Level& L0 = *c->lv[0];
     c->timed(PC_PERMUTE, 0, c->stream, [&] { return launch_gather_vals(L0.di2u.p, dval, L0.val.p, nnz, c->stream); });
     c->have_mass = false;
+    c->have_split = false;
     return rebuild_hierarchy(c);
 }
 
-int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double lap_coeff) {
-    int rc = check_state(c, false);
-    if (rc) return rc;
+// 1-ring pattern of F[0] with the opposite-vertex table of every edge
+// (pattern setup on first use), then the positions gathered into internal
+// order as 32-byte rows in c->Vint.
+static int load_cotan_pattern(mg_ctx* c, const double* V) {
+    int rc;
     if (!V) return c->fail(MG_ERR_INVALID_ARG, "V is null");
     if (c->nF0 <= 0) return c->fail(MG_ERR_STATE, "the hierarchy has no fine faces F[0]");
     Level& L0 = *c->lv[0];
@@ -951,13 +999,73 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
     const double* dV = nullptr;
     rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV);
     if (rc) return rc;
+    c->timed(PC_ASSEMBLY, 0, c->stream, [&] { return launch_gather_rows(3, L0.dperm.p, dV, c->Vint.p, n, c->stream); });
+    return MG_OK;
+}
+
+int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double lap_coeff) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if ((rc = load_cotan_pattern(c, V))) return rc;
+    Level& L0 = *c->lv[0];
+    const int32_t n = L0.n;
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
-        return launch_gather_rows(3, L0.dperm.p, dV, c->Vint.p, n, c->stream) +
-               launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, c->Mint.p, c->stream) +
+        return launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, L0.val.p, c->Mint.p, c->stream) +
                launch_scatter_vec(L0.dperm.p, c->Mint.p, c->Muser.p, n, c->stream);
     });
     c->have_mass = true;
+    c->have_split = false;
     return rebuild_hierarchy(c);
+}
+
+int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col,
+                        const double* q_val, const double* m_val) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!q_val || !m_val) return c->fail(MG_ERR_INVALID_ARG, "null Q or M value array");
+    if ((rc = load_csr_pattern(c, n, nnz, row_ptr, col))) return rc;
+    Level& L0 = *c->lv[0];
+    cudaError_t e;
+    if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)))
+        return c->cuda_fail(e, "split operator alloc");
+    const double* dq = nullptr;
+    if ((rc = to_device(c, q_val, c->stageVal, (size_t)nnz, &dq))) return rc;
+    c->timed(PC_PERMUTE, 0, c->stream, [&] { return launch_gather_vals(L0.di2u.p, dq, L0.qv.p, nnz, c->stream); });
+    const double* dm = nullptr;
+    if ((rc = to_device(c, m_val, c->stageVal2, (size_t)nnz, &dm))) return rc;
+    c->timed(PC_PERMUTE, 0, c->stream, [&] { return launch_gather_vals(L0.di2u.p, dm, L0.mv.p, nnz, c->stream); });
+    c->have_mass = false;
+    return split_hierarchy(c);
+}
+
+int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if ((rc = load_cotan_pattern(c, V))) return rc;
+    Level& L0 = *c->lv[0];
+    cudaError_t e;
+    if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)))
+        return c->cuda_fail(e, "split operator alloc");
+    c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
+        return launch_cotan(L0, c->opp.p, c->Vint.p, 0.0, 1.0, L0.qv.p, c->Mint.p, c->stream) +
+               launch_cotan(L0, c->opp.p, c->Vint.p, 1.0, 0.0, L0.mv.p, c->Mint.p, c->stream) +
+               launch_scatter_vec(L0.dperm.p, c->Mint.p, c->Muser.p, L0.n, c->stream);
+    });
+    c->have_mass = true;
+    return split_hierarchy(c);
+}
+
+int mg_set_alpha(mg_ctx* c, double alpha) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!c->have_split) return c->fail(MG_ERR_STATE, "no split operators (call mg_set_matrix_split*)");
+    if (!std::isfinite(alpha)) return c->fail(MG_ERR_INVALID_ARG, "alpha must be finite");
+    cudaStream_t s = c->stream;
+    for (int l = 0; l <= c->H; ++l) {
+        Level& L = *c->lv[l];
+        c->timed(PC_ALPHA, l, s, [&] { return launch_axpby(L.qv.p, L.mv.p, alpha, 1.0 - alpha, L.val.p, L.nnz, s); });
+    }
+    return factor_coarsest(c);
 }
 
 int mg_apply_mass(mg_ctx* c, int32_t k, const double* X, double* B) {

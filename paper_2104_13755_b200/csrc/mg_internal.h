@@ -11,12 +11,12 @@
 namespace mg {
 
 constexpr int kMaxK = 4;          // right-hand sides per solve supported by the kernels
-constexpr int kProfClasses = 10;  // see mg.h mg_get_profile
+constexpr int kProfClasses = 11;  // see mg.h mg_get_profile
 constexpr int kProfLevels = 16;
 
 enum ProfClass {
     PC_GS = 0, PC_RESTRICT = 1, PC_PROLONG = 2, PC_COARSE = 3, PC_RESNORM = 4,
-    PC_GALERKIN = 5, PC_ASSEMBLY = 6, PC_FACTOR = 7, PC_PERMUTE = 8, PC_TAIL = 9
+    PC_GALERKIN = 5, PC_ASSEMBLY = 6, PC_FACTOR = 7, PC_PERMUTE = 8, PC_TAIL = 9, PC_ALPHA = 10
 };
 
 // Device buffer owned by the context.
@@ -78,6 +78,7 @@ struct Level {
 
     DBuf<int32_t> rp, col;                // internal CSR pattern
     DBuf<double> val;                     // internal values
+    DBuf<double> qv, mv;                  // App. D split operators Q_l, M_l (internal order, same pattern)
     DBuf<int32_t> pc;                     // P_l SoA [3][n], coarse internal column
     DBuf<double> pw;                      // P_l SoA [3][n]
     DBuf<int32_t> cptr, cidx;             // transpose of P_{l-1} (this level coarse): children
@@ -158,10 +159,12 @@ int launch_gather_rows(int K, const int32_t* perm, const double* src_user, doubl
 int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
 int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
-                 double* M_int, cudaStream_t s);
+                 double* val, double* M_int, cudaStream_t s);
+int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, double* out, int64_t nnz,
+                 cudaStream_t s);
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);
 int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
-int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s);
+int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s);
 int galerkin_max_row();
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);

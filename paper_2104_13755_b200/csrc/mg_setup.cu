@@ -109,6 +109,23 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
     if (ediag >= 0) val[ediag] = mass_coeff * m + lap_coeff * (-lsum);
 }
 
+// ---------------------------------------------------------------------------
+// App. D: A_h(alpha) = alpha Q_h + (1 - alpha) M_h on one level's
+// value array (identical patterns), a scaled sparse addition with 16-byte
+// loads; no triple product.  Grid-stride over pairs of entries.
+__global__ void __launch_bounds__(kBlock) k_axpby(const double* __restrict__ Q, const double* __restrict__ M,
+                                                  double alpha, double beta, double* __restrict__ out, int64_t nnz) {
+    const int64_t n2 = nnz / 2;
+    const double2* Q2 = reinterpret_cast<const double2*>(Q);
+    const double2* M2 = reinterpret_cast<const double2*>(M);
+    double2* O2 = reinterpret_cast<double2*>(out);
+    for (int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x; t < n2; t += (int64_t)gridDim.x * kBlock) {
+        const double2 q = __ldcs(Q2 + t), m = __ldcs(M2 + t);
+        O2[t] = make_double2(alpha * q.x + beta * m.x, alpha * q.y + beta * m.y);
+    }
+    if ((nnz & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[nnz - 1] = alpha * Q[nnz - 1] + beta * M[nnz - 1];
+}
+
 __global__ void k_scatter_vec(const int* __restrict__ perm, const double* __restrict__ src, double* __restrict__ dst,
                               int n) {
     const int i = blockIdx.x * kBlock + threadIdx.x;
@@ -894,9 +911,9 @@ int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64
     return 1;
 }
 int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
-                 double* M_int, cudaStream_t s) {
+                 double* val, double* M_int, cudaStream_t s) {
     k_cotan_assemble<<<nblk(L0.n, kBlock), kBlock, 0, s>>>(L0.rp.p, L0.col.p, opp, Vint, mass_coeff, lap_coeff,
-                                                            L0.val.p, M_int, L0.n);
+                                                            val, M_int, L0.n);
     return 1;
 }
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s) {
@@ -913,25 +930,33 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
     k_scatter_vec<<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src_int, dst_user, n);
     return 1;
 }
-int launch_galerkin(const Level& fine, Level& coarse, cudaStream_t s) {
+int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s) {
     const int nc = coarse.n;
     if (coarse.gal2 && fine.prow_c.p && getenv("MG_GAL_V3")) {
         k_galerkin3<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
-            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
-            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fine.val.p,
+            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p,
+            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fval,
             reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
         return 1;
     }
     if (coarse.gal2 && fine.prow_c.p) {
         k_galerkin2<<<nblk(nc, kGal2Warps), kGal2Warps * 32, 0, s>>>(
-            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p,
-            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fine.val.p,
+            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p,
+            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fval,
             reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
         return 1;
     }
     k_galerkin<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
-        nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, coarse.val.p, coarse.cptr.p, coarse.cidx.p, coarse.cw.p,
-        fine.rp.p, fine.col.p, fine.val.p, fine.pc.p, fine.pw.p, fine.n);
+        nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p, coarse.cidx.p, coarse.cw.p,
+        fine.rp.p, fine.col.p, fval, fine.pc.p, fine.pw.p, fine.n);
+    return 1;
+}
+int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, double* out, int64_t nnz,
+                 cudaStream_t s) {
+    if (nnz <= 0) return 0;
+    const int64_t n2 = (nnz + 1) / 2;
+    const int grid = (int)std::min<int64_t>((n2 + kBlock - 1) / kBlock, 148 * 8);
+    k_axpby<<<grid, kBlock, 0, s>>>(Qv, Mv, alpha, beta, out, nnz);
     return 1;
 }
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s) {

@@ -52,6 +52,9 @@ def lib():
             "mg_set_matrix": (C.c_int, [_vp, i32, i64, _vp, _vp, _vp, C.c_int]),
             "mg_set_matrix_cotan": (C.c_int, [_vp, _vp, dbl, dbl]),
             "mg_apply_mass": (C.c_int, [_vp, i32, _vp, _vp]),
+            "mg_set_matrix_split": (C.c_int, [_vp, i32, i64, _vp, _vp, _vp, _vp]),
+            "mg_set_matrix_split_cotan": (C.c_int, [_vp, _vp]),
+            "mg_set_alpha": (C.c_int, [_vp, dbl]),
             "mg_solve": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_level_info": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
             "mg_get_level_csr": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
@@ -148,6 +151,19 @@ def mg_set_matrix(ctx, n, nnz, row_ptr, col, val, on_device=0):
 
 def mg_set_matrix_cotan(ctx, V, mass_coeff, lap_coeff):
     return _check(ctx, lib().mg_set_matrix_cotan(ctx, _ptr(V, np.float64), float(mass_coeff), float(lap_coeff)))
+
+
+def mg_set_matrix_split(ctx, n, nnz, row_ptr, col, q_val, m_val):
+    return _check(ctx, lib().mg_set_matrix_split(ctx, int(n), int(nnz), _ptr(row_ptr, np.int32), _ptr(col, np.int32),
+                                                 _ptr(q_val, np.float64), _ptr(m_val, np.float64)))
+
+
+def mg_set_matrix_split_cotan(ctx, V):
+    return _check(ctx, lib().mg_set_matrix_split_cotan(ctx, _ptr(V, np.float64)))
+
+
+def mg_set_alpha(ctx, alpha):
+    return _check(ctx, lib().mg_set_alpha(ctx, float(alpha)))
 
 
 def mg_apply_mass(ctx, k, X, B):
@@ -295,6 +311,15 @@ class Solver:
 
     def set_matrix_cotan(self, V, mass_coeff, lap_coeff):
         return mg_set_matrix_cotan(self.ctx, V, mass_coeff, lap_coeff)
+
+    def set_matrix_split(self, row_ptr, col, q_val, m_val):
+        return mg_set_matrix_split(self.ctx, self.n, col.shape[0], row_ptr, col, q_val, m_val)
+
+    def set_matrix_split_cotan(self, V):
+        return mg_set_matrix_split_cotan(self.ctx, V)
+
+    def set_alpha(self, alpha):
+        return mg_set_alpha(self.ctx, alpha)
 
     def apply_mass(self, X, B):
         k = 1 if X.ndim == 1 else X.shape[1]

@@ -279,3 +279,66 @@ def test_launch_modes_agree(ora, monkeypatch):
         S.close()
     assert np.array_equal(out["default"], out["nopdl"])
     assert np.array_equal(out["default"], out["nopipe"])
+
+
+@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
+def test_fast_alpha_sweep_matches_slow_path(ora, cid, kw):
+    """SURVEY row f1 (App. D): P^T Q P and P^T M P precomputed once,
+    A_h(alpha) = alpha Q_h + (1 - alpha) M_h by scaled addition.  Every level
+    must equal the oracle's SLOW path (Galerkin of the assembled
+    A = alpha L + (1 - alpha) M, App. D eq. 1) to 1e-12, the solve of
+    (alpha L + (1 - alpha) M) x = (1 - alpha) M f must match, and the alpha
+    loop must run zero triple products (profile counter)."""
+    from paper_2104_13755_b200 import mg
+    p = meshgen.make_config(cid, **kw)
+    V, F = p.levels[0]
+    S = gpu_solver(p)
+    S.set_matrix_split_cotan(V)
+    mg.mg_set_profiling(S.ctx, ["galerkin", "alpha"])
+    mg.mg_get_profile(S.ctx)
+    f = np.random.default_rng(7).standard_normal((p.n, 1))
+    for alpha in (0.0, 0.1, 0.5, 0.9, 1e-4 / (1 + 1e-4)):
+        S.set_alpha(alpha)
+        A, M = ora.assemble(V, F, 1.0 - alpha, alpha)
+        mgo = ora.MG(p.sizes, p.P, A)
+        for l in range(len(p.sizes)):
+            check_level_parity(S, mgo, l)
+        B = np.ascontiguousarray((1.0 - alpha) * M[:, None] * f)
+        Xo, ho, _ = mgo.solve(B, rel_tol=0.0, max_cycles=4)
+        Xg = np.zeros_like(B)
+        rc, cyc, hg = S.solve(B, Xg, rel_tol=0.0, max_cycles=4)
+        check_x(Xg, Xo)
+        check_history(hg, ho, tau_floor(A.to_scipy(), Xo, B))
+    prof = mg.mg_get_profile(S.ctx)
+    assert "galerkin" not in prof, prof                       # no triple product in the alpha loop
+    assert sum(n for _, n in prof["alpha"].values()) == 5 * len(p.sizes)
+
+
+def test_split_csr_equals_split_cotan(ora):
+    """mg_set_matrix_split with user CSR (Q = L, M = diag mass on the same
+    pattern) gives the same operators as the GPU-assembled split path."""
+    import scipy.sparse as sp
+    from paper_2104_13755_b200 import mg
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    L, _ = ora.assemble(V, F, 0.0, 1.0)
+    _, M = ora.assemble(V, F, 1.0, 0.0)
+    Ls = L.to_scipy().tocsr()
+    Ls.sort_indices()
+    Ms = (Ls * 0 + sp.diags(M)).tocsr()
+    Ms.sort_indices()
+    assert np.array_equal(Ls.indptr, Ms.indptr) and np.array_equal(Ls.indices, Ms.indices)
+    S1 = gpu_solver(p)
+    S1.set_matrix_split(Ls.indptr.astype(np.int32), Ls.indices.astype(np.int32), Ls.data, Ms.data)
+    S2 = gpu_solver(p)
+    S2.set_matrix_split_cotan(V)
+    for alpha in (0.25, 0.75):
+        S1.set_alpha(alpha)
+        S2.set_alpha(alpha)
+        A, _ = ora.assemble(V, F, 1.0 - alpha, alpha)
+        mgo = ora.MG(p.sizes, p.P, A)
+        for l in range(len(p.sizes)):
+            check_level_parity(S1, mgo, l)
+            check_level_parity(S2, mgo, l)
+    with pytest.raises(mg.MGError):
+        gpu_solver(p).set_alpha(0.5)                          # MG_ERR_STATE: no split operators
