@@ -94,6 +94,13 @@ __device__ __forceinline__ void tile_row(const int* cs, const double* vs, int qb
     }
 }
 
+// gathers per batch in the pipelined tile kernel: one batch covers a whole
+// 1-ring row (7 entries incl. the skipped diagonal) for every K
+template <int K>
+struct PipeUnroll {
+    static constexpr int value = 8;
+};
+
 template <int K>
 struct Unroll {
     static constexpr int value = K == 1 ? 8 : 4;
@@ -297,18 +304,20 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
         const StageView v = view_tile(d, stage[sidx], cap);
         if (tid < d.nrow) {
             const int row = d.row0 + tid;
-            double s[K], dg;
-            stage_row<K, Unroll<K>::value>(v, tid, row, x, s, dg, xpol);
-            double bv[K];
+            // b (and the row's own x for the residual modes) go out before the
+            // neighbour gathers so all loads of the row share one round trip
+            double bv[K], xr[K];
             ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
+            if (MODE != 0) ldrow_pol<K>(x + (size_t)row * VS<K>::S, xr, xpol);
+            double s[K], dg;
+            stage_row<K, PipeUnroll<K>::value>(v, tid, row, x, s, dg, xpol);
             if (MODE == 0) {
                 double xn[K];
 #pragma unroll
                 for (int c = 0; c < K; ++c) xn[c] = (bv[c] - s[c]) / dg;
                 strow_pol<K>(x + (size_t)row * VS<K>::S, xn, xpol);
             } else {
-                double xr[K], rr[K];
-                ldrow_pol<K>(x + (size_t)row * VS<K>::S, xr, xpol);
+                double rr[K];
 #pragma unroll
                 for (int c = 0; c < K; ++c) rr[c] = bv[c] - fma(dg, xr[c], s[c]);
                 if (MODE == 1) {
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1) {
     constexpr int U = 32 / LPR;
-    constexpr int GB = (K >= 3) ? (U < 2 ? U : 2) : (U < 4 ? U : 4);
+    constexpr int GB = U <= 8 ? U : 8;   // gathers in flight per lane (one batch for LPR >= 4)
     const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
     const int lane = threadIdx.x & (LPR - 1);
     const int row = r0 + g;
@@ -377,6 +386,9 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     if (!active) return;   // whole groups leave together
     const unsigned mask = group_mask(LPR);
     const uint64_t xpol = evict_last_policy();
+    // the row's right-hand side goes out with the gathers (one round trip)
+    double bv[K];
+    if (lane == 0) ldrow<K>(b + (size_t)row * VS<K>::S, bv);
     double s[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = 0.0;
@@ -417,8 +429,7 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
     if (MODE == 0) d = group_sum<LPR>(d, mask);
     if (lane == 0) {
-        double bv[K], out[K];
-        ldrow<K>(b + (size_t)row * VS<K>::S, bv);
+        double out[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) out[c] = MODE == 0 ? (bv[c] - s[c]) / d : bv[c] - s[c];
         if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);

@@ -21,7 +21,7 @@ MG_OK, MG_ERR_INVALID_ARG, MG_ERR_SHAPE, MG_ERR_INPUT, MG_ERR_NOT_SPD, MG_ERR_ST
 STATUS_NAMES = ["MG_OK", "MG_ERR_INVALID_ARG", "MG_ERR_SHAPE", "MG_ERR_INPUT", "MG_ERR_NOT_SPD", "MG_ERR_STATE",
                 "MG_ERR_CUDA", "MG_ERR_NUMERIC", "MG_NOT_CONVERGED"]
 PROF_CLASSES = ["gs_sweep", "residual_restrict", "prolong", "coarse_solve", "resnorm", "galerkin", "assembly",
-                "factor", "permute", "coarse_tail"]
+                "factor", "permute", "coarse_tail", "alpha"]
 PROF_LEVELS = 16
 
 

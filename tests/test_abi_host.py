@@ -104,3 +104,14 @@ def test_symbolic_zero_weights_carry_no_structure(mglib):
     col1 = np.array([0, 1], np.int32)
     crp, ccol = mglib.mg_util_galerkin_pattern(rp1, col1, 2, Pc, Pw2)
     assert crp.tolist() == [0, 1, 2] and ccol.tolist() == [0, 1]
+
+
+def test_profile_classes_match_library():
+    """The binding's kernel-class list must match the library's enum (the
+    profile arrays are sized from it)."""
+    import re
+    from paper_2104_13755_b200 import mg
+    src = open(os.path.join(ROOT, "paper_2104_13755_b200", "csrc", "mg_internal.h")).read()
+    n = int(re.search(r"constexpr int kProfClasses = (\d+);", src).group(1))
+    enum = re.findall(r"PC_\w+ = (\d+)", src)
+    assert len(mg.PROF_CLASSES) == n == len(enum) == max(map(int, enum)) + 1
