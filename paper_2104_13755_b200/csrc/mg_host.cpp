@@ -548,9 +548,15 @@ int factor_coarsest(mg_ctx* c) {
     if (e) return c->cuda_fail(e, "factor");
     c->timed(PC_FACTOR, c->H, s, [&] {
         int n = launch_densify(LH, c->D.p, c->npad, s);
-        const int nc = (c->coarse_mode == 1 && !getenv("MG_CHOL_LAUNCHES"))
-                           ? launch_chol_cluster(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s)
-                           : -1;
+        // default: one cooperative launch (factor + inverse); MG_CHOL=cluster
+        // selects the single-cluster kernel, MG_CHOL_LAUNCHES per-panel launches
+        const char* mode = getenv("MG_CHOL");
+        int nc = -1;
+        if (c->coarse_mode == 1 && !getenv("MG_CHOL_LAUNCHES")) {
+            if (!mode || std::string(mode) == "grid")
+                nc = launch_chol_grid(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s);
+            if (nc < 0) nc = launch_chol_cluster(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s);
+        }
         if (nc > 0) return n + nc;
         n += launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
         if (c->coarse_mode == 1) n += launch_chol_inverse(c->D.p, c->Linv.p, c->npad, c->Ainv.p, s);

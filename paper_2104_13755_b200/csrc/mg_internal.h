@@ -169,6 +169,7 @@ int galerkin_max_row();
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);
+int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s);
 int launch_chol_cluster(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s);
 
 }  // namespace mg

@@ -872,6 +872,257 @@ __global__ void __launch_bounds__(512) k_chol_inverse(const double* __restrict__
     for (int i = tid; i < npad * kInvCols; i += 512) Z[(size_t)(i / kInvCols) * npad + c0 + (i % kInvCols)] = Y[i];
 }
 
+// ---------------------------------------------------------------------------
+// K7a v3 (default): Cholesky factor AND explicit inverse of A_H in ONE
+// cooperative launch over up to one CTA per SM; dependent phases are
+// separated by a software grid barrier (monotone counter, co-residency
+// guaranteed by the cooperative launch).  32x32 tiles, 256 threads per CTA,
+// every tile product register-blocked 2x2 per thread from shared memory.
+//   factor (right-looking, 2 barriers per panel k):
+//     P1  L_ik = A_ik L_kk^{-T} for i > k (one tile product with the
+//         inverse of the diagonal block, computed when L_kk was factored);
+//     P2  A_ij -= L_ik L_jk^T for k < j <= i; the CTA that owns tile
+//         (k+1, k+1) takes it first and immediately factors it (one warp,
+//         column by column) and inverts it, so panel k+1 is ready at the
+//         barrier;
+//   W = L^{-1} (right-looking, 1 barrier per step k): T_ij += L_ik W_kj for
+//     i > k >= j, and the task of block row k+1 finishes W_{k+1,j} =
+//     -L_{k+1,k+1}^{-1} T_{k+1,j} right after its last accumulation;
+//   Z = A_H^{-1} = W^T W (lower tiles, mirrored) for the per-cycle GEMV.
+// The factor L (lower triangle of D) and the diagonal-block inverses (Linv)
+// are kept for mg_get_coarse_factor and the one-CTA triangular solve.
+constexpr int kCgThreads = 256;
+
+__device__ __forceinline__ void gbar(unsigned* ctr, unsigned& target) {
+    __syncthreads();
+    target += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// S = 32x32 tile at G (row-major, leading dimension ld), transposed if T; through L2.
+template <bool T>
+__device__ __forceinline__ void cg_load(double (*S)[33], const double* G, int ld) {
+    for (int q = threadIdx.x; q < 1024; q += kCgThreads) {
+        const int r = q >> 5, c = q & 31;
+        const double v = __ldcg(G + (size_t)r * ld + c);
+        if (T) S[c][r] = v;
+        else S[r][c] = v;
+    }
+}
+
+// acc[2x2 block of thread] += As * Bs  (As[r][p], Bs[p][c])
+__device__ __forceinline__ void cg_mma(double (&acc)[4], const double (*As)[33], const double (*Bs)[33]) {
+    const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+#pragma unroll 8
+    for (int p = 0; p < 32; ++p) {
+        const double a0 = As[r0][p], a1 = As[r0 + 1][p];
+        const double b0 = Bs[p][c0], b1 = Bs[p][c0 + 1];
+        acc[0] = fma(a0, b0, acc[0]);
+        acc[1] = fma(a0, b1, acc[1]);
+        acc[2] = fma(a1, b0, acc[2]);
+        acc[3] = fma(a1, b1, acc[3]);
+    }
+}
+
+__device__ __forceinline__ void cg_store(double* G, int ld, const double (&v)[4]) {
+    const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+    G[(size_t)r0 * ld + c0] = v[0];
+    G[(size_t)r0 * ld + c0 + 1] = v[1];
+    G[(size_t)(r0 + 1) * ld + c0] = v[2];
+    G[(size_t)(r0 + 1) * ld + c0 + 1] = v[3];
+}
+__device__ __forceinline__ void cg_fetch(const double* G, int ld, double (&v)[4]) {
+    const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+    v[0] = __ldcg(G + (size_t)r0 * ld + c0);
+    v[1] = __ldcg(G + (size_t)r0 * ld + c0 + 1);
+    v[2] = __ldcg(G + (size_t)(r0 + 1) * ld + c0);
+    v[3] = __ldcg(G + (size_t)(r0 + 1) * ld + c0 + 1);
+}
+
+// Factor the SPD 32x32 tile S in place (lower triangle, warp 0, lane = row)
+// and write its inverse to Li; then every thread stores L (upper part of the
+// tile zeroed) to D and Li to Linv_k and to W_kk.
+__device__ void cg_factor_diag(double (*S)[33], double (*Li)[33], double* Dkk, double* Linvk, double* Wkk, int npad,
+                               int* err) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        for (int p = 0; p < 32; ++p) {
+            double d = S[p][p];
+            if (!(d > 0.0)) {
+                if (lane == 0) atomicExch(err, 1);
+                d = 1.0;
+            }
+            d = sqrt(d);
+            __syncwarp();
+            if (lane == p) S[p][p] = d;
+            if (lane > p) S[lane][p] /= d;
+            __syncwarp();
+            if (lane > p) {
+                const double lrp = S[lane][p];
+                for (int c = p + 1; c <= lane; ++c) S[lane][c] -= lrp * S[c][p];
+            }
+            __syncwarp();
+        }
+        // column `lane` of L^{-1} by forward substitution (zero above the diagonal)
+        double xv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            double sacc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+            for (int q = 0; q < i; ++q) sacc -= S[i][q] * xv[q];
+            xv[i] = sacc / S[i][i];
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) Li[i][lane] = xv[i];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < 1024; q += kCgThreads) {
+        const int r = q >> 5, c = q & 31;
+        Dkk[(size_t)r * npad + c] = c <= r ? S[r][c] : 0.0;
+        Linvk[q] = Li[r][c];
+        Wkk[(size_t)r * npad + c] = Li[r][c];
+    }
+}
+
+__global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D, double* __restrict__ Linv,
+                                                          double* __restrict__ W, double* __restrict__ Z, int npad,
+                                                          int* err, unsigned* ctr) {
+    __shared__ double As[32][33];
+    __shared__ double Bs[32][33];
+    const int nb = npad / 32;
+    unsigned target = 0;
+    // W lower off-diagonal tiles start at 0 (they accumulate T_ij)
+    for (int t = blockIdx.x; t < nb * (nb - 1) / 2; t += gridDim.x) {
+        int ti = (int)((sqrt(8.0 * t + 1.0) + 1.0) * 0.5);
+        while (ti * (ti - 1) / 2 > t) --ti;
+        while ((ti + 1) * ti / 2 <= t) ++ti;
+        const int tj = t - ti * (ti - 1) / 2;
+        const double zero[4] = {0.0, 0.0, 0.0, 0.0};
+        cg_store(W + (size_t)(ti * 32) * npad + tj * 32, npad, zero);
+    }
+    if (blockIdx.x == 0) {
+        cg_load<false>(As, D, npad);
+        __syncthreads();
+        cg_factor_diag(As, Bs, D, Linv, W, npad, err);
+    }
+    gbar(ctr, target);
+    // ---- factor
+    for (int k = 0; k + 1 < nb; ++k) {
+        const int m = nb - k - 1;
+        for (int t = blockIdx.x; t < m; t += gridDim.x) {   // P1: panel solve
+            const int i = k + 1 + t;
+            __syncthreads();
+            cg_load<false>(As, D + (size_t)(i * 32) * npad + k * 32, npad);
+            cg_load<true>(Bs, Linv + (size_t)k * 1024, 32);
+            __syncthreads();
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            cg_mma(acc, As, Bs);
+            cg_store(D + (size_t)(i * 32) * npad + k * 32, npad, acc);
+        }
+        gbar(ctr, target);
+        const int ntile = m * (m + 1) / 2;
+        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {   // P2: trailing update
+            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            while (ti * (ti + 1) / 2 > t) --ti;
+            const int tj = t - ti * (ti + 1) / 2;
+            const int bi = k + 1 + ti, bj = k + 1 + tj;
+            __syncthreads();
+            cg_load<false>(As, D + (size_t)(bi * 32) * npad + k * 32, npad);
+            cg_load<true>(Bs, D + (size_t)(bj * 32) * npad + k * 32, npad);
+            __syncthreads();
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            cg_mma(acc, As, Bs);
+            double* C = D + (size_t)(bi * 32) * npad + bj * 32;
+            double cv[4];
+            cg_fetch(C, npad, cv);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cv[e] -= acc[e];
+            if (t == 0) {   // tile (k+1, k+1): factor it now for panel k+1
+                __syncthreads();
+                const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+                As[r0][c0] = cv[0];
+                As[r0][c0 + 1] = cv[1];
+                As[r0 + 1][c0] = cv[2];
+                As[r0 + 1][c0 + 1] = cv[3];
+                __syncthreads();
+                const int kk = k + 1;
+                cg_factor_diag(As, Bs, D + (size_t)(kk * 32) * npad + kk * 32, Linv + (size_t)kk * 1024,
+                               W + (size_t)(kk * 32) * npad + kk * 32, npad, err);
+            } else {
+                cg_store(C, npad, cv);
+            }
+        }
+        gbar(ctr, target);
+    }
+    // ---- W = L^{-1}
+    for (int k = 0; k + 1 < nb; ++k) {
+        const int m = nb - k - 1, w = k + 1;
+        for (int t = blockIdx.x; t < m * w; t += gridDim.x) {
+            const int i = k + 1 + t / w, j = t % w;
+            __syncthreads();
+            cg_load<false>(As, D + (size_t)(i * 32) * npad + k * 32, npad);   // L_ik
+            cg_load<false>(Bs, W + (size_t)(k * 32) * npad + j * 32, npad);   // W_kj
+            __syncthreads();
+            double acc[4];
+            double* Tij = W + (size_t)(i * 32) * npad + j * 32;
+            cg_fetch(Tij, npad, acc);
+            cg_mma(acc, As, Bs);
+            if (i == k + 1) {   // last contribution to block row k+1: W_ij = -inv(L_ii) T_ij
+                __syncthreads();
+                const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+                Bs[r0][c0] = acc[0];
+                Bs[r0][c0 + 1] = acc[1];
+                Bs[r0 + 1][c0] = acc[2];
+                Bs[r0 + 1][c0 + 1] = acc[3];
+                cg_load<false>(As, Linv + (size_t)i * 1024, 32);
+                __syncthreads();
+                double o[4] = {0.0, 0.0, 0.0, 0.0};
+                cg_mma(o, As, Bs);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[e] = -o[e];
+                cg_store(Tij, npad, o);
+            } else {
+                cg_store(Tij, npad, acc);
+            }
+        }
+        gbar(ctr, target);
+    }
+    // ---- Z = W^T W (lower tiles, mirrored)
+    const int ntz = nb * (nb + 1) / 2;
+    for (int t = blockIdx.x; t < ntz; t += gridDim.x) {
+        int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((I + 1) * (I + 2) / 2 <= t) ++I;
+        while (I * (I + 1) / 2 > t) --I;
+        const int J = t - I * (I + 1) / 2;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = I; k < nb; ++k) {
+            __syncthreads();
+            cg_load<true>(As, W + (size_t)(k * 32) * npad + I * 32, npad);    // As[r][p] = W_kI[p][r]
+            cg_load<false>(Bs, W + (size_t)(k * 32) * npad + J * 32, npad);   // Bs[p][c] = W_kJ[p][c]
+            __syncthreads();
+            cg_mma(acc, As, Bs);
+        }
+        const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+        double* Zt = Z + (size_t)(I * 32) * npad + J * 32;
+        cg_store(Zt, npad, acc);
+        double* Zm = Z + (size_t)(J * 32) * npad + I * 32;   // mirror: Z_JI = Z_IJ^T
+        Zm[(size_t)c0 * npad + r0] = acc[0];
+        Zm[(size_t)(c0 + 1) * npad + r0] = acc[1];
+        Zm[(size_t)c0 * npad + r0 + 1] = acc[2];
+        Zm[(size_t)(c0 + 1) * npad + r0 + 1] = acc[3];
+    }
+}
+
 template <int K>
 void dispatch_rows(bool gather, const int32_t* perm, const double* src, double* dst, int n, cudaStream_t s) {
     if (gather) k_gather_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n);
@@ -1041,6 +1292,28 @@ int launch_chol_cluster(double* D, double* Linv, double* W, double* Z, int npad,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_chol_cluster, D, Linv, W, Z, npad, err) == cudaSuccess ? 1 : -1;
+}
+
+int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s) {
+    static unsigned* ctr = nullptr;
+    static int grid_max = -1;
+    if (grid_max < 0) {
+        int dev = 0, nsm = 0, per = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_grid, kCgThreads, 0);
+        grid_max = (coop && per > 0 && cudaMalloc(&ctr, sizeof(unsigned)) == cudaSuccess) ? nsm : 0;
+        cudaGetLastError();
+    }
+    if (grid_max <= 0) return -1;
+    const int nb = npad / 32;
+    const int grid = std::max(1, std::min(grid_max, nb * (nb + 1) / 2));
+    if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess) return -1;
+    void* args[] = {&D, &Linv, &W, &Z, &npad, &err, &ctr};
+    return cudaLaunchCooperativeKernel((const void*)k_chol_grid, dim3(grid), dim3(kCgThreads), args, 0, s) == cudaSuccess
+               ? 1
+               : -1;
 }
 
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s) {

@@ -263,10 +263,12 @@ def test_launch_modes_agree(ora, monkeypatch):
         "gal1": {"MG_GAL2": "0"},
         "gal3": {"MG_GAL_V3": "1"},
         "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
+        "chol_cluster": {"MG_CHOL": "cluster"},
     }
     out = {}
     for name, env in variants.items():
-        for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES"):
+        for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
+                  "MG_CHOL"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -325,9 +327,10 @@ def test_split_csr_equals_split_cotan(ora):
     _, M = ora.assemble(V, F, 1.0, 0.0)
     Ls = L.to_scipy().tocsr()
     Ls.sort_indices()
-    Ms = (Ls * 0 + sp.diags(M)).tocsr()
-    Ms.sort_indices()
-    assert np.array_equal(Ls.indptr, Ms.indptr) and np.array_equal(Ls.indices, Ms.indices)
+    Mv = np.zeros_like(Ls.data)
+    rows = np.repeat(np.arange(p.n), np.diff(Ls.indptr))
+    Mv[Ls.indices == rows] = M                                # M on the diagonal slots of the same pattern
+    Ms = sp.csr_matrix((Mv, Ls.indices.copy(), Ls.indptr.copy()), shape=Ls.shape)
     S1 = gpu_solver(p)
     S1.set_matrix_split(Ls.indptr.astype(np.int32), Ls.indices.astype(np.int32), Ls.data, Ms.data)
     S2 = gpu_solver(p)
