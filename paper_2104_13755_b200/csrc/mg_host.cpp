@@ -416,6 +416,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     L.lpr = w;
                     break;
                 }
+            // whole-level passes (residual, norm) have C times the rows of a
+            // colour pass: a few entries per lane instead of one wave
+            L.lpr_all = avg <= 24.0 ? 4 : 8;
+            const std::string lv = std::to_string(l);
+            if (const char* e = getenv(("MG_LPR_L" + lv).c_str())) L.lpr = atoi(e);
+            if (const char* e = getenv(("MG_LPR_ALL_L" + lv).c_str())) L.lpr_all = atoi(e);
         }
     }
     cudaStream_t s = c->stream;

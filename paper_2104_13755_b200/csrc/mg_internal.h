@@ -56,6 +56,7 @@ struct Level {
     int64_t nnz = 0;
     int32_t ncolours = 0;
     int lpr = 8;                          // lanes per row of the CSR kernels (untiled fallback)
+    int lpr_all = 4;                      // lanes per row of whole-level passes (residual, norm)
     bool tiled = false;                   // tile-staged kernels usable (tiles fit in shared memory)
     int cap_gs = 0;                       // max nnz of a kTile-row tile inside one colour range
     int cap_all = 0;                      // max nnz of a kTile-row tile of the whole matrix

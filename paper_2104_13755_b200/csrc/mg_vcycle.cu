@@ -361,7 +361,9 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1) {
     constexpr int U = 32 / LPR;
-    constexpr int GB = U <= 8 ? U : 8;   // gathers in flight per lane (one batch for LPR >= 4)
+    // gathers in flight per lane: the whole prefetch for LPR >= 8, batches of
+    // 4 for LPR = 4 (8 entries per lane) to keep registers / occupancy
+    constexpr int GB = U <= 4 ? U : 4;
     const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
     const int lane = threadIdx.x & (LPR - 1);
     const int row = r0 + g;
@@ -865,8 +867,9 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s)
                  L.b.p, L.x.p, r, r0, r1, cap);
         return 1;
     }
-    const int grid = nblk((int64_t)rows * L.lpr, kBlock);
-    switch (L.lpr) {
+    const int lpr = MODE == 0 ? L.lpr : L.lpr_all;
+    const int grid = nblk((int64_t)rows * lpr, kBlock);
+    switch (lpr) {
         case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
         case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
         case 16: launch_k(pdl, k_lpr_sweep<K, 16, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
@@ -887,8 +890,8 @@ int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, doub
         launch_k(pdl, k_resnorm_tiled<K>, grid, kTile, tile_smem(L.cap_all), s, L.rp.p, L.col.p, L.val.p, L.b.p,
                  L.x.p, partial, L.n, L.cap_all);
     } else {
-        grid = std::min(nb, nblk((int64_t)L.n * L.lpr, kBlock));
-        switch (L.lpr) {
+        grid = std::min(nb, nblk((int64_t)L.n * L.lpr_all, kBlock));
+        switch (L.lpr_all) {
             case 4: launch_k(pdl, k_resnorm_lpr<K, 4>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
             case 8: launch_k(pdl, k_resnorm_lpr<K, 8>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
             case 16: launch_k(pdl, k_resnorm_lpr<K, 16>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, partial, L.n); break;
