@@ -406,16 +406,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             if (e) return c->cuda_fail(e, "tile upload");
         }
         if (!L.tiled) {
-            // lanes per row: the widest group for which one colour pass is about one wave
-            // (148 SMs x 2048 threads); each lane prefetches 32 / LPR entries
+            // lanes per row of a colour pass (each lane prefetches 32 / LPR entries
+            // of its row before the PDL wait).  Measured on B200 (profiles/r01,
+            // LPR sweep on config 4): many entries per lane win while the pass
+            // still has >= ~4k rows; tiny passes use a full warp per row.
             const double rows = (double)L.n / std::max(1, (int)L.colour_off.size() - 1);
-            const double wave = 148.0 * 2048.0;
-            L.lpr = 4;
-            for (int w : {32, 16, 8})
-                if (rows * w <= wave) {
-                    L.lpr = w;
-                    break;
-                }
+            L.lpr = rows >= 20000.0 ? 4 : rows >= 4000.0 ? 8 : 32;
             // whole-level passes (residual, norm) have C times the rows of a
             // colour pass: a few entries per lane instead of one wave
             L.lpr_all = avg <= 24.0 ? 4 : 8;
@@ -433,7 +429,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         rpad.resize(rpad.size() + 8, L.irp.back());
         cpad.resize(cpad.size() + 8, 0);
         if ((e = L.rp.upload(rpad, s)) || (e = L.col.upload(cpad, s)) || (e = L.val.alloc(std::max<int64_t>(L.nnz, 1) + 8)) ||
-            (e = L.dperm.upload(L.perm, s)) || (e = L.x.alloc((size_t)L.n * kMaxK)) ||
+            (e = L.dperm.upload(L.perm, s)) || (e = L.diperm.upload(L.iperm, s)) || (e = L.x.alloc((size_t)L.n * kMaxK)) ||
             (e = L.b.alloc((size_t)L.n * kMaxK)) || (e = L.r.alloc((size_t)L.n * kMaxK)))
             return c->cuda_fail(e, "pattern upload");
         if (l == 0 && (e = L.di2u.upload(L.i2u, s))) return c->cuda_fail(e, "pattern upload");
@@ -1011,7 +1007,7 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
     const double* dV = nullptr;
     rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV);
     if (rc) return rc;
-    c->timed(PC_ASSEMBLY, 0, c->stream, [&] { return launch_gather_rows(3, L0.dperm.p, dV, c->Vint.p, n, c->stream); });
+    c->timed(PC_ASSEMBLY, 0, c->stream, [&] { return launch_gather_rows(3, L0.diperm.p, dV, c->Vint.p, n, c->stream); });
     return MG_OK;
 }
 
@@ -1023,7 +1019,7 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
     const int32_t n = L0.n;
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
         return launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, L0.val.p, c->Mint.p, c->stream) +
-               launch_scatter_vec(L0.dperm.p, c->Mint.p, c->Muser.p, n, c->stream);
+               launch_scatter_vec(L0.diperm.p, c->Mint.p, c->Muser.p, n, c->stream);
     });
     c->have_mass = true;
     c->have_split = false;
@@ -1061,7 +1057,7 @@ int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
         return launch_cotan(L0, c->opp.p, c->Vint.p, 0.0, 1.0, L0.qv.p, c->Mint.p, c->stream) +
                launch_cotan(L0, c->opp.p, c->Vint.p, 1.0, 0.0, L0.mv.p, c->Mint.p, c->stream) +
-               launch_scatter_vec(L0.dperm.p, c->Mint.p, c->Muser.p, L0.n, c->stream);
+               launch_scatter_vec(L0.diperm.p, c->Mint.p, c->Muser.p, L0.n, c->stream);
     });
     c->have_mass = true;
     return split_hierarchy(c);
@@ -1118,7 +1114,7 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
     if ((rc = to_device(c, B, c->stageB, (size_t)n * k, &dB))) return rc;
     if ((rc = to_device(c, X, c->stageX, (size_t)n * k, &dX))) return rc;
     c->timed(PC_PERMUTE, 0, s, [&] {
-        return launch_gather_rows(k, L0.dperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.dperm.p, dX, L0.x.p, n, s) +
+        return launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s) +
                vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
     });
     c->timed(PC_RESNORM, 0, s, [&] {
@@ -1157,7 +1153,7 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
     }
     if (status == MG_NOT_CONVERGED && !(rel_tol > 0.0)) status = MG_OK;   // fixed-cycle mode
     double* dXout = devX ? X : c->stageX.p;
-    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.dperm.p, L0.x.p, dXout, n, s); });
+    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.diperm.p, L0.x.p, dXout, n, s); });
     if (!devX && (e = cudaMemcpyAsync(X, dXout, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s)))
         return c->cuda_fail(e, "mg_solve");
     if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "mg_solve");

@@ -90,6 +90,7 @@ struct Level {
     DBuf<int32_t> prow_c;                 // P rows packed: {c0, c1, c2, 0} (this level fine)
     DBuf<double> prow_w;                  //                {w0, w1, w2, 0}
     DBuf<int32_t> dperm;                  // perm on device
+    DBuf<int32_t> diperm;                 // iperm on device (user -> internal)
     DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
     DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
     DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
@@ -156,15 +157,15 @@ int tail_cluster_size();
 int vc_tail(int K, const TailParams& p, int cs, bool pdl, cudaStream_t s);
 // mg_setup.cu
 void init_setup_attributes();
-int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s);
-int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
+int launch_gather_rows(int K, const int32_t* iperm, const double* src_user, double* dst_int, int n, cudaStream_t s);
+int launch_scatter_rows(int K, const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
 int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
                  double* val, double* M_int, cudaStream_t s);
 int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, double* out, int64_t nnz,
                  cudaStream_t s);
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);
-int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s);
+int launch_scatter_vec(const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s);
 int galerkin_max_row();
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);

@@ -18,25 +18,31 @@ namespace mg {
 namespace {
 
 // ---------------------------------------------------------------------------
-// K9: user <-> internal permutations (row blocks of K values).
+// K9: user <-> internal permutations (row blocks of K values).  Both walk the
+// USER order (coalesced user-side rows) and index the internal side through
+// iperm[u], whose rows are aligned (32-byte rows for K = 3, 4): one full
+// sector per random access instead of partial, straddling user-side rows.
 template <int K>
-__global__ void __launch_bounds__(kBlock) k_gather_rows(const int* __restrict__ perm, const double* __restrict__ src,
+__global__ void __launch_bounds__(kBlock) k_gather_rows(const int* __restrict__ iperm, const double* __restrict__ src,
                                                         double* __restrict__ dst, int n) {
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
-    const size_t u = (size_t)perm[i];
+    const int u = blockIdx.x * kBlock + threadIdx.x;
+    if (u >= n) return;
+    const size_t i = (size_t)__ldg(iperm + u);
+    double v[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) dst[(size_t)i * VS<K>::S + c] = src[u * K + c];
-    if (VS<K>::S > K) dst[(size_t)i * VS<K>::S + K] = 0.0;
+    for (int c = 0; c < K; ++c) v[c] = __ldcs(src + (size_t)u * K + c);
+    strow<K>(dst + i * VS<K>::S, v);   // K = 3: the pad lane is written as 0
 }
 template <int K>
-__global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__ perm, const double* __restrict__ src,
+__global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__ iperm, const double* __restrict__ src,
                                                          double* __restrict__ dst, int n) {
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
-    const size_t u = (size_t)perm[i];
+    const int u = blockIdx.x * kBlock + threadIdx.x;
+    if (u >= n) return;
+    const size_t i = (size_t)__ldg(iperm + u);
+    double v[K];
+    ldrow<K>(src + i * VS<K>::S, v);
 #pragma unroll
-    for (int c = 0; c < K; ++c) dst[u * K + c] = src[(size_t)i * VS<K>::S + c];
+    for (int c = 0; c < K; ++c) __stcs(dst + (size_t)u * K + c, v[c]);
 }
 __global__ void __launch_bounds__(kBlock) k_gather_vals(const int64_t* __restrict__ i2u, const double* __restrict__ src,
                                                         double* __restrict__ dst, int64_t nnz) {
@@ -62,33 +68,40 @@ __global__ void __launch_bounds__(kBlock) k_apply_mass(const double* __restrict_
 //   L_ij = -1/2 sum_o cot(angle at o),  cot = (vi-vo).(vj-vo) / |(vi-vo)x(vj-vo)|
 //   L_ii = -sum_{j != i} L_ij
 //   M_ii = 1/3 sum_{faces f at i} area_f = 1/6 sum_{(i,j)} sum_o |(vi-vo)x(vj-vo)|/2
-// (every face at i is seen from both of its edges at i).  One thread per row,
-// deterministic (no atomics).  A = mass_coeff M + lap_coeff L.
+// (every face at i is seen from both of its edges at i).  kCotG lanes per row
+// (one stored entry each: coalesced column / opposite-vertex / value streams),
+// row sums by a fixed-order group reduction: deterministic, no atomics.
+// A = mass_coeff M + lap_coeff L.
+constexpr int kCotG = 8;
 __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict__ rp, const int* __restrict__ col,
                                                            const int* __restrict__ opp, const double* __restrict__ V,
                                                            double mass_coeff, double lap_coeff,
                                                            double* __restrict__ val, double* __restrict__ M, int n) {
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i >= n) return;
+    const int i = (blockIdx.x * kBlock + threadIdx.x) / kCotG;
+    const int lane = threadIdx.x & (kCotG - 1);
+    if (i >= n) return;   // whole groups leave together
+    const unsigned mask = group_mask(kCotG);
     // internal positions: 32-byte rows (x, y, z, pad), one 256-bit load each
     double pi[3];
     ldrow<3>(V + 4 * (size_t)i, pi);
     const double xi = pi[0], yi = pi[1], zi = pi[2];
     double lsum = 0.0, area2 = 0.0;
     int ediag = -1;
-    for (int e = rp[i]; e < rp[i + 1]; ++e) {
-        const int j = col[e];
+    const int e0 = rp[i], e1 = rp[i + 1];
+    for (int e = e0 + lane; e < e1; e += kCotG) {
+        const int j = __ldcs(col + e);
         if (j == i) {
             ediag = e;
             continue;
         }
+        const int2 oo = __ldcs(reinterpret_cast<const int2*>(opp) + e);
         double pj[3];
         ldrow<3>(V + 4 * (size_t)j, pj);
         const double xj = pj[0], yj = pj[1], zj = pj[2];
         double cot_sum = 0.0;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const int o = opp[2 * (size_t)e + s];
+            const int o = s == 0 ? oo.x : oo.y;
             if (o < 0) continue;
             double po[3];
             ldrow<3>(V + 4 * (size_t)o, po);
@@ -102,10 +115,12 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
         }
         const double lij = -0.5 * cot_sum;
         lsum += lij;
-        val[e] = lap_coeff * lij;
+        __stcs(val + e, lap_coeff * lij);
     }
+    lsum = group_sum<kCotG>(lsum, mask);
+    area2 = group_sum<kCotG>(area2, mask);
     const double m = area2 / 12.0;   // (1/6) * sum (|cross| / 2)
-    M[i] = m;
+    if (lane == 0) M[i] = m;
     if (ediag >= 0) val[ediag] = mass_coeff * m + lap_coeff * (-lsum);
 }
 
@@ -126,10 +141,10 @@ __global__ void __launch_bounds__(kBlock) k_axpby(const double* __restrict__ Q, 
     if ((nnz & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[nnz - 1] = alpha * Q[nnz - 1] + beta * M[nnz - 1];
 }
 
-__global__ void k_scatter_vec(const int* __restrict__ perm, const double* __restrict__ src, double* __restrict__ dst,
+__global__ void k_scatter_vec(const int* __restrict__ iperm, const double* __restrict__ src, double* __restrict__ dst,
                               int n) {
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i < n) dst[perm[i]] = src[i];
+    const int u = blockIdx.x * kBlock + threadIdx.x;
+    if (u < n) dst[u] = src[__ldg(iperm + u)];
 }
 
 // ---------------------------------------------------------------------------
@@ -1163,7 +1178,7 @@ int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64
 }
 int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
                  double* val, double* M_int, cudaStream_t s) {
-    k_cotan_assemble<<<nblk(L0.n, kBlock), kBlock, 0, s>>>(L0.rp.p, L0.col.p, opp, Vint, mass_coeff, lap_coeff,
+    k_cotan_assemble<<<nblk((int64_t)L0.n * kCotG, kBlock), kBlock, 0, s>>>(L0.rp.p, L0.col.p, opp, Vint, mass_coeff, lap_coeff,
                                                             val, M_int, L0.n);
     return 1;
 }
