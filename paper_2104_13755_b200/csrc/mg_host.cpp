@@ -196,6 +196,7 @@ struct mg_ctx {
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool use_gal2 = true;            // Galerkin v2 kernel
+    bool use_gal4 = true;            // Galerkin v4 kernel (group-of-rows, A P rows once per group)
     int64_t l2_persist = -1;         // bytes of L2 set aside for the fine iterate (-1: auto, 0: off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
@@ -486,6 +487,67 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             int maxrow = 0;
             for (int32_t I = 0; I < C.n; ++I) maxrow = std::max(maxrow, C.irp[I + 1] - C.irp[I]);
             C.gal2 = c->use_gal2 && maxrow <= galerkin_max_row();
+            // Galerkin v4 structure: T_i = (A P)_i row sizes, groups of coarse rows
+            C.gal4_maxt = 0;
+            if (c->use_gal4) {
+                int maxT = 0;
+                std::vector<int32_t> seen(C.n, -1);
+                for (int32_t i = 0; i < L.n; ++i) {
+                    int cnt_t = 0;
+                    for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
+                        const int32_t j = L.icol[e];
+                        for (int q = 0; q < 3; ++q) {
+                            if (pw[(size_t)q * L.n + j] == 0.0) continue;
+                            const int32_t J = pc[(size_t)q * L.n + j];
+                            if (seen[J] != i) {
+                                seen[J] = i;
+                                ++cnt_t;
+                            }
+                        }
+                    }
+                    maxT = std::max(maxT, cnt_t);
+                }
+                const int capc = galerkin4_capc();
+                int maxch = 0;
+                for (int32_t I = 0; I < C.n; ++I) maxch = std::max(maxch, cnt[I + 1] - cnt[I]);
+                if (maxT <= 24 && maxch <= capc) {
+                    C.gal4_maxt = maxT <= 12 ? 12 : 24;
+                    std::vector<int32_t> grows(1, 0), gcoff(1, 0), gch, rcl(cidx.size());
+                    std::vector<int32_t> loc(L.n, -1);
+                    std::vector<int32_t> cur;
+                    size_t r = 0;
+                    while (r < order.size()) {
+                        // grow the group while its distinct children fit
+                        cur.clear();
+                        size_t r1 = r;
+                        while (r1 < order.size()) {
+                            const int32_t I = order[r1];
+                            int add = 0;
+                            for (int32_t t = cnt[I]; t < cnt[I + 1]; ++t)
+                                if (loc[cidx[t]] < 0) ++add;
+                            if ((int)cur.size() + add > capc && r1 > r) break;
+                            for (int32_t t = cnt[I]; t < cnt[I + 1]; ++t) {
+                                const int32_t i = cidx[t];
+                                if (loc[i] < 0) {
+                                    loc[i] = (int32_t)cur.size();
+                                    cur.push_back(i);
+                                }
+                                rcl[t] = loc[i];
+                            }
+                            ++r1;
+                        }
+                        for (int32_t i : cur) loc[i] = -1;
+                        gch.insert(gch.end(), cur.begin(), cur.end());
+                        grows.push_back((int32_t)r1);
+                        gcoff.push_back((int32_t)gch.size());
+                        r = r1;
+                    }
+                    C.gal4_ngroups = (int)grows.size() - 1;
+                    if ((e = C.g4_rows.upload(grows, s)) || (e = C.g4_coff.upload(gcoff, s)) ||
+                        (e = C.g4_children.upload(gch, s)) || (e = C.g4_rcl.upload(rcl, s)))
+                        return c->cuda_fail(e, "pattern upload");
+                }
+            }
             if ((e = L.prow_c.upload(prc, s)) || (e = L.prow_w.upload(prw, s)) || (e = C.cinfo.upload(cinfo, s)))
                 return c->cuda_fail(e, "pattern upload");
             if ((e = L.pc.upload(pc, s)) || (e = L.pw.upload(pw, s)) || (e = C.cptr.upload(cnt, s)) ||
@@ -758,6 +820,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
     if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
     if (const char* m = getenv("MG_GAL2")) c->use_gal2 = std::string(m) != "0";
+    if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) != "0";
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     c->tail_cs = tail_cluster_size();

@@ -86,6 +86,15 @@ struct Level {
     DBuf<double> cw;
     DBuf<int32_t> gal_order;              // rows of this level in locality order (Galerkin)
     bool gal2 = false;                    // Galerkin v2 usable for this (coarse) level
+    // Galerkin v4 (this level coarse): coarse rows in groups of consecutive
+    // gal_order rows; per group the distinct children (fine rows) and, for
+    // every children-list entry, the child's index inside its group
+    int gal4_maxt = 0;                    // 0: v4 not usable; else T-row capacity (12 or 24)
+    int gal4_ngroups = 0;
+    DBuf<int32_t> g4_rows;                // [ngroups+1] offsets into gal_order
+    DBuf<int32_t> g4_coff;                // [ngroups+1] offsets into g4_children
+    DBuf<int32_t> g4_children;            // distinct fine rows per group
+    DBuf<int32_t> g4_rcl;                 // parallel to cidx: local child index within the group
     DBuf<int32_t> cinfo;                  // children as {i, row start, row length, 0} (this level coarse)
     DBuf<int32_t> prow_c;                 // P rows packed: {c0, c1, c2, 0} (this level fine)
     DBuf<double> prow_w;                  //                {w0, w1, w2, 0}
@@ -168,6 +177,7 @@ int launch_apply_mass(int K, const double* M_user, const double* X, double* B, i
 int launch_scatter_vec(const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s);
 int galerkin_max_row();
+int galerkin4_capc();
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);

@@ -372,6 +372,109 @@ __global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
     }
 }
 
+// K2 v4 (default where it applies): A_c = P^T (A P), one CTA per group of
+// consecutive coarse rows (locality order).
+//   phase 1: every distinct child i of the group (fine row with P[i,I] != 0
+//            for a row I of the group) computes its row T_i = (A P)_i ONCE, in
+//            registers: the row's stored entries in ascending order, the three
+//            barycentric parents of each neighbour, accumulated into a small
+//            key/value map (<= MAXT distinct coarse columns, checked at
+//            pattern setup), then staged in shared memory;
+//   phase 2: owner computes: one thread per stored coarse entry (I, J) sums
+//            P[i,I] T_i[J] over the children list of I in its fixed order.
+// No atomics, every sum in a fixed order: deterministic.  Versus v2 the
+// triple-product terms per fine row drop from 3 x (|row| x 3) (recomputed for
+// each parent) to |row| x 3, and the P-row gathers by the same factor 3.
+constexpr int kGal4Threads = 256;
+constexpr int kGal4Capc = 256;   // distinct children per group (= threads: one child per thread)
+
+template <int MAXT>
+__global__ void __launch_bounds__(kGal4Threads) k_galerkin4(
+    const int* __restrict__ order, const int* __restrict__ grows, const int* __restrict__ gcoff,
+    const int* __restrict__ gch, const int* __restrict__ crp, const int* __restrict__ ccol, double* __restrict__ cval,
+    const int* __restrict__ cptr, const int* __restrict__ rcl, const double* __restrict__ cw,
+    const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
+    const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
+    extern __shared__ __align__(16) unsigned char g4_smem[];
+    double* Tv = reinterpret_cast<double*>(g4_smem);                          // [capc][MAXT]
+    int* Tk = reinterpret_cast<int*>(Tv + (size_t)kGal4Capc * MAXT);         // [capc][MAXT]
+    unsigned char* Tn = reinterpret_cast<unsigned char*>(Tk + (size_t)kGal4Capc * MAXT);   // [capc]
+    const int g = blockIdx.x;
+    const int c0 = gcoff[g], nch = gcoff[g + 1] - c0;
+    // ---- phase 1: T rows of the group's children
+    for (int c = threadIdx.x; c < nch; c += kGal4Threads) {
+        const int i = gch[c0 + c];
+        int key[MAXT];
+        double v[MAXT];
+#pragma unroll
+        for (int q = 0; q < MAXT; ++q) {
+            key[q] = -1;
+            v[q] = 0.0;
+        }
+        int cnt = 0;
+        const int e0 = rp[i], e1 = rp[i + 1];
+        for (int e = e0; e < e1; ++e) {
+            const int j = col[e];
+            const double a = val[e];
+            const int4 pc = prow_c[j];
+            const double4 pw = prow_w[j];
+            const int Js[3] = {pc.x, pc.y, pc.z};
+            const double ws[3] = {pw.x, pw.y, pw.z};
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                if (ws[r] == 0.0) continue;   // padding carries no structure (reading A9)
+                const int J = Js[r];
+                const double t = a * ws[r];
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < MAXT; ++q)
+                    if (key[q] == J) {
+                        v[q] += t;
+                        found = true;
+                    }
+                if (!found) {
+#pragma unroll
+                    for (int q = 0; q < MAXT; ++q)
+                        if (q == cnt) {
+                            key[q] = J;
+                            v[q] = t;
+                        }
+                    ++cnt;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < MAXT; ++q) {
+            Tk[(size_t)c * MAXT + q] = key[q];
+            Tv[(size_t)c * MAXT + q] = v[q];
+        }
+        Tn[c] = (unsigned char)cnt;
+    }
+    __syncthreads();
+    // ---- phase 2: one thread per stored entry (I, J) of the group's rows
+    const int r0 = grows[g], r1 = grows[g + 1];
+    for (int rr = r0; rr < r1; ++rr) {
+        const int I = order[rr];
+        const int a0 = crp[I], m = crp[I + 1] - a0;
+        const int t0 = cptr[I], t1 = cptr[I + 1];
+        for (int sidx = threadIdx.x; sidx < m; sidx += kGal4Threads) {
+            const int J = ccol[a0 + sidx];
+            double acc = 0.0;
+            for (int t = t0; t < t1; ++t) {
+                const int c = rcl[t];
+                const double w = cw[t];
+                const int* kk = Tk + (size_t)c * MAXT;
+                const int n_t = Tn[c];
+                double tv = 0.0;
+                for (int q = 0; q < n_t; ++q)
+                    if (kk[q] == J) tv = Tv[(size_t)c * MAXT + q];
+                acc = fma(w, tv, acc);
+            }
+            cval[a0 + sidx] = acc;
+        }
+    }
+}
+
 // K2 v3 (MG_GAL_V3=1, measured slower): slot-owner formulation, atomic-free and deterministic.
 // One warp per coarse row I; lane l owns coarse columns J_l = col(I, l) and
 // J_l' = col(I, l + 32).  The warp walks every (child i, neighbour j) pair of
@@ -1154,11 +1257,15 @@ void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* 
 
 }  // namespace
 
+size_t galerkin4_smem(int maxt) { return (size_t)kGal4Capc * maxt * 12 + kGal4Capc; }
+int galerkin4_capc() { return kGal4Capc; }
 int galerkin_max_row() { return 64; }   // v2 private rows <= 32, shared copy <= 96; v3 <= 64
 
 void init_setup_attributes() {
     const int big = 200 * 1024;
     cudaFuncSetAttribute(k_chol_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_galerkin4<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galerkin4_smem(12));
+    cudaFuncSetAttribute(k_galerkin4<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galerkin4_smem(24));
 }
 
 int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s) {
@@ -1198,6 +1305,19 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
 }
 int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s) {
     const int nc = coarse.n;
+    if (coarse.gal4_maxt > 0 && fine.prow_c.p) {
+        if (coarse.gal4_maxt <= 12)
+            k_galerkin4<12><<<coarse.gal4_ngroups, kGal4Threads, galerkin4_smem(12), s>>>(
+                coarse.gal_order.p, coarse.g4_rows.p, coarse.g4_coff.p, coarse.g4_children.p, coarse.rp.p, coarse.col.p,
+                cval, coarse.cptr.p, coarse.g4_rcl.p, coarse.cw.p, fine.rp.p, fine.col.p, fval,
+                reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
+        else
+            k_galerkin4<24><<<coarse.gal4_ngroups, kGal4Threads, galerkin4_smem(24), s>>>(
+                coarse.gal_order.p, coarse.g4_rows.p, coarse.g4_coff.p, coarse.g4_children.p, coarse.rp.p, coarse.col.p,
+                cval, coarse.cptr.p, coarse.g4_rcl.p, coarse.cw.p, fine.rp.p, fine.col.p, fval,
+                reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
+        return 1;
+    }
     if (coarse.gal2 && fine.prow_c.p && getenv("MG_GAL_V3")) {
         k_galerkin3<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
             nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p,

@@ -260,15 +260,16 @@ def test_launch_modes_agree(ora, monkeypatch):
         "nopipe": {"MG_PIPE": "0"},
         "trsv": {"MG_COARSE_SOLVE": "trsv"},
         "tail": {"MG_TAIL_ROWS": "20000"},
-        "gal1": {"MG_GAL2": "0"},
-        "gal3": {"MG_GAL_V3": "1"},
+        "gal1": {"MG_GAL2": "0", "MG_GAL4": "0"},
+        "gal2": {"MG_GAL4": "0"},
+        "gal3": {"MG_GAL_V3": "1", "MG_GAL4": "0"},
         "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
         "chol_cluster": {"MG_CHOL": "cluster"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
-                  "MG_CHOL"):
+                  "MG_CHOL", "MG_GAL4"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
