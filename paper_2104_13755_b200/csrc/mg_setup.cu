@@ -389,7 +389,7 @@ constexpr int kGal4Threads = 256;
 constexpr int kGal4Capc = 256;   // distinct children per group (= threads: one child per thread)
 
 template <int MAXT>
-__global__ void __launch_bounds__(kGal4Threads) k_galerkin4(
+__global__ void __launch_bounds__(kGal4Threads, 2) k_galerkin4(
     const int* __restrict__ order, const int* __restrict__ grows, const int* __restrict__ gcoff,
     const int* __restrict__ gch, const int* __restrict__ crp, const int* __restrict__ ccol, double* __restrict__ cval,
     const int* __restrict__ cptr, const int* __restrict__ rcl, const double* __restrict__ cw,
@@ -397,80 +397,114 @@ __global__ void __launch_bounds__(kGal4Threads) k_galerkin4(
     const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
     extern __shared__ __align__(16) unsigned char g4_smem[];
     double* Tv = reinterpret_cast<double*>(g4_smem);                          // [capc][MAXT]
-    int* Tk = reinterpret_cast<int*>(Tv + (size_t)kGal4Capc * MAXT);         // [capc][MAXT]
+    int* Tk = reinterpret_cast<int*>(Tv + (size_t)kGal4Capc * MAXT);         // [capc][MAXT], ascending keys
     unsigned char* Tn = reinterpret_cast<unsigned char*>(Tk + (size_t)kGal4Capc * MAXT);   // [capc]
+    constexpr int EB = MAXT <= 12 ? 8 : 4;   // row entries fetched per batch (independent loads in flight)
     const int g = blockIdx.x;
     const int c0 = gcoff[g], nch = gcoff[g + 1] - c0;
-    // ---- phase 1: T rows of the group's children
+    // ---- phase 1: T rows of the group's children (one child per thread)
     for (int c = threadIdx.x; c < nch; c += kGal4Threads) {
         const int i = gch[c0 + c];
         int key[MAXT];
         double v[MAXT];
 #pragma unroll
         for (int q = 0; q < MAXT; ++q) {
-            key[q] = -1;
+            key[q] = 0x7fffffff;
             v[q] = 0.0;
         }
         int cnt = 0;
         const int e0 = rp[i], e1 = rp[i + 1];
-        for (int e = e0; e < e1; ++e) {
-            const int j = col[e];
-            const double a = val[e];
-            const int4 pc = prow_c[j];
-            const double4 pw = prow_w[j];
-            const int Js[3] = {pc.x, pc.y, pc.z};
-            const double ws[3] = {pw.x, pw.y, pw.z};
+        for (int eb = e0; eb < e1; eb += EB) {
+            int jj[EB];
+            double aa[EB];
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                if (ws[r] == 0.0) continue;   // padding carries no structure (reading A9)
-                const int J = Js[r];
-                const double t = a * ws[r];
-                bool found = false;
+            for (int u = 0; u < EB; ++u) {
+                const bool ok = eb + u < e1;
+                jj[u] = ok ? __ldcs(col + eb + u) : -1;
+                aa[u] = ok ? __ldcs(val + eb + u) : 0.0;
+            }
+            int4 pcs[EB];
+            double4 pws[EB];
 #pragma unroll
-                for (int q = 0; q < MAXT; ++q)
-                    if (key[q] == J) {
-                        v[q] += t;
-                        found = true;
-                    }
-                if (!found) {
+            for (int u = 0; u < EB; ++u) {
+                if (jj[u] >= 0) {
+                    pcs[u] = prow_c[jj[u]];
+                    pws[u] = prow_w[jj[u]];
+                } else {
+                    pcs[u] = make_int4(0, 0, 0, 0);
+                    pws[u] = make_double4(0.0, 0.0, 0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < EB; ++u) {
+                const int Js[3] = {pcs[u].x, pcs[u].y, pcs[u].z};
+                const double ws[3] = {pws[u].x, pws[u].y, pws[u].z};
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    if (ws[r] == 0.0) continue;   // padding carries no structure (reading A9)
+                    const int J = Js[r];
+                    const double t = aa[u] * ws[r];
+                    bool found = false;
 #pragma unroll
                     for (int q = 0; q < MAXT; ++q)
-                        if (q == cnt) {
-                            key[q] = J;
-                            v[q] = t;
+                        if (key[q] == J) {
+                            v[q] += t;
+                            found = true;
                         }
-                    ++cnt;
+                    if (!found) {
+#pragma unroll
+                        for (int q = 0; q < MAXT; ++q)
+                            if (q == cnt) {
+                                key[q] = J;
+                                v[q] = t;
+                            }
+                        ++cnt;
+                    }
                 }
             }
         }
+        // store sorted by key (rank = number of smaller keys; unused slots hold INT_MAX)
 #pragma unroll
         for (int q = 0; q < MAXT; ++q) {
-            Tk[(size_t)c * MAXT + q] = key[q];
-            Tv[(size_t)c * MAXT + q] = v[q];
+            int rk = 0;
+#pragma unroll
+            for (int q2 = 0; q2 < MAXT; ++q2) rk += (key[q2] < key[q]) ? 1 : 0;
+            if (q < cnt) {
+                Tk[(size_t)c * MAXT + rk] = key[q];
+                Tv[(size_t)c * MAXT + rk] = v[q];
+            }
         }
         Tn[c] = (unsigned char)cnt;
     }
     __syncthreads();
-    // ---- phase 2: one thread per stored entry (I, J) of the group's rows
+    // ---- phase 2: one warp per coarse row, one lane per stored entry (I, J);
+    // the row's children (<= 32) are loaded once and broadcast by shuffles
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = grows[g], r1 = grows[g + 1];
-    for (int rr = r0; rr < r1; ++rr) {
+    for (int rr = r0 + warp; rr < r1; rr += kGal4Threads / 32) {
         const int I = order[rr];
         const int a0 = crp[I], m = crp[I + 1] - a0;
-        const int t0 = cptr[I], t1 = cptr[I + 1];
-        for (int sidx = threadIdx.x; sidx < m; sidx += kGal4Threads) {
-            const int J = ccol[a0 + sidx];
+        const int t0 = cptr[I], nt = cptr[I + 1] - t0;
+        const int cl = lane < nt ? rcl[t0 + lane] : 0;
+        const double wl = lane < nt ? cw[t0 + lane] : 0.0;
+        for (int sb = 0; sb < m; sb += 32) {
+            const int sidx = sb + lane;
+            const int J = sidx < m ? ccol[a0 + sidx] : -1;
             double acc = 0.0;
-            for (int t = t0; t < t1; ++t) {
-                const int c = rcl[t];
-                const double w = cw[t];
+            for (int t = 0; t < nt; ++t) {
+                const int c = __shfl_sync(0xffffffffu, cl, t);
+                const double w = __shfl_sync(0xffffffffu, wl, t);
                 const int* kk = Tk + (size_t)c * MAXT;
-                const int n_t = Tn[c];
-                double tv = 0.0;
-                for (int q = 0; q < n_t; ++q)
-                    if (kk[q] == J) tv = Tv[(size_t)c * MAXT + q];
+                int lo = 0, hi = Tn[c];
+                while (lo < hi) {   // first key >= J
+                    const int mid = (lo + hi) >> 1;
+                    if (kk[mid] < J) lo = mid + 1;
+                    else hi = mid;
+                }
+                const double tv = (lo < Tn[c] && kk[lo] == J) ? Tv[(size_t)c * MAXT + lo] : 0.0;
                 acc = fma(w, tv, acc);
             }
-            cval[a0 + sidx] = acc;
+            if (sidx < m) cval[a0 + sidx] = acc;
         }
     }
 }
