@@ -196,7 +196,7 @@ struct mg_ctx {
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool use_gal2 = true;            // Galerkin v2 kernel
-    bool use_gal4 = true;            // Galerkin v4 kernel (group-of-rows, A P rows once per group)
+    bool use_gal4 = false;           // Galerkin v4 kernel (group-of-rows, A P rows once per group; measured slower, opt-in)
     int64_t l2_persist = -1;         // bytes of L2 set aside for the fine iterate (-1: auto, 0: off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
@@ -820,7 +820,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
     if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
     if (const char* m = getenv("MG_GAL2")) c->use_gal2 = std::string(m) != "0";
-    if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) != "0";
+    if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) == "1";
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     c->tail_cs = tail_cluster_size();

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 constexpr int kHash = 256;   // power of two > 2 * kGalMaxM
 constexpr int kGal2Warps = 4;
 constexpr int kPriv = 33;    // padded row of the private accumulators
+constexpr int kCopies = 16;  // accumulator copies per warp: lanes l and l + 16 share copy l (two phases)
 
 __device__ __forceinline__ unsigned hslot(int J) { return ((unsigned)J * 2654435761u) >> (32 - 8); }
 
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
     double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
     const double* __restrict__ cw, const int* __restrict__ col, const double* __restrict__ val,
     const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
-    __shared__ double accp[kGal2Warps][32 * kPriv];   // private copies (m <= 32) or one shared copy (m <= 96)
+    __shared__ double accp[kGal2Warps][kCopies * kPriv];   // copies (m <= 32) or one shared copy (m <= 96)
     __shared__ int hkey[kGal2Warps][kHash];
     __shared__ unsigned char hval[kGal2Warps][kHash];
     __shared__ int ch_start[kGal2Warps][32];
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
     const int c0 = crp[I];
     const int m = crp[I + 1] - c0;
     const bool priv = m <= 32;
-    double* mine = priv ? &accp[w][lane * kPriv] : &accp[w][0];
+    double* mine = priv ? &accp[w][(lane & (kCopies - 1)) * kPriv] : &accp[w][0];
     for (int h = lane; h < kHash; h += 32) hkey[w][h] = -1;
     if (priv) {
         for (int s2 = 0; s2 < m; ++s2) mine[s2] = 0.0;
@@ -342,20 +343,41 @@ __global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
                 pc[u] = prow_c[j[u]];
                 pw[u] = prow_w[j[u]];
             }
+            int slot[2][3];
+            double tv[2][3];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                if (!ok[u]) continue;
                 const int Js[3] = {pc[u].x, pc[u].y, pc[u].z};
                 const double ws[3] = {pw[u].x, pw[u].y, pw[u].z};
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
-                    if (ws[q] == 0.0) continue;
+                    slot[u][q] = -1;
+                    tv[u][q] = a[u] * ws[q];
+                    if (!ok[u] || ws[q] == 0.0) continue;
                     unsigned h = hslot(Js[q]);
                     while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
-                    const int slot = hval[w][h];
-                    if (priv) mine[slot] += a[u] * ws[q];
-                    else atomicAdd(&accp[w][slot], a[u] * ws[q]);
+                    slot[u][q] = hval[w][h];
                 }
+            }
+            if (priv) {
+                // lanes l and l + 16 share a copy: they accumulate in two phases
+#pragma unroll
+                for (int ph = 0; ph < 32 / kCopies; ++ph) {
+                    if ((lane / kCopies) == ph) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u)
+#pragma unroll
+                            for (int q = 0; q < 3; ++q)
+                                if (slot[u][q] >= 0) mine[slot[u][q]] += tv[u][q];
+                    }
+                    __syncwarp();
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q)
+                        if (slot[u][q] >= 0) atomicAdd(&accp[w][slot[u][q]], tv[u][q]);
             }
         }
         __syncwarp();
@@ -364,7 +386,7 @@ __global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
     if (priv) {
         if (lane < m) {
             double sum = 0.0;
-            for (int l = 0; l < 32; ++l) sum += accp[w][l * kPriv + lane];
+            for (int l = 0; l < kCopies; ++l) sum += accp[w][l * kPriv + lane];
             cval[c0 + lane] = sum;
         }
     } else {

@@ -260,9 +260,9 @@ def test_launch_modes_agree(ora, monkeypatch):
         "nopipe": {"MG_PIPE": "0"},
         "trsv": {"MG_COARSE_SOLVE": "trsv"},
         "tail": {"MG_TAIL_ROWS": "20000"},
-        "gal1": {"MG_GAL2": "0", "MG_GAL4": "0"},
-        "gal2": {"MG_GAL4": "0"},
-        "gal3": {"MG_GAL_V3": "1", "MG_GAL4": "0"},
+        "gal1": {"MG_GAL2": "0"},
+        "gal4": {"MG_GAL4": "1"},
+        "gal3": {"MG_GAL_V3": "1"},
         "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
         "chol_cluster": {"MG_CHOL": "cluster"},
     }
