@@ -197,7 +197,8 @@ struct mg_ctx {
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool use_gal2 = true;            // Galerkin v2 kernel
     bool use_gal4 = false;           // Galerkin v4 kernel (group-of-rows, A P rows once per group; measured slower, opt-in)
-    int64_t l2_persist = -1;         // bytes of L2 set aside for the fine iterate (-1: auto, 0: off)
+    int64_t l2_persist = 0;          // bytes of L2 set aside for the fine iterate (-1: auto, 0: off;
+                                     // measured slightly slower than eviction hints alone, so off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
     int tail_cs = 0;                 // cluster size of the tail kernel
