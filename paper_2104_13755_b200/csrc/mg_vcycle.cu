@@ -15,7 +15,6 @@
 
 #include <algorithm>
 #include <cstdint>
-#include <unordered_map>
 
 #include "mg_common.cuh"
 #include "mg_internal.h"
@@ -358,7 +357,7 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
 // The group width is chosen per level so that one colour pass is about one
 // wave of the GPU (see choose_lpr in mg_host.cpp).
 template <int K, int LPR, int MODE>
-__global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 3) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
+__global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1) {
     constexpr int U = 32 / LPR;
@@ -367,32 +366,28 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 3) k_lpr_sweep(const in
     constexpr int GB = U <= 4 ? U : 4;
     const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
     const int lane = threadIdx.x & (LPR - 1);
-    // grid-stride over rows (the grid is at most one wave): groups handle
-    // rows g, g + stride, ...; the first row is prefetched before the wait
-    const int stride = gridDim.x * (kBlock / LPR);
-    int row = r0 + g;
+    const int row = r0 + g;
     pdl_launch_dependents();
+    const bool active = row < r1;
     const uint64_t pol = evict_first_policy();
     int e0 = 0, e1 = 0;
     int j[U];
     double a[U];
-    auto fetch = [&](int rw) {
-        const bool act = rw < r1;
-        e0 = act ? rp[rw] : 0;
-        e1 = act ? rp[rw + 1] : 0;
+    if (active) {
+        e0 = rp[row];
+        e1 = rp[row + 1];
+    }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = e0 + lane + u * LPR;
-            const bool ok = act && e < e1;
-            j[u] = ok ? ld_stream(col + e, pol) : -1;
-            a[u] = ok ? ld_stream(val + e, pol) : 0.0;
-        }
-    };
-    fetch(row);
+    for (int u = 0; u < U; ++u) {
+        const int e = e0 + lane + u * LPR;
+        const bool ok = active && e < e1;
+        j[u] = ok ? ld_stream(col + e, pol) : -1;
+        a[u] = ok ? ld_stream(val + e, pol) : 0.0;
+    }
     pdl_wait();
+    if (!active) return;   // whole groups leave together
     const unsigned mask = group_mask(LPR);
     const uint64_t xpol = evict_last_policy();
-    for (; row < r1; row += stride, fetch(row)) {   // whole groups iterate together
     // the row's right-hand side goes out with the gathers (one round trip)
     double bv[K];
     if (lane == 0) ldrow<K>(b + (size_t)row * VS<K>::S, bv);
@@ -441,7 +436,6 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 3) k_lpr_sweep(const in
         for (int c = 0; c < K; ++c) out[c] = MODE == 0 ? (bv[c] - s[c]) / d : bv[c] - s[c];
         if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
         else strow<K>(r + (size_t)row * VS<K>::S, out);
-    }
     }
 }
 
@@ -848,21 +842,6 @@ void pipe_launch(const Level& L, int t0, int t1, double* r, double* partial, int
              L.pipe_cap);
 }
 
-// Resident blocks of one full wave for a kBlock-thread kernel (cached per kernel).
-int wave_blocks(const void* kern) {
-    static std::unordered_map<const void*, int> cache;
-    auto it = cache.find(kern);
-    if (it != cache.end()) return it->second;
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kBlock, 0);
-    cudaGetLastError();
-    const int w = std::max(1, nsm * std::max(1, per));
-    cache[kern] = w;
-    return w;
-}
-
 template <int K, int MODE>
 int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s) {
     const int rows = r1 - r0;
@@ -889,14 +868,7 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s)
         return 1;
     }
     const int lpr = MODE == 0 ? L.lpr : L.lpr_all;
-    const int need = nblk((int64_t)rows * lpr, kBlock);
-    int grid = need;
-    switch (lpr) {
-        case 4: grid = std::min(need, wave_blocks((const void*)k_lpr_sweep<K, 4, MODE>)); break;
-        case 8: grid = std::min(need, wave_blocks((const void*)k_lpr_sweep<K, 8, MODE>)); break;
-        case 16: grid = std::min(need, wave_blocks((const void*)k_lpr_sweep<K, 16, MODE>)); break;
-        default: grid = std::min(need, wave_blocks((const void*)k_lpr_sweep<K, 32, MODE>)); break;
-    }
+    const int grid = nblk((int64_t)rows * lpr, kBlock);
     switch (lpr) {
         case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
         case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
