@@ -235,6 +235,47 @@ void gs_sweep(const Csr& A, const std::vector<std::vector<int32_t>>& classes, in
     }
 }
 
+// Reverse-order multicolour GS sweep: colours in DESCENDING id (rows of a
+// colour ascending).  The post-relaxation of the symmetric V-cycle used as a
+// CG preconditioner (future work P:738): with the reversed
+// order the post-smoother is the adjoint of the pre-smoother, so the V-cycle
+// is a symmetric operator.
+void gs_sweep_reverse(const Csr& A, const std::vector<std::vector<int32_t>>& classes, int k, const double* B,
+                      double* X) {
+    for (size_t cc = classes.size(); cc-- > 0;) {
+        for (int32_t i : classes[cc]) {
+            for (int c = 0; c < k; ++c) {
+                double s = B[(int64_t)i * k + c];
+                double aii = 0.0;
+                for (int64_t e = A.rowptr[i]; e < A.rowptr[i + 1]; ++e) {
+                    const int32_t j = A.col[e];
+                    if (j == i) aii = A.val[e];
+                    else s -= A.val[e] * X[(int64_t)j * k + c];
+                }
+                X[(int64_t)i * k + c] = s / aii;
+            }
+        }
+    }
+}
+
+// Damped Jacobi sweep (App. E, "(damped) Jacobi"; damping omega,
+// SPEC reading 0.8): x_i <- x_i + omega (b_i - sum_j a_ij x_j) / a_ii, every
+// row from the OLD iterate.
+void jacobi_sweep(const Csr& A, int k, const double* B, double* X, double omega) {
+    const int32_t n = A.nrows;
+    std::vector<double> old(X, X + (size_t)n * k);
+    for (int32_t i = 0; i < n; ++i)
+        for (int c = 0; c < k; ++c) {
+            double s = B[(int64_t)i * k + c];
+            double aii = 0.0;
+            for (int64_t e = A.rowptr[i]; e < A.rowptr[i + 1]; ++e) {
+                if (A.col[e] == i) aii = A.val[e];
+                s -= A.val[e] * old[(int64_t)A.col[e] * k + c];
+            }
+            X[(int64_t)i * k + c] = old[(int64_t)i * k + c] + omega * s / aii;
+        }
+}
+
 // ------------------------------------------------------------------------
 struct Level {
     Csr A;                                        // A_l
@@ -247,6 +288,9 @@ struct Level {
 struct MG {
     std::vector<Level> lv;
     int mu_pre = 2, mu_post = 2;                  // V(2,2): P:504
+    int smoother = 0;                             // 0 multicolour GS (reading A2), 1 damped Jacobi (App. E)
+    double omega = 0.8;                           // Jacobi damping
+    int symmetric = 0;                            // 1: post-relaxation in reverse colour order
     std::vector<double> Lfac;                     // dense Cholesky factor of A_H
     int status = 0;
 };
@@ -268,7 +312,10 @@ void vcycle(MG& mg, int h, int k, const double* b, double* x) {
         return;
     }
     // pre-relaxation
-    for (int s = 0; s < mg.mu_pre; ++s) gs_sweep(L.A, L.classes, k, b, x);
+    for (int s = 0; s < mg.mu_pre; ++s) {
+        if (mg.smoother == 1) jacobi_sweep(L.A, k, b, x, mg.omega);
+        else gs_sweep(L.A, L.classes, k, b, x);
+    }
     // r_{h+1} <- P^T (b - A x'_old)
     std::vector<double> r((size_t)n * k);
     for (int32_t i = 0; i < n; ++i)
@@ -289,7 +336,11 @@ void vcycle(MG& mg, int h, int k, const double* b, double* x) {
             x[(size_t)i * k + c] += s;
         }
     // post-relaxation
-    for (int s = 0; s < mg.mu_post; ++s) gs_sweep(L.A, L.classes, k, b, x);
+    for (int s = 0; s < mg.mu_post; ++s) {
+        if (mg.smoother == 1) jacobi_sweep(L.A, k, b, x, mg.omega);
+        else if (mg.symmetric) gs_sweep_reverse(L.A, L.classes, k, b, x);
+        else gs_sweep(L.A, L.classes, k, b, x);
+    }
 }
 
 // rho_j = ||b_j - A x_j||_2 / ||b_j||_2 (reading A3; absolute norm if ||b_j|| = 0)
@@ -506,6 +557,88 @@ int ora_mg_solve(ora_mg* mg, int32_t k, const double* B, double* X, double rel_t
     }
     *cycles_out = cyc;
     if (rc == 8 && !(rel_tol > 0.0)) rc = 0;   // fixed-cycle mode (config 1)
+    return rc;
+}
+
+// Smoother selection: kind 0 multicolour GS, 1 damped Jacobi (omega);
+// symmetric = 1 runs the post-relaxation colours in reverse order.
+void ora_mg_set_smoother(ora_mg* mg, int32_t kind, double omega, int32_t symmetric) {
+    mg->smoother = kind;
+    mg->omega = omega;
+    mg->symmetric = symmetric;
+}
+
+void ora_jacobi_sweep(const ora_csr* A, int32_t k, const double* B, double* X, double omega) {
+    jacobi_sweep(*A, k, B, X, omega);
+}
+
+// Multigrid-preconditioned conjugate gradients ("use our
+// multigrid solver as the pre-conditioner for ... the conjugate gradient
+// method").  Textbook PCG, every column independently:
+//   r = b - A x, z = M^{-1} r, p = z;  repeat: q = A p, alpha = (r,z)/(p,q),
+//   x += alpha p, r -= alpha q, z = M^{-1} r, beta = (r,z)_new/(r,z)_old,
+//   p = z + beta p.
+// M^{-1} r = one V-cycle from a zero guess with the symmetric smoother
+// ordering (forced here).  hist[(it * k) + j] = ||r_it||_2 / ||b_j||_2 of the
+// recursively updated residual; stops when every column <= rel_tol.
+// Returns 0 converged, 8 not converged, 7 NaN/Inf, 4 coarsest not SPD.
+int ora_mg_pcg(ora_mg* mg, int32_t k, const double* B, double* X, double rel_tol, int32_t max_iters, double* hist,
+               int32_t* iters_out) {
+    if (mg->status != 0) return mg->status;
+    const int sym_saved = mg->symmetric;
+    mg->symmetric = 1;
+    const Csr& A = mg->lv[0].A;
+    const int32_t n = A.nrows;
+    const size_t nk = (size_t)n * k;
+    std::vector<double> r(nk), z(nk), p(nk), q(nk);
+    std::vector<double> bnorm(k, 0.0), rz(k), pq(k), rr(k);
+    for (size_t t = 0; t < nk; ++t) bnorm[t % k] += B[t] * B[t];
+    for (int c = 0; c < k; ++c) bnorm[c] = std::sqrt(bnorm[c]);
+    for (int32_t i = 0; i < n; ++i)
+        for (int c = 0; c < k; ++c) r[(size_t)i * k + c] = B[(size_t)i * k + c] - row_dot(A, i, X, k, c);
+    auto record = [&](int it) {
+        std::fill(rr.begin(), rr.end(), 0.0);
+        for (size_t t = 0; t < nk; ++t) rr[t % k] += r[t] * r[t];
+        bool fin = true, done = rel_tol > 0.0;
+        for (int c = 0; c < k; ++c) {
+            const double v = std::sqrt(rr[c]) / (bnorm[c] > 0.0 ? bnorm[c] : 1.0);
+            hist[(size_t)it * k + c] = v;
+            fin &= std::isfinite(v);
+            done &= v <= rel_tol;
+        }
+        return !fin ? 7 : done ? 0 : 8;
+    };
+    int rc = record(0);
+    int32_t it = 0;
+    while (rc == 8 && it < max_iters) {
+        std::fill(z.begin(), z.end(), 0.0);
+        vcycle(*mg, 0, k, r.data(), z.data());
+        std::vector<double> rz_new(k, 0.0);
+        for (size_t t = 0; t < nk; ++t) rz_new[t % k] += r[t] * z[t];
+        for (size_t t = 0; t < nk; ++t) {
+            const int c = (int)(t % k);
+            const double beta = it == 0 ? 0.0 : rz_new[c] / rz[c];
+            p[t] = z[t] + beta * p[t];
+        }
+        rz = rz_new;
+        std::fill(pq.begin(), pq.end(), 0.0);
+        for (int32_t i = 0; i < n; ++i)
+            for (int c = 0; c < k; ++c) {
+                q[(size_t)i * k + c] = row_dot(A, i, p.data(), k, c);
+                pq[c] += p[(size_t)i * k + c] * q[(size_t)i * k + c];
+            }
+        for (size_t t = 0; t < nk; ++t) {
+            const int c = (int)(t % k);
+            const double alpha = rz[c] / pq[c];
+            X[t] += alpha * p[t];
+            r[t] -= alpha * q[t];
+        }
+        ++it;
+        rc = record(it);
+    }
+    mg->symmetric = sym_saved;
+    *iters_out = it;
+    if (rc == 8 && !(rel_tol > 0.0)) rc = 0;
     return rc;
 }
 

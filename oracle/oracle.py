@@ -70,6 +70,10 @@ def lib():
             "ora_mg_vcycle": (None, [_vp, C.c_int32, _f64p, _f64p]),
             "ora_mg_solve": (C.c_int, [_vp, C.c_int32, _f64p, _f64p, C.c_double, C.c_int32, _f64p,
                                        C.POINTER(C.c_int32)]),
+            "ora_mg_set_smoother": (None, [_vp, C.c_int32, C.c_double, C.c_int32]),
+            "ora_jacobi_sweep": (None, [_vp, C.c_int32, _f64p, _f64p, C.c_double]),
+            "ora_mg_pcg": (C.c_int, [_vp, C.c_int32, _f64p, _f64p, C.c_double, C.c_int32, _f64p,
+                                     C.POINTER(C.c_int32)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -202,6 +206,15 @@ def gs_sweep(A, colour, ncolours, B, X):
     return X
 
 
+def jacobi_sweep(A, B, X, omega=0.8):
+    """One damped Jacobi sweep (App. E), X updated in place."""
+    B = _f64(B)
+    k = 1 if B.ndim == 1 else B.shape[1]
+    assert X.dtype == np.float64 and X.flags.c_contiguous
+    lib().ora_jacobi_sweep(A.h, k, B, X, float(omega))
+    return X
+
+
 class MG:
     """Oracle multigrid: setup on construction; vcycle / solve."""
 
@@ -250,6 +263,22 @@ class MG:
         assert X.dtype == np.float64 and X.flags.c_contiguous
         lib().ora_mg_vcycle(self.h, k, B, X)
         return X
+
+    def set_smoother(self, kind=0, omega=0.8, symmetric=False):
+        """kind 0 multicolour GS (reading A2), 1 damped Jacobi (App. E P:885);
+        symmetric: post-relaxation colours in reverse order (row f4)."""
+        lib().ora_mg_set_smoother(self.h, int(kind), float(omega), int(bool(symmetric)))
+        return self
+
+    def pcg(self, B, X0=None, rel_tol=1e-10, max_iters=100):
+        """MG-preconditioned CG (row f4); returns (X, history, rc)."""
+        B = _f64(B)
+        k = 1 if B.ndim == 1 else B.shape[1]
+        X = np.zeros(B.shape) if X0 is None else _f64(X0).copy()
+        hist = np.full((max_iters + 1) * k, np.nan)
+        it = C.c_int32()
+        rc = lib().ora_mg_pcg(self.h, k, B, X, float(rel_tol), int(max_iters), hist, C.byref(it))
+        return X, hist.reshape(max_iters + 1, k)[: it.value + 1], rc
 
     def solve(self, B, X0=None, rel_tol=1e-10, max_cycles=100):
         B = _f64(B)

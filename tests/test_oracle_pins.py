@@ -519,3 +519,118 @@ def test_mcf_sphere_radius(ora):
     r = np.linalg.norm(X, axis=1).mean()
     assert abs(r - g["radius"]) < 1e-3
     assert max(cycles) <= 10
+
+
+# --------------------------------------------------------------------- f4: Jacobi smoother, symmetric V-cycle, MG-PCG
+
+
+def test_jacobi_worked_example_and_splitting_form(ora):
+    g = GOLD["jacobi_2x2"]
+    A = _csr_from_dense(ora, g["A"])
+    x = np.zeros(2)
+    ora.jacobi_sweep(A, np.array(g["b"]), x, g["omega"])
+    assert np.allclose(x, g["x1"], rtol=0, atol=1e-15)
+    ora.jacobi_sweep(A, np.array(g["b"]), x, g["omega"])
+    assert np.allclose(x, g["x2"], rtol=0, atol=1e-15)
+    # splitting form x + omega D^{-1}(b - A x) on a random SPD matrix (numpy, independent)
+    rng = np.random.default_rng(11)
+    Q = rng.standard_normal((9, 9))
+    D = Q @ Q.T + 9 * np.eye(9)
+    A = _csr_from_dense(ora, D)
+    b, x0 = rng.standard_normal((9, 2)), rng.standard_normal((9, 2))
+    ref = x0 + 0.7 * (b - D @ x0) / np.diag(D)[:, None]
+    y = x0.copy()
+    ora.jacobi_sweep(A, b, y, 0.7)
+    assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def _vcycle_operator(mg, n):
+    """Dense matrix of the map b -> V(0, b) (zero initial guess)."""
+    Mi = np.empty((n, n))
+    for j in range(n):
+        e = np.zeros((n, 1))
+        e[j, 0] = 1.0
+        z = np.zeros((n, 1))
+        mg.vcycle(e, z)
+        Mi[:, j] = z[:, 0]
+    return Mi
+
+
+def test_symmetric_vcycle_is_spd_preconditioner(ora):
+    """Row f4: with the post-relaxation colours reversed (and Jacobi, whose
+    sweep is symmetric), the V-cycle map b -> V(0, b) is symmetric positive
+    definite, as CG needs; the default ascending post order is not symmetric."""
+    p = meshgen.make_config(1, subdiv=3)                  # 642 -> 162 -> 42 (nested)
+    V, F = p.levels[0]
+    A, _ = ora.assemble(V, F, 1.0, 1e-2)
+    n = V.shape[0]
+    assert len(p.sizes) == 3
+    mg = ora.MG(p.sizes, p.P, A)
+    Mi = _vcycle_operator(mg, n)
+    asym = np.abs(Mi - Mi.T).max() / np.abs(Mi).max()
+    assert asym > 1e-6                                   # A2: not symmetric as a stand-alone solver
+    for kind in (0, 1):
+        mg.set_smoother(kind, 0.8, symmetric=True)
+        Mi = _vcycle_operator(mg, n)
+        assert np.abs(Mi - Mi.T).max() <= 1e-12 * np.abs(Mi).max()
+        assert np.linalg.eigvalsh(0.5 * (Mi + Mi.T)).min() > 0
+
+
+def test_pcg_special_cases_and_dense_solve(ora):
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    A, M = ora.assemble(V, F, 1.0, 1e-2)
+    n = V.shape[0]
+    D = A.to_scipy().toarray()
+    rng = np.random.default_rng(12)
+    B = rng.standard_normal((n, 2))
+    XS = np.linalg.solve(D, B)
+    # one level: M^{-1} = A^{-1} -> PCG converges in one iteration
+    X, hist, rc = ora.MG([n], [], A).pcg(B, rel_tol=1e-12, max_iters=5)
+    assert rc == 0 and hist.shape[0] == 2
+    assert np.linalg.norm(X - XS) / np.linalg.norm(XS) <= 1e-12
+    # multigrid preconditioner (GS and Jacobi smoothers): dense solution to 1e-10
+    for kind in (0, 1):
+        mg = ora.MG(p.sizes, p.P, A).set_smoother(kind, 0.8)
+        X, hist, rc = mg.pcg(B, rel_tol=1e-12, max_iters=60)
+        assert rc == 0
+        for c in range(2):
+            assert np.linalg.norm(X[:, c] - XS[:, c]) / np.linalg.norm(XS[:, c]) <= 1e-10
+        # the recursive residual ends within the tolerance; and the true residual agrees
+        assert (hist[-1] <= 1e-12).all()
+        tr = np.linalg.norm(B - D @ X, axis=0) / np.linalg.norm(B, axis=0)
+        assert (tr <= 1e-11).all()
+    # b = 0 -> converged at iteration 0
+    X, hist, rc = ora.MG(p.sizes, p.P, A).pcg(np.zeros((n, 1)), rel_tol=1e-10, max_iters=5)
+    assert rc == 0 and hist.shape[0] == 1 and not X.any()
+
+
+def test_pcg_energy_error_decreases(ora):
+    """CG theory: the A-norm error decreases monotonically per iteration."""
+    p = meshgen.make_config(3, grid=(48, 40))
+    V, F = p.levels[0]
+    A, _ = ora.assemble(V, F, 1.0, 1e-2)
+    D = A.to_scipy().toarray()
+    b = np.random.default_rng(13).standard_normal((V.shape[0], 1))
+    xs = np.linalg.solve(D, b)
+    mg = ora.MG(p.sizes, p.P, A)
+    x = np.zeros_like(b)
+    prev = float((xs - x).T @ D @ (xs - x))
+    for it in range(1, 6):
+        X, hist, rc = mg.pcg(b, rel_tol=0.0, max_iters=it)
+        e = float((xs - X).T @ D @ (xs - X))
+        assert e < prev
+        prev = e
+
+
+def test_jacobi_multigrid_converges(ora):
+    """App. E: damped-Jacobi-smoothed V(2,2) still converges (each cycle
+    contracts), more slowly than Gauss-Seidel."""
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    A, _ = ora.assemble(V, F, 1.0, 1e-2)
+    b = np.random.default_rng(14).standard_normal((V.shape[0], 1))
+    _, hg, _ = ora.MG(p.sizes, p.P, A).solve(b, rel_tol=0.0, max_cycles=6)
+    _, hj, _ = ora.MG(p.sizes, p.P, A).set_smoother(1, 0.8).solve(b, rel_tol=0.0, max_cycles=6)
+    assert (np.diff(hj[:, 0]) < 0).all()
+    assert hj[-1, 0] > hg[-1, 0]
