@@ -125,6 +125,31 @@ int mg_apply_mass(mg_ctx* ctx, int32_t k, const double* X, double* B);
 int mg_solve(mg_ctx* ctx, int32_t k, const double* B, double* X, double rel_tol, int32_t max_cycles,
              double* res_hist, int32_t* cycles_out);
 
+/* ---- smoother variants and MG-preconditioned CG ---------- */
+
+/* Relaxation used by every level of the V-cycle.
+ *   kind 0: multicolour Gauss-Seidel over the Alg. 3 colouring (default,
+ *           reading A2: pre- and post-sweeps in ascending colour order);
+ *   kind 1: damped Jacobi x <- x + omega D^{-1} (b - A x) ("(damped) Jacobi",
+ *           App. E), omega in (0, 1] (default 0.8, SPEC reading).
+ *   symmetric != 0: post-relaxation colours in DESCENDING order, so the
+ *           post-smoother is the adjoint of the pre-smoother and the V-cycle
+ *           is a symmetric operator (mg_solve_pcg always uses it).
+ * Errors: MG_ERR_INVALID_ARG (unknown kind, omega out of range). */
+int mg_set_smoother(mg_ctx* ctx, int kind, double omega, int symmetric);
+
+/* Solve A X = B by conjugate gradients preconditioned with one symmetric
+ * V-cycle from a zero guess per iteration ("use our multigrid solver as the
+ * pre-conditioner for ... the conjugate gradient method").  Every
+ * column independently (own alpha, beta), all columns iterated until every
+ * column meets rel_tol.  Arguments and layout as mg_solve; res_hist[it*k + j]
+ * = ||r_it||_2 / ||b_j||_2 of the recursively updated PCG residual, entry 0
+ * the initial residual.  Requires mu_pre == mu_post (symmetric
+ * preconditioner).  Returns MG_OK, MG_NOT_CONVERGED (X holds the last
+ * iterate), MG_ERR_NUMERIC, MG_ERR_STATE, MG_ERR_INVALID_ARG. */
+int mg_solve_pcg(mg_ctx* ctx, int32_t k, const double* B, double* X, double rel_tol, int32_t max_iters,
+                 double* res_hist, int32_t* iters_out);
+
 /* ---- fast data smoothing (App. D) -------------
  * The data-smoothing system (alpha Q + (1 - alpha) M) x = (1 - alpha) M f
  * (App. D eq. 1) has coarse operators

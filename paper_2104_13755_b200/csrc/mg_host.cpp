@@ -193,6 +193,9 @@ struct mg_ctx {
     int npad = 0;
     DBuf<double> D, Linv, Ainv, Wbuf;
     int coarse_mode = 1;             // 1: explicit inverse + GEMV (default), 0: one-CTA triangular solves
+    int smoother = 0;                // 0 multicolour GS (reading A2), 1 damped Jacobi (App. E)
+    double omega = 0.8;              // Jacobi damping
+    bool symmetric = false;          // post-relaxation colours reversed (symmetric V-cycle)
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool use_gal2 = true;            // Galerkin v2 kernel
@@ -211,6 +214,10 @@ struct mg_ctx {
 
     cudaGraphExec_t vc_exec[kMaxK + 1] = {};
     int vc_launches[kMaxK + 1] = {};
+    cudaGraphExec_t pcg_exec[kMaxK + 1] = {};   // one MG-PCG iteration (row f4)
+    int pcg_launches[kMaxK + 1] = {};
+    DBuf<double> pcg_x, pcg_r, pcg_p, pcg_q, pcg_partial, pcg_sc;
+    DBuf<int> pcg_first;
 
     uint32_t prof_mask = 0;          // bit c: time kernel class c (see mg.h)
     uint32_t prof_levels = 0xffff;   // bit l: time level l
@@ -221,6 +228,7 @@ struct mg_ctx {
     };
     std::vector<Ev> ev_pending;             // eager launches, harvested at the next sync
     std::vector<Ev> graph_ev[kMaxK + 1];    // event-record nodes inside the V-cycle graphs
+    std::vector<Ev> pcg_graph_ev[kMaxK + 1];
     std::vector<Ev>* cap_events = nullptr;
     std::vector<cudaEvent_t> ev_pool;
     double prof_ms[kProfClasses * kProfLevels] = {};
@@ -245,11 +253,17 @@ struct mg_ctx {
                 cudaGraphExecDestroy(vc_exec[k]);
                 vc_exec[k] = nullptr;
             }
-            for (auto& ev : graph_ev[k]) {
-                ev_pool.push_back(ev.a);
-                ev_pool.push_back(ev.b);
+            if (pcg_exec[k]) {
+                cudaGraphExecDestroy(pcg_exec[k]);
+                pcg_exec[k] = nullptr;
             }
-            graph_ev[k].clear();
+            for (auto* v : {&graph_ev[k], &pcg_graph_ev[k]}) {
+                for (auto& ev : *v) {
+                    ev_pool.push_back(ev.a);
+                    ev_pool.push_back(ev.b);
+                }
+                v->clear();
+            }
         }
     }
     cudaEvent_t get_event() {
@@ -302,6 +316,9 @@ struct mg_ctx {
     }
     void harvest_graph(int K) {
         for (auto& ev : graph_ev[K]) accumulate(ev);
+    }
+    void harvest_pcg_graph(int K) {
+        for (auto& ev : pcg_graph_ev[K]) accumulate(ev);
     }
     ~mg_ctx() {
         drop_graphs();
@@ -677,19 +694,39 @@ int split_hierarchy(mg_ctx* c) {
 
 // One V-cycle (Alg. 2; reading A1) on all K columns, then the
 // residual norm of the new iterate into c->rho.
-void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
+// mu relaxation sweeps on level L: multicolour GS in ascending colour order
+// (reading A2; descending when `reverse`, the adjoint used by the symmetric
+// V-cycle), or damped Jacobi (App. E) alternating x -> r -> x.
+int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    int n = 0;
+    if (c->smoother == 1) {
+        for (int it = 0; it < mu; ++it)
+            n += (it & 1) ? vc_jacobi(K, L, L.r.p, L.x.p, c->omega, pdl, s) : vc_jacobi(K, L, L.x.p, L.r.p, c->omega, pdl, s);
+        if (mu & 1) {
+            cudaMemcpyAsync(L.x.p, L.r.p, sizeof(double) * (size_t)L.n * kMaxK, cudaMemcpyDeviceToDevice, s);
+        }
+        return n;
+    }
+    for (int it = 0; it < mu; ++it)
+        for (int q = 0; q < L.ncolours; ++q) {
+            const int k = reverse ? L.ncolours - 1 - q : q;
+            n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
+        }
+    return n;
+}
+
+// One V-cycle (Alg. 2) on all K columns of level 0's x / b, without the
+// residual norm.  symmetric: post-relaxation in reverse colour order.
+void enqueue_vcycle_body(mg_ctx* c, int K, cudaStream_t s, bool symmetric) {
     const int H = c->H;
     const bool pdl = c->pdl;
-    const int lt = c->tail_start >= 0 ? c->tail_start : H;   // levels >= lt: tail (or coarsest solve)
+    // the cluster tail implements forward multicolour GS only
+    const bool tail_ok = c->smoother == 0 && !symmetric;
+    const int lt = (tail_ok && c->tail_start >= 0) ? c->tail_start : H;   // levels >= lt: tail (or coarsest solve)
     for (int l = 0; l < lt; ++l) {
         Level& L = *c->lv[l];
         WindowScope ws(L.has_win ? &L.win : nullptr);
-        c->timed(PC_GS, l, s, [&] {
-            int n = 0;
-            for (int it = 0; it < c->mu_pre; ++it)
-                for (int k = 0; k < L.ncolours; ++k) n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
-            return n;
-        });
+        c->timed(PC_GS, l, s, [&] { return relax(c, K, L, c->mu_pre, false, pdl, s); });
         c->timed(PC_RESTRICT, l, s, [&] {
             return vc_residual(K, L, pdl, s) + vc_restrict(K, *c->lv[l + 1], L, pdl, s);
         });
@@ -731,16 +768,16 @@ void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
         Level& L = *c->lv[l];
         WindowScope ws(L.has_win ? &L.win : nullptr);
         c->timed(PC_PROLONG, l, s, [&] { return vc_prolong(K, L, *c->lv[l + 1], pdl, s); });
-        c->timed(PC_GS, l, s, [&] {
-            int n = 0;
-            for (int it = 0; it < c->mu_post; ++it)
-                for (int k = 0; k < L.ncolours; ++k) n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
-            return n;
-        });
+        c->timed(PC_GS, l, s, [&] { return relax(c, K, L, c->mu_post, symmetric, pdl, s); });
     }
+}
+
+// One V-cycle and the residual norm of the new iterate into c->rho.
+void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
+    enqueue_vcycle_body(c, K, s, c->symmetric);
     WindowScope ws(c->lv[0]->has_win ? &c->lv[0]->win : nullptr);
     c->timed(PC_RESNORM, 0, s, [&] {
-        return vc_resnorm(K, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p, c->rho.p, pdl, s);
+        return vc_resnorm(K, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p, c->rho.p, c->pdl, s);
     });
 }
 
@@ -767,6 +804,44 @@ int get_vcycle_graph(mg_ctx* c, int K, cudaGraphExec_t* out) {
     cudaGraphDestroy(g);
     if (e) return c->cuda_fail(e, "graph instantiate");
     *out = c->vc_exec[K];
+    return MG_OK;
+}
+
+// One MG-PCG iteration (row f4) on level-0 internal vectors:
+// z = V(0, r) with the symmetric V-cycle, then the PCG direction and step,
+// then rho = |r| / |b| copied to the host.
+int get_pcg_graph(mg_ctx* c, int K, cudaGraphExec_t* out) {
+    if (c->pcg_exec[K]) {
+        *out = c->pcg_exec[K];
+        return MG_OK;
+    }
+    Level& L0 = *c->lv[0];
+    const int n = L0.n;
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal);
+    if (e) return c->cuda_fail(e, "graph capture");
+    const int64_t before = c->launches;
+    c->capturing = true;
+    c->cap_events = &c->pcg_graph_ev[K];
+    cudaStream_t s = c->cap;
+    c->launches += pcg_prep(K, c->pcg_r.p, L0.b.p, L0.x.p, n, c->pdl, s);
+    enqueue_vcycle_body(c, K, s, true);
+    c->launches += pcg_direction(K, c->pcg_r.p, L0.x.p, c->pcg_p.p, n, c->pcg_partial.p, c->pcg_sc.p, c->pcg_first.p,
+                                 c->pdl, s);
+    c->launches += pcg_step(K, L0, c->pcg_x.p, c->pcg_r.p, c->pcg_p.p, c->pcg_q.p, c->pcg_partial.p, c->pcg_sc.p,
+                            c->pdl, s);
+    c->launches += vc_norm_finalize(K, c->pcg_partial.p, pcg_update_blocks(n), c->bnorm.p, c->rho.p, c->pdl, s);
+    c->capturing = false;
+    c->cap_events = nullptr;
+    c->pcg_launches[K] = (int)(c->launches - before);
+    c->launches = before;
+    e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * K, cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = cudaStreamEndCapture(c->cap, &g);
+    if (e || e2) return c->cuda_fail(e ? e : e2, "graph capture");
+    e = cudaGraphInstantiate(&c->pcg_exec[K], g, 0);
+    cudaGraphDestroy(g);
+    if (e) return c->cuda_fail(e, "graph instantiate");
+    *out = c->pcg_exec[K];
     return MG_OK;
 }
 
@@ -1226,6 +1301,99 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
     if (cycles_out) *cycles_out = cyc;
     if (status == MG_ERR_NUMERIC) c->fail(MG_ERR_NUMERIC, "non-finite residual norm at cycle %d", cyc);
     if (status == MG_NOT_CONVERGED) c->fail(MG_NOT_CONVERGED, "not converged after %d cycles", cyc);
+    return status;
+}
+
+int mg_set_smoother(mg_ctx* c, int kind, double omega, int symmetric) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (kind != 0 && kind != 1) return c->fail(MG_ERR_INVALID_ARG, "smoother kind must be 0 (GS) or 1 (Jacobi)");
+    if (kind == 1 && !(omega > 0.0 && omega <= 1.0)) return c->fail(MG_ERR_INVALID_ARG, "Jacobi damping must be in (0, 1]");
+    c->smoother = kind;
+    c->omega = kind == 1 ? omega : 0.8;
+    c->symmetric = symmetric != 0;
+    c->drop_graphs();
+    return MG_OK;
+}
+
+int mg_solve_pcg(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, int32_t max_iters,
+                 double* res_hist, int32_t* iters_out) {
+    int rc = check_state(c, true);
+    if (rc) return rc;
+    if (k < 1 || k > kMaxK || !B || !X || max_iters < 0)
+        return c->fail(MG_ERR_INVALID_ARG, "need 1 <= k <= %d, non-null B and X, max_iters >= 0", kMaxK);
+    if (c->mu_pre != c->mu_post)
+        return c->fail(MG_ERR_INVALID_ARG, "MG-PCG needs a symmetric preconditioner: mu_pre == mu_post");
+    cudaStream_t s = c->stream;
+    Level& L0 = *c->lv[0];
+    const int32_t n = L0.n;
+    const size_t nv = (size_t)n * kMaxK;
+    cudaError_t e;
+    if ((e = c->pcg_x.alloc(nv)) || (e = c->pcg_r.alloc(nv)) || (e = c->pcg_p.alloc(nv)) || (e = c->pcg_q.alloc(nv)) ||
+        (e = c->pcg_partial.alloc((size_t)pcg_blocks() * kMaxK)) || (e = c->pcg_sc.alloc(3 * kMaxK)) ||
+        (e = c->pcg_first.alloc(1)))
+        return c->cuda_fail(e, "mg_solve_pcg alloc");
+    const bool devX = is_device_ptr(X);
+    const double* dB = nullptr;
+    const double* dX = nullptr;
+    if ((rc = to_device(c, B, c->stageB, (size_t)n * k, &dB))) return rc;
+    if ((rc = to_device(c, X, c->stageX, (size_t)n * k, &dX))) return rc;
+    c->timed(PC_PERMUTE, 0, s, [&] {
+        return launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s) +
+               vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
+    });
+    // r0 = b - A x0; x <- x0; p <- 0; rho_0
+    c->launches += vc_residual(k, L0, false, s);
+    if ((e = cudaMemcpyAsync(c->pcg_r.p, L0.r.p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s)) ||
+        (e = cudaMemcpyAsync(c->pcg_x.p, L0.x.p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s)) ||
+        (e = cudaMemsetAsync(c->pcg_p.p, 0, sizeof(double) * nv, s)) ||
+        (e = cudaMemsetAsync(c->pcg_first.p, 1, sizeof(int), s)))
+        return c->cuda_fail(e, "mg_solve_pcg init");
+    c->launches += vc_sumsq(k, c->pcg_r.p, n, c->partial.p, resnorm_blocks(n), c->rho.p, s);
+    double bn[kMaxK];
+    if ((e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s)) ||
+        (e = cudaMemcpyAsync(bn, c->bnorm.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s)) ||
+        (e = cudaStreamSynchronize(s)))
+        return c->cuda_fail(e, "mg_solve_pcg");
+    for (int j = 0; j < k; ++j) c->h_rho[j] /= (bn[j] > 0.0 ? bn[j] : 1.0);
+    cudaGraphExec_t exec = nullptr;
+    if ((rc = get_pcg_graph(c, k, &exec))) return rc;
+    int32_t it = 0;
+    int status = MG_NOT_CONVERGED;
+    while (true) {
+        bool finite = true, done = rel_tol > 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double r = c->h_rho[j];
+            if (res_hist) res_hist[(size_t)it * k + j] = r;
+            finite &= std::isfinite(r);
+            done &= (r <= rel_tol);
+        }
+        if (!finite) {
+            status = MG_ERR_NUMERIC;
+            break;
+        }
+        if (done) {
+            status = MG_OK;
+            break;
+        }
+        if (it >= max_iters) break;
+        e = cudaGraphLaunch(exec, s);
+        c->launches += c->pcg_launches[k];
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) return c->cuda_fail(e, "mg_solve_pcg iteration");
+        if (c->prof_mask) c->harvest_pcg_graph(k);
+        ++it;
+    }
+    if (status == MG_NOT_CONVERGED && !(rel_tol > 0.0)) status = MG_OK;   // fixed-iteration mode
+    double* dXout = devX ? X : c->stageX.p;
+    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.diperm.p, c->pcg_x.p, dXout, n, s); });
+    if (!devX && (e = cudaMemcpyAsync(X, dXout, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s)))
+        return c->cuda_fail(e, "mg_solve_pcg");
+    if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "mg_solve_pcg");
+    if ((e = cudaGetLastError())) return c->cuda_fail(e, "mg_solve_pcg kernels");
+    c->harvest_events();
+    if (iters_out) *iters_out = it;
+    if (status == MG_ERR_NUMERIC) c->fail(MG_ERR_NUMERIC, "non-finite residual norm at iteration %d", it);
+    if (status == MG_NOT_CONVERGED) c->fail(MG_NOT_CONVERGED, "not converged after %d iterations", it);
     return status;
 }
 

@@ -147,7 +147,8 @@ struct TailParams {
 // (V-cycle graph).
 // mg_vcycle.cu
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
-int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);                    // L.r = L.b - A L.x
+int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
+int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
 int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
 int vc_prolong(int K, const Level& fine, const Level& coarse, bool pdl, cudaStream_t s);   // fine.x += P coarse.x
 int vc_coarse_gemv(int K, const double* Z, int npad, int n, const double* b, double* x, bool pdl, cudaStream_t s);
@@ -156,11 +157,20 @@ int vc_coarse_trsv(int K, const double* L, const double* Linv, int npad, int n, 
 int vc_resnorm(int K, const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl,
                cudaStream_t s);
 int vc_sumsq(int K, const double* v, int n, double* partial, int nb, double* out, cudaStream_t s);
+int vc_norm_finalize(int K, const double* partial, int nb, const double* denom, double* out, bool pdl, cudaStream_t s);
 int resnorm_blocks(int n);
 int tile_rows();
 size_t tile_smem_limit();
 size_t pipe_smem_bytes(int cap);
 void init_vcycle_attributes();
+// mg_krylov.cu (MG-preconditioned CG, row f4)
+int pcg_blocks();
+int pcg_update_blocks(int n);
+int pcg_prep(int K, const double* r, double* b0, double* x0, int n, bool pdl, cudaStream_t s);
+int pcg_direction(int K, const double* r, const double* z, double* p, int n, double* partial, double* sc, int* first,
+                  bool pdl, cudaStream_t s);
+int pcg_step(int K, const Level& L0, double* x, double* r, const double* p, double* q, double* partial, double* sc,
+             bool pdl, cudaStream_t s);
 // mg_tail.cu
 int tail_cluster_size();
 int vc_tail(int K, const TailParams& p, int cs, bool pdl, cudaStream_t s);

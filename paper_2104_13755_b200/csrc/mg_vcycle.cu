@@ -108,11 +108,12 @@ struct Unroll {
 
 // MODE 0: GS colour pass  x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii  on rows [r0, r1)
 // MODE 1: residual        r_i = b_i - sum_j a_ij x_j                   on rows [r0, r1)
+// MODE 3: damped Jacobi   r_i = x_i + omega (b_i - sum_j a_ij x_j) / a_ii (App. E; into r)
 template <int K, int MODE>
 __global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp, const int* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1,
-                                                      int cap) {
+                                                      int cap, double omega) {
     extern __shared__ double smem_d[];
     __shared__ int rps[kTile + 1];
     double* vs = smem_d;
@@ -136,8 +137,11 @@ __global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp
         strow<K>(x + (size_t)row * VS<K>::S, xn);
     } else {
 #pragma unroll
-        for (int c = 0; c < K; ++c)
-            r[(size_t)row * VS<K>::S + c] = b[(size_t)row * VS<K>::S + c] - fma(d, x[(size_t)row * VS<K>::S + c], s[c]);
+        for (int c = 0; c < K; ++c) {
+            const double xi = x[(size_t)row * VS<K>::S + c];
+            const double rr = b[(size_t)row * VS<K>::S + c] - fma(d, xi, s[c]);
+            r[(size_t)row * VS<K>::S + c] = MODE == 3 ? xi + omega * rr / d : rr;
+        }
     }
 }
 
@@ -149,7 +153,8 @@ __global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp
 // evict-first) completing on an mbarrier, while all threads compute tile i.
 // Tile descriptors {row0, nrow, e0, e1} are precomputed per level, so no
 // pointer chase precedes a copy.  Gathers of x skip the diagonal (predicated).
-// MODE 0: GS pass, 1: residual r = b - A x, 2: residual-norm partial sums.
+// MODE 0: GS pass, 1: residual r = b - A x, 2: residual-norm partial sums,
+// 3: damped Jacobi r = x + omega D^{-1} (b - A x).
 struct TileDesc {
     int row0, nrow, e0, e1;
 };
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
                                                      const int* __restrict__ rp, const int* __restrict__ col,
                                                      const double* __restrict__ val, const double* __restrict__ b,
                                                      double* __restrict__ x, double* __restrict__ r,
-                                                     double* __restrict__ partial, int cap) {
+                                                     double* __restrict__ partial, int cap, double omega) {
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
     const int tid = threadIdx.x;
@@ -322,6 +327,11 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
                 for (int c = 0; c < K; ++c) rr[c] = bv[c] - fma(dg, xr[c], s[c]);
                 if (MODE == 1) {
                     strow_pol<K>(r + (size_t)row * VS<K>::S, rr, xpol);
+                } else if (MODE == 3) {
+                    double xo[K];
+#pragma unroll
+                    for (int c = 0; c < K; ++c) xo[c] = xr[c] + omega * rr[c] / dg;
+                    strow_pol<K>(r + (size_t)row * VS<K>::S, xo, xpol);
                 } else {
 #pragma unroll
                     for (int c = 0; c < K; ++c) acc[c] = fma(rr[c], rr[c], acc[c]);
@@ -359,7 +369,8 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
 template <int K, int LPR, int MODE>
 __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ b,
-                                                      double* __restrict__ x, double* __restrict__ r, int r0, int r1) {
+                                                      double* __restrict__ x, double* __restrict__ r, int r0, int r1,
+                                                      double omega) {
     constexpr int U = 32 / LPR;
     // gathers in flight per lane: the whole prefetch for LPR >= 8, batches of
     // 4 for LPR = 4 (8 entries per lane) to keep registers / occupancy
@@ -391,9 +402,9 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
     // the row's right-hand side goes out with the gathers (one round trip)
     double bv[K];
     if (lane == 0) ldrow<K>(b + (size_t)row * VS<K>::S, bv);
-    double s[K];
+    double s[K], xi[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) s[c] = 0.0;
+    for (int c = 0; c < K; ++c) s[c] = xi[c] = 0.0;
     double d = 0.0;
 #pragma unroll
     for (int u0 = 0; u0 < U; u0 += GB) {
@@ -410,6 +421,11 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
             if (MODE == 0 && jj == row) {
                 d += a[u0 + u];
             } else {
+                if (MODE == 3 && jj == row) {
+                    d += a[u0 + u];
+#pragma unroll
+                    for (int c = 0; c < K; ++c) xi[c] = xv[u][c];
+                }
 #pragma unroll
                 for (int c = 0; c < K; ++c) s[c] = fma(a[u0 + u], xv[u][c], s[c]);
             }
@@ -423,17 +439,26 @@ __global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp
         } else {
             double xv[K];
             ldrow_pol<K>(x + (size_t)jj * VS<K>::S, xv, xpol);
+            if (MODE == 3 && jj == row) {
+                d += av;
+#pragma unroll
+                for (int c = 0; c < K; ++c) xi[c] = xv[c];
+            }
 #pragma unroll
             for (int c = 0; c < K; ++c) s[c] = fma(av, xv[c], s[c]);
         }
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
-    if (MODE == 0) d = group_sum<LPR>(d, mask);
+    if (MODE == 0 || MODE == 3) d = group_sum<LPR>(d, mask);
+    if (MODE == 3)
+#pragma unroll
+        for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], mask);   // only the diagonal's lane holds x_i
     if (lane == 0) {
         double out[K];
 #pragma unroll
-        for (int c = 0; c < K; ++c) out[c] = MODE == 0 ? (bv[c] - s[c]) / d : bv[c] - s[c];
+        for (int c = 0; c < K; ++c)
+            out[c] = MODE == 0 ? (bv[c] - s[c]) / d : MODE == 3 ? xi[c] + omega * (bv[c] - s[c]) / d : bv[c] - s[c];
         if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
         else strow<K>(r + (size_t)row * VS<K>::S, out);
     }
@@ -834,16 +859,21 @@ inline int pipe_grid(int ntiles, int cap) {
 }
 inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
 
-// MODE 0/1 over tiles [t0, t1) of level L
+// MODE 0..3 over tiles [t0, t1) of level L (iterate read from xin)
 template <int K, int MODE>
-void pipe_launch(const Level& L, int t0, int t1, double* r, double* partial, int grid, bool pdl, cudaStream_t s) {
+void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double* partial, int grid, double omega,
+                 bool pdl, cudaStream_t s) {
     launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, pipe_smem(L.pipe_cap), s,
-             reinterpret_cast<const TileDesc*>(L.tiles.p), t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, partial,
-             L.pipe_cap);
+             reinterpret_cast<const TileDesc*>(L.tiles.p), t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial,
+             L.pipe_cap, omega);
 }
 
+// MODE 0: GS pass on rows [r0, r1) in place on L.x; MODE 1: r = b - A x;
+// MODE 3: Jacobi out = x + omega D^{-1}(b - A x).  xin: iterate read (L.x if null).
 template <int K, int MODE>
-int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s) {
+int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s, double* xin = nullptr,
+            double omega = 0.0) {
+    double* xp = xin ? xin : L.x.p;
     const int rows = r1 - r0;
     if (rows <= 0) return 0;
     if (L.pipe) {
@@ -858,22 +888,22 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s)
             t0 = L.tile_off[L.tile_off.size() - 2];   // whole-level tiles are the last range
             t1 = L.tile_off.back();
         }
-        pipe_launch<K, MODE>(L, t0, t1, r, nullptr, pipe_grid(t1 - t0, L.pipe_cap), pdl, s);
+        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(t1 - t0, L.pipe_cap), omega, pdl, s);
         return 1;
     }
     if (L.tiled) {
         const int cap = MODE == 0 ? L.cap_gs : L.cap_all;
         launch_k(pdl, k_tile_sweep<K, MODE>, nblk(rows, kTile), kTile, tile_smem(cap), s, L.rp.p, L.col.p, L.val.p,
-                 L.b.p, L.x.p, r, r0, r1, cap);
+                 L.b.p, xp, r, r0, r1, cap, omega);
         return 1;
     }
     const int lpr = MODE == 0 ? L.lpr : L.lpr_all;
     const int grid = nblk((int64_t)rows * lpr, kBlock);
     switch (lpr) {
-        case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
-        case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
-        case 16: launch_k(pdl, k_lpr_sweep<K, 16, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
-        default: launch_k(pdl, k_lpr_sweep<K, 32, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, L.x.p, r, r0, r1); break;
+        case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        case 16: launch_k(pdl, k_lpr_sweep<K, 16, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        default: launch_k(pdl, k_lpr_sweep<K, 32, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
     }
     return 1;
 }
@@ -884,7 +914,7 @@ int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, doub
     if (L.pipe) {
         const int t0 = L.tile_off[L.tile_off.size() - 2], t1 = L.tile_off.back();
         grid = std::min(nb, pipe_grid(t1 - t0, L.pipe_cap));
-        pipe_launch<K, 2>(L, t0, t1, nullptr, partial, grid, pdl, s);
+        pipe_launch<K, 2>(L, t0, t1, L.x.p, nullptr, partial, grid, 0.0, pdl, s);
     } else if (L.tiled) {
         grid = std::min(nb, nblk(L.n, kTile));
         launch_k(pdl, k_resnorm_tiled<K>, grid, kTile, tile_smem(L.cap_all), s, L.rp.p, L.col.p, L.val.p, L.b.p,
@@ -912,6 +942,8 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_pipe<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_sweep<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 }
 
 #define MG_K_SWITCH(K, EXPR_T)                  \
@@ -939,6 +971,9 @@ void init_vcycle_attributes() {
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
 }
+int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (sweep_k<KK, 3>(L, 0, L.n, xout, pdl, s, xin, omega)))
+}
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 1>(L, 0, L.n, L.r.p, pdl, s)))
 }
@@ -960,6 +995,9 @@ int vc_coarse_trsv(int K, const double* L, const double* Linv, int npad, int n, 
 int vc_resnorm(int K, const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl,
                cudaStream_t s) {
     MG_K_SWITCH(K, (resnorm_k<KK>(L, partial, nb, bnorm, rho, pdl, s)))
+}
+int vc_norm_finalize(int K, const double* partial, int nb, const double* denom, double* out, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_k(pdl, k_norm_finalize<KK>, 1, kBlock, 0, s, partial, nb, denom, out), 1))
 }
 int vc_sumsq(int K, const double* v, int n, double* partial, int nb, double* out, cudaStream_t s) {
     const int grid = std::min(nb, std::max(1, nblk(n, kBlock)));

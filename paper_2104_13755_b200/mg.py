@@ -55,6 +55,8 @@ def lib():
             "mg_set_matrix_split": (C.c_int, [_vp, i32, i64, _vp, _vp, _vp, _vp]),
             "mg_set_matrix_split_cotan": (C.c_int, [_vp, _vp]),
             "mg_set_alpha": (C.c_int, [_vp, dbl]),
+            "mg_set_smoother": (C.c_int, [_vp, C.c_int, dbl, C.c_int]),
+            "mg_solve_pcg": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_solve": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_level_info": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
             "mg_get_level_csr": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
@@ -178,6 +180,20 @@ def mg_solve(ctx, k, B, X, rel_tol, max_cycles, res_hist=None):
                         _ptr(res_hist, np.float64), C.byref(cyc))
     _check(ctx, rc, allow=(MG_NOT_CONVERGED,))
     return rc, cyc.value
+
+
+def mg_set_smoother(ctx, kind=0, omega=0.8, symmetric=False):
+    """kind 0 multicolour GS, 1 damped Jacobi; symmetric: reversed post colours."""
+    return _check(ctx, lib().mg_set_smoother(ctx, int(kind), float(omega), int(bool(symmetric))))
+
+
+def mg_solve_pcg(ctx, k, B, X, rel_tol, max_iters, res_hist=None):
+    """MG-preconditioned CG; returns (status, iterations)."""
+    it = C.c_int32(0)
+    rc = lib().mg_solve_pcg(ctx, int(k), _ptr(B, np.float64), _ptr(X, np.float64), float(rel_tol), int(max_iters),
+                            _ptr(res_hist, np.float64), C.byref(it))
+    _check(ctx, rc, allow=(MG_NOT_CONVERGED,))
+    return rc, it.value
 
 
 def mg_level_info(ctx, l):
@@ -332,6 +348,17 @@ class Solver:
         if hist is not None:
             hist = hist.reshape(max_cycles + 1, k)[: cyc + 1]
         return rc, cyc, hist
+
+    def set_smoother(self, kind=0, omega=0.8, symmetric=False):
+        return mg_set_smoother(self.ctx, kind, omega, symmetric)
+
+    def solve_pcg(self, B, X, rel_tol=1e-10, max_iters=100, history=True):
+        k = 1 if B.ndim == 1 else B.shape[1]
+        hist = np.full((max_iters + 1) * k, np.nan) if history else None
+        rc, it = mg_solve_pcg(self.ctx, k, B, X, rel_tol, max_iters, hist)
+        if hist is not None:
+            hist = hist.reshape(max_iters + 1, k)[: it + 1]
+        return rc, it, hist
 
     def level(self, l, values=True):
         rp, col, val = mg_get_level_csr(self.ctx, l, values)

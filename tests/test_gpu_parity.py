@@ -346,3 +346,54 @@ def test_split_csr_equals_split_cotan(ora):
             check_level_parity(S2, mgo, l)
     with pytest.raises(mg.MGError):
         gpu_solver(p).set_alpha(0.5)                          # MG_ERR_STATE: no split operators
+
+
+@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
+def test_smoother_variants_parity(ora, cid, kw):
+    """Row f4: damped-Jacobi smoothing (App. E) and the symmetric
+    (reversed post colours) V-cycle match the oracle's same variants."""
+    p = meshgen.make_config(cid, **kw)
+    A, M, _ = oracle_problem(ora, p)
+    Bo = oracle_rhs(ora, p, M)
+    for kind, omega, sym in ((1, 0.8, False), (1, 0.6, True), (0, 0.8, True)):
+        mgo = ora.MG(p.sizes, p.P, A).set_smoother(kind, omega, sym)
+        Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=4)
+        S = gpu_solver(p)
+        S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+        S.set_smoother(kind, omega, sym)
+        Xg = np.zeros_like(Bo)
+        rc, cyc, hg = S.solve(Bo, Xg, rel_tol=0.0, max_cycles=4)
+        check_x(Xg, Xo)
+        check_history(hg, ho, tau_floor(A.to_scipy(), Xo, Bo))
+        S.close()
+
+
+@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)}), (2, {"subdiv": 5})])
+def test_pcg_parity(ora, cid, kw):
+    """Row f4: MG-preconditioned CG on the GPU against the oracle's
+    PCG: same iterate after the same iterations, same recursive-residual
+    history; its own stopping rule within +-1 iteration."""
+    p = meshgen.make_config(cid, **kw)
+    A, M, _ = oracle_problem(ora, p)
+    Bo = oracle_rhs(ora, p, M)
+    for kind in (0, 1):
+        mgo = ora.MG(p.sizes, p.P, A).set_smoother(kind, 0.8)
+        Xo, ho, rco = mgo.pcg(Bo, rel_tol=1e-10, max_iters=60)
+        it_o = ho.shape[0] - 1
+        S = gpu_solver(p)
+        S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+        S.set_smoother(kind, 0.8)
+        Xg = np.zeros_like(Bo)
+        rc, it, hg = S.solve_pcg(Bo, Xg, rel_tol=0.0, max_iters=it_o)
+        assert it == it_o
+        check_x(Xg, Xo)
+        check_history(hg, ho, tau_floor(A.to_scipy(), Xo, Bo))
+        Xg2 = np.zeros_like(Bo)
+        rc2, it2, _ = S.solve_pcg(Bo, Xg2, rel_tol=1e-10, max_iters=60)
+        assert rc2 == 0 and abs(it2 - it_o) <= 1
+        S.close()
+    from paper_2104_13755_b200 import mg
+    S = gpu_solver(p, mu=(2, 1))
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    with pytest.raises(mg.MGError):
+        S.solve_pcg(Bo, np.zeros_like(Bo))                # mu_pre != mu_post: not a symmetric preconditioner
