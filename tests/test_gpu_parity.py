@@ -226,9 +226,11 @@ def test_errors_are_reported():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cid", [2, 3])
+@pytest.mark.parametrize("cid", [2, 3, 4])
 def test_full_size_parity(ora, cid):
-    """BASELINE.json configs 2 and 3 at full size, full-vector comparison."""
+    """BASELINE.json configs 2, 3 and 4 at full size (the launch configuration
+    bench.py times), full-vector comparison: every level's pattern, colouring
+    and values, and the solve at the oracle's own cycle count."""
     p = meshgen.make_config(cid)
     A, M, mgo = oracle_problem(ora, p)
     S = gpu_solver(p)
@@ -397,3 +399,29 @@ def test_pcg_parity(ora, cid, kw):
     S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
     with pytest.raises(mg.MGError):
         S.solve_pcg(Bo, np.zeros_like(Bo))                # mu_pre != mu_post: not a symmetric preconditioner
+
+
+@pytest.mark.slow
+def test_full_size_mcf_steps(ora):
+    """BASELINE.json config 5 at full size (655,362 vertices): the first two
+    implicit MCF steps (GPU assembly -> Galerkin -> factor -> B = M X ->
+    warm-started solve to 1e-8) against the oracle's loop."""
+    p = meshgen.make_config(5)
+    V, F = p.levels[0]
+    Xo, cyc_o = ora.mcf(p.sizes, p.P, V, F, p.lap_coeff, 2, rel_tol=p.rel_tol)
+    S = gpu_solver(p)
+    X = np.ascontiguousarray(V, np.float64).copy()
+    for t in range(2):                                  # the oracle's cycle count per step
+        S.set_matrix_cotan(X, p.mass_coeff, p.lap_coeff)
+        B = np.empty_like(X)
+        S.apply_mass(X, B)
+        rc, cyc, _ = S.solve(B, X, rel_tol=0.0, max_cycles=cyc_o[t])
+        assert cyc == cyc_o[t]
+    check_x(X, Xo)
+    X2 = np.ascontiguousarray(V, np.float64).copy()    # own stopping rule: within +-1 cycle per step
+    for t in range(2):
+        S.set_matrix_cotan(X2, p.mass_coeff, p.lap_coeff)
+        B = np.empty_like(X2)
+        S.apply_mass(X2, B)
+        rc, cyc, _ = S.solve(B, X2, rel_tol=p.rel_tol, max_cycles=p.max_cycles)
+        assert rc == 0 and abs(cyc - cyc_o[t]) <= 1
