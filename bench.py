@@ -84,6 +84,31 @@ def vcycle_bytes(levels, k, mu=4):
     return tot
 
 
+def level_rooflines(breakdown, levels, k, cycles, peak):
+    """Achieved GB/s and fraction of the HBM peak per level for the GS sweeps
+    (4 sweeps per cycle) and the Galerkin product, from the per-class event
+    breakdown of one step (bench's separate profiled pass)."""
+    out = {}
+    gs = breakdown.get("gs_sweep", {})
+    gal = breakdown.get("galerkin", {})
+    for l in range(len(levels) - 1):
+        n, nnz = levels[l]
+        row = {}
+        if str(l) in gs and cycles:
+            t = gs[str(l)]["ms"] / 1e3
+            b = 4 * cycles * gs_sweep_bytes(n, nnz, k)
+            row["gs_GBps"] = round(b / t / 1e9, 1)
+            row["gs_frac"] = round(b / t / 1e9 / peak, 3)
+        if str(l) in gal:
+            t = gal[str(l)]["ms"] / 1e3
+            nc, nnzc = levels[l + 1]
+            b = level_bytes(n, nnz) + 36 * n + 12 * nnzc + 4 * nc
+            row["galerkin_GBps"] = round(b / t / 1e9, 1)
+            row["galerkin_frac"] = round(b / t / 1e9 / peak, 3)
+        out[str(l)] = row
+    return out
+
+
 def galerkin_bytes(levels):
     tot = 0
     for l in range(len(levels) - 1):
@@ -108,7 +133,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=open(self.path, "w"),
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=open(self.path, "w"),
                 stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -409,7 +434,10 @@ def run_mg(args):
         traffic = tr.get(f"config{args.config}", {}).get("gs_sweep_level0_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": f"k_gs_colour (level 0, {nc0} colour launches per sweep)",
+    kname = "k_tile_pipe<K,0>" if nnz0 / max(n0, 1) <= 12 else "k_lpr_sweep<K,LPR,0>"
+    roofline = {"bound": "hbm",
+                "kernel": f"{kname}: level-0 multicolour GS sweep ({nc0} colour launches per sweep; "
+                          f"algorithmic bytes per sweep = 12 nnz + 4 n + 24 k n, DESIGN.md §5)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind, "traffic": traffic,
                 "algorithmic_bytes_per_launch": sweep_bytes / nc0 if nc0 else None,
@@ -477,6 +505,7 @@ def run_mg(args):
                             "achieved_GBps": vc_bytes / (mean_solve / mean_cyc / 1e3) / 1e9 if mean_cyc else None,
                             "frac": (vc_bytes / (mean_solve / mean_cyc / 1e3) / 1e9) / peak if mean_cyc else None},
         "galerkin_bytes": galerkin_bytes(levels_nnz),
+        "level_rooflines": level_rooflines(breakdown, levels_nnz, k, mean_cyc, peak),
         "breakdown_ms": breakdown,
         "setup_s_first_call": t_setup,
     }
