@@ -306,3 +306,61 @@ def mcf(sizes, Ps, V0, F, dt, steps, rel_tol=1e-8, max_cycles=100, mu_pre=2, mu_
         if rc not in (0,):
             raise RuntimeError(f"oracle mcf: solve returned {rc}")
     return X, cycles
+
+
+def dirichlet_reduce(sizes, Ps, known):
+    """Dirichlet reduction of the hierarchy (App. B; row f2), plain
+    numpy.  Returns (u, sizes', Ps', keep) where u = ascending unknown fine
+    indices, P_0' = P_{u:} with its coarse columns renumbered, and, at every
+    level, coarse columns whose maximum (absolute) weight over the kept rows
+    is zero are removed together with "the corresponding rows in the
+    prolongation at the next level".  Reading A24: the paper states
+    the rule for the second-finest level; it is applied at every level until no
+    column is all-zero, and the hierarchy stops at the last non-empty level.
+    keep[l] = kept (original) indices of level l."""
+    n0 = sizes[0]
+    mask = np.ones(n0, bool)
+    mask[np.asarray(known, np.int64)] = False
+    keep = [np.nonzero(mask)[0]]
+    new_sizes = [keep[0].size]
+    new_P = []
+    for l in range(len(sizes) - 1):
+        if keep[-1].size == 0:
+            break
+        c, w = np.asarray(Ps[l][0]), np.asarray(Ps[l][1], np.float64)
+        rows_c, rows_w = c[keep[-1]], w[keep[-1]]
+        colmax = np.zeros(sizes[l + 1])
+        np.maximum.at(colmax, rows_c.ravel(), np.abs(rows_w).ravel())
+        kept_cols = np.nonzero(colmax > 0.0)[0]
+        remap = -np.ones(sizes[l + 1], np.int64)
+        remap[kept_cols] = np.arange(kept_cols.size)
+        nc = np.where(rows_w != 0.0, remap[rows_c], 0)
+        assert (nc >= 0).all()
+        new_P.append((nc.astype(np.int32), np.where(rows_w != 0.0, rows_w, 0.0)))
+        keep.append(kept_cols)
+        new_sizes.append(kept_cols.size)
+    if new_sizes[-1] == 0 and len(new_sizes) > 1:   # nothing survives below: stop at the last non-empty level
+        new_sizes.pop()
+        new_P.pop()
+        keep.pop()
+    return keep[0], new_sizes, new_P, keep
+
+
+def dirichlet_solve(sizes, Ps, A, B, X0, known, rel_tol=1e-10, max_cycles=100, mu_pre=2, mu_post=2):
+    """Constrained solve (App. B): x_k = X0[known] fixed; the reduced system
+    A_uu x_u = b_u - A_uk x_k (eq. "reduced LHS/RHS") solved by the V-cycle on
+    the reduced hierarchy of dirichlet_reduce.  Returns (X, history, rc,
+    reduced MG object or None)."""
+    B, X = _f64(B), _f64(X0).copy()
+    u, rs, rP, _ = dirichlet_reduce(sizes, Ps, known)
+    if u.size == 0:
+        k = 1 if B.ndim == 1 else B.shape[1]
+        return X, np.zeros((0, k)), 0, None
+    S = A.to_scipy().tocsr()
+    kn = np.setdiff1d(np.arange(S.shape[0]), u)
+    Auu = S[u][:, u]
+    bu = B[u] - S[u][:, kn] @ X[kn]
+    mg = MG(rs, rP, Csr.from_scipy(Auu), mu_pre, mu_post)
+    xu, hist, rc = mg.solve(bu, X0=X[u], rel_tol=rel_tol, max_cycles=max_cycles)
+    X[u] = xu
+    return X, hist, rc, mg

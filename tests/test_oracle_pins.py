@@ -634,3 +634,74 @@ def test_jacobi_multigrid_converges(ora):
     _, hj, _ = ora.MG(p.sizes, p.P, A).set_smoother(1, 0.8).solve(b, rel_tol=0.0, max_cycles=6)
     assert (np.diff(hj[:, 0]) < 0).all()
     assert hj[-1, 0] > hg[-1, 0]
+
+
+# --------------------------------------------------------------------- f2: Dirichlet reduction (App. B)
+
+
+def test_dirichlet_no_constraints_is_identity(ora):
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    A, M = ora.assemble(V, F, 1.0, 1e-2)
+    b = np.random.default_rng(21).standard_normal((p.n, 1))
+    X1, h1, _ = ora.MG(p.sizes, p.P, A).solve(b, rel_tol=0.0, max_cycles=4)
+    X2, h2, _, _ = ora.dirichlet_solve(p.sizes, p.P, A, b, np.zeros((p.n, 1)), [], rel_tol=0.0, max_cycles=4)
+    assert np.array_equal(X1, X2) and np.array_equal(h1, h2)
+
+
+def test_dirichlet_all_known(ora):
+    p = meshgen.make_config(1, subdiv=2)
+    V, F = p.levels[0]
+    A, M = ora.assemble(V, F, 1.0, 1e-2)
+    X0 = np.random.default_rng(22).standard_normal((p.n, 2))
+    X, hist, rc, mg = ora.dirichlet_solve(p.sizes, p.P, A, np.ones((p.n, 2)), X0, np.arange(p.n))
+    assert rc == 0 and hist.shape[0] == 0 and np.array_equal(X, X0) and mg is None
+
+
+def test_dirichlet_matches_dense_constrained_solve(ora):
+    """SPEC S:561 worked example: 10% random constraints; the reduced-system
+    multigrid solution equals the dense solve of the constrained system."""
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    A, M = ora.assemble(V, F, 1.0, 1e-2)
+    rng = np.random.default_rng(23)
+    known = np.sort(rng.choice(p.n, p.n // 10, replace=False))
+    X0 = np.zeros((p.n, 2))
+    X0[known] = rng.standard_normal((known.size, 2))
+    B = M[:, None] * rng.standard_normal((p.n, 2))
+    X, hist, rc, mg = ora.dirichlet_solve(p.sizes, p.P, A, B, X0, known, rel_tol=1e-12, max_cycles=60)
+    assert rc == 0
+    D = A.to_scipy().toarray()
+    u = np.setdiff1d(np.arange(p.n), known)
+    xu = np.linalg.solve(D[np.ix_(u, u)], B[u] - D[np.ix_(u, known)] @ X0[known])
+    assert np.linalg.norm(X[u] - xu) / np.linalg.norm(xu) <= 1e-10
+    assert np.array_equal(X[known], X0[known])
+    # the full-system residual vanishes on the unknown rows
+    r = B - D @ X
+    assert np.abs(r[u]).max() <= 1e-9 * np.abs(B).max()
+
+
+def test_dirichlet_zero_column_removal(ora):
+    """constraining every child of a coarse vertex zeroes its column
+    of P_{u:}; it must be removed (with its row of the next prolongation) so
+    the reduced coarse operators have no zero rows and stay SPD."""
+    p = meshgen.make_config(1, subdiv=3)                 # 642 -> 162 -> 42, nested P
+    V, F = p.levels[0]
+    A, M = ora.assemble(V, F, 1.0, 1e-2)
+    c0, w0 = p.P[0]
+    J = 7
+    children = np.nonzero(((c0 == J) & (w0 != 0.0)).any(axis=1))[0]
+    u, rs, rP, keep = ora.dirichlet_reduce(p.sizes, p.P, children)
+    assert rs[1] == p.sizes[1] - 1 and J not in keep[1]
+    for l in range(len(rs) - 1):
+        c, w = rP[l]
+        assert c.shape == (rs[l], 3) and c.max() < rs[l + 1]
+        assert np.allclose(w.sum(axis=1), 1.0)                    # dropped columns carried zero weight only
+    X0 = np.zeros((p.n, 1))
+    X, hist, rc, mg = ora.dirichlet_solve(p.sizes, p.P, A, M[:, None], X0, children, rel_tol=1e-12, max_cycles=60)
+    assert rc == 0 and mg.status == 0
+    for l in range(mg.n_levels):
+        lv = mg.level(l)
+        rows = np.repeat(np.arange(lv["n"]), np.diff(lv["rowptr"]))
+        diag = lv["val"][lv["col"] == rows]
+        assert diag.size == lv["n"] and (diag > 0).all()
