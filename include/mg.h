@@ -125,6 +125,32 @@ int mg_apply_mass(mg_ctx* ctx, int32_t k, const double* X, double* B);
 int mg_solve(mg_ctx* ctx, int32_t k, const double* B, double* X, double rel_tol, int32_t max_cycles,
              double* res_hist, int32_t* cycles_out);
 
+/* ---- Dirichlet constraints (App. B) ------------- */
+
+/* Prescribe the values of the fine vertices known[0..n_known) (user indices,
+ * unique; host array, copied).  The solver then works on the reduced system
+ *   A_uu x_u = b_u - A_uk x_k           (App. B, "reduced LHS" / "reduced RHS")
+ * over the reduced hierarchy: the finest prolongation keeps the rows of the
+ * unknowns, P_{u:}; at every level, coarse columns whose largest weight over
+ * the kept rows is 0 are removed together with their row of the next
+ * prolongation (reading A24 applies the rule level by level), and
+ * the hierarchy ends at the last non-empty level.  After this call:
+ *   - mg_set_matrix / mg_set_matrix_cotan take the FULL fine operator
+ *     (n_verts[0] rows) and extract A_uu and A_uk on the GPU;
+ *   - mg_solve / mg_solve_pcg take FULL [n_verts[0]][k] B and X: X holds the
+ *     known values at known rows (read, never written) and the initial guess
+ *     elsewhere; only the unknown rows of X are written; rho is the relative
+ *     residual of the reduced system;
+ *   - mg_apply_mass / mg_get_mass stay full-size; the level exports
+ *     (mg_level_info, mg_get_level_csr, mg_get_colouring) describe the
+ *     reduced levels (level 0 rows = unknowns in ascending user order);
+ *   - the App. D split operators are not available (MG_ERR_STATE).
+ * Every vertex known: solves return at once (0 cycles, X unchanged).
+ * n_known = 0 restores the unconstrained hierarchy.  Invalidates the matrix.
+ * Errors: MG_ERR_STATE (no hierarchy), MG_ERR_INVALID_ARG, MG_ERR_INPUT
+ * (index out of range or repeated), MG_ERR_SHAPE (reduced coarsest > 4096). */
+int mg_set_dirichlet(mg_ctx* ctx, int32_t n_known, const int32_t* known);
+
 /* ---- smoother variants and MG-preconditioned CG ---------- */
 
 /* Relaxation used by every level of the V-cycle.

@@ -186,6 +186,27 @@ struct mg_ctx {
     bool have_mass = false;
     bool have_split = false;         // App. D: Q_l, M_l stored at every level
 
+    // Dirichlet reduction (App. B, row f2): the hierarchy as loaded,
+    // and the reduced one in lv when constraints are set
+    struct Orig {
+        int32_t n = 0;
+        std::vector<double> V;
+        std::vector<int32_t> Pc;
+        std::vector<double> Pw;
+    };
+    std::vector<Orig> orig;
+    bool dir = false;                // constraints active: lv is the reduced hierarchy
+    bool dir_all = false;            // every fine vertex is known
+    uint64_t dir_version = 0;        // bumps on every mg_set_dirichlet (pattern cache key)
+    int32_t n_full = 0;              // fine vertices of the loaded hierarchy
+    std::vector<int32_t> dir_u;      // reduced index r -> full vertex (ascending)
+    std::vector<int32_t> dir_red;    // full vertex -> reduced index (-1: known)
+    DBuf<int32_t> d_umap, uk_rp, uk_col, d_ident;
+    DBuf<int64_t> uk_src;
+    DBuf<double> uk_val, full_val, full_V;
+    DBuf<int32_t> full_opp;
+    Level full0;                     // full 1-ring pattern (user order) for cotan assembly in Dirichlet mode
+
     std::vector<int32_t> opp_user;   // cotan: 2 opposite vertices per user nnz (-1 none)
     DBuf<int32_t> opp;               // internal
     DBuf<double> Vstage, Vint, Mint, Muser;
@@ -997,15 +1018,183 @@ int mg_hierarchy_load(mg_ctx* c, int n_levels, const int32_t* n_verts, const int
     }
     c->lv = std::move(lv);
     c->H = n_levels - 1;
+    c->orig.clear();
+    for (auto& L : c->lv) {
+        mg_ctx::Orig o;
+        o.n = L->n;
+        o.V = L->V;
+        o.Pc = L->Pc_user;
+        o.Pw = L->Pw_user;
+        c->orig.push_back(std::move(o));
+    }
+    c->dir = c->dir_all = false;
+    c->n_full = c->lv[0]->n;
+    ++c->dir_version;
+    return MG_OK;
+}
+
+// Dirichlet reduction of the hierarchy (App. B; reading A24).
+// known: fine vertex indices with prescribed values (any order, unique).
+// Unknown fine rows keep their P rows; at every level, coarse columns whose
+// largest weight over the kept rows is zero are removed together with their
+// row of the next prolongation; the hierarchy ends at the last non-empty level.
+int mg_set_dirichlet(mg_ctx* c, int32_t n_known, const int32_t* known) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (c->H < 0 || c->orig.empty()) return c->fail(MG_ERR_STATE, "no hierarchy loaded (call mg_hierarchy_load)");
+    if (n_known < 0 || (n_known > 0 && !known)) return c->fail(MG_ERR_INVALID_ARG, "n_known >= 0 and known required");
+    const int32_t n0 = c->orig[0].n;
+    std::vector<char> isk(n0, 0);
+    for (int32_t t = 0; t < n_known; ++t) {
+        const int32_t v = known[t];
+        if (v < 0 || v >= n0) return c->fail(MG_ERR_INPUT, "known[%d] = %d out of range", t, v);
+        if (isk[v]) return c->fail(MG_ERR_INPUT, "known vertex %d listed twice", v);
+        isk[v] = 1;
+    }
+    cudaStreamSynchronize(c->stream);
+    c->drop_graphs();
+    c->have_pattern = c->have_matrix = c->have_mass = c->have_split = false;
+    ++c->dir_version;
+    const int nl0 = (int)c->orig.size();
+    // level 0 kept rows, then columns level by level
+    std::vector<std::vector<int32_t>> keep(1);
+    for (int32_t i = 0; i < n0; ++i)
+        if (!isk[i]) keep[0].push_back(i);
+    std::vector<std::vector<int32_t>> Pc;
+    std::vector<std::vector<double>> Pw;
+    for (int l = 0; l + 1 < nl0 && !keep.back().empty(); ++l) {
+        const auto& O = c->orig[l];
+        const int32_t ncl = c->orig[l + 1].n;
+        std::vector<char> used(ncl, 0);
+        for (int32_t i : keep[l])
+            for (int q = 0; q < 3; ++q)
+                if (O.Pw[3 * (size_t)i + q] != 0.0) used[O.Pc[3 * (size_t)i + q]] = 1;
+        std::vector<int32_t> kc, remap(ncl, -1);
+        for (int32_t J = 0; J < ncl; ++J)
+            if (used[J]) {
+                remap[J] = (int32_t)kc.size();
+                kc.push_back(J);
+            }
+        if (kc.empty()) break;
+        std::vector<int32_t> pc(3 * keep[l].size());
+        std::vector<double> pw(3 * keep[l].size());
+        for (size_t r = 0; r < keep[l].size(); ++r)
+            for (int q = 0; q < 3; ++q) {
+                const double w = O.Pw[3 * (size_t)keep[l][r] + q];
+                pw[3 * r + q] = w;
+                pc[3 * r + q] = w != 0.0 ? remap[O.Pc[3 * (size_t)keep[l][r] + q]] : 0;
+            }
+        Pc.push_back(std::move(pc));
+        Pw.push_back(std::move(pw));
+        keep.push_back(std::move(kc));
+    }
+    c->dir_u = keep[0];
+    c->dir_red.assign(n0, -1);
+    for (size_t r = 0; r < keep[0].size(); ++r) c->dir_red[keep[0][r]] = (int32_t)r;
+    std::vector<std::unique_ptr<Level>> lv;
+    if (n_known == 0) {
+        for (const auto& O : c->orig) {
+            auto L = std::make_unique<Level>();
+            L->n = O.n;
+            L->V = O.V;
+            L->Pc_user = O.Pc;
+            L->Pw_user = O.Pw;
+            lv.push_back(std::move(L));
+        }
+        c->dir = c->dir_all = false;
+    } else if (keep[0].empty()) {
+        c->dir = c->dir_all = true;
+        return MG_OK;
+    } else {
+        for (size_t l = 0; l < keep.size(); ++l) {
+            auto L = std::make_unique<Level>();
+            L->n = (int32_t)keep[l].size();
+            L->V.resize(3 * (size_t)L->n);
+            for (int32_t r = 0; r < L->n; ++r)
+                for (int d = 0; d < 3; ++d) L->V[3 * (size_t)r + d] = c->orig[l].V[3 * (size_t)keep[l][r] + d];
+            if (l + 1 < keep.size()) {
+                L->Pc_user = Pc[l];
+                L->Pw_user = Pw[l];
+            }
+            lv.push_back(std::move(L));
+        }
+        c->dir = true;
+        c->dir_all = false;
+        cudaError_t e = c->d_umap.upload(c->dir_u, c->stream);
+        if (e) return c->cuda_fail(e, "mg_set_dirichlet");
+    }
+    if (lv.back()->n > 4096)
+        return c->fail(MG_ERR_SHAPE, "reduced coarsest level has %d vertices (> 4096)", lv.back()->n);
+    c->lv = std::move(lv);
+    c->H = (int)c->lv.size() - 1;
     return MG_OK;
 }
 
 // Validate a user CSR pattern (host or device arrays) and run the pattern
 // setup when it differs from the cached one.
+// Dirichlet mode (App. B): from a FULL fine pattern (rp, cl, user order) derive
+// A_uu's pattern in reduced numbering and the A_uk entries, run the pattern
+// setup on A_uu, and store the value maps: internal A_uu nnz -> full nnz
+// (L0.di2u) and A_uk in internal row order (columns = full known vertices).
+static int dir_pattern(mg_ctx* c, const std::vector<int32_t>& rp, const std::vector<int32_t>& cl) {
+    const int32_t nr = (int32_t)c->dir_u.size();
+    std::vector<int32_t> urp(nr + 1, 0), ucl;
+    std::vector<int64_t> usrc;
+    std::vector<std::vector<std::pair<int32_t, int64_t>>> ukr(nr);
+    for (int32_t r = 0; r < nr; ++r) {
+        const int32_t f = c->dir_u[r];
+        for (int32_t t = rp[f]; t < rp[f + 1]; ++t) {
+            const int32_t j = cl[t];
+            const int32_t rj = c->dir_red[j];
+            if (rj >= 0) {
+                ucl.push_back(rj);
+                usrc.push_back(t);
+            } else {
+                ukr[r].push_back({j, (int64_t)t});
+            }
+        }
+        urp[r + 1] = (int32_t)ucl.size();
+    }
+    int rc = setup_pattern(c, urp, ucl);
+    if (rc) return rc;
+    Level& L0 = *c->lv[0];
+    std::vector<int64_t> comp(L0.nnz);
+    for (int64_t e = 0; e < L0.nnz; ++e) comp[e] = usrc[L0.i2u[e]];
+    std::vector<int32_t> krp(L0.n + 1, 0), kcol;
+    std::vector<int64_t> ksrc;
+    for (int32_t i = 0; i < L0.n; ++i) {
+        for (const auto& pr : ukr[L0.perm[i]]) {
+            kcol.push_back(pr.first);
+            ksrc.push_back(pr.second);
+        }
+        krp[i + 1] = (int32_t)kcol.size();
+    }
+    if (kcol.empty()) {   // keep the device arrays non-empty
+        kcol.push_back(0);
+        ksrc.push_back(0);
+    }
+    cudaError_t e;
+    if ((e = L0.di2u.upload(comp, c->stream)) || (e = c->uk_rp.upload(krp, c->stream)) ||
+        (e = c->uk_col.upload(kcol, c->stream)) || (e = c->uk_src.upload(ksrc, c->stream)) ||
+        (e = c->uk_val.alloc(kcol.size())) || (e = cudaStreamSynchronize(c->stream)))
+        return c->cuda_fail(e, "dirichlet pattern upload");
+    return MG_OK;
+}
+
+// Gather the values of A_uu (into level 0, internal order) and A_uk from the
+// full value array (device, full-pattern order).
+static int dir_values(mg_ctx* c, const double* full_vals) {
+    Level& L0 = *c->lv[0];
+    c->timed(PC_PERMUTE, 0, c->stream, [&] {
+        return launch_gather_vals(L0.di2u.p, full_vals, L0.val.p, L0.nnz, c->stream) +
+               launch_gather_vals(c->uk_src.p, full_vals, c->uk_val.p, (int64_t)c->uk_src.n, c->stream);
+    });
+    return MG_OK;
+}
+
 static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col) {
     int rc;
     if (!row_ptr || !col || nnz < 0) return c->fail(MG_ERR_INVALID_ARG, "null CSR array or nnz < 0");
-    if (n != c->lv[0]->n) return c->fail(MG_ERR_SHAPE, "n = %d but the hierarchy's finest level has %d", n, c->lv[0]->n);
+    if (n != c->n_full) return c->fail(MG_ERR_SHAPE, "n = %d but the hierarchy's finest level has %d", n, c->n_full);
     if (nnz > INT32_MAX) return c->fail(MG_ERR_SHAPE, "nnz exceeds int32");
     const bool dev = is_device_ptr(row_ptr);
     std::vector<int32_t> rp(n + 1), cl(nnz);
@@ -1037,9 +1226,11 @@ static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* ro
         }
     uint64_t h = fnv1a(1469598103934665603ULL, rp.data(), rp.size() * 4);
     h = fnv1a(h, cl.data(), cl.size() * 4);
+    h = fnv1a(h, &c->dir_version, sizeof(c->dir_version));
+    if (c->dir_all) return MG_OK;   // every vertex known: nothing to factor
     if (!c->have_pattern || c->pattern_kind != 0 || c->pattern_hash != h) {
         c->have_pattern = false;
-        rc = setup_pattern(c, rp, cl);
+        rc = c->dir ? dir_pattern(c, rp, cl) : setup_pattern(c, rp, cl);
         if (rc) return rc;
         c->pattern_hash = h;
         c->pattern_kind = 0;
@@ -1054,13 +1245,21 @@ int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, con
     if (!val) return c->fail(MG_ERR_INVALID_ARG, "null CSR value array");
     (void)on_device;
     if ((rc = load_csr_pattern(c, n, nnz, row_ptr, col))) return rc;
+    c->have_mass = false;
+    c->have_split = false;
+    if (c->dir_all) {
+        c->have_matrix = true;
+        return MG_OK;
+    }
     const double* dval = nullptr;
     rc = to_device(c, val, c->stageVal, (size_t)nnz, &dval);
     if (rc) return rc;
     Level& L0 = *c->lv[0];
-    c->timed(PC_PERMUTE, 0, c->stream, [&] { return launch_gather_vals(L0.di2u.p, dval, L0.val.p, nnz, c->stream); });
-    c->have_mass = false;
-    c->have_split = false;
+    if (c->dir) {
+        if ((rc = dir_values(c, dval))) return rc;
+    } else {
+        c->timed(PC_PERMUTE, 0, c->stream, [&] { return launch_gather_vals(L0.di2u.p, dval, L0.val.p, nnz, c->stream); });
+    }
     return rebuild_hierarchy(c);
 }
 
@@ -1072,8 +1271,9 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
     if (!V) return c->fail(MG_ERR_INVALID_ARG, "V is null");
     if (c->nF0 <= 0) return c->fail(MG_ERR_STATE, "the hierarchy has no fine faces F[0]");
     Level& L0 = *c->lv[0];
-    const int32_t n = L0.n;
-    if (!c->have_pattern || c->pattern_kind != 1) {
+    const int32_t n = c->n_full;   // the 1-ring is built on the full fine mesh
+    const bool full_mode = c->dir || c->dir_all;
+    if (!c->have_pattern || c->pattern_kind != 1 || c->pattern_hash != c->dir_version) {
         // 1-ring pattern of F[0] and the opposite vertices of every edge
         struct HalfEdge {
             int32_t i, j, o;
@@ -1125,10 +1325,30 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
             rp[i + 1] = (int32_t)cl.size();
         }
         c->have_pattern = false;
+        if (full_mode) {
+            // Dirichlet mode: assemble on the full mesh in user order, then
+            // extract A_uu / A_uk (App. B)
+            std::vector<int32_t> rpad(rp), cpad(cl), ident(n);
+            rpad.resize(rpad.size() + 8, rp.back());
+            cpad.resize(cpad.size() + 8, 0);
+            std::iota(ident.begin(), ident.end(), 0);
+            c->full0.n = n;
+            c->full0.nnz = (int64_t)cl.size();
+            cudaError_t e;
+            if ((e = c->full0.rp.upload(rpad, c->stream)) || (e = c->full0.col.upload(cpad, c->stream)) ||
+                (e = c->full_opp.upload(opp, c->stream)) || (e = c->d_ident.upload(ident, c->stream)) ||
+                (e = c->full_V.alloc(4 * (size_t)n)) || (e = c->full_val.alloc(cl.size() + 8)) ||
+                (e = c->Muser.alloc(n)))
+                return c->cuda_fail(e, "cotan setup");
+            if (!c->dir_all && (rc = dir_pattern(c, rp, cl))) return rc;
+            c->have_pattern = !c->dir_all;
+            c->pattern_kind = 1;
+            c->pattern_hash = c->dir_version;
+        } else {
         rc = setup_pattern(c, rp, cl);
         if (rc) return rc;
         c->pattern_kind = 1;
-        c->pattern_hash = 0;
+        c->pattern_hash = c->dir_version;
         // opposite vertices in internal order
         std::vector<int32_t> oi(2 * (size_t)L0.nnz);
         for (int64_t e = 0; e < L0.nnz; ++e) {
@@ -1142,11 +1362,15 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
         if ((e = c->opp.upload(oi, c->stream)) || (e = c->Vint.alloc(4 * (size_t)n)) || (e = c->Mint.alloc(n)) ||
             (e = c->Muser.alloc(n)))
             return c->cuda_fail(e, "cotan setup");
+        }
     }
     const double* dV = nullptr;
     rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV);
     if (rc) return rc;
-    c->timed(PC_ASSEMBLY, 0, c->stream, [&] { return launch_gather_rows(3, L0.diperm.p, dV, c->Vint.p, n, c->stream); });
+    c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
+        return full_mode ? launch_gather_rows(3, c->d_ident.p, dV, c->full_V.p, n, c->stream)
+                         : launch_gather_rows(3, L0.diperm.p, dV, c->Vint.p, n, c->stream);
+    });
     return MG_OK;
 }
 
@@ -1156,12 +1380,27 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
     if ((rc = load_cotan_pattern(c, V))) return rc;
     Level& L0 = *c->lv[0];
     const int32_t n = L0.n;
+    c->have_mass = true;
+    c->have_split = false;
+    if (c->dir || c->dir_all) {
+        // full mesh, user order: M lands directly in Muser
+        c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
+            return launch_cotan(c->full0, c->full_opp.p, c->full_V.p, mass_coeff, lap_coeff, c->full_val.p, c->Muser.p,
+                                c->stream);
+        });
+        if (c->dir_all) {
+            cudaError_t e = cudaStreamSynchronize(c->stream);
+            if (e) return c->cuda_fail(e, "mg_set_matrix_cotan");
+            c->have_matrix = true;
+            return MG_OK;
+        }
+        if ((rc = dir_values(c, c->full_val.p))) return rc;
+        return rebuild_hierarchy(c);
+    }
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
         return launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, L0.val.p, c->Mint.p, c->stream) +
                launch_scatter_vec(L0.diperm.p, c->Mint.p, c->Muser.p, n, c->stream);
     });
-    c->have_mass = true;
-    c->have_split = false;
     return rebuild_hierarchy(c);
 }
 
@@ -1169,6 +1408,7 @@ int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_pt
                         const double* q_val, const double* m_val) {
     int rc = check_state(c, false);
     if (rc) return rc;
+    if (c->dir || c->dir_all) return c->fail(MG_ERR_STATE, "split operators are not available with Dirichlet constraints");
     if (!q_val || !m_val) return c->fail(MG_ERR_INVALID_ARG, "null Q or M value array");
     if ((rc = load_csr_pattern(c, n, nnz, row_ptr, col))) return rc;
     Level& L0 = *c->lv[0];
@@ -1188,6 +1428,7 @@ int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_pt
 int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
     int rc = check_state(c, false);
     if (rc) return rc;
+    if (c->dir || c->dir_all) return c->fail(MG_ERR_STATE, "split operators are not available with Dirichlet constraints");
     if ((rc = load_cotan_pattern(c, V))) return rc;
     Level& L0 = *c->lv[0];
     cudaError_t e;
@@ -1220,7 +1461,7 @@ int mg_apply_mass(mg_ctx* c, int32_t k, const double* X, double* B) {
     if (rc) return rc;
     if (!c->have_mass) return c->fail(MG_ERR_STATE, "no mass matrix (call mg_set_matrix_cotan)");
     if (k < 1 || k > kMaxK || !X || !B) return c->fail(MG_ERR_INVALID_ARG, "1 <= k <= %d and non-null X, B", kMaxK);
-    const int32_t n = c->lv[0]->n;
+    const int32_t n = c->n_full;
     const bool devB = is_device_ptr(B);
     const double* dX = nullptr;
     rc = to_device(c, X, c->stageX, (size_t)n * k, &dX);
@@ -1238,24 +1479,63 @@ int mg_apply_mass(mg_ctx* c, int32_t k, const double* X, double* B) {
     return MG_OK;
 }
 
+// User [n_full][k] B, X -> level-0 internal b, x (reduced rows and the
+// Dirichlet right-hand side -A_uk x_k + b_u in constrained mode, App. B),
+// then |b|.  *dXout: where the solution is scattered back (the user's device
+// X, or the staging copy of a host X, which keeps the known rows).
+static int prep_solve(mg_ctx* c, int32_t k, const double* B, double* X, double** dXout) {
+    int rc;
+    cudaStream_t s = c->stream;
+    Level& L0 = *c->lv[0];
+    const int32_t n = L0.n;
+    const size_t nu = (size_t)c->n_full * k;
+    const double* dB = nullptr;
+    const double* dX = nullptr;
+    if ((rc = to_device(c, B, c->stageB, nu, &dB))) return rc;
+    if ((rc = to_device(c, X, c->stageX, nu, &dX))) return rc;
+    *dXout = is_device_ptr(X) ? X : c->stageX.p;
+    const int32_t* um = c->dir ? c->d_umap.p : nullptr;
+    c->timed(PC_PERMUTE, 0, s, [&] {
+        int nl = launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s, um) +
+                 launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s, um);
+        if (c->dir) nl += launch_dirichlet_rhs(k, c->uk_rp.p, c->uk_col.p, c->uk_val.p, dX, L0.b.p, n, s);
+        return nl + vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
+    });
+    return MG_OK;
+}
+
+// Solution back to the user's [n_full][k] X (only the unknown rows in constrained mode).
+static int finish_solve(mg_ctx* c, int32_t k, const double* xint, double* X, double* dXout) {
+    cudaStream_t s = c->stream;
+    Level& L0 = *c->lv[0];
+    const int32_t* um = c->dir ? c->d_umap.p : nullptr;
+    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.diperm.p, xint, dXout, L0.n, s, um); });
+    cudaError_t e;
+    if (!is_device_ptr(X) &&
+        (e = cudaMemcpyAsync(X, dXout, sizeof(double) * c->n_full * k, cudaMemcpyDeviceToHost, s)))
+        return c->cuda_fail(e, "solve");
+    if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "solve");
+    if ((e = cudaGetLastError())) return c->cuda_fail(e, "solve kernels");
+    return MG_OK;
+}
+
 int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, int32_t max_cycles, double* res_hist,
              int32_t* cycles_out) {
     int rc = check_state(c, true);
     if (rc) return rc;
     if (k < 1 || k > kMaxK || !B || !X || max_cycles < 0)
         return c->fail(MG_ERR_INVALID_ARG, "need 1 <= k <= %d, non-null B and X, max_cycles >= 0", kMaxK);
+    if (c->dir_all) {   // every vertex known: X already holds the solution
+        if (res_hist)
+            for (int j = 0; j < k; ++j) res_hist[j] = 0.0;
+        if (cycles_out) *cycles_out = 0;
+        return MG_OK;
+    }
     cudaStream_t s = c->stream;
     Level& L0 = *c->lv[0];
     const int32_t n = L0.n;
-    const bool devX = is_device_ptr(X);
-    const double* dB = nullptr;
-    const double* dX = nullptr;
-    if ((rc = to_device(c, B, c->stageB, (size_t)n * k, &dB))) return rc;
-    if ((rc = to_device(c, X, c->stageX, (size_t)n * k, &dX))) return rc;
-    c->timed(PC_PERMUTE, 0, s, [&] {
-        return launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s) +
-               vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
-    });
+    double* dXout = nullptr;
+    if ((rc = prep_solve(c, k, B, X, &dXout))) return rc;
     c->timed(PC_RESNORM, 0, s, [&] {
         return vc_resnorm(k, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, false, s);
     });
@@ -1291,12 +1571,7 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
         ++cyc;
     }
     if (status == MG_NOT_CONVERGED && !(rel_tol > 0.0)) status = MG_OK;   // fixed-cycle mode
-    double* dXout = devX ? X : c->stageX.p;
-    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.diperm.p, L0.x.p, dXout, n, s); });
-    if (!devX && (e = cudaMemcpyAsync(X, dXout, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s)))
-        return c->cuda_fail(e, "mg_solve");
-    if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "mg_solve");
-    if ((e = cudaGetLastError())) return c->cuda_fail(e, "mg_solve kernels");
+    if ((rc = finish_solve(c, k, L0.x.p, X, dXout))) return rc;
     c->harvest_events();
     if (cycles_out) *cycles_out = cyc;
     if (status == MG_ERR_NUMERIC) c->fail(MG_ERR_NUMERIC, "non-finite residual norm at cycle %d", cyc);
@@ -1323,6 +1598,12 @@ int mg_solve_pcg(mg_ctx* c, int32_t k, const double* B, double* X, double rel_to
         return c->fail(MG_ERR_INVALID_ARG, "need 1 <= k <= %d, non-null B and X, max_iters >= 0", kMaxK);
     if (c->mu_pre != c->mu_post)
         return c->fail(MG_ERR_INVALID_ARG, "MG-PCG needs a symmetric preconditioner: mu_pre == mu_post");
+    if (c->dir_all) {
+        if (res_hist)
+            for (int j = 0; j < k; ++j) res_hist[j] = 0.0;
+        if (iters_out) *iters_out = 0;
+        return MG_OK;
+    }
     cudaStream_t s = c->stream;
     Level& L0 = *c->lv[0];
     const int32_t n = L0.n;
@@ -1332,15 +1613,8 @@ int mg_solve_pcg(mg_ctx* c, int32_t k, const double* B, double* X, double rel_to
         (e = c->pcg_partial.alloc((size_t)pcg_blocks() * kMaxK)) || (e = c->pcg_sc.alloc(3 * kMaxK)) ||
         (e = c->pcg_first.alloc(1)))
         return c->cuda_fail(e, "mg_solve_pcg alloc");
-    const bool devX = is_device_ptr(X);
-    const double* dB = nullptr;
-    const double* dX = nullptr;
-    if ((rc = to_device(c, B, c->stageB, (size_t)n * k, &dB))) return rc;
-    if ((rc = to_device(c, X, c->stageX, (size_t)n * k, &dX))) return rc;
-    c->timed(PC_PERMUTE, 0, s, [&] {
-        return launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s) + launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s) +
-               vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
-    });
+    double* dXout = nullptr;
+    if ((rc = prep_solve(c, k, B, X, &dXout))) return rc;
     // r0 = b - A x0; x <- x0; p <- 0; rho_0
     c->launches += vc_residual(k, L0, false, s);
     if ((e = cudaMemcpyAsync(c->pcg_r.p, L0.r.p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, s)) ||
@@ -1384,12 +1658,7 @@ int mg_solve_pcg(mg_ctx* c, int32_t k, const double* B, double* X, double rel_to
         ++it;
     }
     if (status == MG_NOT_CONVERGED && !(rel_tol > 0.0)) status = MG_OK;   // fixed-iteration mode
-    double* dXout = devX ? X : c->stageX.p;
-    c->timed(PC_PERMUTE, 0, s, [&] { return launch_scatter_rows(k, L0.diperm.p, c->pcg_x.p, dXout, n, s); });
-    if (!devX && (e = cudaMemcpyAsync(X, dXout, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s)))
-        return c->cuda_fail(e, "mg_solve_pcg");
-    if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "mg_solve_pcg");
-    if ((e = cudaGetLastError())) return c->cuda_fail(e, "mg_solve_pcg kernels");
+    if ((rc = finish_solve(c, k, c->pcg_x.p, X, dXout))) return rc;
     c->harvest_events();
     if (iters_out) *iters_out = it;
     if (status == MG_ERR_NUMERIC) c->fail(MG_ERR_NUMERIC, "non-finite residual norm at iteration %d", it);
@@ -1438,7 +1707,7 @@ int mg_get_mass(mg_ctx* c, double* M) {
     int rc = check_state(c, false);
     if (rc) return rc;
     if (!c->have_mass || !M) return c->fail(MG_ERR_STATE, "no mass matrix");
-    cudaError_t e = cudaMemcpyAsync(M, c->Muser.p, sizeof(double) * c->lv[0]->n, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaMemcpyAsync(M, c->Muser.p, sizeof(double) * c->n_full, cudaMemcpyDeviceToHost, c->stream);
     if (!e) e = cudaStreamSynchronize(c->stream);
     return e ? c->cuda_fail(e, "mg_get_mass") : MG_OK;
 }

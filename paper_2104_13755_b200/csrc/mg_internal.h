@@ -176,8 +176,12 @@ int tail_cluster_size();
 int vc_tail(int K, const TailParams& p, int cs, bool pdl, cudaStream_t s);
 // mg_setup.cu
 void init_setup_attributes();
-int launch_gather_rows(int K, const int32_t* iperm, const double* src_user, double* dst_int, int n, cudaStream_t s);
-int launch_scatter_rows(int K, const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
+int launch_gather_rows(int K, const int32_t* iperm, const double* src_user, double* dst_int, int n, cudaStream_t s,
+                       const int32_t* umap = nullptr);
+int launch_scatter_rows(int K, const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s,
+                        const int32_t* umap = nullptr);
+int launch_dirichlet_rhs(int K, const int32_t* krp, const int32_t* kcol, const double* kval, const double* X,
+                         double* b, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
 int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
                  double* val, double* M_int, cudaStream_t s);

@@ -22,27 +22,54 @@ namespace {
 // USER order (coalesced user-side rows) and index the internal side through
 // iperm[u], whose rows are aligned (32-byte rows for K = 3, 4): one full
 // sector per random access instead of partial, straddling user-side rows.
+// umap (nullable): user-side row of user index u is umap[u] (Dirichlet mode:
+// reduced index -> full vertex index, App. B).
 template <int K>
 __global__ void __launch_bounds__(kBlock) k_gather_rows(const int* __restrict__ iperm, const double* __restrict__ src,
-                                                        double* __restrict__ dst, int n) {
+                                                        double* __restrict__ dst, int n, const int* __restrict__ umap) {
     const int u = blockIdx.x * kBlock + threadIdx.x;
     if (u >= n) return;
     const size_t i = (size_t)__ldg(iperm + u);
+    const size_t us = umap ? (size_t)__ldg(umap + u) : (size_t)u;
     double v[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) v[c] = __ldcs(src + (size_t)u * K + c);
+    for (int c = 0; c < K; ++c) v[c] = __ldcs(src + us * K + c);
     strow<K>(dst + i * VS<K>::S, v);   // K = 3: the pad lane is written as 0
 }
 template <int K>
 __global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__ iperm, const double* __restrict__ src,
-                                                         double* __restrict__ dst, int n) {
+                                                         double* __restrict__ dst, int n, const int* __restrict__ umap) {
     const int u = blockIdx.x * kBlock + threadIdx.x;
     if (u >= n) return;
     const size_t i = (size_t)__ldg(iperm + u);
+    const size_t us = umap ? (size_t)__ldg(umap + u) : (size_t)u;
     double v[K];
     ldrow<K>(src + i * VS<K>::S, v);
 #pragma unroll
-    for (int c = 0; c < K; ++c) __stcs(dst + (size_t)u * K + c, v[c]);
+    for (int c = 0; c < K; ++c) __stcs(dst + us * K + c, v[c]);
+}
+
+// Dirichlet right-hand side (App. B, "reduced RHS" -A_uk x_k + b_u): for every
+// internal row i of the reduced level 0, b_i -= sum_e A_uk[i, e] X[col_e]
+// with X the user's full [n_full][K] array (known values at known rows).
+template <int K>
+__global__ void __launch_bounds__(kBlock) k_dirichlet_rhs(const int* __restrict__ krp, const int* __restrict__ kcol,
+                                                          const double* __restrict__ kval,
+                                                          const double* __restrict__ X, double* __restrict__ b,
+                                                          int n) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    const int e0 = krp[i], e1 = krp[i + 1];
+    if (e0 == e1) return;
+    double bv[K];
+    ldrow<K>(b + (size_t)i * VS<K>::S, bv);
+    for (int e = e0; e < e1; ++e) {
+        const double a = kval[e];
+        const size_t j = (size_t)kcol[e];
+#pragma unroll
+        for (int c = 0; c < K; ++c) bv[c] = fma(-a, X[j * K + c], bv[c]);
+    }
+    strow<K>(b + (size_t)i * VS<K>::S, bv);
 }
 __global__ void __launch_bounds__(kBlock) k_gather_vals(const int64_t* __restrict__ i2u, const double* __restrict__ src,
                                                         double* __restrict__ dst, int64_t nnz) {
@@ -1298,16 +1325,18 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
 }
 
 template <int K>
-void dispatch_rows(bool gather, const int32_t* perm, const double* src, double* dst, int n, cudaStream_t s) {
-    if (gather) k_gather_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n);
-    else k_scatter_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n);
+void dispatch_rows(bool gather, const int32_t* perm, const double* src, double* dst, int n, const int32_t* umap,
+                   cudaStream_t s) {
+    if (gather) k_gather_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n, umap);
+    else k_scatter_rows<K><<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src, dst, n, umap);
 }
-void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* dst, int n, cudaStream_t s) {
+void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* dst, int n, const int32_t* umap,
+            cudaStream_t s) {
     switch (K) {
-        case 1: dispatch_rows<1>(gather, perm, src, dst, n, s); break;
-        case 2: dispatch_rows<2>(gather, perm, src, dst, n, s); break;
-        case 3: dispatch_rows<3>(gather, perm, src, dst, n, s); break;
-        default: dispatch_rows<4>(gather, perm, src, dst, n, s); break;
+        case 1: dispatch_rows<1>(gather, perm, src, dst, n, umap, s); break;
+        case 2: dispatch_rows<2>(gather, perm, src, dst, n, umap, s); break;
+        case 3: dispatch_rows<3>(gather, perm, src, dst, n, umap, s); break;
+        default: dispatch_rows<4>(gather, perm, src, dst, n, umap, s); break;
     }
 }
 
@@ -1324,14 +1353,27 @@ void init_setup_attributes() {
     cudaFuncSetAttribute(k_galerkin4<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galerkin4_smem(24));
 }
 
-int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s) {
+int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s,
+                       const int32_t* umap) {
     if (n <= 0) return 0;
-    rows_k(K, true, perm, src_user, dst_int, n, s);
+    rows_k(K, true, perm, src_user, dst_int, n, umap, s);
     return 1;
 }
-int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s) {
+int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, double* dst_user, int n, cudaStream_t s,
+                        const int32_t* umap) {
     if (n <= 0) return 0;
-    rows_k(K, false, perm, src_int, dst_user, n, s);
+    rows_k(K, false, perm, src_int, dst_user, n, umap, s);
+    return 1;
+}
+int launch_dirichlet_rhs(int K, const int32_t* krp, const int32_t* kcol, const double* kval, const double* X,
+                         double* b, int n, cudaStream_t s) {
+    if (n <= 0) return 0;
+    switch (K) {
+        case 1: k_dirichlet_rhs<1><<<nblk(n, kBlock), kBlock, 0, s>>>(krp, kcol, kval, X, b, n); break;
+        case 2: k_dirichlet_rhs<2><<<nblk(n, kBlock), kBlock, 0, s>>>(krp, kcol, kval, X, b, n); break;
+        case 3: k_dirichlet_rhs<3><<<nblk(n, kBlock), kBlock, 0, s>>>(krp, kcol, kval, X, b, n); break;
+        default: k_dirichlet_rhs<4><<<nblk(n, kBlock), kBlock, 0, s>>>(krp, kcol, kval, X, b, n); break;
+    }
     return 1;
 }
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s) {

@@ -56,6 +56,7 @@ def lib():
             "mg_set_matrix_split_cotan": (C.c_int, [_vp, _vp]),
             "mg_set_alpha": (C.c_int, [_vp, dbl]),
             "mg_set_smoother": (C.c_int, [_vp, C.c_int, dbl, C.c_int]),
+            "mg_set_dirichlet": (C.c_int, [_vp, i32, _vp]),
             "mg_solve_pcg": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_solve": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_level_info": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
@@ -180,6 +181,12 @@ def mg_solve(ctx, k, B, X, rel_tol, max_cycles, res_hist=None):
                         _ptr(res_hist, np.float64), C.byref(cyc))
     _check(ctx, rc, allow=(MG_NOT_CONVERGED,))
     return rc, cyc.value
+
+
+def mg_set_dirichlet(ctx, known):
+    """Known fine vertices (App. B); an empty list removes the constraints."""
+    known = np.ascontiguousarray(np.asarray(known, dtype=np.int32))
+    return _check(ctx, lib().mg_set_dirichlet(ctx, int(known.size), known.ctypes.data if known.size else None))
 
 
 def mg_set_smoother(ctx, kind=0, omega=0.8, symmetric=False):
@@ -348,6 +355,9 @@ class Solver:
         if hist is not None:
             hist = hist.reshape(max_cycles + 1, k)[: cyc + 1]
         return rc, cyc, hist
+
+    def set_dirichlet(self, known):
+        return mg_set_dirichlet(self.ctx, known)
 
     def set_smoother(self, kind=0, omega=0.8, symmetric=False):
         return mg_set_smoother(self.ctx, kind, omega, symmetric)

@@ -425,3 +425,106 @@ def test_full_size_mcf_steps(ora):
         S.apply_mass(X2, B)
         rc, cyc, _ = S.solve(B, X2, rel_tol=p.rel_tol, max_cycles=p.max_cycles)
         assert rc == 0 and abs(cyc - cyc_o[t]) <= 1
+
+
+def _dirichlet_case(ora, p, known, k, seed):
+    rng = np.random.default_rng(seed)
+    A, M = ora.assemble(p.levels[0][0], p.levels[0][1], p.mass_coeff, p.lap_coeff)
+    X0 = np.zeros((p.n, k))
+    X0[known] = rng.standard_normal((len(known), k))
+    B = np.ascontiguousarray(M[:, None] * rng.standard_normal((p.n, k)))
+    return A, M, X0, B
+
+
+@pytest.mark.parametrize("cid,kw,frac", [(2, {"subdiv": 5}, 0.1), (3, {"grid": (96, 80)}, 0.0), (1, {}, 0.3)])
+def test_dirichlet_parity(ora, cid, kw, frac):
+    """Row f2 (App. B): constrained solves through both matrix paths (user
+    CSR and GPU cotan assembly) against the oracle's reduction: reduced
+    patterns and colourings bit-exact, X and history within tolerance, known
+    rows untouched.  Config 3 constrains both boundary loops (Dirichlet BC
+    on the open cylinder)."""
+    import torch
+    p = meshgen.make_config(cid, **kw)
+    rng = np.random.default_rng(31)
+    if cid == 3:
+        z = p.levels[0][0][:, 2]
+        known = np.nonzero((z <= z.min() + 1e-12) | (z >= z.max() - 1e-12))[0]
+    else:
+        known = np.sort(rng.choice(p.n, int(frac * p.n), replace=False))
+    A, M, X0, B = _dirichlet_case(ora, p, known, 2, 32)
+    Xo, ho, rco, mgo = ora.dirichlet_solve(p.sizes, p.P, A, B, X0, known, rel_tol=0.0, max_cycles=5)
+    rp, col, val = A.arrays()
+    for path in ("csr", "cotan", "csr_device"):
+        S = gpu_solver(p)
+        S.set_dirichlet(known)
+        if path == "cotan":
+            S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+        elif path == "csr":
+            S.set_matrix(rp.astype(np.int32), col, val)
+        else:
+            S.set_matrix(torch.from_numpy(rp.astype(np.int32)).cuda(), torch.from_numpy(col).cuda(),
+                         torch.from_numpy(val).cuda())
+        for l in range(mgo.n_levels):
+            check_level_parity(S, mgo, l)
+        if path == "csr_device":
+            Xt = torch.from_numpy(X0.copy()).cuda()
+            rc, cyc, hg = S.solve(torch.from_numpy(B).cuda(), Xt, rel_tol=0.0, max_cycles=5)
+            Xg = Xt.cpu().numpy()
+        else:
+            Xg = X0.copy()
+            rc, cyc, hg = S.solve(B, Xg, rel_tol=0.0, max_cycles=5)
+        assert np.array_equal(Xg[known], X0[known])
+        check_x(Xg, Xo)
+        Su = A.to_scipy()
+        u = np.setdiff1d(np.arange(p.n), known)
+        bu = B[u] - Su[u][:, known] @ X0[known]
+        check_history(hg, ho, tau_floor(Su[u][:, u], Xo[u], bu))
+        if path == "cotan":
+            Mg = np.empty((p.n, 2))
+            S.apply_mass(np.ones((p.n, 2)), Mg)
+            assert np.abs(Mg[:, 0] - M).max() <= 1e-12 * M.max()
+        S.close()
+
+
+def test_dirichlet_edge_cases(ora):
+    from paper_2104_13755_b200 import mg
+    p = meshgen.make_config(1, subdiv=3)                  # nested: 642 -> 162 -> 42
+    A, M = ora.assemble(p.levels[0][0], p.levels[0][1], p.mass_coeff, p.lap_coeff)
+    rp, col, val = A.arrays()
+    rp = rp.astype(np.int32)
+    rng = np.random.default_rng(33)
+    # every child of coarse vertex 7 known: its column of P_{u:} vanishes (P:870-871)
+    c0, w0 = p.P[0]
+    children = np.nonzero(((c0 == 7) & (w0 != 0.0)).any(axis=1))[0]
+    A_, M_, X0, B = _dirichlet_case(ora, p, children, 1, 34)
+    Xo, ho, _, mgo = ora.dirichlet_solve(p.sizes, p.P, A, B, X0, children, rel_tol=0.0, max_cycles=6)
+    S = gpu_solver(p)
+    S.set_dirichlet(children)
+    S.set_matrix(rp, col, val)
+    assert mg.mg_level_info(S.ctx, 1)[0] == p.sizes[1] - 1
+    for l in range(mgo.n_levels):
+        check_level_parity(S, mgo, l)
+    Xg = X0.copy()
+    S.solve(B, Xg, rel_tol=0.0, max_cycles=6)
+    check_x(Xg, Xo)
+    # all known: nothing to solve, X unchanged
+    S.set_dirichlet(np.arange(p.n))
+    S.set_matrix(rp, col, val)
+    Xa = rng.standard_normal((p.n, 1))
+    Xc = Xa.copy()
+    rc, cyc, h = S.solve(B, Xc, rel_tol=1e-10, max_cycles=5)
+    assert rc == 0 and cyc == 0 and np.array_equal(Xc, Xa)
+    # no constraints again: identical to a fresh unconstrained context
+    S.set_dirichlet([])
+    S.set_matrix(rp, col, val)
+    X1 = np.zeros_like(B)
+    S.solve(B, X1, rel_tol=0.0, max_cycles=4)
+    S2 = gpu_solver(p)
+    S2.set_matrix(rp, col, val)
+    X2 = np.zeros_like(B)
+    S2.solve(B, X2, rel_tol=0.0, max_cycles=4)
+    assert np.array_equal(X1, X2)
+    with pytest.raises(mg.MGError):
+        S.set_dirichlet([0, 0])                           # repeated index
+    with pytest.raises(mg.MGError):
+        S.set_dirichlet([p.n])                            # out of range
