@@ -103,7 +103,20 @@ int mg_set_matrix(mg_ctx* ctx, int32_t n, int64_t nnz, const int32_t* row_ptr, c
  * MG_ERR_NOT_SPD, MG_ERR_CUDA. */
 int mg_set_matrix_cotan(mg_ctx* ctx, const double* V, double mass_coeff, double lap_coeff);
 
-/* B = M X with the lumped mass of the last mg_set_matrix_cotan; X, B are
+/* Row f3: the squared-Laplacian (bilaplacian) smoothing operator, E_{Delta^2}
+ * of the data-smoothing application ("the Bilaplacian (2-ring sparsity)",
+ * P:595), assembled on the GPU from positions V ([n_verts[0]][3], host
+ * or device) over F[0]:
+ *     A = mass_coeff * M + bilap_coeff * Q,   Q = L M^{-1} L
+ * with L the cotan Laplacian (A13) and M the lumped mass (A14); the pattern is
+ * the 2-ring of F[0].  For the data-smoothing system of App. D eq. 1 use
+ * mass_coeff = 1 - alpha, bilap_coeff = alpha and B = (1 - alpha) M f
+ * (mg_apply_mass).  Then as mg_set_matrix (Galerkin + factor; honours
+ * mg_set_dirichlet).  M is kept for mg_apply_mass.
+ * Errors: as mg_set_matrix_cotan. */
+int mg_set_matrix_bilaplacian(mg_ctx* ctx, const double* V, double mass_coeff, double bilap_coeff);
+
+/* B = M X with the lumped mass of the last mg_set_matrix_cotan / _bilaplacian; X, B are
  * [n][k] (host or device; both of the same kind).  Errors: MG_ERR_STATE. */
 int mg_apply_mass(mg_ctx* ctx, int32_t k, const double* X, double* B);
 

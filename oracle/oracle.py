@@ -165,6 +165,27 @@ def assemble(V, F, mass_coeff, lap_coeff):
     return mass_plus_laplacian(L, M, mass_coeff, lap_coeff), M
 
 
+def bilaplacian(V, F):
+    """Row f3: Q = L M^{-1} L (E_{Delta^2}) from
+    the oracle's cotan L and lumped M, one scipy sparse product (a library
+    primitive); returns (Q as Csr, M)."""
+    import scipy.sparse as sp
+    L = cotan_laplacian(V, F).to_scipy()
+    M = lumped_mass(V, F)
+    Q = (L @ sp.diags(1.0 / M) @ L).tocsr()
+    Q.sort_indices()
+    return Csr.from_scipy(Q), M
+
+
+def assemble_bilaplacian(V, F, mass_coeff, bilap_coeff):
+    """A = mass_coeff M + bilap_coeff L M^{-1} L on the 2-ring pattern (and M)."""
+    import scipy.sparse as sp
+    Q, M = bilaplacian(V, F)
+    A = (bilap_coeff * Q.to_scipy() + mass_coeff * sp.diags(M)).tocsr()
+    A.sort_indices()
+    return Csr.from_scipy(A), M
+
+
 def prolongation(n_coarse, cols, w):
     cols, w = _i32(cols), _f64(w)
     return Csr(lib().ora_prolongation(cols.shape[0], n_coarse, cols, w))

@@ -206,6 +206,8 @@ struct mg_ctx {
     DBuf<double> uk_val, full_val, full_V;
     DBuf<int32_t> full_opp;
     Level full0;                     // full 1-ring pattern (user order) for cotan assembly in Dirichlet mode
+    DBuf<int32_t> bl_rp, bl_col;     // 2-ring pattern (user order) of the bilaplacian (row f3)
+    DBuf<double> bl_val;
 
     std::vector<int32_t> opp_user;   // cotan: 2 opposite vertices per user nnz (-1 none)
     DBuf<int32_t> opp;               // internal
@@ -1263,6 +1265,84 @@ int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, con
     return rebuild_hierarchy(c);
 }
 
+// Full-mesh 1-ring structures in user order (Dirichlet-mode cotan assembly and
+// the bilaplacian): pattern, opposite vertices, identity map, positions / L /
+// M buffers.
+static int upload_full_one_ring(mg_ctx* c, const std::vector<int32_t>& rp, const std::vector<int32_t>& cl,
+                                const std::vector<int32_t>& opp) {
+    const int32_t n = c->n_full;
+    std::vector<int32_t> rpad(rp), cpad(cl), ident(n);
+    rpad.resize(rpad.size() + 8, rp.back());
+    cpad.resize(cpad.size() + 8, 0);
+    std::iota(ident.begin(), ident.end(), 0);
+    c->full0.n = n;
+    c->full0.nnz = (int64_t)cl.size();
+    cudaError_t e;
+    if ((e = c->full0.rp.upload(rpad, c->stream)) || (e = c->full0.col.upload(cpad, c->stream)) ||
+        (e = c->full_opp.upload(opp, c->stream)) || (e = c->d_ident.upload(ident, c->stream)) ||
+        (e = c->full_V.alloc(4 * (size_t)n)) || (e = c->full_val.alloc(cl.size() + 8)) || (e = c->Muser.alloc(n)))
+        return c->cuda_fail(e, "full 1-ring setup");
+    return MG_OK;
+}
+
+// 1-ring CSR pattern of F[0] (sorted, diagonal included) and the two opposite
+// vertices of every stored edge (-1: none / diagonal), user order.
+static int build_one_ring(mg_ctx* c, std::vector<int32_t>& rp, std::vector<int32_t>& cl, std::vector<int32_t>& opp) {
+    const int32_t n = c->n_full;
+    rp.assign(n + 1, 0);
+    cl.clear();
+    opp.clear();
+    // half-edges (i, j, opposite vertex o) of every face, sorted by (i, j)
+    struct HalfEdge {
+        int32_t i, j, o;
+    };
+    std::vector<HalfEdge> he;
+    he.reserve(6 * (size_t)c->nF0);
+    for (int32_t f = 0; f < c->nF0; ++f)
+        for (int k = 0; k < 3; ++k) {
+            const int32_t o = c->F0[3 * (size_t)f + k];
+            const int32_t i = c->F0[3 * (size_t)f + (k + 1) % 3];
+            const int32_t j = c->F0[3 * (size_t)f + (k + 2) % 3];
+            he.push_back({i, j, o});
+            he.push_back({j, i, o});
+        }
+    std::sort(he.begin(), he.end(), [](const HalfEdge& a, const HalfEdge& b) {
+        return a.i != b.i ? a.i < b.i : a.j < b.j;
+    });
+    cl.reserve(n + he.size() / 2);
+    size_t t = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        bool diag_done = false;
+        bool any = false;
+        while (t < he.size() && he[t].i == i) {
+            const int32_t j = he[t].j;
+            if (!diag_done && j > i) {
+                cl.push_back(i);
+                opp.push_back(-1);
+                opp.push_back(-1);
+                diag_done = true;
+            }
+            cl.push_back(j);
+            opp.push_back(he[t].o);
+            opp.push_back(-1);
+            ++t;
+            if (t < he.size() && he[t].i == i && he[t].j == j) {
+                opp.back() = he[t].o;
+                ++t;
+            }
+            any = true;
+        }
+        if (!any) return c->fail(MG_ERR_INPUT, "vertex %d is in no face of F[0]", i);
+        if (!diag_done) {
+            cl.push_back(i);
+            opp.push_back(-1);
+            opp.push_back(-1);
+        }
+        rp[i + 1] = (int32_t)cl.size();
+    }
+    return MG_OK;
+}
+
 // 1-ring pattern of F[0] with the opposite-vertex table of every edge
 // (pattern setup on first use), then the positions gathered into internal
 // order as 32-byte rows in c->Vint.
@@ -1274,72 +1354,13 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
     const int32_t n = c->n_full;   // the 1-ring is built on the full fine mesh
     const bool full_mode = c->dir || c->dir_all;
     if (!c->have_pattern || c->pattern_kind != 1 || c->pattern_hash != c->dir_version) {
-        // 1-ring pattern of F[0] and the opposite vertices of every edge
-        struct HalfEdge {
-            int32_t i, j, o;
-        };
-        std::vector<HalfEdge> he;
-        he.reserve(6 * (size_t)c->nF0);
-        for (int32_t f = 0; f < c->nF0; ++f)
-            for (int k = 0; k < 3; ++k) {
-                const int32_t o = c->F0[3 * (size_t)f + k];
-                const int32_t i = c->F0[3 * (size_t)f + (k + 1) % 3];
-                const int32_t j = c->F0[3 * (size_t)f + (k + 2) % 3];
-                he.push_back({i, j, o});
-                he.push_back({j, i, o});
-            }
-        std::sort(he.begin(), he.end(), [](const HalfEdge& a, const HalfEdge& b) {
-            return a.i != b.i ? a.i < b.i : a.j < b.j;
-        });
-        std::vector<int32_t> rp(n + 1, 0), cl;
-        std::vector<int32_t> opp;
-        cl.reserve(n + he.size() / 2);
-        size_t t = 0;
-        for (int32_t i = 0; i < n; ++i) {
-            bool diag_done = false;
-            bool any = false;
-            while (t < he.size() && he[t].i == i) {
-                const int32_t j = he[t].j;
-                if (!diag_done && j > i) {
-                    cl.push_back(i);
-                    opp.push_back(-1);
-                    opp.push_back(-1);
-                    diag_done = true;
-                }
-                cl.push_back(j);
-                opp.push_back(he[t].o);
-                opp.push_back(-1);
-                ++t;
-                if (t < he.size() && he[t].i == i && he[t].j == j) {
-                    opp.back() = he[t].o;
-                    ++t;
-                }
-                any = true;
-            }
-            if (!any) return c->fail(MG_ERR_INPUT, "vertex %d is in no face of F[0]", i);
-            if (!diag_done) {
-                cl.push_back(i);
-                opp.push_back(-1);
-                opp.push_back(-1);
-            }
-            rp[i + 1] = (int32_t)cl.size();
-        }
+        std::vector<int32_t> rp, cl, opp;
+        if ((rc = build_one_ring(c, rp, cl, opp))) return rc;
         c->have_pattern = false;
         if (full_mode) {
             // Dirichlet mode: assemble on the full mesh in user order, then
             // extract A_uu / A_uk (App. B)
-            std::vector<int32_t> rpad(rp), cpad(cl), ident(n);
-            rpad.resize(rpad.size() + 8, rp.back());
-            cpad.resize(cpad.size() + 8, 0);
-            std::iota(ident.begin(), ident.end(), 0);
-            c->full0.n = n;
-            c->full0.nnz = (int64_t)cl.size();
-            cudaError_t e;
-            if ((e = c->full0.rp.upload(rpad, c->stream)) || (e = c->full0.col.upload(cpad, c->stream)) ||
-                (e = c->full_opp.upload(opp, c->stream)) || (e = c->d_ident.upload(ident, c->stream)) ||
-                (e = c->full_V.alloc(4 * (size_t)n)) || (e = c->full_val.alloc(cl.size() + 8)) ||
-                (e = c->Muser.alloc(n)))
-                return c->cuda_fail(e, "cotan setup");
+            if ((rc = upload_full_one_ring(c, rp, cl, opp))) return rc;
             if (!c->dir_all && (rc = dir_pattern(c, rp, cl))) return rc;
             c->have_pattern = !c->dir_all;
             c->pattern_kind = 1;
@@ -1401,6 +1422,72 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
         return launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, L0.val.p, c->Mint.p, c->stream) +
                launch_scatter_vec(L0.diperm.p, c->Mint.p, c->Muser.p, n, c->stream);
     });
+    return rebuild_hierarchy(c);
+}
+
+// Row f3: A = mass_coeff M + bilap_coeff L M^{-1} L on the 2-ring pattern.
+int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, double bilap_coeff) {
+    int rc = check_state(c, false);
+    if (rc) return rc;
+    if (!V) return c->fail(MG_ERR_INVALID_ARG, "V is null");
+    if (c->nF0 <= 0) return c->fail(MG_ERR_STATE, "the hierarchy has no fine faces F[0]");
+    const int32_t n = c->n_full;
+    cudaStream_t s = c->stream;
+    if (!c->have_pattern || c->pattern_kind != 2 || c->pattern_hash != c->dir_version) {
+        std::vector<int32_t> rp1, cl1, opp;
+        if ((rc = build_one_ring(c, rp1, cl1, opp))) return rc;
+        if ((rc = upload_full_one_ring(c, rp1, cl1, opp))) return rc;
+        // 2-ring: union of the 1-rings of i's 1-ring (sorted, unique)
+        std::vector<int32_t> rp2(n + 1, 0), cl2, row;
+        std::vector<int32_t> mark(n, -1);
+        for (int32_t i = 0; i < n; ++i) {
+            row.clear();
+            for (int32_t t = rp1[i]; t < rp1[i + 1]; ++t) {
+                const int32_t k = cl1[t];
+                for (int32_t u = rp1[k]; u < rp1[k + 1]; ++u)
+                    if (mark[cl1[u]] != i) {
+                        mark[cl1[u]] = i;
+                        row.push_back(cl1[u]);
+                    }
+            }
+            std::sort(row.begin(), row.end());
+            cl2.insert(cl2.end(), row.begin(), row.end());
+            rp2[i + 1] = (int32_t)cl2.size();
+        }
+        cudaError_t e;
+        if ((e = c->bl_rp.upload(rp2, s)) || (e = c->bl_col.upload(cl2, s)) || (e = c->bl_val.alloc(cl2.size() + 8)))
+            return c->cuda_fail(e, "bilaplacian setup");
+        c->have_pattern = false;
+        if (!c->dir_all) {
+            rc = c->dir ? dir_pattern(c, rp2, cl2) : setup_pattern(c, rp2, cl2);
+            if (rc) return rc;
+        }
+        c->have_pattern = !c->dir_all;
+        c->pattern_kind = 2;
+        c->pattern_hash = c->dir_version;
+    }
+    const double* dV = nullptr;
+    if ((rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV))) return rc;
+    c->timed(PC_ASSEMBLY, 0, s, [&] {
+        return launch_gather_rows(3, c->d_ident.p, dV, c->full_V.p, n, s) +
+               launch_cotan(c->full0, c->full_opp.p, c->full_V.p, 0.0, 1.0, c->full_val.p, c->Muser.p, s) +
+               launch_bilaplacian(c->bl_rp.p, c->bl_col.p, c->full0.rp.p, c->full0.col.p, c->full_val.p, c->Muser.p,
+                                  mass_coeff, bilap_coeff, c->bl_val.p, n, s);
+    });
+    c->have_mass = true;
+    c->have_split = false;
+    if (c->dir_all) {
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e) return c->cuda_fail(e, "mg_set_matrix_bilaplacian");
+        c->have_matrix = true;
+        return MG_OK;
+    }
+    Level& L0 = *c->lv[0];
+    if (c->dir) {
+        if ((rc = dir_values(c, c->bl_val.p))) return rc;
+    } else {
+        c->timed(PC_PERMUTE, 0, s, [&] { return launch_gather_vals(L0.di2u.p, c->bl_val.p, L0.val.p, L0.nnz, s); });
+    }
     return rebuild_hierarchy(c);
 }
 

@@ -185,6 +185,9 @@ int launch_dirichlet_rhs(int K, const int32_t* krp, const int32_t* kcol, const d
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
 int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
                  double* val, double* M_int, cudaStream_t s);
+int launch_bilaplacian(const int32_t* rp2, const int32_t* col2, const int32_t* rp1, const int32_t* col1,
+                       const double* Lv, const double* M, double mass_coeff, double bilap_coeff, double* out, int n,
+                       cudaStream_t s);
 int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, double* out, int64_t nnz,
                  cudaStream_t s);
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);

@@ -168,6 +168,44 @@ __global__ void __launch_bounds__(kBlock) k_axpby(const double* __restrict__ Q, 
     if ((nnz & 1) && blockIdx.x == 0 && threadIdx.x == 0) out[nnz - 1] = alpha * Q[nnz - 1] + beta * M[nnz - 1];
 }
 
+// ---------------------------------------------------------------------------
+// Row f3: squared-Laplacian (bilaplacian) data-smoothing operator (E_{Delta^2},
+// P:595; SPEC S:212-219 Q = L^T M^{-1} L with lumped M), user order on
+// the 2-ring pattern:  Q_ij = sum_{k in N(i) cap N(j)} L_ik L_kj / M_k  (L
+// symmetric: L_kj = L_jk), A = mass_coeff M + bilap_coeff Q.  kBlG lanes per
+// row, one 2-ring entry per lane: the two sorted 1-ring rows of i and j are
+// merged in ascending k (fixed order, deterministic).
+constexpr int kBlG = 8;
+__global__ void __launch_bounds__(kBlock) k_bilaplacian(const int* __restrict__ rp2, const int* __restrict__ col2,
+                                                        const int* __restrict__ rp1, const int* __restrict__ col1,
+                                                        const double* __restrict__ Lv, const double* __restrict__ M,
+                                                        double mass_coeff, double bilap_coeff,
+                                                        double* __restrict__ out, int n) {
+    const int i = (blockIdx.x * kBlock + threadIdx.x) / kBlG;
+    const int lane = threadIdx.x & (kBlG - 1);
+    if (i >= n) return;
+    const int a0 = rp1[i], a1 = rp1[i + 1];
+    for (int e = rp2[i] + lane; e < rp2[i + 1]; e += kBlG) {
+        const int j = col2[e];
+        int p = a0, r = rp1[j];
+        const int r1 = rp1[j + 1];
+        double q = 0.0;
+        while (p < a1 && r < r1) {
+            const int kp = col1[p], kr = col1[r];
+            if (kp == kr) {
+                q += Lv[p] * Lv[r] / M[kp];
+                ++p;
+                ++r;
+            } else if (kp < kr) {
+                ++p;
+            } else {
+                ++r;
+            }
+        }
+        out[e] = bilap_coeff * q + (j == i ? mass_coeff * M[i] : 0.0);
+    }
+}
+
 __global__ void k_scatter_vec(const int* __restrict__ iperm, const double* __restrict__ src, double* __restrict__ dst,
                               int n) {
     const int u = blockIdx.x * kBlock + threadIdx.x;
@@ -1441,6 +1479,14 @@ int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, 
     const int64_t n2 = (nnz + 1) / 2;
     const int grid = (int)std::min<int64_t>((n2 + kBlock - 1) / kBlock, 148 * 8);
     k_axpby<<<grid, kBlock, 0, s>>>(Qv, Mv, alpha, beta, out, nnz);
+    return 1;
+}
+int launch_bilaplacian(const int32_t* rp2, const int32_t* col2, const int32_t* rp1, const int32_t* col1,
+                       const double* Lv, const double* M, double mass_coeff, double bilap_coeff, double* out, int n,
+                       cudaStream_t s) {
+    if (n <= 0) return 0;
+    k_bilaplacian<<<nblk((int64_t)n * kBlG, kBlock), kBlock, 0, s>>>(rp2, col2, rp1, col1, Lv, M, mass_coeff,
+                                                                      bilap_coeff, out, n);
     return 1;
 }
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s) {

@@ -57,6 +57,7 @@ def lib():
             "mg_set_alpha": (C.c_int, [_vp, dbl]),
             "mg_set_smoother": (C.c_int, [_vp, C.c_int, dbl, C.c_int]),
             "mg_set_dirichlet": (C.c_int, [_vp, i32, _vp]),
+            "mg_set_matrix_bilaplacian": (C.c_int, [_vp, _vp, dbl, dbl]),
             "mg_solve_pcg": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_solve": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
             "mg_level_info": (C.c_int, [_vp, C.c_int, _vp, _vp, _vp]),
@@ -181,6 +182,10 @@ def mg_solve(ctx, k, B, X, rel_tol, max_cycles, res_hist=None):
                         _ptr(res_hist, np.float64), C.byref(cyc))
     _check(ctx, rc, allow=(MG_NOT_CONVERGED,))
     return rc, cyc.value
+
+
+def mg_set_matrix_bilaplacian(ctx, V, mass_coeff, bilap_coeff):
+    return _check(ctx, lib().mg_set_matrix_bilaplacian(ctx, _ptr(V, np.float64), float(mass_coeff), float(bilap_coeff)))
 
 
 def mg_set_dirichlet(ctx, known):
@@ -355,6 +360,9 @@ class Solver:
         if hist is not None:
             hist = hist.reshape(max_cycles + 1, k)[: cyc + 1]
         return rc, cyc, hist
+
+    def set_matrix_bilaplacian(self, V, mass_coeff, bilap_coeff):
+        return mg_set_matrix_bilaplacian(self.ctx, V, mass_coeff, bilap_coeff)
 
     def set_dirichlet(self, known):
         return mg_set_dirichlet(self.ctx, known)

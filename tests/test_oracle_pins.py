@@ -705,3 +705,54 @@ def test_dirichlet_zero_column_removal(ora):
         rows = np.repeat(np.arange(lv["n"]), np.diff(lv["rowptr"]))
         diag = lv["val"][lv["col"] == rows]
         assert diag.size == lv["n"] and (diag > 0).all()
+
+
+# --------------------------------------------------------------------- f3: bilaplacian L M^-1 L
+
+
+def test_bilaplacian_invariants_and_pattern(ora):
+    """Q 1 = 0, symmetric PSD, pattern = the 2-ring."""
+    p = meshgen.make_config(2, subdiv=3)
+    V, F = p.levels[0]
+    Q, M = ora.bilaplacian(V, F)
+    Qs = Q.to_scipy()
+    n = V.shape[0]
+    assert np.abs(Qs @ np.ones(n)).max() <= 1e-10 * abs(Qs).max()
+    assert abs(Qs - Qs.T).max() <= 1e-12 * abs(Qs).max()
+    assert np.linalg.eigvalsh(Qs.toarray()).min() >= -1e-10 * abs(Qs).max()
+    G = sp.csr_matrix((np.ones(3 * F.shape[0] * 2), (np.r_[F[:, 0], F[:, 1], F[:, 2], F[:, 1], F[:, 2], F[:, 0]],
+                                                      np.r_[F[:, 1], F[:, 2], F[:, 0], F[:, 0], F[:, 1], F[:, 2]])),
+                      shape=(n, n)) + sp.eye(n)
+    two_ring = (G @ G).tocsr()
+    two_ring.sort_indices()
+    assert np.array_equal(two_ring.indptr, Qs.indptr) and np.array_equal(two_ring.indices, Qs.indices)
+
+
+def test_bilaplacian_sphere_closed_form(ora):
+    """Closed form on the unit sphere: -Delta z = 2 z, so int (Delta z)^2 =
+    4 int z^2: the Rayleigh quotient z^T Q z / z^T M z -> 4 at O(h^2) (error
+    ~4x smaller per subdivision; the pointwise strong form does not converge
+    for cotan operators, the energy does)."""
+    errs = []
+    for k in (3, 4, 5):
+        V, F = meshgen.icosphere(k)
+        Q, M = ora.bilaplacian(V, F)
+        z = V[:, 2]
+        errs.append(abs(z @ (Q.to_scipy() @ z) / (z @ (M * z)) - 4.0))
+    assert errs[0] / errs[1] > 3.5 and errs[1] / errs[2] > 3.5 and errs[2] < 1e-4
+
+
+def test_bilaplacian_smoothing_solve(ora):
+    """The data-smoothing system (alpha Q + (1 - alpha) M) x = (1 - alpha) M f
+    (App. D eq. 1 with E_{Delta^2}) on the intrinsic hierarchy reaches the
+    dense solution."""
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    alpha = 1e-4
+    A, M = ora.assemble_bilaplacian(V, F, 1 - alpha, alpha)
+    f = np.random.default_rng(41).standard_normal((p.n, 1))
+    B = (1 - alpha) * M[:, None] * f
+    X, hist, rc = ora.MG(p.sizes, p.P, A).solve(B, rel_tol=1e-11, max_cycles=200)
+    assert rc == 0
+    xs = np.linalg.solve(A.to_scipy().toarray(), B)
+    assert np.linalg.norm(X - xs) / np.linalg.norm(xs) <= 1e-9
