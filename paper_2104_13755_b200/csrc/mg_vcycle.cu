@@ -201,28 +201,8 @@ struct StageView {
     const double* vs; // vs[q] = val[e0 + q]
 };
 
-// Row-vector part of a stage (after the matrix part): b rows, then (residual
-// modes) the rows' own x; rows [row0, row0 + nrow) rounded to 16-byte
-// boundaries for K = 1.
-template <int K>
-__host__ __device__ inline size_t vec_stage_doubles() { return (size_t)(kTile + 2) * VS<K>::S; }
-template <int K>
-__device__ __forceinline__ int vec_row_base(const TileDesc& d) {
-    return VS<K>::S == 1 ? (d.row0 & ~1) : d.row0;
-}
-template <int K>
-__device__ __forceinline__ unsigned vec_bytes(const TileDesc& d) {
-    const int ra = vec_row_base<K>(d);
-    int cnt = d.row0 + d.nrow - ra;
-    if (VS<K>::S == 1) cnt = (cnt + 1) & ~1;
-    return (unsigned)(cnt * VS<K>::S * 8);
-}
-
-// Matrix part of a stage; `extra` bytes (the row vectors, issued separately)
-// are added to the barrier's expected transaction count.
 __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* stage, int cap, uint64_t* bar,
-                                           const int* rp, const int* col, const double* val, uint64_t pol,
-                                           unsigned extra = 0) {
+                                           const int* rp, const int* col, const double* val, uint64_t pol) {
     const int ra = d.row0 & ~3;
     const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
     const int ca = d.e0 & ~3;
@@ -233,20 +213,10 @@ __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* sta
     int* cs = rps + (kTile + 8);
     double* vs = reinterpret_cast<double*>(stage + ((size_t)stage_ints(cap) * 4 + 15) / 16 * 16);
     const unsigned bytes = (unsigned)(rcnt * 4 + ccnt * 4 + vcnt * 8);
-    mbar_expect_tx(bar, bytes + extra);
+    mbar_expect_tx(bar, bytes);
     bulk_g2s(rps, rp + ra, rcnt * 4, bar, pol);
     if (ccnt > 0) bulk_g2s(cs, col + ca, ccnt * 4, bar, pol);
     if (vcnt > 0) bulk_g2s(vs, val + va, vcnt * 8, bar, pol);
-}
-
-// Row vectors of a stage: b rows into vstage[0 ..), own x rows after them.
-template <int K>
-__device__ __forceinline__ void issue_vec(const TileDesc& d, double* vstage, const double* b, const double* x,
-                                          bool with_x, uint64_t* bar, uint64_t pol_b, uint64_t pol_x) {
-    const int ra = vec_row_base<K>(d);
-    const unsigned nb = vec_bytes<K>(d);
-    bulk_g2s(vstage, b + (size_t)ra * VS<K>::S, nb, bar, pol_b);
-    if (with_x) bulk_g2s(vstage + vec_stage_doubles<K>(), x + (size_t)ra * VS<K>::S, nb, bar, pol_x);
 }
 
 __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned char* stage, int cap) {
@@ -307,12 +277,8 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
     const int tid = threadIdx.x;
-    const size_t sa = (stage_bytes(cap) + 127) / 128 * 128;                 // matrix part
-    const size_t sv = vec_stage_doubles<K>() * 8 * (MODE == 0 ? 1 : 2);     // row vectors
-    const size_t sb = (sa + sv + 127) / 128 * 128;
+    const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
     unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
-    double* vst[2] = {reinterpret_cast<double*>(smem_pipe + sa), reinterpret_cast<double*>(smem_pipe + sb + sa)};
-    constexpr bool kWithX = MODE != 0;
     pdl_launch_dependents();
     const int nt = t_end - t_begin;
     const int mine = nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
@@ -324,22 +290,15 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // matrix part of the first two tiles before the wait (no kernel of the
-    // solve writes A); the row vectors only after it (b / x are produced by
-    // earlier kernels of the V-cycle)
-    TileDesc d0[2];
     if (tid == 0) {
         for (int i = 0; i < 2 && i < mine; ++i) {
-            d0[i] = tiles[t_begin + blockIdx.x + i * gridDim.x];
-            const unsigned vb = vec_bytes<K>(d0[i]) * (kWithX ? 2u : 1u);
-            issue_tile(d0[i], stage[i], cap, &bar[i], rp, col, val, pol, vb);
+            const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+            issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
         }
     }
     pdl_wait();
     const uint64_t xpol = evict_last_policy();
     const uint64_t spol = evict_first_policy();
-    if (tid == 0)
-        for (int i = 0; i < 2 && i < mine; ++i) issue_vec<K>(d0[i], vst[i], b, x, kWithX, &bar[i], spol, xpol);
     double acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
@@ -350,14 +309,11 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
         const StageView v = view_tile(d, stage[sidx], cap);
         if (tid < d.nrow) {
             const int row = d.row0 + tid;
-            // b (and the row's own x for the residual modes) from the stage
-            const int vo = (row - vec_row_base<K>(d)) * VS<K>::S;
+            // b (and the row's own x for the residual modes) go out before the
+            // neighbour gathers so all loads of the row share one round trip
             double bv[K], xr[K];
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-                bv[c] = vst[sidx][vo + c];
-                xr[c] = kWithX ? vst[sidx][vec_stage_doubles<K>() + vo + c] : 0.0;
-            }
+            ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
+            if (MODE != 0) ldrow_pol<K>(x + (size_t)row * VS<K>::S, xr, xpol);
             double s[K], dg;
             stage_row<K, PipeUnroll<K>::value>(v, tid, row, x, s, dg, xpol);
             if (MODE == 0) {
@@ -385,8 +341,7 @@ __global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict_
         __syncthreads();   // stage sidx fully consumed
         if (tid == 0 && i + 2 < mine) {
             const TileDesc dn = tiles[t_begin + blockIdx.x + (i + 2) * gridDim.x];
-            issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol, vec_bytes<K>(dn) * (kWithX ? 2u : 1u));
-            issue_vec<K>(dn, vst[sidx], b, x, kWithX, &bar[sidx], spol, xpol);
+            issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
         }
     }
     if (MODE == 2) {
@@ -891,13 +846,6 @@ __global__ void __launch_bounds__(kBlock) k_sumsq_partial(const double* __restri
 // ---------------------------------------------------------------------------
 inline size_t tile_smem(int cap) { return (size_t)cap * (sizeof(double) + sizeof(int)); }
 
-template <int K, int MODE>
-inline size_t pipe_smem(int cap) {
-    const size_t sa = (stage_bytes(cap) + 127) / 128 * 128;
-    const size_t sv = vec_stage_doubles<K>() * 8 * (MODE == 0 ? 1 : 2);
-    return 2 * ((sa + sv + 127) / 128 * 128);
-}
-template <int K, int MODE>
 inline int pipe_grid(int ntiles, int cap) {
     static int nsm = 0;
     if (!nsm) {
@@ -905,17 +853,17 @@ inline int pipe_grid(int ntiles, int cap) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = pipe_smem<K, MODE>(cap) + 2048;
+    const size_t smem = 2 * ((stage_bytes(cap) + 127) / 128 * 128) + 2048;
     const int per_sm = std::max(1, std::min<int>(8, (int)((227 * 1024) / smem)));
     return std::max(1, std::min(ntiles, nsm * per_sm));
 }
-inline size_t pipe_smem_max(int cap) { return pipe_smem<4, 1>(cap); }
+inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
 
 // MODE 0..3 over tiles [t0, t1) of level L (iterate read from xin)
 template <int K, int MODE>
 void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double* partial, int grid, double omega,
                  bool pdl, cudaStream_t s) {
-    launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, pipe_smem<K, MODE>(L.pipe_cap), s,
+    launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, pipe_smem(L.pipe_cap), s,
              reinterpret_cast<const TileDesc*>(L.tiles.p), t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial,
              L.pipe_cap, omega);
 }
@@ -940,7 +888,7 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
             t0 = L.tile_off[L.tile_off.size() - 2];   // whole-level tiles are the last range
             t1 = L.tile_off.back();
         }
-        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid<K, MODE>(t1 - t0, L.pipe_cap), omega, pdl, s);
+        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(t1 - t0, L.pipe_cap), omega, pdl, s);
         return 1;
     }
     if (L.tiled) {
@@ -965,7 +913,7 @@ int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, doub
     int grid;
     if (L.pipe) {
         const int t0 = L.tile_off[L.tile_off.size() - 2], t1 = L.tile_off.back();
-        grid = std::min(nb, pipe_grid<K, 2>(t1 - t0, L.pipe_cap));
+        grid = std::min(nb, pipe_grid(t1 - t0, L.pipe_cap));
         pipe_launch<K, 2>(L, t0, t1, L.x.p, nullptr, partial, grid, 0.0, pdl, s);
     } else if (L.tiled) {
         grid = std::min(nb, nblk(L.n, kTile));
@@ -1010,7 +958,7 @@ void set_attrs_k() {
 
 int resnorm_blocks(int) { return kNormBlocks; }
 int tile_rows() { return kTile; }
-size_t pipe_smem_bytes(int cap) { return pipe_smem_max(cap); }
+size_t pipe_smem_bytes(int cap) { return pipe_smem(cap); }
 size_t tile_smem_limit() { return 160 * 1024; }
 
 void init_vcycle_attributes() {
