@@ -62,15 +62,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // ---- internal vector layout ------------------------------------------------
 // Internal iterate / right-hand side / residual vectors are row-major with a
-// row stride of VS<K>::S doubles.  k = 3 uses packed 24-byte rows: padding
-// them to 32 bytes (one sector, one 256-bit load) made the config-4 iterate
-// 84 MB instead of 63 MB, which no longer stays L2-resident across the
-// colour passes (measured: level-0 GS time per cycle k=2 0.34 ms, k=3 padded
-// 0.55 ms, k=4 0.61 ms).  The user-facing [n][k] layout is converted by the
-// permutation kernels.
+// row stride of VS<K>::S doubles: K rounded up to an aligned vector width
+// (k = 3 is padded to 4 so every row is one 32-byte sector and one 256-bit
+// load).  The user-facing [n][k] layout is converted by the permutation
+// kernels.
 template <int K>
 struct VS {
-    static constexpr int S = K;
+    static constexpr int S = (K == 3) ? 4 : K;
 };
 
 template <int K>
@@ -80,9 +78,8 @@ __device__ __forceinline__ void ldrow(const double* p, double (&v)[K]) {
     } else if constexpr (K == 2) {
         asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
     } else if constexpr (K == 3) {
-        asm volatile("ld.global.f64 %0, [%3];\n\tld.global.f64 %1, [%3+8];\n\tld.global.f64 %2, [%3+16];"
-                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2])
-                     : "l"(p));
+        double pad;
+        asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(pad) : "l"(p));
     } else {
         asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
     }
@@ -101,11 +98,10 @@ __device__ __forceinline__ void ldrow_pol(const double* p, double (&v)[K], uint6
     } else if constexpr (K == 2) {
         asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v[0]), "=d"(v[1]) : "l"(p), "l"(pol));
     } else if constexpr (K == 3) {
-        asm volatile(
-            "ld.global.L2::cache_hint.f64 %0, [%3], %4;\n\tld.global.L2::cache_hint.f64 %1, [%3+8], %4;\n\t"
-            "ld.global.L2::cache_hint.f64 %2, [%3+16], %4;"
-            : "=d"(v[0]), "=d"(v[1]), "=d"(v[2])
-            : "l"(p), "l"(pol));
+        double pad;
+        asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(pad)
+                     : "l"(p), "l"(pol));
     } else {
         asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
@@ -120,11 +116,9 @@ __device__ __forceinline__ void strow_pol(double* p, const double (&v)[K], uint6
         asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p), "d"(v[0]), "d"(v[1]), "l"(pol)
                      : "memory");
     } else if constexpr (K == 3) {
-        asm volatile(
-            "st.global.L2::cache_hint.f64 [%0], %1, %4;\n\tst.global.L2::cache_hint.f64 [%0+8], %2, %4;\n\t"
-            "st.global.L2::cache_hint.f64 [%0+16], %3, %4;" ::"l"(p),
-            "d"(v[0]), "d"(v[1]), "d"(v[2]), "l"(pol)
-            : "memory");
+        asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                     "d"(v[2]), "d"(0.0), "l"(pol)
+                     : "memory");
     } else {
         asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
                      "d"(v[2]), "d"(v[3]), "l"(pol)
@@ -140,9 +134,8 @@ __device__ __forceinline__ void ldrow_cg(const double* p, double (&v)[K]) {
     } else if constexpr (K == 2) {
         asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
     } else if constexpr (K == 3) {
-        v[0] = __ldcg(p);
-        v[1] = __ldcg(p + 1);
-        v[2] = __ldcg(p + 2);
+        double pad;
+        asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(pad) : "l"(p));
     } else {
         asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
     }
@@ -154,8 +147,7 @@ __device__ __forceinline__ void strow(double* p, const double (&v)[K]) {
     } else if constexpr (K == 2) {
         asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v[0]), "d"(v[1]) : "memory");
     } else if constexpr (K == 3) {
-        asm volatile("st.global.f64 [%0], %1;\n\tst.global.f64 [%0+8], %2;\n\tst.global.f64 [%0+16], %3;" ::"l"(p),
-                     "d"(v[0]), "d"(v[1]), "d"(v[2])
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(0.0)
                      : "memory");
     } else {
         asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])

@@ -1389,8 +1389,8 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
     rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV);
     if (rc) return rc;
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
-        return full_mode ? launch_gather_pos(c->d_ident.p, dV, c->full_V.p, n, c->stream)
-                         : launch_gather_pos(L0.diperm.p, dV, c->Vint.p, n, c->stream);
+        return full_mode ? launch_gather_rows(3, c->d_ident.p, dV, c->full_V.p, n, c->stream)
+                         : launch_gather_rows(3, L0.diperm.p, dV, c->Vint.p, n, c->stream);
     });
     return MG_OK;
 }
@@ -1469,7 +1469,7 @@ int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, dou
     const double* dV = nullptr;
     if ((rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV))) return rc;
     c->timed(PC_ASSEMBLY, 0, s, [&] {
-        return launch_gather_pos(c->d_ident.p, dV, c->full_V.p, n, s) +
+        return launch_gather_rows(3, c->d_ident.p, dV, c->full_V.p, n, s) +
                launch_cotan(c->full0, c->full_opp.p, c->full_V.p, 0.0, 1.0, c->full_val.p, c->Muser.p, s) +
                launch_bilaplacian(c->bl_rp.p, c->bl_col.p, c->full0.rp.p, c->full0.col.p, c->full_val.p, c->Muser.p,
                                   mass_coeff, bilap_coeff, c->bl_val.p, n, s);

@@ -180,7 +180,6 @@ int launch_gather_rows(int K, const int32_t* iperm, const double* src_user, doub
                        const int32_t* umap = nullptr);
 int launch_scatter_rows(int K, const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s,
                         const int32_t* umap = nullptr);
-int launch_gather_pos(const int32_t* iperm, const double* V, double* dst, int n, cudaStream_t s);   // 32-byte rows
 int launch_dirichlet_rhs(int K, const int32_t* krp, const int32_t* kcol, const double* kval, const double* X,
                          double* b, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);

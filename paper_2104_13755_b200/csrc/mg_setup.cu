@@ -49,18 +49,6 @@ __global__ void __launch_bounds__(kBlock) k_scatter_rows(const int* __restrict__
     for (int c = 0; c < K; ++c) __stcs(dst + us * K + c, v[c]);
 }
 
-// Positions into 32-byte rows (x, y, z, 0) for the assembly kernels: one
-// 256-bit load per vertex; dst[iperm[u]] = V[u].
-__global__ void __launch_bounds__(kBlock) k_gather_pos(const int* __restrict__ iperm, const double* __restrict__ V,
-                                                       double* __restrict__ dst, int n) {
-    const int u = blockIdx.x * kBlock + threadIdx.x;
-    if (u >= n) return;
-    const size_t i = (size_t)__ldg(iperm + u);
-    const double x = __ldcs(V + 3 * (size_t)u), y = __ldcs(V + 3 * (size_t)u + 1), z = __ldcs(V + 3 * (size_t)u + 2);
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(dst + 4 * i), "d"(x), "d"(y), "d"(z), "d"(0.0)
-                 : "memory");
-}
-
 // Dirichlet right-hand side (App. B, "reduced RHS" -A_uk x_k + b_u): for every
 // internal row i of the reduced level 0, b_i -= sum_e A_uk[i, e] X[col_e]
 // with X the user's full [n_full][K] array (known values at known rows).
@@ -121,8 +109,8 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
     if (i >= n) return;   // whole groups leave together
     const unsigned mask = group_mask(kCotG);
     // internal positions: 32-byte rows (x, y, z, pad), one 256-bit load each
-    double pi[4];
-    ldrow<4>(V + 4 * (size_t)i, pi);
+    double pi[3];
+    ldrow<3>(V + 4 * (size_t)i, pi);
     const double xi = pi[0], yi = pi[1], zi = pi[2];
     double lsum = 0.0, area2 = 0.0;
     int ediag = -1;
@@ -134,16 +122,16 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
             continue;
         }
         const int2 oo = __ldcs(reinterpret_cast<const int2*>(opp) + e);
-        double pj[4];
-        ldrow<4>(V + 4 * (size_t)j, pj);
+        double pj[3];
+        ldrow<3>(V + 4 * (size_t)j, pj);
         const double xj = pj[0], yj = pj[1], zj = pj[2];
         double cot_sum = 0.0;
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int o = s == 0 ? oo.x : oo.y;
             if (o < 0) continue;
-            double po[4];
-            ldrow<4>(V + 4 * (size_t)o, po);
+            double po[3];
+            ldrow<3>(V + 4 * (size_t)o, po);
             const double xo = po[0], yo = po[1], zo = po[2];
             const double ax = xi - xo, ay = yi - yo, az = zi - zo;
             const double bx = xj - xo, by = yj - yo, bz = zj - zo;
@@ -1413,11 +1401,6 @@ int launch_scatter_rows(int K, const int32_t* perm, const double* src_int, doubl
                         const int32_t* umap) {
     if (n <= 0) return 0;
     rows_k(K, false, perm, src_int, dst_user, n, umap, s);
-    return 1;
-}
-int launch_gather_pos(const int32_t* iperm, const double* V, double* dst, int n, cudaStream_t s) {
-    if (n <= 0) return 0;
-    k_gather_pos<<<nblk(n, kBlock), kBlock, 0, s>>>(iperm, V, dst, n);
     return 1;
 }
 int launch_dirichlet_rhs(int K, const int32_t* krp, const int32_t* kcol, const double* kval, const double* X,
