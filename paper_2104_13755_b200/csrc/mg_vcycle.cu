@@ -98,7 +98,7 @@ __device__ __forceinline__ void tile_row(const int* cs, const double* vs, int qb
 // 1-ring row (7 entries incl. the skipped diagonal) for every K
 template <int K>
 struct PipeUnroll {
-    static constexpr int value = 8;
+    static constexpr int value = K >= 3 ? 4 : 8;
 };
 
 template <int K>
@@ -269,7 +269,7 @@ __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, co
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(kTile) k_tile_pipe(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
+__global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
                                                      const int* __restrict__ rp, const int* __restrict__ col,
                                                      const double* __restrict__ val, const double* __restrict__ b,
                                                      double* __restrict__ x, double* __restrict__ r,
