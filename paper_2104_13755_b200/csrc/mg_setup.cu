@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "mg_common.cuh"
@@ -1190,39 +1191,83 @@ __device__ __forceinline__ void cg_fetch(const double* G, int ld, double (&v)[4]
 // Factor the SPD 32x32 tile S in place (lower triangle, warp 0, lane = row)
 // and write its inverse to Li; then every thread stores L (upper part of the
 // tile zeroed) to D and Li to Linv_k and to W_kk.
+// 1/sqrt(x) to fp64 accuracy: single-precision MUFU seed + two Newton steps
+// (each doubles the correct bits: ~23 -> 46 -> 53).  The sequential pivot
+// chain of the 32x32 factor is dominated by the latency of sqrt and division;
+// this replaces both with ~6 dependent FMAs.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double r = (double)rsqrtf((float)x);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    return r;
+}
+
+// Warp 0 factors the 32x32 SPD tile S in registers (lane = row); the column of
+// each pivot is broadcast through shared memory (one STS + broadcast LDS per
+// step); L is written back to S and 1/L_pp to rdg.  Shuffles behind the
+// thread-index branch made ptxas emit WARPSYNC.COLLECTIVE sequences, and
+// fp64 sqrt + division on the pivot chain cost ~250 cycles per step.
+__device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, double* rdg, int* err) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    double a[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = S[lane][c];
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+        if (lane == p) colb[32] = a[p];
+        __syncwarp();
+        double piv = colb[32];
+        bad |= !(piv > 0.0);
+        piv = piv > 0.0 ? piv : 1.0;
+        const double r = rsqrt_nr(piv);
+        a[p] = lane == p ? piv * r : (lane > p ? a[p] * r : a[p]);
+        colb[lane] = a[p];
+        if (lane == p) rdg[p] = r;
+        __syncwarp();
+        const double lp = a[p];
+#pragma unroll
+        for (int c = p + 1; c < 32; ++c) {
+            const double upd = fma(-lp, colb[c], a[c]);
+            a[c] = lane >= c ? upd : a[c];
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) S[lane][c] = a[c];
+    if (bad && lane == 0) atomicExch(err, 1);
+    __syncwarp();
+}
+
+// Warp 0: column `lane` of L^{-1} (L lower in S, 1/L_ii in rdg) into Li,
+// forward substitution with four independent partial sums per row.
+__device__ __forceinline__ void cg_trinv32_warp(const double (*S)[33], const double* rdg, double (*Li)[33]) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    double xv[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int q = 0; q < i; ++q) {
+            const double t = S[i][q] * xv[q];
+            if ((q & 3) == 0) s0 -= t;
+            else if ((q & 3) == 1) s1 -= t;
+            else if ((q & 3) == 2) s2 -= t;
+            else s3 -= t;
+        }
+        xv[i] = ((s0 + s1) + (s2 + s3)) * rdg[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) Li[i][lane] = xv[i];
+}
+
 __device__ void cg_factor_diag(double (*S)[33], double (*Li)[33], double* Dkk, double* Linvk, double* Wkk, int npad,
                                int* err) {
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        for (int p = 0; p < 32; ++p) {
-            double d = S[p][p];
-            if (!(d > 0.0)) {
-                if (lane == 0) atomicExch(err, 1);
-                d = 1.0;
-            }
-            d = sqrt(d);
-            __syncwarp();
-            if (lane == p) S[p][p] = d;
-            if (lane > p) S[lane][p] /= d;
-            __syncwarp();
-            if (lane > p) {
-                const double lrp = S[lane][p];
-                for (int c = p + 1; c <= lane; ++c) S[lane][c] -= lrp * S[c][p];
-            }
-            __syncwarp();
-        }
-        // column `lane` of L^{-1} by forward substitution (zero above the diagonal)
-        double xv[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            double sacc = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-            for (int q = 0; q < i; ++q) sacc -= S[i][q] * xv[q];
-            xv[i] = sacc / S[i][i];
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) Li[i][lane] = xv[i];
-    }
+    __shared__ double colb[40], rdg[32];
+    cg_chol32_warp(S, colb, rdg, err);
+    cg_trinv32_warp(S, rdg, Li);
     __syncthreads();
     for (int q = threadIdx.x; q < 1024; q += kCgThreads) {
         const int r = q >> 5, c = q & 31;
@@ -1232,9 +1277,17 @@ __device__ void cg_factor_diag(double (*S)[33], double (*Li)[33], double* Dkk, d
     }
 }
 
+__device__ __forceinline__ void cg_trace(unsigned long long* tr, int slot) {
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[slot] = t;
+    }
+}
+
 __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D, double* __restrict__ Linv,
                                                           double* __restrict__ W, double* __restrict__ Z, int npad,
-                                                          int* err, unsigned* ctr) {
+                                                          int* err, unsigned* ctr, unsigned long long* tr) {
     __shared__ double As[32][33];
     __shared__ double Bs[32][33];
     const int nb = npad / 32;
@@ -1248,12 +1301,18 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
         const double zero[4] = {0.0, 0.0, 0.0, 0.0};
         cg_store(W + (size_t)(ti * 32) * npad + tj * 32, npad, zero);
     }
+    cg_trace(tr, 0);
     if (blockIdx.x == 0) {
         cg_load<false>(As, D, npad);
         __syncthreads();
+        cg_trace(tr, 200);
         cg_factor_diag(As, Bs, D, Linv, W, npad, err);
+        cg_trace(tr, 201);
+        cg_trace(tr, 202);
     }
+    cg_trace(tr, 1);
     gbar(ctr, target);
+    cg_trace(tr, 2);
     // ---- factor
     for (int k = 0; k + 1 < nb; ++k) {
         const int m = nb - k - 1;
@@ -1267,7 +1326,9 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
             cg_mma(acc, As, Bs);
             cg_store(D + (size_t)(i * 32) * npad + k * 32, npad, acc);
         }
+        cg_trace(tr, 3 + 4 * k);
         gbar(ctr, target);
+        cg_trace(tr, 4 + 4 * k);
         const int ntile = m * (m + 1) / 2;
         for (int t = blockIdx.x; t < ntile; t += gridDim.x) {   // P2: trailing update
             int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
@@ -1301,8 +1362,11 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
                 cg_store(C, npad, cv);
             }
         }
+        cg_trace(tr, 5 + 4 * k);
         gbar(ctr, target);
+        cg_trace(tr, 6 + 4 * k);
     }
+    cg_trace(tr, 100);
     // ---- W = L^{-1}
     for (int k = 0; k + 1 < nb; ++k) {
         const int m = nb - k - 1, w = k + 1;
@@ -1336,6 +1400,7 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
         }
         gbar(ctr, target);
     }
+    cg_trace(tr, 101);
     // ---- Z = W^T W (lower tiles, mirrored)
     const int ntz = nb * (nb + 1) / 2;
     for (int t = blockIdx.x; t < ntz; t += gridDim.x) {
@@ -1589,10 +1654,33 @@ int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, in
     const int nb = npad / 32;
     const int grid = std::max(1, std::min(grid_max, nb * (nb + 1) / 2));
     if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess) return -1;
-    void* args[] = {&D, &Linv, &W, &Z, &npad, &err, &ctr};
-    return cudaLaunchCooperativeKernel((const void*)k_chol_grid, dim3(grid), dim3(kCgThreads), args, 0, s) == cudaSuccess
-               ? 1
-               : -1;
+    // MG_CHOL_TRACE: CTA 0 phase timestamps (%globaltimer), printed to stderr
+    static unsigned long long* tr = nullptr;
+    const bool trace = getenv("MG_CHOL_TRACE") != nullptr;
+    if (trace && !tr && cudaMalloc(&tr, 256 * sizeof(unsigned long long)) != cudaSuccess) tr = nullptr;
+    unsigned long long* trp = trace ? tr : nullptr;
+    if (trp) cudaMemsetAsync(trp, 0, 256 * sizeof(unsigned long long), s);
+    void* args[] = {&D, &Linv, &W, &Z, &npad, &err, &ctr, &trp};
+    const bool ok = cudaLaunchCooperativeKernel((const void*)k_chol_grid, dim3(grid), dim3(kCgThreads), args, 0, s) ==
+                    cudaSuccess;
+    if (ok && trp) {
+        // one ZERO-sized extra slot marks the end of Z: the kernel's completion
+        unsigned long long h[256];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, trp, sizeof(h), cudaMemcpyDeviceToHost);
+        double p1 = 0, b1 = 0, p2 = 0, b2 = 0;
+        for (int k = 0; k + 1 < nb; ++k) {
+            p1 += (h[3 + 4 * k] - (k ? h[6 + 4 * (k - 1)] : h[2])) * 1e-3;
+            b1 += (h[4 + 4 * k] - h[3 + 4 * k]) * 1e-3;
+            p2 += (h[5 + 4 * k] - h[4 + 4 * k]) * 1e-3;
+            b2 += (h[6 + 4 * k] - h[5 + 4 * k]) * 1e-3;
+        }
+        fprintf(stderr, "[chol trace] prelude: load %.1f chol32 %.1f trinv32 %.1f\n", (h[200] - h[0]) * 1e-3,
+                (h[201] - h[200]) * 1e-3, (h[202] - h[201]) * 1e-3);
+        fprintf(stderr, "[chol trace] prelude %.1f us, P1 %.1f, bar1 %.1f, P2 %.1f, bar2 %.1f, W %.1f us (npad %d)\n",
+                (h[2] - h[0]) * 1e-3, p1, b1, p2, b2, (h[101] - h[100]) * 1e-3, npad);
+    }
+    return ok ? 1 : -1;
 }
 
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s) {
