@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
 // The group width is chosen per level so that one colour pass is about one
 // wave of the GPU (see choose_lpr in mg_host.cpp).
 template <int K, int LPR, int MODE>
-__global__ void __launch_bounds__(kBlock) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
+__global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1,
                                                       double omega) {
