@@ -428,7 +428,8 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         L.cap_gs = std::max(L.cap_gs, 1);
         L.cap_all = std::max(L.cap_all, 1);
         // tile-staged kernels for short rows (few gather batches per thread), lanes-per-row otherwise
-        L.tiled = avg <= 12.0 && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
+        static const double tile_avg = getenv("MG_TILE_MAX_AVG") ? atof(getenv("MG_TILE_MAX_AVG")) : 12.0;
+        L.tiled = avg <= tile_avg && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
         // persistent pipelined variant: tile descriptors for every colour class, then the whole level
         L.pipe = L.tiled && c->use_pipe && pipe_smem_bytes(std::max(L.cap_gs, L.cap_all)) <= 200 * 1024;
         if (L.pipe) {
