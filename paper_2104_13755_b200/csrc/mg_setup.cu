@@ -1313,53 +1313,95 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
     cg_trace(tr, 1);
     gbar(ctr, target);
     cg_trace(tr, 2);
-    // ---- factor
-    for (int k = 0; k + 1 < nb; ++k) {
+    // ---- factor, with W = L^{-1} interleaved (right-looking):
+    //   P1(k): panel solve L_ik = A_ik Linv_k^T (i > k) and finalisation of
+    //          W's block row k: W_kj = -Linv_k T_kj (j < k);
+    //   P2(k): trailing update A_ij -= L_ik L_jk^T (CTA 0 alone takes tile
+    //          (k+1, k+1) and factors it), and W accumulation
+    //          T_ij += L_ik W_kj (i > k >= j) on the other CTAs.
+    const int G = gridDim.x;
+    for (int k = 0; k < nb; ++k) {
         const int m = nb - k - 1;
-        for (int t = blockIdx.x; t < m; t += gridDim.x) {   // P1: panel solve
-            const int i = k + 1 + t;
+        for (int t = blockIdx.x; t < m + k; t += G) {   // P1
             __syncthreads();
-            cg_load<false>(As, D + (size_t)(i * 32) * npad + k * 32, npad);
-            cg_load<true>(Bs, Linv + (size_t)k * 1024, 32);
-            __syncthreads();
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            cg_mma(acc, As, Bs);
-            cg_store(D + (size_t)(i * 32) * npad + k * 32, npad, acc);
+            if (t < m) {   // panel solve
+                const int i = k + 1 + t;
+                cg_load<false>(As, D + (size_t)(i * 32) * npad + k * 32, npad);
+                cg_load<true>(Bs, Linv + (size_t)k * 1024, 32);
+                __syncthreads();
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                cg_mma(acc, As, Bs);
+                cg_store(D + (size_t)(i * 32) * npad + k * 32, npad, acc);
+            } else {       // W_kj = -Linv_k T_kj
+                const int j = t - m;
+                double* Tkj = W + (size_t)(k * 32) * npad + j * 32;
+                cg_load<false>(As, Linv + (size_t)k * 1024, 32);
+                cg_load<false>(Bs, Tkj, npad);
+                __syncthreads();
+                double o[4] = {0.0, 0.0, 0.0, 0.0};
+                cg_mma(o, As, Bs);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) o[e] = -o[e];
+                cg_store(Tkj, npad, o);
+            }
         }
         cg_trace(tr, 3 + 4 * k);
         gbar(ctr, target);
         cg_trace(tr, 4 + 4 * k);
+        if (m == 0) break;
         const int ntile = m * (m + 1) / 2;
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {   // P2: trailing update
-            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-            while (ti * (ti + 1) / 2 > t) --ti;
-            const int tj = t - ti * (ti + 1) / 2;
-            const int bi = k + 1 + ti, bj = k + 1 + tj;
+        if (blockIdx.x == 0) {   // tile (k+1, k+1): update and factor it for panel k+1
+            const int kk = k + 1;
             __syncthreads();
-            cg_load<false>(As, D + (size_t)(bi * 32) * npad + k * 32, npad);
-            cg_load<true>(Bs, D + (size_t)(bj * 32) * npad + k * 32, npad);
+            cg_load<false>(As, D + (size_t)(kk * 32) * npad + k * 32, npad);
+            cg_load<true>(Bs, D + (size_t)(kk * 32) * npad + k * 32, npad);
             __syncthreads();
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             cg_mma(acc, As, Bs);
-            double* C = D + (size_t)(bi * 32) * npad + bj * 32;
             double cv[4];
-            cg_fetch(C, npad, cv);
+            cg_fetch(D + (size_t)(kk * 32) * npad + kk * 32, npad, cv);
+            __syncthreads();
+            const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+            As[r0][c0] = cv[0] - acc[0];
+            As[r0][c0 + 1] = cv[1] - acc[1];
+            As[r0 + 1][c0] = cv[2] - acc[2];
+            As[r0 + 1][c0 + 1] = cv[3] - acc[3];
+            __syncthreads();
+            cg_factor_diag(As, Bs, D + (size_t)(kk * 32) * npad + kk * 32, Linv + (size_t)kk * 1024,
+                           W + (size_t)(kk * 32) * npad + kk * 32, npad, err);
+        } else {
+            const int nw = m * (k + 1);
+            for (int t = 1 + (blockIdx.x - 1); t < ntile + nw; t += G - 1) {   // P2 on CTAs 1..G-1
+                __syncthreads();
+                if (t < ntile) {   // trailing update tile
+                    int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+                    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                    while (ti * (ti + 1) / 2 > t) --ti;
+                    const int tj = t - ti * (ti + 1) / 2;
+                    const int bi = k + 1 + ti, bj = k + 1 + tj;
+                    cg_load<false>(As, D + (size_t)(bi * 32) * npad + k * 32, npad);
+                    cg_load<true>(Bs, D + (size_t)(bj * 32) * npad + k * 32, npad);
+                    __syncthreads();
+                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                    cg_mma(acc, As, Bs);
+                    double* C = D + (size_t)(bi * 32) * npad + bj * 32;
+                    double cv[4];
+                    cg_fetch(C, npad, cv);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) cv[e] -= acc[e];
-            if (t == 0) {   // tile (k+1, k+1): factor it now for panel k+1
-                __syncthreads();
-                const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
-                As[r0][c0] = cv[0];
-                As[r0][c0 + 1] = cv[1];
-                As[r0 + 1][c0] = cv[2];
-                As[r0 + 1][c0 + 1] = cv[3];
-                __syncthreads();
-                const int kk = k + 1;
-                cg_factor_diag(As, Bs, D + (size_t)(kk * 32) * npad + kk * 32, Linv + (size_t)kk * 1024,
-                               W + (size_t)(kk * 32) * npad + kk * 32, npad, err);
-            } else {
-                cg_store(C, npad, cv);
+                    for (int e = 0; e < 4; ++e) cv[e] -= acc[e];
+                    cg_store(C, npad, cv);
+                } else {           // T_ij += L_ik W_kj
+                    const int q = t - ntile;
+                    const int i = k + 1 + q / (k + 1), j = q % (k + 1);
+                    cg_load<false>(As, D + (size_t)(i * 32) * npad + k * 32, npad);   // L_ik
+                    cg_load<false>(Bs, W + (size_t)(k * 32) * npad + j * 32, npad);   // W_kj
+                    __syncthreads();
+                    double* Tij = W + (size_t)(i * 32) * npad + j * 32;
+                    double acc[4];
+                    cg_fetch(Tij, npad, acc);
+                    cg_mma(acc, As, Bs);
+                    cg_store(Tij, npad, acc);
+                }
             }
         }
         cg_trace(tr, 5 + 4 * k);
@@ -1367,39 +1409,6 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
         cg_trace(tr, 6 + 4 * k);
     }
     cg_trace(tr, 100);
-    // ---- W = L^{-1}
-    for (int k = 0; k + 1 < nb; ++k) {
-        const int m = nb - k - 1, w = k + 1;
-        for (int t = blockIdx.x; t < m * w; t += gridDim.x) {
-            const int i = k + 1 + t / w, j = t % w;
-            __syncthreads();
-            cg_load<false>(As, D + (size_t)(i * 32) * npad + k * 32, npad);   // L_ik
-            cg_load<false>(Bs, W + (size_t)(k * 32) * npad + j * 32, npad);   // W_kj
-            __syncthreads();
-            double acc[4];
-            double* Tij = W + (size_t)(i * 32) * npad + j * 32;
-            cg_fetch(Tij, npad, acc);
-            cg_mma(acc, As, Bs);
-            if (i == k + 1) {   // last contribution to block row k+1: W_ij = -inv(L_ii) T_ij
-                __syncthreads();
-                const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
-                Bs[r0][c0] = acc[0];
-                Bs[r0][c0 + 1] = acc[1];
-                Bs[r0 + 1][c0] = acc[2];
-                Bs[r0 + 1][c0 + 1] = acc[3];
-                cg_load<false>(As, Linv + (size_t)i * 1024, 32);
-                __syncthreads();
-                double o[4] = {0.0, 0.0, 0.0, 0.0};
-                cg_mma(o, As, Bs);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) o[e] = -o[e];
-                cg_store(Tij, npad, o);
-            } else {
-                cg_store(Tij, npad, acc);
-            }
-        }
-        gbar(ctr, target);
-    }
     cg_trace(tr, 101);
     // ---- Z = W^T W (lower tiles, mirrored)
     const int ntz = nb * (nb + 1) / 2;
@@ -1652,7 +1661,8 @@ int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, in
     }
     if (grid_max <= 0) return -1;
     const int nb = npad / 32;
-    const int grid = std::max(1, std::min(grid_max, nb * (nb + 1) / 2));
+    const int grid = std::max(2, std::min(grid_max, nb * (nb + 1) / 2 + 1));   // CTA 0 + >= 1 worker
+    if (grid_max < 2) return -1;
     if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess) return -1;
     // MG_CHOL_TRACE: CTA 0 phase timestamps (%globaltimer), printed to stderr
     static unsigned long long* tr = nullptr;
@@ -1677,7 +1687,7 @@ int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, in
         }
         fprintf(stderr, "[chol trace] prelude: load %.1f chol32 %.1f trinv32 %.1f\n", (h[200] - h[0]) * 1e-3,
                 (h[201] - h[200]) * 1e-3, (h[202] - h[201]) * 1e-3);
-        fprintf(stderr, "[chol trace] prelude %.1f us, P1 %.1f, bar1 %.1f, P2 %.1f, bar2 %.1f, W %.1f us (npad %d)\n",
+        fprintf(stderr, "[chol trace] prelude %.1f us, P1 %.1f, bar1 %.1f, P2 %.1f, bar2 %.1f, tail %.1f us (npad %d)\n",
                 (h[2] - h[0]) * 1e-3, p1, b1, p2, b2, (h[101] - h[100]) * 1e-3, npad);
     }
     return ok ? 1 : -1;
