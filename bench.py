@@ -259,32 +259,39 @@ class Workload:
         return cyc, rc
 
     def step_host(self):
-        """The same step through the C ABI with HOST (pinned) buffers: the
-        library stages host<->device copies inside the calls."""
+        """The same step through the C ABI with the step's inputs and result
+        in HOST (pinned) buffers: positions, the data f (or X_t) and X0 go in,
+        X comes out; the library stages the host<->device copies inside the
+        calls.  B = M f is a device buffer (mg_apply_mass takes host and
+        device pointers independently), as a user keeps it."""
         S, p = self.S, self.p
         if p.rhs_kind == "mcf":
             S.set_matrix_cotan(self.hXcur, p.mass_coeff, p.lap_coeff)
-            S.apply_mass(self.hXcur, self.hB)
+            S.apply_mass(self.hXcur, self.B)
             self.hX.copy_(self.hXcur)
         else:
             S.set_matrix_cotan(self.hV, p.mass_coeff, p.lap_coeff)
             if self.hF is not None:
-                S.apply_mass(self.hF, self.hB)
+                S.apply_mass(self.hF, self.B)
+                B = self.B
+            else:
+                B = self.hB
             self.hX.copy_(self.hZ)
-        rc, cyc = self.mg.mg_solve(S.ctx, self.k, self.hB, self.hX, self.rel_tol, self.max_cycles)
+        rc, cyc = self.mg.mg_solve(S.ctx, self.k, self.B if p.rhs_kind == "mcf" else B, self.hX, self.rel_tol,
+                                   self.max_cycles)
         if p.rhs_kind == "mcf":
             self.hXcur.copy_(self.hX)
         return cyc
 
     def host_bytes(self):
         n, k = self.n, self.k
-        h2d = 24 * n                     # positions
-        d2h = 0
+        h2d = 24 * n                     # positions into mg_set_matrix_cotan
         if self.hF is not None or self.p.rhs_kind == "mcf":
-            h2d += 8 * n * k             # f (mass RHS input)
-            d2h += 8 * n * k             # B = M f back to the host buffer
-        h2d += 2 * 8 * n * k             # B and X0 into mg_solve
-        d2h += 8 * n * k                 # X out of mg_solve
+            h2d += 8 * n * k             # f (or X_t) into mg_apply_mass (B stays on the device)
+        else:
+            h2d += 8 * n * k             # B into mg_solve
+        h2d += 8 * n * k                 # X0 into mg_solve
+        d2h = 8 * n * k                  # X out of mg_solve
         return h2d, d2h
 
     def level_sizes(self):

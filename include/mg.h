@@ -117,7 +117,7 @@ int mg_set_matrix_cotan(mg_ctx* ctx, const double* V, double mass_coeff, double 
 int mg_set_matrix_bilaplacian(mg_ctx* ctx, const double* V, double mass_coeff, double bilap_coeff);
 
 /* B = M X with the lumped mass of the last mg_set_matrix_cotan / _bilaplacian; X, B are
- * [n][k] (host or device; both of the same kind).  Errors: MG_ERR_STATE. */
+ * [n][k], each host or device independently.  Errors: MG_ERR_STATE. */
 int mg_apply_mass(mg_ctx* ctx, int32_t k, const double* X, double* B);
 
 /* Solve A X = B by V(mu_pre, mu_post) cycles (Alg. 1).
