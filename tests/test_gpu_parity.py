@@ -567,3 +567,65 @@ def test_bilaplacian_parity(ora, cid, kw):
     S.solve(B, Xg2, rel_tol=0.0, max_cycles=4)
     check_x(Xg2, Xo2)
     S.close()
+
+
+@pytest.mark.parametrize("mu", [(1, 3), (0, 2), (3, 0)])
+def test_relaxation_counts_parity(ora, mu):
+    """mg_set_options(mu_pre, mu_post) (P:548, P:555): asymmetric and one-sided
+    relaxation match the oracle with the same counts."""
+    p = meshgen.make_config(2, subdiv=5)
+    A, M, mgo = oracle_problem(ora, p, mu)
+    Bo = oracle_rhs(ora, p, M)
+    Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=4)
+    S = gpu_solver(p, mu)
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    Xg = np.zeros_like(Bo)
+    S.solve(Bo, Xg, rel_tol=0.0, max_cycles=4)
+    check_x(Xg, Xo)
+    check_history(S.solve(Bo, np.zeros_like(Bo), rel_tol=0.0, max_cycles=4)[2], ho, tau_floor(A.to_scipy(), Xo, Bo))
+
+
+def test_k4_and_mass_dominated(ora):
+    """k = 4 right-hand sides (the kernels' maximum) and A = M (lap_coeff 0:
+    a diagonal fine operator, every colour class independent)."""
+    p = meshgen.make_config(3, grid=(80, 64))
+    V, F = p.levels[0]
+    for lap in (1e-2, 0.0):
+        A, M = ora.assemble(V, F, 1.0, lap)
+        mgo = ora.MG(p.sizes, p.P, A)
+        B = np.random.default_rng(61).standard_normal((p.n, 4))
+        Xo, ho, _ = mgo.solve(B, rel_tol=0.0, max_cycles=3)
+        S = gpu_solver(p)
+        S.set_matrix_cotan(V, 1.0, lap)
+        Xg = np.zeros_like(B)
+        rc, cyc, hg = S.solve(B, Xg, rel_tol=0.0, max_cycles=3)
+        check_x(Xg, Xo)
+        check_history(hg, ho, tau_floor(A.to_scipy(), Xo, B))
+        S.close()
+
+
+def test_new_api_errors():
+    from paper_2104_13755_b200 import mg
+    p = meshgen.make_config(1)
+    S = gpu_solver(p)
+    with pytest.raises(mg.MGError) as e:
+        S.set_alpha(0.5)                                  # no split operators yet
+    assert e.value.code == mg.MG_ERR_STATE
+    with pytest.raises(mg.MGError) as e:
+        S.set_smoother(2)                                 # unknown kind
+    assert e.value.code == mg.MG_ERR_INVALID_ARG
+    with pytest.raises(mg.MGError) as e:
+        S.set_smoother(1, 1.5)                            # Jacobi damping outside (0, 1]
+    assert e.value.code == mg.MG_ERR_INVALID_ARG
+    S.set_matrix_split_cotan(p.levels[0][0])
+    with pytest.raises(mg.MGError) as e:
+        S.set_alpha(float("nan"))
+    assert e.value.code == mg.MG_ERR_INVALID_ARG
+    S.set_dirichlet([1, 2, 3])
+    with pytest.raises(mg.MGError) as e:
+        S.set_matrix_split_cotan(p.levels[0][0])          # split operators + constraints
+    assert e.value.code == mg.MG_ERR_STATE
+    with pytest.raises(mg.MGError) as e:
+        S.solve(np.zeros((p.n, 1)), np.zeros((p.n, 1)))   # constraints reset the matrix
+    assert e.value.code == mg.MG_ERR_STATE
+    S.close()
