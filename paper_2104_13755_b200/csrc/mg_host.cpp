@@ -229,6 +229,8 @@ struct mg_ctx {
     int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
     int tail_cs = 0;                 // cluster size of the tail kernel
     DBuf<int> errflag;
+    DBuf<int> flow_err;              // set by a dataflow GS kernel whose wait timed out
+    int64_t flow_rows = 0;           // levels 1.. with at most this many rows use dataflow GS (0: off)
 
     DBuf<double> partial, bnorm, rho;
     double* h_rho = nullptr;         // pinned, kMaxK
@@ -620,6 +622,20 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             cudaGetLastError();
         }
     }
+    // dataflow GS levels (coarse, latency-bound colour passes)
+    {
+        cudaError_t e = c->flow_err.alloc(1);
+        if (!e) e = cudaMemsetAsync(c->flow_err.p, 0, sizeof(int), c->stream);
+        if (e) return c->cuda_fail(e, "flow setup");
+        for (int l = 0; l < H; ++l) {
+            Level& L = *c->lv[l];
+            L.flow = l >= 1 && c->flow_rows > 0 && L.n <= c->flow_rows && !L.tiled;
+            if (L.flow) {
+                if ((e = L.done.alloc(L.n)) || (e = cudaMemsetAsync(L.done.p, 0, sizeof(int) * L.n, c->stream)))
+                    return c->cuda_fail(e, "flow setup");
+            }
+        }
+    }
     // levels run by the cluster tail: the coarsest ones with <= tail_rows rows.
     // Off by default: measured slower than per-launch PDL kernels.
     c->tail_start = -1;
@@ -730,6 +746,10 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
             cudaMemcpyAsync(L.x.p, L.r.p, sizeof(double) * (size_t)L.n * kMaxK, cudaMemcpyDeviceToDevice, s);
         }
         return n;
+    }
+    if (L.flow && mu > 0) {
+        const int nl = vc_gs_flow(K, L, mu, reverse, c->flow_err.p, s);
+        if (nl > 0) return nl;
     }
     for (int it = 0; it < mu; ++it)
         for (int q = 0; q < L.ncolours; ++q) {
@@ -923,6 +943,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) == "1";
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
+    if (const char* m = getenv("MG_FLOW_ROWS")) c->flow_rows = atoll(m);
     c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
@@ -1604,6 +1625,11 @@ static int finish_solve(mg_ctx* c, int32_t k, const double* xint, double* X, dou
         return c->cuda_fail(e, "solve");
     if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "solve");
     if ((e = cudaGetLastError())) return c->cuda_fail(e, "solve kernels");
+    if (c->flow_rows > 0 && c->flow_err.p) {
+        int fe = 0;
+        if ((e = cudaMemcpy(&fe, c->flow_err.p, sizeof(int), cudaMemcpyDeviceToHost))) return c->cuda_fail(e, "solve");
+        if (fe) return c->fail(MG_ERR_CUDA, "dataflow Gauss-Seidel: dependency wait timed out");
+    }
     return MG_OK;
 }
 

@@ -103,6 +103,8 @@ struct Level {
     DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
     DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
     DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
+    bool flow = false;                    // GS by the dataflow kernel (per-row sweep counters)
+    DBuf<int> done;                       // [n] completed sweeps per row (monotone, dataflow GS)
 };
 
 // L2 access-policy window applied to the next launches issued by this host
@@ -148,6 +150,7 @@ struct TailParams {
 // mg_vcycle.cu
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
+int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s);   // mu dataflow GS sweeps
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
 int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
 int vc_prolong(int K, const Level& fine, const Level& coarse, bool pdl, cudaStream_t s);   // fine.x += P coarse.x

@@ -465,6 +465,130 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
 }
 
 // ---------------------------------------------------------------------------
+// Dataflow multicolour Gauss-Seidel (all mu sweeps of one level in ONE
+// cooperative launch).  The colour classes are dependency levels, not global
+// barriers: row i of colour c in sweep s needs its neighbours of colours
+// processed before c to have finished sweep s and its other neighbours to
+// have finished sweep s-1 (and, by the same rule applied to them, not sweep s:
+// they wait for i).  Every row carries a monotone counter done[i] of completed
+// sweeps (release store after its x is written; neighbours poll it with
+// acquire loads and read x through L2), so each colour step costs a flag
+// round trip instead of a kernel launch + drain.  The arithmetic of a row is
+// exactly the per-launch kernel's (same entries, same order).  Groups walk
+// their rows in (sweep, colour) order and every dependency points to an
+// earlier step, so with all CTAs co-resident (cooperative launch) the
+// earliest pending row can always run; a bounded spin sets *err instead of
+// hanging if that is ever violated.
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int K, int LPR>
+__global__ void __launch_bounds__(kBlock) k_gs_flow(const int* __restrict__ rp, const int* __restrict__ col,
+                                                    const double* __restrict__ val, const double* __restrict__ b,
+                                                    double* __restrict__ x, int* __restrict__ done,
+                                                    const int* __restrict__ coff, int ncol, int mu, int reverse,
+                                                    int* __restrict__ err) {
+    const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
+    const int lane = threadIdx.x & (LPR - 1);
+    const int ngroups = gridDim.x * (kBlock / LPR);
+    const unsigned mask = group_mask(LPR);
+    const int base = ld_acquire_i32(done);   // every row holds the same count at launch
+    for (int sw = 0; sw < mu; ++sw) {
+        for (int q = 0; q < ncol; ++q) {
+            const int c = reverse ? ncol - 1 - q : q;
+            const int r0 = __ldg(coff + c), r1 = __ldg(coff + c + 1);
+            for (int row = r0 + g; row < r1; row += ngroups) {   // whole groups iterate together
+                const int e0 = __ldg(rp + row), e1 = __ldg(rp + row + 1);
+                double sacc[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) sacc[k] = 0.0;
+                double d = 0.0;
+                for (int e = e0 + lane; e < e1; e += LPR) {
+                    const int j = __ldg(col + e);
+                    const double a = __ldg(val + e);
+                    if (j == row) {
+                        d += a;
+                        continue;
+                    }
+                    const bool before = reverse ? (j >= r1) : (j < r0);   // j's colour is processed before c
+                    const int need = base + sw + (before ? 1 : 0);
+                    int spins = 0;
+                    while (ld_acquire_i32(done + j) < need) {
+                        if (++spins > (1 << 22)) {
+                            atomicExch(err, 1);
+                            break;
+                        }
+                    }
+                    double xv[K];
+                    ldrow_cg<K>(x + (size_t)j * VS<K>::S, xv);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) sacc[k] = fma(a, xv[k], sacc[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) sacc[k] = group_sum<LPR>(sacc[k], mask);
+                d = group_sum<LPR>(d, mask);
+                if (lane == 0) {
+                    double bv[K], xn[K];
+                    ldrow<K>(b + (size_t)row * VS<K>::S, bv);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) xn[k] = (bv[k] - sacc[k]) / d;
+                    strow<K>(x + (size_t)row * VS<K>::S, xn);
+                    st_release_i32(done + row, base + sw + 1);
+                }
+                __syncwarp(mask);
+            }
+        }
+    }
+}
+
+template <int K, int LPR>
+int launch_gs_flow_k(const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
+    static int per_sm = -1, nsm = 0;
+    if (per_sm < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_flow<K, LPR>, kBlock, 0);
+        cudaGetLastError();
+    }
+    if (per_sm <= 0) return -1;
+    int maxrows = 0;
+    for (int c = 0; c < L.ncolours; ++c) maxrows = std::max(maxrows, L.colour_off[c + 1] - L.colour_off[c]);
+    const int grid = std::max(1, std::min(per_sm * nsm, nblk((int64_t)maxrows * LPR, kBlock)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int rev = reverse ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_gs_flow<K, LPR>, (const int*)L.rp.p, (const int*)L.col.p, (const double*)L.val.p,
+                              (const double*)L.b.p, L.x.p, L.done.p, (const int*)L.dcoff.p, L.ncolours, mu, rev,
+                              err) == cudaSuccess
+               ? 1
+               : -1;
+}
+
+template <int K>
+int launch_gs_flow_kk(const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
+    switch (L.lpr) {
+        case 4: return launch_gs_flow_k<K, 4>(L, mu, reverse, err, s);
+        case 8: return launch_gs_flow_k<K, 8>(L, mu, reverse, err, s);
+        case 16: return launch_gs_flow_k<K, 16>(L, mu, reverse, err, s);
+        default: return launch_gs_flow_k<K, 32>(L, mu, reverse, err, s);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K5b: r_c = P^T r gathered through the children lists of the coarse
 // vertices (transpose of P): deterministic, no atomics.  G lanes per coarse
 // row; children indices and weights prefetched before the wait.  Zeroes the
@@ -970,6 +1094,14 @@ void init_vcycle_attributes() {
 
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
+}
+int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
+    switch (K) {
+        case 1: return launch_gs_flow_kk<1>(L, mu, reverse, err, s);
+        case 2: return launch_gs_flow_kk<2>(L, mu, reverse, err, s);
+        case 3: return launch_gs_flow_kk<3>(L, mu, reverse, err, s);
+        default: return launch_gs_flow_kk<4>(L, mu, reverse, err, s);
+    }
 }
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 3>(L, 0, L.n, xout, pdl, s, xin, omega)))

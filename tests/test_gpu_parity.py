@@ -629,3 +629,27 @@ def test_new_api_errors():
         S.solve(np.zeros((p.n, 1)), np.zeros((p.n, 1)))   # constraints reset the matrix
     assert e.value.code == mg.MG_ERR_STATE
     S.close()
+
+
+@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 6}), (3, {"grid": (128, 96)})])
+def test_dataflow_gs_parity(ora, cid, kw, monkeypatch):
+    """Dataflow multicolour GS (per-row sweep counters instead of one launch
+    per colour, MG_FLOW_ROWS) reproduces multicolour GS: same V-cycle iterate
+    as the per-colour launches to rounding, forward and symmetric (PCG)."""
+    p = meshgen.make_config(cid, **kw)
+    A, M, mgo = oracle_problem(ora, p)
+    Bo = oracle_rhs(ora, p, M)
+    Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=4)
+    Xp, hp, _ = ora.MG(p.sizes, p.P, A).pcg(Bo, rel_tol=0.0, max_iters=4)
+    monkeypatch.setenv("MG_FLOW_ROWS", "100000000")
+    S = gpu_solver(p)
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    for _ in range(2):                                   # counters keep increasing across solves
+        Xg = np.zeros_like(Bo)
+        rc, cyc, hg = S.solve(Bo, Xg, rel_tol=0.0, max_cycles=4)
+        check_x(Xg, Xo)
+        check_history(hg, ho, tau_floor(A.to_scipy(), Xo, Bo))
+    Xg = np.zeros_like(Bo)
+    rc, it, hg = S.solve_pcg(Bo, Xg, rel_tol=0.0, max_iters=4)
+    check_x(Xg, Xp)
+    S.close()
