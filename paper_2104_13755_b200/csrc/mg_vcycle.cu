@@ -484,6 +484,11 @@ __device__ __forceinline__ int ld_acquire_i32(const int* p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed_i32(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release_i32(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -509,26 +514,45 @@ __global__ void __launch_bounds__(kBlock) k_gs_flow(const int* __restrict__ rp, 
 #pragma unroll
                 for (int k = 0; k < K; ++k) sacc[k] = 0.0;
                 double d = 0.0;
-                for (int e = e0 + lane; e < e1; e += LPR) {
-                    const int j = __ldg(col + e);
-                    const double a = __ldg(val + e);
-                    if (j == row) {
-                        d += a;
-                        continue;
+                constexpr int U = 32 / LPR;
+                for (int eb = e0; eb < e1; eb += U * LPR) {
+                    int j[U], need[U];
+                    double a[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int e = eb + lane + u * LPR;
+                        const bool ok = e < e1;
+                        j[u] = ok ? __ldg(col + e) : -1;
+                        a[u] = ok ? __ldg(val + e) : 0.0;
+                        const bool before = reverse ? (j[u] >= r1) : (j[u] < r0);
+                        need[u] = base + sw + (before ? 1 : 0);
                     }
-                    const bool before = reverse ? (j >= r1) : (j < r0);   // j's colour is processed before c
-                    const int need = base + sw + (before ? 1 : 0);
+                    // poll every neighbour flag of the chunk with independent relaxed
+                    // loads, then one acquire fence before the x gathers
                     int spins = 0;
-                    while (ld_acquire_i32(done + j) < need) {
-                        if (++spins > (1 << 22)) {
-                            atomicExch(err, 1);
-                            break;
+                    bool ready;
+                    do {
+                        ready = true;
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (j[u] >= 0 && j[u] != row) ready &= ld_relaxed_i32(done + j[u]) >= need[u];
+                    } while (!ready && ++spins < (1 << 22));
+                    if (!ready) atomicExch(err, 1);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    double xv[U][K];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (j[u] >= 0 && j[u] != row) ldrow_cg<K>(x + (size_t)j[u] * VS<K>::S, xv[u]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (j[u] < 0) continue;
+                        if (j[u] == row) {
+                            d += a[u];
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < K; ++k) sacc[k] = fma(a[u], xv[u][k], sacc[k]);
                         }
                     }
-                    double xv[K];
-                    ldrow_cg<K>(x + (size_t)j * VS<K>::S, xv);
-#pragma unroll
-                    for (int k = 0; k < K; ++k) sacc[k] = fma(a, xv[k], sacc[k]);
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) sacc[k] = group_sum<LPR>(sacc[k], mask);
