@@ -20,6 +20,14 @@
 //   ora_gs_sweep          pinned (worked example, A-norm decrease theorem)
 //   ora_mg_vcycle         pinned (two-grid error-propagator formula, special cases)
 //   ora_mg_solve          pinned (dense direct solve, closed forms)
+//   ora_jacobi_sweep      pinned (worked example jacobi_2x2, splitting form vs numpy)
+//   gs_sweep_reverse      pinned (the symmetric V-cycle operator is SPD; the forward one is not)
+//   ora_mg_pcg            pinned (one level = one iteration, dense solve, CG energy monotonicity)
+// oracle.py (numpy): dirichlet_reduce / dirichlet_solve pinned (no constraints =
+// unconstrained, all known, dense constrained solve S:561, zero-column removal);
+// bilaplacian pinned (Q1 = 0, symmetric PSD, 2-ring pattern, sphere Rayleigh
+// quotient -> 4, dense smoothing solve).  Cycle / iteration COUNTS on the
+// synthetic configs are parity unpinned (the paper prints none).
 
 #include <algorithm>
 #include <cmath>
