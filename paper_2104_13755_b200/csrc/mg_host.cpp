@@ -554,7 +554,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 const int capc = galerkin4_capc();
                 int maxch = 0;
                 for (int32_t I = 0; I < C.n; ++I) maxch = std::max(maxch, cnt[I + 1] - cnt[I]);
-                if (maxT <= 24 && maxch <= 32) {
+                if (maxT <= 24 && maxch <= 32 && maxrow <= 64) {
                     C.gal4_maxt = maxT <= 12 ? 12 : 24;
                     std::vector<int32_t> grows(1, 0), gcoff(1, 0), gch, rcl(cidx.size());
                     std::vector<int32_t> loc(L.n, -1);

@@ -477,7 +477,7 @@ constexpr int kGal4Threads = 256;
 constexpr int kGal4Capc = 256;   // distinct children per group (= threads: one child per thread)
 
 template <int MAXT>
-__global__ void __launch_bounds__(kGal4Threads, 2) k_galerkin4(
+__global__ void __launch_bounds__(kGal4Threads, MAXT <= 12 ? 3 : 2) k_galerkin4(
     const int* __restrict__ order, const int* __restrict__ grows, const int* __restrict__ gcoff,
     const int* __restrict__ gch, const int* __restrict__ crp, const int* __restrict__ ccol, double* __restrict__ cval,
     const int* __restrict__ cptr, const int* __restrict__ rcl, const double* __restrict__ cw,
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kGal4Threads, 2) k_galerkin4(
     double* Tv = reinterpret_cast<double*>(g4_smem);                          // [capc][MAXT]
     int* Tk = reinterpret_cast<int*>(Tv + (size_t)kGal4Capc * MAXT);         // [capc][MAXT], ascending keys
     unsigned char* Tn = reinterpret_cast<unsigned char*>(Tk + (size_t)kGal4Capc * MAXT);   // [capc]
-    constexpr int EB = MAXT <= 12 ? 8 : 4;   // row entries fetched per batch (independent loads in flight)
+    constexpr int EB = 4;   // row entries fetched per batch (independent loads in flight)
     const int g = blockIdx.x;
     const int c0 = gcoff[g], nch = gcoff[g + 1] - c0;
     // ---- phase 1: T rows of the group's children (one child per thread)
@@ -565,35 +565,49 @@ __global__ void __launch_bounds__(kGal4Threads, 2) k_galerkin4(
         Tn[c] = (unsigned char)cnt;
     }
     __syncthreads();
-    // ---- phase 2: one warp per coarse row, one lane per stored entry (I, J);
-    // the row's children (<= 32) are loaded once and broadcast by shuffles
+    // ---- phase 2: one warp per coarse row.  The row's columns go into a
+    // per-warp hash (column -> slot); the children are visited in their fixed
+    // order and, for each child, one lane per entry of its T row adds
+    // P[i,I] T_i[J] into the slot of J.  The keys of one T row are distinct,
+    // so the lanes of one step never hit the same slot: no atomics, and every
+    // entry sums its contributions in the children's order (deterministic).
+    constexpr int kH = 128;   // hash slots per warp (rows have <= 64 entries)
+    __shared__ int hk[kGal4Threads / 32][kH];
+    __shared__ unsigned char hv[kGal4Threads / 32][kH];
+    __shared__ double acc2[kGal4Threads / 32][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = grows[g], r1 = grows[g + 1];
     for (int rr = r0 + warp; rr < r1; rr += kGal4Threads / 32) {
         const int I = order[rr];
         const int a0 = crp[I], m = crp[I + 1] - a0;
         const int t0 = cptr[I], nt = cptr[I + 1] - t0;
+        for (int h = lane; h < kH; h += 32) hk[warp][h] = -1;
+        for (int q = lane; q < m; q += 32) acc2[warp][q] = 0.0;
+        __syncwarp();
+        for (int q = lane; q < m; q += 32) {
+            const int J = ccol[a0 + q];
+            unsigned h = ((unsigned)J * 2654435761u) >> 25;
+            while (atomicCAS(&hk[warp][h], -1, J) != -1) h = (h + 1) & (kH - 1);
+            hv[warp][h] = (unsigned char)q;
+        }
         const int cl = lane < nt ? rcl[t0 + lane] : 0;
         const double wl = lane < nt ? cw[t0 + lane] : 0.0;
-        for (int sb = 0; sb < m; sb += 32) {
-            const int sidx = sb + lane;
-            const int J = sidx < m ? ccol[a0 + sidx] : -1;
-            double acc = 0.0;
-            for (int t = 0; t < nt; ++t) {
-                const int c = __shfl_sync(0xffffffffu, cl, t);
-                const double w = __shfl_sync(0xffffffffu, wl, t);
-                const int* kk = Tk + (size_t)c * MAXT;
-                int lo = 0, hi = Tn[c];
-                while (lo < hi) {   // first key >= J
-                    const int mid = (lo + hi) >> 1;
-                    if (kk[mid] < J) lo = mid + 1;
-                    else hi = mid;
-                }
-                const double tv = (lo < Tn[c] && kk[lo] == J) ? Tv[(size_t)c * MAXT + lo] : 0.0;
-                acc = fma(w, tv, acc);
+        __syncwarp();
+        for (int t = 0; t < nt; ++t) {
+            const int c = __shfl_sync(0xffffffffu, cl, t);
+            const double w = __shfl_sync(0xffffffffu, wl, t);
+            if (lane < Tn[c]) {
+                const int J = Tk[(size_t)c * MAXT + lane];
+                const double v = Tv[(size_t)c * MAXT + lane];
+                unsigned h = ((unsigned)J * 2654435761u) >> 25;
+                while (hk[warp][h] != J) h = (h + 1) & (kH - 1);
+                const int slot = hv[warp][h];
+                acc2[warp][slot] = fma(w, v, acc2[warp][slot]);
             }
-            if (sidx < m) cval[a0 + sidx] = acc;
+            __syncwarp();
         }
+        for (int q = lane; q < m; q += 32) cval[a0 + q] = acc2[warp][q];
+        __syncwarp();
     }
 }
 
