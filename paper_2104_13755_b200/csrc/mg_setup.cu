@@ -18,6 +18,17 @@
 namespace mg {
 namespace {
 
+// 1/sqrt(x) to fp64 accuracy: single-precision MUFU seed + two Newton steps
+// (each doubles the correct bits: ~23 -> 46 -> 53).  The sequential pivot
+// chain of the 32x32 factor is dominated by the latency of sqrt and division;
+// this replaces both with ~6 dependent FMAs.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double r = (double)rsqrtf((float)x);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // K9: user <-> internal permutations (row blocks of K values).  Both walk the
 // USER order (coalesced user-side rows) and index the internal side through
@@ -137,9 +148,10 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
             const double ax = xi - xo, ay = yi - yo, az = zi - zo;
             const double bx = xj - xo, by = yj - yo, bz = zj - zo;
             const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
-            const double cr = sqrt(cx * cx + cy * cy + cz * cz);
-            cot_sum += (ax * bx + ay * by + az * bz) / cr;
-            area2 += cr;
+            const double c2 = cx * cx + cy * cy + cz * cz;
+            const double ic = rsqrt_nr(c2);   // 1 / |cross| without fp64 sqrt + division
+            cot_sum += (ax * bx + ay * by + az * bz) * ic;
+            area2 += c2 * ic;
         }
         const double lij = -0.5 * cot_sum;
         lsum += lij;
@@ -1205,17 +1217,6 @@ __device__ __forceinline__ void cg_fetch(const double* G, int ld, double (&v)[4]
 // Factor the SPD 32x32 tile S in place (lower triangle, warp 0, lane = row)
 // and write its inverse to Li; then every thread stores L (upper part of the
 // tile zeroed) to D and Li to Linv_k and to W_kk.
-// 1/sqrt(x) to fp64 accuracy: single-precision MUFU seed + two Newton steps
-// (each doubles the correct bits: ~23 -> 46 -> 53).  The sequential pivot
-// chain of the 32x32 factor is dominated by the latency of sqrt and division;
-// this replaces both with ~6 dependent FMAs.
-__device__ __forceinline__ double rsqrt_nr(double x) {
-    double r = (double)rsqrtf((float)x);
-    r = r * fma(-0.5 * x, r * r, 1.5);
-    r = r * fma(-0.5 * x, r * r, 1.5);
-    return r;
-}
-
 // Warp 0 factors the 32x32 SPD tile S in registers (lane = row); the column of
 // each pivot is broadcast through shared memory (one STS + broadcast LDS per
 // step); L is written back to S and 1/L_pp to rdg.  Shuffles behind the
