@@ -230,6 +230,8 @@ struct mg_ctx {
     int tail_cs = 0;                 // cluster size of the tail kernel
     DBuf<int> errflag;
     DBuf<int> flow_err;              // set by a dataflow GS kernel whose wait timed out
+    bool gs_persist = false;         // tiled levels: all colour passes of a smoothing phase in one launch
+    DBuf<unsigned long long> persist_ctr;   // its grid-barrier counter (monotone)
     int64_t flow_rows = 0;           // levels 1.. with at most this many rows use dataflow GS (0: off)
 
     DBuf<double> partial, bnorm, rho;
@@ -448,6 +450,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             add_tiles(0, L.n);
             L.pipe_cap = std::max(L.cap_gs, L.cap_all);
             cudaError_t e = L.tiles.upload(td, c->stream);
+            if (!e) e = L.dtoff.upload(L.tile_off, c->stream);
             if (e) return c->cuda_fail(e, "tile upload");
         }
         if (!L.tiled) {
@@ -626,6 +629,10 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
     {
         cudaError_t e = c->flow_err.alloc(1);
         if (!e) e = cudaMemsetAsync(c->flow_err.p, 0, sizeof(int), c->stream);
+        if (!e && !c->persist_ctr.p) {
+            e = c->persist_ctr.alloc(1);
+            if (!e) e = cudaMemsetAsync(c->persist_ctr.p, 0, sizeof(unsigned long long), c->stream);
+        }
         if (e) return c->cuda_fail(e, "flow setup");
         for (int l = 0; l < H; ++l) {
             Level& L = *c->lv[l];
@@ -749,6 +756,10 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
     }
     if (L.flow && mu > 0) {
         const int nl = vc_gs_flow(K, L, mu, reverse, c->flow_err.p, s);
+        if (nl > 0) return nl;
+    }
+    if (c->gs_persist && L.pipe && mu > 0 && c->persist_ctr.p) {
+        const int nl = vc_gs_persist(K, L, mu, reverse, c->persist_ctr.p, s);
         if (nl > 0) return nl;
     }
     for (int it = 0; it < mu; ++it)
@@ -944,6 +955,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     if (const char* m = getenv("MG_FLOW_ROWS")) c->flow_rows = atoll(m);
+    if (const char* m = getenv("MG_GS_PERSIST")) c->gs_persist = std::string(m) == "1";
     c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {

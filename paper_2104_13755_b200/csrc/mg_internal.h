@@ -64,6 +64,7 @@ struct Level {
     int pipe_cap = 0;                     // max nnz of any tile (GS or whole-level tiles)
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
+    DBuf<int32_t> dtoff;                  // tile_off on device (persistent GS)
     bool has_win = false;                 // L2 persisting window over this level's iterate x
     cudaAccessPolicyWindow win = {};
     std::vector<double> V;                // user-order positions [n][3]
@@ -150,6 +151,7 @@ struct TailParams {
 // mg_vcycle.cu
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
+int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s);  // all colours of mu sweeps
 int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s);   // mu dataflow GS sweeps
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
 int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0

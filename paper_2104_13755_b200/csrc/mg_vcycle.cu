@@ -361,6 +361,155 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
 }
 
 // ---------------------------------------------------------------------------
+// Persistent multicolour GS for the tiled levels (level 0): ALL colour passes
+// of mu sweeps in ONE cooperative launch.  Each CTA walks its tiles of
+// colour c (t = off[c] + blockIdx.x + i * G), colour after colour, sweep
+// after sweep, through the same double-buffered TMA-bulk stage ring as
+// k_tile_pipe; the matrix part of the next tiles is streamed ACROSS colour
+// boundaries (A never changes during the solve), so HBM stays busy while the
+// CTAs meet at the grid barrier that separates colour classes (multicolour GS
+// semantics: colour c reads the x written by colours < c of this sweep).
+// The barrier is a monotone 64-bit counter (base taken modulo G at entry);
+// its acquire fence also invalidates L1, so gathers after it see the
+// neighbours' new x.  Same arithmetic per row as k_tile_pipe<K, 0>.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kTile, 4) k_gs_persist(const TileDesc* __restrict__ tiles,
+                                                         const int* __restrict__ toff, int ncol, int mu, int reverse,
+                                                         const int* __restrict__ rp, const int* __restrict__ col,
+                                                         const double* __restrict__ val, const double* __restrict__ b,
+                                                         double* __restrict__ x, int cap,
+                                                         unsigned long long* __restrict__ ctr) {
+    extern __shared__ __align__(128) unsigned char smem_pipe[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ unsigned long long s_base;
+    const int tid = threadIdx.x;
+    const int G = gridDim.x;
+    const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
+    unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
+    uint64_t pol = 0;
+    if (tid == 0) {
+        pol = evict_first_policy();
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_base = ld_acquire_u64(ctr) / (unsigned long long)G * (unsigned long long)G;
+    }
+    __syncthreads();
+    unsigned long long target = s_base;
+    // task cursor over (sweep, colour step, i); ntask(c) = this CTA's tiles of colour c
+    auto colour_of = [&](int q) { return reverse ? ncol - 1 - q : q; };
+    auto ntask = [&](int c) {
+        const int nt = __ldg(toff + c + 1) - __ldg(toff + c);
+        return nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + G - 1) / G : 0;
+    };
+    const int nsteps = mu * ncol;
+    // prefetch cursor: (step ps, index pi) of the next task whose A data is issued
+    int ps = 0, pi = 0, issued = 0;
+    auto issue_next = [&]() {   // thread 0 only
+        while (ps < nsteps && pi >= ntask(colour_of(ps % ncol))) {
+            ++ps;
+            pi = 0;
+        }
+        if (ps >= nsteps) return;
+        const int c = colour_of(ps % ncol);
+        const TileDesc d = tiles[__ldg(toff + c) + blockIdx.x + pi * G];
+        issue_tile(d, stage[issued & 1], cap, &bar[issued & 1], rp, col, val, pol);
+        ++pi;
+        ++issued;
+    };
+    if (tid == 0) {
+        issue_next();
+        issue_next();
+    }
+    const uint64_t xpol = evict_last_policy();
+    const uint64_t spol = evict_first_policy();
+    int done = 0;   // tasks consumed by this CTA
+    for (int step = 0; step < nsteps; ++step) {
+        const int c = colour_of(step % ncol);
+        const int mine = ntask(c);
+        const int t0 = __ldg(toff + c);
+        for (int i = 0; i < mine; ++i) {
+            const int sidx = done & 1;
+            const TileDesc d = tiles[t0 + blockIdx.x + i * G];
+            mbar_wait(&bar[sidx], (unsigned)((done >> 1) & 1));
+            const StageView v = view_tile(d, stage[sidx], cap);
+            if (tid < d.nrow) {
+                const int row = d.row0 + tid;
+                double bv[K];
+                ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
+                double sacc[K], dg;
+                stage_row<K, PipeUnroll<K>::value>(v, tid, row, x, sacc, dg, xpol);
+                double xn[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) xn[k] = (bv[k] - sacc[k]) / dg;
+                strow_pol<K>(x + (size_t)row * VS<K>::S, xn, xpol);
+            }
+            __syncthreads();   // stage consumed
+            ++done;
+            if (tid == 0) issue_next();
+        }
+        if (step + 1 < nsteps) {   // colour boundary: grid barrier
+            target += (unsigned long long)G;
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(ctr, 1ull);
+                while (ld_acquire_u64(ctr) < target) {
+                }
+                __threadfence();
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int K>
+int launch_gs_persist_k(const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s) {
+    static int per_sm = -2, nsm = 0;
+    const size_t smem = 2 * ((stage_bytes(L.pipe_cap) + 127) / 128 * 128);
+    if (per_sm == -2) {
+        int dev = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaFuncSetAttribute(k_gs_persist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        per_sm = coop ? 0 : -1;
+        cudaGetLastError();
+    }
+    if (per_sm == -1) return -1;
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gs_persist<K>, kTile, smem) != cudaSuccess || per <= 0) {
+        cudaGetLastError();
+        return -1;
+    }
+    int maxt = 1;
+    for (int c = 0; c < L.ncolours; ++c) maxt = std::max(maxt, L.tile_off[c + 1] - L.tile_off[c]);
+    const int grid = std::max(1, std::min(per * nsm, maxt));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTile);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_gs_persist<K>, reinterpret_cast<const TileDesc*>(L.tiles.p),
+                              (const int*)L.dtoff.p, L.ncolours, mu, reverse ? 1 : 0, (const int*)L.rp.p,
+                              (const int*)L.col.p, (const double*)L.val.p, (const double*)L.b.p, L.x.p, L.pipe_cap,
+                              ctr) == cudaSuccess
+               ? 1
+               : -1;
+}
+
+// ---------------------------------------------------------------------------
 // LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
 // prefetches up to U = 32/LPR (col, val) of its row in the PDL prologue;
 // after the wait its x gathers go out in batches of GB independent loads.
@@ -1118,6 +1267,15 @@ void init_vcycle_attributes() {
 
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
+}
+int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s) {
+    if (!L.pipe || !L.dtoff.p) return -1;
+    switch (K) {
+        case 1: return launch_gs_persist_k<1>(L, mu, reverse, ctr, s);
+        case 2: return launch_gs_persist_k<2>(L, mu, reverse, ctr, s);
+        case 3: return launch_gs_persist_k<3>(L, mu, reverse, ctr, s);
+        default: return launch_gs_persist_k<4>(L, mu, reverse, ctr, s);
+    }
 }
 int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
     switch (K) {

@@ -267,11 +267,12 @@ def test_launch_modes_agree(ora, monkeypatch):
         "gal3": {"MG_GAL_V3": "1"},
         "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
         "chol_cluster": {"MG_CHOL": "cluster"},
+        "gs_persist": {"MG_GS_PERSIST": "1"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
-                  "MG_CHOL", "MG_GAL4"):
+                  "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -284,6 +285,7 @@ def test_launch_modes_agree(ora, monkeypatch):
         S.close()
     assert np.array_equal(out["default"], out["nopdl"])
     assert np.array_equal(out["default"], out["nopipe"])
+    assert np.array_equal(out["default"], out["gs_persist"])   # same per-row arithmetic, one launch per phase
 
 
 @pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
