@@ -418,8 +418,25 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         }
         const double avg = L.n ? (double)L.nnz / L.n : 1.0;
         L.lpr = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+        // tile-staged kernels for short rows (a thread per row, few gather
+        // batches); optionally pipelined tiles with pipe_lpr lanes per row for
+        // longer rows (tiles of kTile / pipe_lpr rows); lanes-per-row otherwise
+        const double tile_avg = getenv("MG_TILE_MAX_AVG") ? atof(getenv("MG_TILE_MAX_AVG")) : 12.0;
+        // Measured on B200 (profiles/r01, sweep r01ah): 2 lanes per row win on
+        // config 4's level 1 (avg 17.5 nnz/row, 38k rows per colour: GS 3.72 ->
+        // 3.17 ms/step); on smaller colour classes the untiled LPR kernels'
+        // wider grids win, and 4 or 8 lanes lose everywhere.
+        const double plpr_avg = getenv("MG_PIPE_LPR_MAX_AVG") ? atof(getenv("MG_PIPE_LPR_MAX_AVG")) : 20.0;
+        const double plpr_rows = getenv("MG_PIPE_LPR_MIN_ROWS") ? atof(getenv("MG_PIPE_LPR_MIN_ROWS")) : 32768.0;
+        const int plpr = getenv("MG_PIPE_LPR") ? atoi(getenv("MG_PIPE_LPR")) : 2;
+        const double colour_rows = (double)L.n / std::max(1, (int)L.colour_off.size() - 1);
+        L.pipe_lpr = avg <= tile_avg ? 1
+                     : (avg <= plpr_avg && colour_rows >= plpr_rows && (plpr == 2 || plpr == 4 || plpr == 8)) ? plpr
+                                                                                                            : 0;
+        if (const char* e = getenv(("MG_PIPE_LPR_L" + std::to_string(l)).c_str())) L.pipe_lpr = atoi(e);
+        if (L.pipe_lpr != 0 && L.pipe_lpr != 1 && L.pipe_lpr != 2 && L.pipe_lpr != 4 && L.pipe_lpr != 8) L.pipe_lpr = 0;
         // shared-memory capacity of the tile-staged kernels
-        const int T = tile_rows();
+        const int T = tile_rows() / std::max(1, L.pipe_lpr);
         auto tile_max = [&](int r0, int r1) {
             int m = 0;
             for (int a = r0; a < r1; a += T) m = std::max(m, L.irp[std::min(a + T, r1)] - L.irp[a]);
@@ -431,11 +448,10 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             L.cap_gs = std::max(L.cap_gs, tile_max(L.colour_off[k], L.colour_off[k + 1]));
         L.cap_gs = std::max(L.cap_gs, 1);
         L.cap_all = std::max(L.cap_all, 1);
-        // tile-staged kernels for short rows (few gather batches per thread), lanes-per-row otherwise
-        static const double tile_avg = getenv("MG_TILE_MAX_AVG") ? atof(getenv("MG_TILE_MAX_AVG")) : 12.0;
-        L.tiled = avg <= tile_avg && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
+        L.tiled = L.pipe_lpr == 1 && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
         // persistent pipelined variant: tile descriptors for every colour class, then the whole level
-        L.pipe = L.tiled && c->use_pipe && pipe_smem_bytes(std::max(L.cap_gs, L.cap_all)) <= 200 * 1024;
+        L.pipe = (L.tiled || L.pipe_lpr > 1) && c->use_pipe &&
+                 pipe_smem_bytes(std::max(L.cap_gs, L.cap_all)) <= 200 * 1024;
         if (L.pipe) {
             std::vector<int32_t> td;
             L.tile_off.assign(1, 0);
@@ -636,7 +652,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         if (e) return c->cuda_fail(e, "flow setup");
         for (int l = 0; l < H; ++l) {
             Level& L = *c->lv[l];
-            L.flow = l >= 1 && c->flow_rows > 0 && L.n <= c->flow_rows && !L.tiled;
+            L.flow = l >= 1 && c->flow_rows > 0 && L.n <= c->flow_rows && !L.tiled && !L.pipe;
             if (L.flow) {
                 if ((e = L.done.alloc(L.n)) || (e = cudaMemsetAsync(L.done.p, 0, sizeof(int) * L.n, c->stream)))
                     return c->cuda_fail(e, "flow setup");
@@ -758,7 +774,7 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
         const int nl = vc_gs_flow(K, L, mu, reverse, c->flow_err.p, s);
         if (nl > 0) return nl;
     }
-    if (c->gs_persist && L.pipe && mu > 0 && c->persist_ctr.p) {
+    if (c->gs_persist && L.pipe && L.pipe_lpr == 1 && mu > 0 && c->persist_ctr.p) {
         const int nl = vc_gs_persist(K, L, mu, reverse, c->persist_ctr.p, s);
         if (nl > 0) return nl;
     }

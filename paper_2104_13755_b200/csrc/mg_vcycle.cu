@@ -360,6 +360,130 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
     }
 }
 
+// Pipelined tiles with LPR lanes per row (levels with longer rows, e.g. the
+// first Galerkin level): the same TMA-bulk double-buffered stage ring as
+// k_tile_pipe, tiles of kTile / LPR rows; lane l of a row takes the staged
+// entries qb + l + u * LPR (the assignment and summation order of
+// k_lpr_sweep), so nothing but x and b is loaded after the PDL wait.
+template <int K, int LPR, int MODE>
+__global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
+                                                         const int* __restrict__ rp, const int* __restrict__ col,
+                                                         const double* __restrict__ val, const double* __restrict__ b,
+                                                         double* __restrict__ x, double* __restrict__ r,
+                                                         double* __restrict__ partial, int cap, double omega) {
+    extern __shared__ __align__(128) unsigned char smem_pipe[];
+    __shared__ __align__(8) uint64_t bar[2];
+    constexpr int GB = 4;
+    const int tid = threadIdx.x;
+    const int tr = tid / LPR;
+    const int lane = tid & (LPR - 1);
+    const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
+    unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
+    pdl_launch_dependents();
+    const int nt = t_end - t_begin;
+    const int mine = nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    uint64_t pol = 0;
+    if (tid == 0) {
+        pol = evict_first_policy();
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 0; i < 2 && i < mine; ++i) {
+            const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+            issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
+        }
+    }
+    pdl_wait();
+    const uint64_t xpol = evict_last_policy();
+    const uint64_t spol = evict_first_policy();
+    double acc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc[c] = 0.0;
+    for (int i = 0; i < mine; ++i) {
+        const int sidx = i & 1;
+        const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+        mbar_wait(&bar[sidx], (unsigned)((i >> 1) & 1));
+        const StageView v = view_tile(d, stage[sidx], cap);
+        const bool valid = tr < d.nrow;
+        const int row = d.row0 + tr;
+        double bv[K];
+        if (valid && lane == 0) ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
+        const int qb = valid ? v.rps[tr] : 0, qe = valid ? v.rps[tr + 1] : 0;
+        double s[K], xi[K], dg = 0.0;
+#pragma unroll
+        for (int c = 0; c < K; ++c) s[c] = xi[c] = 0.0;
+        for (int q0 = qb + lane; q0 < qe; q0 += GB * LPR) {
+            int j[GB];
+            double a[GB];
+            double xv[GB][K];
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                const int q = q0 + u * LPR;
+                j[u] = q < qe ? v.cs[q] : -1;
+                a[u] = q < qe ? v.vs[q] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < GB; ++u)
+                if (j[u] >= 0 && (MODE != 0 || j[u] != row)) ldrow_pol<K>(x + (size_t)j[u] * VS<K>::S, xv[u], xpol);
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                if (j[u] < 0) continue;
+                if (MODE == 0 && j[u] == row) {
+                    dg += a[u];
+                } else {
+                    if (MODE == 3 && j[u] == row) {
+                        dg += a[u];
+#pragma unroll
+                        for (int c = 0; c < K; ++c) xi[c] = xv[u][c];
+                    }
+#pragma unroll
+                    for (int c = 0; c < K; ++c) s[c] = fma(a[u], xv[u][c], s[c]);
+                }
+            }
+        }
+        // groups never straddle a warp; every lane of the warp takes part
+#pragma unroll
+        for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], 0xffffffffu);
+        if (MODE == 0 || MODE == 3) dg = group_sum<LPR>(dg, 0xffffffffu);
+        if (MODE == 3)
+#pragma unroll
+            for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], 0xffffffffu);
+        if (valid && lane == 0) {
+            double out[K];
+#pragma unroll
+            for (int c = 0; c < K; ++c)
+                out[c] = MODE == 0 ? (bv[c] - s[c]) / dg : MODE == 3 ? xi[c] + omega * (bv[c] - s[c]) / dg : bv[c] - s[c];
+            if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
+            else if (MODE != 2) strow_pol<K>(r + (size_t)row * VS<K>::S, out, xpol);
+            else
+#pragma unroll
+                for (int c = 0; c < K; ++c) acc[c] = fma(out[c], out[c], acc[c]);
+        }
+        __syncthreads();   // stage sidx fully consumed
+        if (tid == 0 && i + 2 < mine) {
+            const TileDesc dn = tiles[t_begin + blockIdx.x + (i + 2) * gridDim.x];
+            issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
+        }
+    }
+    if (MODE == 2) {
+        __shared__ double red[kTile / 32][K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const double vsum = warp_sum(acc[c]);
+            if ((tid & 31) == 0) red[tid >> 5][c] = vsum;
+        }
+        __syncthreads();
+        if (tid < K) {
+            double vsum = 0.0;
+            for (int w = 0; w < kTile / 32; ++w) vsum += red[w][tid];
+            partial[blockIdx.x * K + tid] = vsum;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Persistent multicolour GS for the tiled levels (level 0): ALL colour passes
 // of mu sweeps in ONE cooperative launch.  Each CTA walks its tiles of
@@ -1160,9 +1284,14 @@ inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 
 template <int K, int MODE>
 void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double* partial, int grid, double omega,
                  bool pdl, cudaStream_t s) {
-    launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, pipe_smem(L.pipe_cap), s,
-             reinterpret_cast<const TileDesc*>(L.tiles.p), t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial,
-             L.pipe_cap, omega);
+    const TileDesc* td = reinterpret_cast<const TileDesc*>(L.tiles.p);
+    const size_t sm = pipe_smem(L.pipe_cap);
+    switch (L.pipe_lpr) {
+        case 1: launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
+        case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
+        case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
+        default: launch_k(pdl, k_tile_pipe_lpr<K, 8, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
+    }
 }
 
 // MODE 0: GS pass on rows [r0, r1) in place on L.x; MODE 1: r = b - A x;
@@ -1240,6 +1369,18 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_pipe<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_sweep<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 }
 

@@ -268,11 +268,16 @@ def test_launch_modes_agree(ora, monkeypatch):
         "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
         "chol_cluster": {"MG_CHOL": "cluster"},
         "gs_persist": {"MG_GS_PERSIST": "1"},
+        "pipe_lpr4": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "4"},
+        "pipe_lpr8": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "8"},
+        "pipe_lpr2_nopdl": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "2",
+                            "MG_PDL": "0"},
+        "pipe_lpr2_l0": {"MG_PIPE_LPR_L0": "2"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
-                  "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST"):
+                  "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -352,10 +357,16 @@ def test_split_csr_equals_split_cotan(ora):
         gpu_solver(p).set_alpha(0.5)                          # MG_ERR_STATE: no split operators
 
 
-@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
-def test_smoother_variants_parity(ora, cid, kw):
+@pytest.mark.parametrize("cid,kw,pipe_lpr", [(4, {"subdiv": 5}, None), (3, {"grid": (96, 80)}, None),
+                                             (4, {"subdiv": 5}, "4")])
+def test_smoother_variants_parity(ora, cid, kw, pipe_lpr, monkeypatch):
     """Row f4: damped-Jacobi smoothing (App. E) and the symmetric
-    (reversed post colours) V-cycle match the oracle's same variants."""
+    (reversed post colours) V-cycle match the oracle's same variants (also
+    with the pipelined lanes-per-row tiles on the coarse levels)."""
+    if pipe_lpr:
+        monkeypatch.setenv("MG_PIPE_LPR_MAX_AVG", "64")
+        monkeypatch.setenv("MG_PIPE_LPR_MIN_ROWS", "0")
+        monkeypatch.setenv("MG_PIPE_LPR", pipe_lpr)
     p = meshgen.make_config(cid, **kw)
     A, M, _ = oracle_problem(ora, p)
     Bo = oracle_rhs(ora, p, M)
