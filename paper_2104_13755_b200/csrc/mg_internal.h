@@ -62,6 +62,9 @@ struct Level {
     int cap_all = 0;                      // max nnz of a kTile-row tile of the whole matrix
     bool pipe = false;                    // persistent TMA-bulk pipelined tile kernels
     int pipe_cap = 0;                     // max nnz of any tile (GS or whole-level tiles)
+    mutable int pass_ctr = 0;             // pipelined launches enqueued on this level (serpentine direction)
+    bool serpentine = true;               // alternate the tile walk direction between passes
+    bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
     int pipe_lpr = 1;                     // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile

@@ -230,6 +230,14 @@ __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned
     return v;
 }
 
+// Tile schedule: CTA b takes tiles b, b + G, ... of [t_begin, t_end), walked
+// backwards when rev != 0 (alternate passes over a level run in opposite
+// directions, so a pass starts where the previous one left its lines in L2;
+// the rows of one pass are independent, so the result does not change).
+__device__ __forceinline__ int tile_ix(int t_begin, int t_end, int t, int rev) {
+    return rev ? t_end - 1 - t : t_begin + t;
+}
+
 template <int K, int UNR>
 __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, const double* __restrict__ x,
                                           double (&s)[K], double& d, uint64_t xpol) {
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
                                                      const int* __restrict__ rp, const int* __restrict__ col,
                                                      const double* __restrict__ val, const double* __restrict__ b,
                                                      double* __restrict__ x, double* __restrict__ r,
-                                                     double* __restrict__ partial, int cap, double omega) {
+                                                     double* __restrict__ partial, int cap, double omega, int rev) {
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
     const int tid = threadIdx.x;
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
     __syncthreads();
     if (tid == 0) {
         for (int i = 0; i < 2 && i < mine; ++i) {
-            const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+            const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
             issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
         }
     }
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
     for (int i = 0; i < mine; ++i) {
         const int sidx = i & 1;
-        const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+        const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
         mbar_wait(&bar[sidx], (unsigned)((i >> 1) & 1));
         const StageView v = view_tile(d, stage[sidx], cap);
         if (tid < d.nrow) {
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
         }
         __syncthreads();   // stage sidx fully consumed
         if (tid == 0 && i + 2 < mine) {
-            const TileDesc dn = tiles[t_begin + blockIdx.x + (i + 2) * gridDim.x];
+            const TileDesc dn = tiles[tile_ix(t_begin, t_end, blockIdx.x + (i + 2) * gridDim.x, rev)];
             issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
         }
     }
@@ -370,7 +378,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
                                                          const int* __restrict__ rp, const int* __restrict__ col,
                                                          const double* __restrict__ val, const double* __restrict__ b,
                                                          double* __restrict__ x, double* __restrict__ r,
-                                                         double* __restrict__ partial, int cap, double omega) {
+                                                         double* __restrict__ partial, int cap, double omega, int rev) {
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
     constexpr int GB = 4;
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
     __syncthreads();
     if (tid == 0) {
         for (int i = 0; i < 2 && i < mine; ++i) {
-            const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+            const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
             issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
         }
     }
@@ -404,7 +412,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
     for (int c = 0; c < K; ++c) acc[c] = 0.0;
     for (int i = 0; i < mine; ++i) {
         const int sidx = i & 1;
-        const TileDesc d = tiles[t_begin + blockIdx.x + i * gridDim.x];
+        const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
         mbar_wait(&bar[sidx], (unsigned)((i >> 1) & 1));
         const StageView v = view_tile(d, stage[sidx], cap);
         const bool valid = tr < d.nrow;
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
         }
         __syncthreads();   // stage sidx fully consumed
         if (tid == 0 && i + 2 < mine) {
-            const TileDesc dn = tiles[t_begin + blockIdx.x + (i + 2) * gridDim.x];
+            const TileDesc dn = tiles[tile_ix(t_begin, t_end, blockIdx.x + (i + 2) * gridDim.x, rev)];
             issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
         }
     }
@@ -894,12 +902,16 @@ constexpr int kRestrictG = 16;
 template <int K>
 __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cptr, const int* __restrict__ cidx,
                                                      const double* __restrict__ cw, const double* __restrict__ r,
-                                                     double* __restrict__ bc, double* __restrict__ xc, int nc) {
+                                                     double* __restrict__ bc, double* __restrict__ xc, int nc,
+                                                     const int* __restrict__ order) {
     constexpr int G = kRestrictG;
-    const int I = (blockIdx.x * kBlock + threadIdx.x) / G;
+    const int g = (blockIdx.x * kBlock + threadIdx.x) / G;
     const int lane = threadIdx.x & (G - 1);
     pdl_launch_dependents();
-    const bool active = I < nc;
+    const bool active = g < nc;
+    // coarse rows in locality order (all colours interleaved): the children's
+    // residual rows are then gathered from a small spatial window (L2 hits)
+    const int I = active ? (order ? order[g] : g) : 0;
     int t0 = 0, t1 = 0, i0 = -1, i1 = -1;
     double w0 = 0.0, w1 = 0.0;
     if (active) {
@@ -1286,11 +1298,12 @@ void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double*
                  bool pdl, cudaStream_t s) {
     const TileDesc* td = reinterpret_cast<const TileDesc*>(L.tiles.p);
     const size_t sm = pipe_smem(L.pipe_cap);
+    const int rev = (MODE != 2 && L.serpentine) ? (L.pass_ctr++ & 1) : 0;   // norm partials keep one order
     switch (L.pipe_lpr) {
-        case 1: launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
-        case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
-        case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
-        default: launch_k(pdl, k_tile_pipe_lpr<K, 8, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega); break;
+        case 1: launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+        case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+        case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+        default: launch_k(pdl, k_tile_pipe_lpr<K, 8, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
     }
 }
 
@@ -1434,7 +1447,8 @@ int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
 }
 int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK>, nblk((int64_t)C.n * kRestrictG, kBlock), kBlock, 0, s, C.cptr.p,
-                             C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n), 1))
+                             C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n,
+                             C.restrict_ordered ? (const int*)C.gal_order.p : nullptr), 1))
 }
 int vc_prolong(int K, const Level& F, const Level& C, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (launch_k(pdl, k_prolong<KK>, nblk(F.n, kBlock), kBlock, 0, s, F.pc.p, F.pw.p, C.x.p, F.x.p, F.n), 1))

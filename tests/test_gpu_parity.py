@@ -273,11 +273,15 @@ def test_launch_modes_agree(ora, monkeypatch):
         "pipe_lpr2_nopdl": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "2",
                             "MG_PDL": "0"},
         "pipe_lpr2_l0": {"MG_PIPE_LPR_L0": "2"},
+        "noserp": {"MG_SERPENTINE": "0"},
+        "nospatial": {"MG_TILE_SPATIAL": "0", "MG_RESTRICT_ORDER": "0"},
+        "restrict_order": {"MG_RESTRICT_ORDER": "1"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
-                  "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0"):
+                  "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
+                  "MG_RESTRICT_ORDER"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -290,7 +294,12 @@ def test_launch_modes_agree(ora, monkeypatch):
         S.close()
     assert np.array_equal(out["default"], out["nopdl"])
     assert np.array_equal(out["default"], out["nopipe"])
-    assert np.array_equal(out["default"], out["gs_persist"])   # same per-row arithmetic, one launch per phase
+    assert np.array_equal(out["default"], out["gs_persist"])
+    # tile walk direction, spatial tile order of the residual and the coarse-row
+    # order of the restriction change no row's arithmetic
+    assert np.array_equal(out["default"], out["noserp"])
+    assert np.array_equal(out["default"], out["nospatial"])
+    assert np.array_equal(out["default"], out["restrict_order"])   # same per-row arithmetic, one launch per phase
 
 
 @pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
