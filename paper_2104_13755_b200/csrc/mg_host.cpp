@@ -490,6 +490,28 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             if (!e) e = L.dtoff.upload(L.tile_off, c->stream);
             if (e) return c->cuda_fail(e, "tile upload");
         }
+        // small levels: all GS sweeps in one CTA with x in shared memory
+        // (opt-in: measured 2x slower than one PDL launch per colour — one SM
+        // issues ~430 warp-instructions per 128-row tile at ~1.6 IPC, 4.3 us
+        // per tile against ~2.2 us per colour launch; profiles/r01/sweeps/al_*)
+        const int small_max = getenv("MG_SMALL_ROWS") ? atoi(getenv("MG_SMALL_ROWS")) : 0;
+        L.small = !L.pipe && L.n > 0 && L.n <= small_max;
+        if (L.small) {
+            const int TS = small_rows_per_tile();
+            std::vector<int32_t> td, toff(1, 0);
+            L.small_cap = 1;
+            for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k) {
+                for (int a = L.colour_off[k]; a < L.colour_off[k + 1]; a += TS) {
+                    const int nr = std::min(TS, L.colour_off[k + 1] - a);
+                    td.insert(td.end(), {a, nr, L.irp[a], L.irp[a + nr]});
+                    L.small_cap = std::max(L.small_cap, L.irp[a + nr] - L.irp[a]);
+                }
+                toff.push_back((int32_t)(td.size() / 4));
+            }
+            cudaError_t e = L.stiles.upload(td, c->stream);
+            if (!e) e = L.stoff.upload(toff, c->stream);
+            if (e) return c->cuda_fail(e, "tile upload");
+        }
         if (!L.tiled) {
             // lanes per row of a colour pass (each lane prefetches 32 / LPR entries
             // of its row before the PDL wait).  Measured on B200 (profiles/r01,
@@ -802,6 +824,10 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
     }
     if (c->gs_persist && L.pipe && L.pipe_lpr == 1 && mu > 0 && c->persist_ctr.p) {
         const int nl = vc_gs_persist(K, L, mu, reverse, c->persist_ctr.p, s);
+        if (nl > 0) return nl;
+    }
+    if (L.small && mu > 0) {
+        const int nl = vc_small_gs(K, L, mu, reverse, pdl, s);
         if (nl > 0) return nl;
     }
     for (int it = 0; it < mu; ++it)

@@ -65,7 +65,12 @@ struct Level {
     mutable int pass_ctr = 0;             // pipelined launches enqueued on this level (serpentine direction)
     bool serpentine = true;               // alternate the tile walk direction between passes
     bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
-    int pipe_lpr = 1;                     // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
+    bool small = false;                   // GS sweeps by the one-CTA shared-memory kernel
+    int small_cap = 0;                    // max nnz of a small-kernel tile
+    DBuf<int32_t> stiles;                 // small-kernel tiles {row0, nrow, e0, e1}, per colour
+    DBuf<int32_t> stoff;                  // [ncolours+1] tile ranges per colour
+    int pipe_lpr = 1;
+                     // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
     DBuf<int32_t> dtoff;                  // tile_off on device (persistent GS)
@@ -157,6 +162,8 @@ int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);     
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
 int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s);  // all colours of mu sweeps
 int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s);   // mu dataflow GS sweeps
+int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one CTA
+int small_rows_per_tile();
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
 int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
 int vc_prolong(int K, const Level& fine, const Level& coarse, bool pdl, cudaStream_t s);   // fine.x += P coarse.x

@@ -642,6 +642,176 @@ int launch_gs_persist_k(const Level& L, int mu, bool reverse, unsigned long long
 }
 
 // ---------------------------------------------------------------------------
+// Small levels (a few thousand rows): all mu GS sweeps of the level in ONE
+// CTA.  The level's iterate lives in shared memory (compact [n][K]); the
+// matrix rows and right-hand side of each 128-row tile of a colour class are
+// streamed into a double-buffered stage with TMA bulk copies while the
+// previous tile is computed, so a colour step costs a __syncthreads instead
+// of a dependent launch + L2 round trips (the per-launch floor measured
+// ~2.2 us per colour pass on these levels).  LPR = 8 lanes per row take
+// entries l, l+8, ... (the order of k_lpr_sweep<K,8>), fixed-order shuffle
+// reduction; tiles of one colour are independent, colours run in order
+// (reversed for the symmetric cycle's post-smoothing).
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallLPR = 8;
+constexpr int kSmallRows = kSmallThreads / kSmallLPR;
+
+template <int K>
+__host__ __device__ inline size_t small_stage_bytes(int cap) {
+    const size_t a = (stage_bytes(cap) + 15) / 16 * 16;
+    return (a + (size_t)(kSmallRows + 2) * VS<K>::S * 8 + 127) / 128 * 128;
+}
+template <int K>
+__host__ __device__ inline size_t small_smem_bytes(int n, int cap) {
+    return ((size_t)n * K * 8 + 127) / 128 * 128 + 2 * small_stage_bytes<K>(cap);
+}
+
+template <int K>
+__device__ __forceinline__ void small_issue(const TileDesc& d, unsigned char* stage, int cap, uint64_t* bar,
+                                            const int* rp, const int* col, const double* val, const double* b,
+                                            uint64_t pol) {
+    constexpr int S = VS<K>::S;
+    const int ra = d.row0 & ~3;
+    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
+    const int ca = d.e0 & ~3;
+    const int ccnt = (d.e1 - ca + 3) & ~3;
+    const int va = d.e0 & ~1;
+    const int vcnt = (d.e1 - va + 1) & ~1;
+    // b rows [row0, row0 + nrow) of S doubles, 16-byte aligned and padded
+    const int ba = S >= 2 ? d.row0 : (d.row0 & ~1);
+    const int bcnt = S >= 2 ? d.nrow * S : ((d.row0 + d.nrow - ba + 1) & ~1);
+    int* rps = reinterpret_cast<int*>(stage);
+    int* cs = rps + (kTile + 8);
+    double* vs = reinterpret_cast<double*>(stage + ((size_t)stage_ints(cap) * 4 + 15) / 16 * 16);
+    double* bs = reinterpret_cast<double*>(stage + (stage_bytes(cap) + 15) / 16 * 16);
+    const unsigned bytes = (unsigned)(rcnt * 4 + ccnt * 4 + vcnt * 8 + bcnt * 8);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(rps, rp + ra, rcnt * 4, bar, pol);
+    if (ccnt > 0) bulk_g2s(cs, col + ca, ccnt * 4, bar, pol);
+    if (vcnt > 0) bulk_g2s(vs, val + va, vcnt * 8, bar, pol);
+    bulk_g2s(bs, b + (size_t)ba * S, bcnt * 8, bar, pol);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_small_gs(const TileDesc* __restrict__ tiles,
+                                                               const int* __restrict__ toff, int ncol, int mu,
+                                                               int reverse, const int* __restrict__ rp,
+                                                               const int* __restrict__ col,
+                                                               const double* __restrict__ val,
+                                                               const double* __restrict__ b, double* __restrict__ x,
+                                                               int n, int cap) {
+    constexpr int S = VS<K>::S;
+    constexpr int G = kSmallLPR;
+    extern __shared__ __align__(128) unsigned char smem_small[];
+    __shared__ __align__(8) uint64_t bar[2];
+    double* xs = reinterpret_cast<double*>(smem_small);
+    const size_t xoff = ((size_t)n * K * 8 + 127) / 128 * 128;
+    const size_t sb = small_stage_bytes<K>(cap);
+    unsigned char* stage[2] = {smem_small + xoff, smem_small + xoff + sb};
+    const int tid = threadIdx.x;
+    const int grp = tid / G;
+    const int lane = tid & (G - 1);
+    pdl_launch_dependents();
+    uint64_t pol = 0;
+    if (tid == 0) {
+        pol = evict_first_policy();
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // task cursor over (sweep, colour step, tile of the colour)
+    const int nsteps = mu * ncol;
+    int ps = 0, pt = 0, issued = 0;
+    auto colour_of = [&](int q) { return reverse ? ncol - 1 - q : q; };
+    auto issue_next = [&]() {   // thread 0 only
+        while (ps < nsteps) {
+            const int c = colour_of(ps % ncol);
+            if (__ldg(toff + c) + pt < __ldg(toff + c + 1)) break;
+            ++ps;
+            pt = 0;
+        }
+        if (ps >= nsteps) return;
+        const int c = colour_of(ps % ncol);
+        const TileDesc d = tiles[__ldg(toff + c) + pt];
+        small_issue<K>(d, stage[issued & 1], cap, &bar[issued & 1], rp, col, val, b, pol);
+        ++pt;
+        ++issued;
+    };
+    pdl_wait();   // x and b come from the previous kernels
+    if (tid == 0) {
+        issue_next();
+        issue_next();
+    }
+    for (int i = tid; i < n; i += kSmallThreads) {
+        double v[K];
+        ldrow<K>(x + (size_t)i * S, v);
+#pragma unroll
+        for (int c = 0; c < K; ++c) xs[(size_t)i * K + c] = v[c];
+    }
+    __syncthreads();
+    int done = 0;
+    for (int step = 0; step < nsteps; ++step) {
+        const int c = colour_of(step % ncol);
+        const int t0 = __ldg(toff + c), t1 = __ldg(toff + c + 1);
+        for (int t = t0; t < t1; ++t) {
+            const int sidx = done & 1;
+            const TileDesc d = tiles[t];
+            mbar_wait(&bar[sidx], (unsigned)((done >> 1) & 1));
+            const StageView v = view_tile(d, stage[sidx], cap);
+            const double* bs = reinterpret_cast<const double*>(stage[sidx] + (stage_bytes(cap) + 15) / 16 * 16) +
+                               (S >= 2 ? 0 : (d.row0 & 1));
+            const bool valid = grp < d.nrow;
+            const int row = d.row0 + grp;
+            const int qb = valid ? v.rps[grp] : 0, qe = valid ? v.rps[grp + 1] : 0;
+            double sacc[K], dg = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) sacc[k] = 0.0;
+            for (int q = qb + lane; q < qe; q += G) {
+                const int j = v.cs[q];
+                const double a = v.vs[q];
+                if (j == row) {
+                    dg += a;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) sacc[k] = fma(a, xs[(size_t)j * K + k], sacc[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) sacc[k] = group_sum<G>(sacc[k], 0xffffffffu);
+            dg = group_sum<G>(dg, 0xffffffffu);
+            if (valid && lane == 0) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) xs[(size_t)row * K + k] = (bs[(size_t)grp * S + k] - sacc[k]) / dg;
+            }
+            __syncthreads();   // stage consumed; this tile's x visible to the next colour
+            ++done;
+            if (tid == 0) issue_next();
+        }
+    }
+    for (int i = tid; i < n; i += kSmallThreads) {
+        double v[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) v[c] = xs[(size_t)i * K + c];
+        strow<K>(x + (size_t)i * S, v);
+    }
+}
+
+template <int K>
+int launch_small_gs_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    const size_t smem = small_smem_bytes<K>(L.n, L.small_cap);
+    if (smem > 220 * 1024) return -1;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_small_gs<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    launch_k(pdl, k_small_gs<K>, 1, kSmallThreads, smem, s, reinterpret_cast<const TileDesc*>(L.stiles.p),
+             (const int*)L.stoff.p, L.ncolours, mu, reverse ? 1 : 0, (const int*)L.rp.p, (const int*)L.col.p,
+             (const double*)L.val.p, (const double*)L.b.p, L.x.p, L.n, L.small_cap);
+    return 1;
+}
+
+// ---------------------------------------------------------------------------
 // LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
 // prefetches up to U = 32/LPR (col, val) of its row in the PDL prologue;
 // after the wait its x gathers go out in batches of GB independent loads.
@@ -1438,6 +1608,10 @@ int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream
         case 3: return launch_gs_flow_kk<3>(L, mu, reverse, err, s);
         default: return launch_gs_flow_kk<4>(L, mu, reverse, err, s);
     }
+}
+int small_rows_per_tile() { return kSmallRows; }
+int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_small_gs_k<KK>(L, mu, reverse, pdl, s)))
 }
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 3>(L, 0, L.n, xout, pdl, s, xin, omega)))

@@ -276,12 +276,14 @@ def test_launch_modes_agree(ora, monkeypatch):
         "noserp": {"MG_SERPENTINE": "0"},
         "nospatial": {"MG_TILE_SPATIAL": "0", "MG_RESTRICT_ORDER": "0"},
         "restrict_order": {"MG_RESTRICT_ORDER": "1"},
+        "nosmall": {"MG_SMALL_ROWS": "0"},
+        "small_all": {"MG_SMALL_ROWS": "100000"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
-                  "MG_RESTRICT_ORDER"):
+                  "MG_RESTRICT_ORDER", "MG_SMALL_ROWS"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
