@@ -177,6 +177,14 @@ int mg_set_dirichlet(mg_ctx* ctx, int32_t n_known, const int32_t* known);
  * Errors: MG_ERR_INVALID_ARG (unknown kind, omega out of range). */
 int mg_set_smoother(mg_ctx* ctx, int kind, double omega, int symmetric);
 
+/* Initial guess of mg_solve / mg_solve_pcg.  on != 0: every solve starts
+ * from X0 = 0 (Alg. 2 applied to a zero iterate, as the paper's solves do)
+ * and X is output only: its input values are not read, so a host X costs no
+ * host-to-device copy.  on = 0 (default): X holds the initial guess on input.
+ * Ignored while Dirichlet constraints are set (X supplies the known values,
+ * App. B).  Errors: MG_ERR_INVALID_ARG (null ctx). */
+int mg_set_zero_guess(mg_ctx* ctx, int32_t on);
+
 /* Solve A X = B by conjugate gradients preconditioned with one symmetric
  * V-cycle from a zero guess per iteration ("use our multigrid solver as the
  * pre-conditioner for ... the conjugate gradient method").  Every

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -14,6 +15,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mg.h"
@@ -115,6 +117,88 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
 }
 
 // 63-bit Morton key of each vertex in its level's bounding box.
+// Galerkin map (numeric P^T A P as a fixed linear map of the fine values; see
+// load_csr_pattern): for coarse slot (I, J) the entries (e, w_iI w_jJ) over
+// children i of I (children-list order), nonzeros e = (i, j) of fine row i
+// (CSR order) and parents J of j (ELL order).  Built in parallel over coarse
+// rows (count, prefix, fill); false if a level would exceed 2^31 entries.
+bool build_galerkin_map(const Level& L, const Level& C, const std::vector<int32_t>& cptr,
+                        const std::vector<int32_t>& cidx, const std::vector<double>& cw,
+                        const std::vector<int32_t>& pc, const std::vector<double>& pw, std::vector<int32_t>& gptr,
+                        std::vector<int32_t>& ge, std::vector<double>& gw) {
+    const int32_t n = L.n, nc = C.n;
+    std::vector<uint8_t> npar(n);
+    for (int32_t j = 0; j < n; ++j)
+        npar[j] = (uint8_t)((pw[j] != 0.0) + (pw[(size_t)n + j] != 0.0) + (pw[2 * (size_t)n + j] != 0.0));
+    std::vector<int64_t> roff((size_t)nc + 1, 0);
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nth = (int)std::max(1u, std::min(hw ? hw : 1u, 64u));
+    auto parallel_rows = [&](auto&& body) {
+        std::atomic<int32_t> next(0);
+        auto worker = [&]() {
+            for (;;) {
+                const int32_t a = next.fetch_add(2048);
+                if (a >= nc) break;
+                const int32_t b = std::min(nc, a + 2048);
+                for (int32_t I = a; I < b; ++I) body(I);
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; ++t) th.emplace_back(worker);
+        worker();
+        for (auto& t : th) t.join();
+    };
+    parallel_rows([&](int32_t I) {
+        int64_t k = 0;
+        for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
+            const int32_t i = cidx[t];
+            for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) k += npar[L.icol[e]];
+        }
+        roff[(size_t)I + 1] = k;
+    });
+    for (int32_t I = 0; I < nc; ++I) roff[(size_t)I + 1] += roff[I];
+    if (roff[nc] > (int64_t)INT32_MAX) return false;
+    gptr.assign((size_t)C.nnz + 1, 0);
+    ge.resize((size_t)roff[nc]);
+    gw.resize((size_t)roff[nc]);
+    struct Q {
+        int32_t slot, e;
+        double w;
+    };
+    parallel_rows([&](int32_t I) {
+        thread_local std::vector<Q> tmp;
+        thread_local std::vector<int32_t> cntl;
+        const int32_t s0 = C.irp[I], s1 = C.irp[I + 1];
+        tmp.clear();
+        for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
+            const int32_t i = cidx[t];
+            const double wI = cw[t];
+            for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
+                const int32_t j = L.icol[e];
+                for (int q = 0; q < 3; ++q) {
+                    const double wJ = pw[(size_t)q * n + j];
+                    if (wJ == 0.0) continue;
+                    const int32_t J = pc[(size_t)q * n + j];
+                    const int32_t* pos = std::lower_bound(C.icol.data() + s0, C.icol.data() + s1, J);
+                    tmp.push_back({(int32_t)(pos - C.icol.data()) - s0, e, wI * wJ});
+                }
+            }
+        }
+        cntl.assign((size_t)(s1 - s0) + 1, 0);
+        for (const Q& x : tmp) cntl[x.slot + 1]++;
+        for (int32_t k = 0; k < s1 - s0; ++k) cntl[k + 1] += cntl[k];
+        const int64_t base = roff[I];
+        for (int32_t k = 0; k < s1 - s0; ++k) gptr[s0 + k] = (int32_t)(base + cntl[k]);
+        for (const Q& x : tmp) {   // stable: enumeration order inside a slot
+            const int64_t at = base + cntl[x.slot]++;
+            ge[at] = x.e;
+            gw[at] = x.w;
+        }
+    });
+    gptr[C.nnz] = (int32_t)roff[nc];
+    return true;
+}
+
 std::vector<uint64_t> morton_keys(const std::vector<double>& V, int32_t n) {
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (int32_t i = 0; i < n; ++i)
@@ -222,7 +306,10 @@ struct mg_ctx {
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool use_gal2 = true;            // Galerkin v2 kernel
-    bool use_gal4 = false;           // Galerkin v4 kernel (group-of-rows, A P rows once per group; measured slower, opt-in)
+    bool zero_guess = false;          // mg_set_zero_guess
+    bool use_galg = true;            // Galerkin through the precomputed linear map (k_galerkin_map)
+    size_t galg_max_bytes = (size_t)16 << 30;   // device bytes allowed for the maps of all levels
+        bool use_gal4 = false;           // Galerkin v4 kernel (group-of-rows, A P rows once per group; measured slower, opt-in)
     int64_t l2_persist = 0;          // bytes of L2 set aside for the fine iterate (-1: auto, 0: off;
                                      // measured slightly slower than eviction hints alone, so off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
@@ -528,6 +615,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         }
     }
     cudaStream_t s = c->stream;
+    size_t galg_bytes = 0;
     for (int l = 0; l <= H; ++l) {
         Level& L = *c->lv[l];
         cudaError_t e;
@@ -652,6 +740,28 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     if ((e = C.g4_rows.upload(grows, s)) || (e = C.g4_coff.upload(gcoff, s)) ||
                         (e = C.g4_children.upload(gch, s)) || (e = C.g4_rcl.upload(rcl, s)))
                         return c->cuda_fail(e, "pattern upload");
+                }
+            }
+            // Galerkin map: P and the patterns are fixed, so every coarse value is
+            // a fixed linear combination of fine values,
+            //   (P^T A P)_IJ = sum_{i child of I} sum_{j in row i, J parent of j} w_iI w_jJ a_ij,
+            // stored per coarse slot as (fine nonzero index, w_iI w_jJ) in
+            // (child, fine nonzero, parent) order.  The numeric Galerkin is then a
+            // deterministic streaming gather (k_galerkin_map) with no slot search.
+            C.galg = false;
+            if (c->use_galg) {
+                std::vector<int32_t> gptr, ge;
+                std::vector<double> gwv;
+                const bool ok = build_galerkin_map(L, C, cnt, cidx, cw, pc, pw, gptr, ge, gwv);
+                const size_t bytes = ge.size() * 12 + gptr.size() * 4;
+                size_t freeb = 0, totb = 0;
+                cudaMemGetInfo(&freeb, &totb);
+                if (ok && galg_bytes + bytes <= c->galg_max_bytes && bytes * 2 < freeb) {
+                    if ((e = C.gmap_ptr.upload(gptr, s)) || (e = C.gmap_e.upload(ge, s)) || (e = C.gmap_w.upload(gwv, s)))
+                        return c->cuda_fail(e, "pattern upload");
+                    cudaStreamSynchronize(s);   // host staging vectors go out of scope
+                    C.galg = true;
+                    galg_bytes += bytes;
                 }
             }
             if ((e = L.prow_c.upload(prc, s)) || (e = L.prow_w.upload(prw, s)) || (e = C.cinfo.upload(cinfo, s)))
@@ -1020,6 +1130,8 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
     if (const char* m = getenv("MG_GAL2")) c->use_gal2 = std::string(m) != "0";
     if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) == "1";
+    if (const char* m = getenv("MG_GAL_MAP")) c->use_galg = std::string(m) != "0";
+    if (const char* m = getenv("MG_GAL_MAP_MAX_MB")) c->galg_max_bytes = (size_t)atoll(m) << 20;
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     if (const char* m = getenv("MG_FLOW_ROWS")) c->flow_rows = atoll(m);
@@ -1683,12 +1795,19 @@ static int prep_solve(mg_ctx* c, int32_t k, const double* B, double* X, double**
     const double* dB = nullptr;
     const double* dX = nullptr;
     if ((rc = to_device(c, B, c->stageB, nu, &dB))) return rc;
-    if ((rc = to_device(c, X, c->stageX, nu, &dX))) return rc;
+    const bool zero = c->zero_guess && !c->dir;
+    if (zero) {
+        cudaError_t e = is_device_ptr(X) ? cudaSuccess : c->stageX.alloc(nu);
+        if (!e) e = cudaMemsetAsync(L0.x.p, 0, sizeof(double) * (size_t)n * kMaxK, s);
+        if (e) return c->cuda_fail(e, "solve");
+    } else if ((rc = to_device(c, X, c->stageX, nu, &dX))) {
+        return rc;
+    }
     *dXout = is_device_ptr(X) ? X : c->stageX.p;
     const int32_t* um = c->dir ? c->d_umap.p : nullptr;
     c->timed(PC_PERMUTE, 0, s, [&] {
-        int nl = launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s, um) +
-                 launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s, um);
+        int nl = launch_gather_rows(k, L0.diperm.p, dB, L0.b.p, n, s, um);
+        if (!zero) nl += launch_gather_rows(k, L0.diperm.p, dX, L0.x.p, n, s, um);
         if (c->dir) nl += launch_dirichlet_rhs(k, c->uk_rp.p, c->uk_col.p, c->uk_val.p, dX, L0.b.p, n, s);
         return nl + vc_sumsq(k, L0.b.p, n, c->partial.p, resnorm_blocks(n), c->bnorm.p, s);
     });
@@ -1712,6 +1831,12 @@ static int finish_solve(mg_ctx* c, int32_t k, const double* xint, double* X, dou
         if ((e = cudaMemcpy(&fe, c->flow_err.p, sizeof(int), cudaMemcpyDeviceToHost))) return c->cuda_fail(e, "solve");
         if (fe) return c->fail(MG_ERR_CUDA, "dataflow Gauss-Seidel: dependency wait timed out");
     }
+    return MG_OK;
+}
+
+int mg_set_zero_guess(mg_ctx* c, int32_t on) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    c->zero_guess = on != 0;
     return MG_OK;
 }
 

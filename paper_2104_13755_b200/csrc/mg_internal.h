@@ -96,6 +96,11 @@ struct Level {
     DBuf<double> cw;
     DBuf<int32_t> gal_order;              // rows of this level in locality order (Galerkin)
     bool gal2 = false;                    // Galerkin v2 usable for this (coarse) level
+    // Galerkin as a fixed linear map of the fine values (this level coarse):
+    // val[slot] = sum_t gmap_w[t] * fine.val[gmap_e[t]], t in [gmap_ptr[slot], gmap_ptr[slot+1])
+    bool galg = false;
+    DBuf<int32_t> gmap_ptr, gmap_e;
+    DBuf<double> gmap_w;
     // Galerkin v4 (this level coarse): coarse rows in groups of consecutive
     // gal_order rows; per group the distinct children (fine rows) and, for
     // every children-list entry, the child's index inside its group

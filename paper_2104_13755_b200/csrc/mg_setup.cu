@@ -1528,8 +1528,61 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
     k_scatter_vec<<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src_int, dst_user, n);
     return 1;
 }
+namespace {
+// Numeric Galerkin through the precomputed map (see mg_host.cpp, "Galerkin
+// map"): one warp per coarse row (locality order, so the fine values the rows
+// gather are shared in L2 by neighbouring warps), 4 lanes per coarse slot;
+// lane l takes the slot's entries l, l+4, ... (map entries stream once,
+// evict-first), then a fixed-order shuffle reduction.  Deterministic.
+constexpr int kGmapLanes = 4;
+__global__ void __launch_bounds__(256) k_galerkin_map(int nc, const int* __restrict__ order, const int* __restrict__ crp,
+                                                      const int* __restrict__ gptr, const int* __restrict__ ge,
+                                                      const double* __restrict__ gw, const double* __restrict__ fval,
+                                                      double* __restrict__ cval) {
+    const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+    if (w >= nc) return;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / kGmapLanes;
+    const int sl = lane & (kGmapLanes - 1);
+    const int I = order[w];
+    const int s0 = crp[I], s1 = crp[I + 1];
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (int sb = s0; sb < s1; sb += 32 / kGmapLanes) {
+        const int slot = sb + grp;
+        double acc = 0.0;
+        if (slot < s1) {
+            const int t0 = gptr[slot], t1 = gptr[slot + 1];
+            int t = t0 + sl;
+            for (; t + 3 * kGmapLanes < t1; t += 4 * kGmapLanes) {
+                int e[4];
+                double g[4], a[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(e[u]) : "l"(ge + t + u * kGmapLanes), "l"(pol));
+                    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(g[u]) : "l"(gw + t + u * kGmapLanes), "l"(pol));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) a[u] = __ldg(fval + e[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = fma(g[u], a[u], acc);
+            }
+            for (; t < t1; t += kGmapLanes) acc = fma(__ldg(gw + t), __ldg(fval + __ldg(ge + t)), acc);
+        }
+#pragma unroll
+        for (int off = kGmapLanes / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, kGmapLanes);
+        if (slot < s1 && sl == 0) cval[slot] = acc;
+    }
+}
+}  // namespace
+
 int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s) {
     const int nc = coarse.n;
+    if (coarse.galg) {
+        k_galerkin_map<<<(int)(((int64_t)nc * 32 + 255) / 256), 256, 0, s>>>(
+            nc, coarse.gal_order.p, coarse.rp.p, coarse.gmap_ptr.p, coarse.gmap_e.p, coarse.gmap_w.p, fval, cval);
+        return 1;
+    }
     if (coarse.gal4_maxt > 0 && fine.prow_c.p) {
         if (coarse.gal4_maxt <= 12)
             k_galerkin4<12><<<coarse.gal4_ngroups, kGal4Threads, galerkin4_smem(12), s>>>(

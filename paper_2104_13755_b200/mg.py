@@ -56,6 +56,7 @@ def lib():
             "mg_set_matrix_split_cotan": (C.c_int, [_vp, _vp]),
             "mg_set_alpha": (C.c_int, [_vp, dbl]),
             "mg_set_smoother": (C.c_int, [_vp, C.c_int, dbl, C.c_int]),
+            "mg_set_zero_guess": (C.c_int, [_vp, C.c_int32]),
             "mg_set_dirichlet": (C.c_int, [_vp, i32, _vp]),
             "mg_set_matrix_bilaplacian": (C.c_int, [_vp, _vp, dbl, dbl]),
             "mg_solve_pcg": (C.c_int, [_vp, i32, _vp, _vp, dbl, i32, _vp, _vp]),
@@ -197,6 +198,11 @@ def mg_set_dirichlet(ctx, known):
 def mg_set_smoother(ctx, kind=0, omega=0.8, symmetric=False):
     """kind 0 multicolour GS, 1 damped Jacobi; symmetric: reversed post colours."""
     return _check(ctx, lib().mg_set_smoother(ctx, int(kind), float(omega), int(bool(symmetric))))
+
+
+def mg_set_zero_guess(ctx, on=True):
+    """Solves start from X0 = 0 and X is output only (not read, no H2D copy)."""
+    return _check(ctx, lib().mg_set_zero_guess(ctx, int(bool(on))))
 
 
 def mg_solve_pcg(ctx, k, B, X, rel_tol, max_iters, res_hist=None):
@@ -369,6 +375,9 @@ class Solver:
 
     def set_smoother(self, kind=0, omega=0.8, symmetric=False):
         return mg_set_smoother(self.ctx, kind, omega, symmetric)
+
+    def set_zero_guess(self, on=True):
+        return mg_set_zero_guess(self.ctx, on)
 
     def solve_pcg(self, B, X, rel_tol=1e-10, max_iters=100, history=True):
         k = 1 if B.ndim == 1 else B.shape[1]

@@ -277,13 +277,15 @@ def test_launch_modes_agree(ora, monkeypatch):
         "nospatial": {"MG_TILE_SPATIAL": "0", "MG_RESTRICT_ORDER": "0"},
         "restrict_order": {"MG_RESTRICT_ORDER": "1"},
         "nosmall": {"MG_SMALL_ROWS": "0"},
+        "nogalmap": {"MG_GAL_MAP": "0"},
+        "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
-                  "MG_RESTRICT_ORDER", "MG_SMALL_ROWS"):
+                  "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -676,4 +678,34 @@ def test_dataflow_gs_parity(ora, cid, kw, monkeypatch):
     Xg = np.zeros_like(Bo)
     rc, it, hg = S.solve_pcg(Bo, Xg, rel_tol=0.0, max_iters=4)
     check_x(Xg, Xp)
+    S.close()
+
+
+def test_zero_guess(ora):
+    """mg_set_zero_guess: X is output only — garbage on input gives the same
+    iterate (bitwise) as an explicit zero guess, for host and device X, for
+    mg_solve and mg_solve_pcg; ignored under Dirichlet constraints."""
+    import torch
+    p = meshgen.make_config(4, subdiv=5)
+    A, M, mgo = oracle_problem(ora, p)
+    Bo = oracle_rhs(ora, p, M)
+    Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=3)
+    S = gpu_solver(p)
+    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+    X0 = np.zeros_like(Bo)
+    S.solve(Bo, X0, rel_tol=0.0, max_cycles=3)
+    check_x(X0, Xo)
+    S.set_zero_guess(True)
+    Xg = np.full_like(Bo, 1e30)
+    S.solve(Bo, Xg, rel_tol=0.0, max_cycles=3)
+    assert np.array_equal(Xg, X0)
+    Xd = torch.full(Bo.shape, float("nan"), dtype=torch.float64, device="cuda")
+    S.solve(torch.from_numpy(Bo).cuda(), Xd, rel_tol=0.0, max_cycles=3)
+    assert np.array_equal(Xd.cpu().numpy(), X0)
+    P1 = np.full_like(Bo, -7.0)
+    S.solve_pcg(Bo, P1, rel_tol=0.0, max_iters=3)
+    S.set_zero_guess(False)
+    P0 = np.zeros_like(Bo)
+    S.solve_pcg(Bo, P0, rel_tol=0.0, max_iters=3)
+    assert np.array_equal(P1, P0)
     S.close()
