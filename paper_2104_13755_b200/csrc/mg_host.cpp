@@ -124,8 +124,9 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
 // rows (count, prefix, fill); false if a level would exceed 2^31 entries.
 bool build_galerkin_map(const Level& L, const Level& C, const std::vector<int32_t>& cptr,
                         const std::vector<int32_t>& cidx, const std::vector<double>& cw,
-                        const std::vector<int32_t>& pc, const std::vector<double>& pw, std::vector<int32_t>& gptr,
-                        std::vector<int32_t>& ge, std::vector<double>& gw) {
+                        const std::vector<int32_t>& pc, const std::vector<double>& pw, bool half,
+                        std::vector<int32_t>& gptr, std::vector<int32_t>& ge, std::vector<double>& gw,
+                        std::vector<int32_t>& diag, std::vector<int32_t>& tpos) {
     const int32_t n = L.n, nc = C.n;
     std::vector<uint8_t> npar(n);
     for (int32_t j = 0; j < n; ++j)
@@ -152,7 +153,15 @@ bool build_galerkin_map(const Level& L, const Level& C, const std::vector<int32_
         int64_t k = 0;
         for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
             const int32_t i = cidx[t];
-            for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) k += npar[L.icol[e]];
+            for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
+                const int32_t j = L.icol[e];
+                if (!half) {
+                    k += npar[j];
+                    continue;
+                }
+                for (int q = 0; q < 3; ++q)
+                    if (pw[(size_t)q * n + j] != 0.0 && pc[(size_t)q * n + j] >= I) ++k;
+            }
         }
         roff[(size_t)I + 1] = k;
     });
@@ -179,6 +188,7 @@ bool build_galerkin_map(const Level& L, const Level& C, const std::vector<int32_
                     const double wJ = pw[(size_t)q * n + j];
                     if (wJ == 0.0) continue;
                     const int32_t J = pc[(size_t)q * n + j];
+                    if (half && J < I) continue;
                     const int32_t* pos = std::lower_bound(C.icol.data() + s0, C.icol.data() + s1, J);
                     tmp.push_back({(int32_t)(pos - C.icol.data()) - s0, e, wI * wJ});
                 }
@@ -196,6 +206,24 @@ bool build_galerkin_map(const Level& L, const Level& C, const std::vector<int32_
         }
     });
     gptr[C.nnz] = (int32_t)roff[nc];
+    if (half) {
+        diag.assign(nc, 0);
+        tpos.assign((size_t)C.nnz, 0);
+        parallel_rows([&](int32_t I) {
+            for (int32_t q = C.irp[I]; q < C.irp[I + 1]; ++q) {
+                const int32_t J = C.icol[q];
+                if (J == I) diag[I] = q;
+                const int32_t* pos = std::lower_bound(C.icol.data() + C.irp[J], C.icol.data() + C.irp[J + 1], I);
+                tpos[q] = (int32_t)(pos - C.icol.data());
+            }
+        });
+        for (int32_t I = 0; I < nc; ++I)   // the half map needs a symmetric pattern with every diagonal stored
+            if (C.icol[diag[I]] != I) return false;
+        for (int64_t q = 0; q < C.nnz; ++q) {
+            const int32_t t = tpos[q];
+            if (t >= C.nnz || tpos[t] != q) return false;
+        }
+    }
     return true;
 }
 
@@ -307,6 +335,8 @@ struct mg_ctx {
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool use_gal2 = true;            // Galerkin v2 kernel
     bool zero_guess = false;          // mg_set_zero_guess
+    bool galg_half = true;            // upper-triangle map for symmetric sources (cotan, bilaplacian)
+    bool sym_source = false;          // the current matrix source is symmetric by construction
     bool use_galg = true;            // Galerkin through the precomputed linear map (k_galerkin_map)
     size_t galg_max_bytes = (size_t)16 << 30;   // device bytes allowed for the maps of all levels
         bool use_gal4 = false;           // Galerkin v4 kernel (group-of-rows, A P rows once per group; measured slower, opt-in)
@@ -750,17 +780,19 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             // deterministic streaming gather (k_galerkin_map) with no slot search.
             C.galg = false;
             if (c->use_galg) {
-                std::vector<int32_t> gptr, ge;
+                std::vector<int32_t> gptr, ge, gdiag, gtpos;
                 std::vector<double> gwv;
-                const bool ok = build_galerkin_map(L, C, cnt, cidx, cw, pc, pw, gptr, ge, gwv);
-                const size_t bytes = ge.size() * 12 + gptr.size() * 4;
+                const bool ok = build_galerkin_map(L, C, cnt, cidx, cw, pc, pw, c->galg_half, gptr, ge, gwv, gdiag, gtpos);
+                const size_t bytes = ge.size() * 12 + gptr.size() * 4 + gtpos.size() * 4 + gdiag.size() * 4;
                 size_t freeb = 0, totb = 0;
                 cudaMemGetInfo(&freeb, &totb);
                 if (ok && galg_bytes + bytes <= c->galg_max_bytes && bytes * 2 < freeb) {
-                    if ((e = C.gmap_ptr.upload(gptr, s)) || (e = C.gmap_e.upload(ge, s)) || (e = C.gmap_w.upload(gwv, s)))
+                    if ((e = C.gmap_ptr.upload(gptr, s)) || (e = C.gmap_e.upload(ge, s)) || (e = C.gmap_w.upload(gwv, s)) ||
+                        (e = C.gmap_diag.upload(gdiag, s)) || (e = C.gmap_tpos.upload(gtpos, s)))
                         return c->cuda_fail(e, "pattern upload");
                     cudaStreamSynchronize(s);   // host staging vectors go out of scope
                     C.galg = true;
+                    C.galg_half = c->galg_half;
                     galg_bytes += bytes;
                 }
             }
@@ -882,7 +914,7 @@ int rebuild_hierarchy(mg_ctx* c) {
     cudaStream_t s = c->stream;
     for (int l = 0; l < c->H; ++l)
         c->timed(PC_GALERKIN, l, s, [&] {
-            return launch_galerkin(*c->lv[l], c->lv[l]->val.p, *c->lv[l + 1], c->lv[l + 1]->val.p, s);
+            return launch_galerkin(*c->lv[l], c->lv[l]->val.p, *c->lv[l + 1], c->lv[l + 1]->val.p, s, c->sym_source);
         });
     return factor_coarsest(c);
 }
@@ -902,7 +934,8 @@ int split_hierarchy(mg_ctx* c) {
         c->timed(PC_GALERKIN, l, s, [&] {
             Level& F = *c->lv[l];
             Level& C = *c->lv[l + 1];
-            return launch_galerkin(F, F.qv.p, C, C.qv.p, s) + launch_galerkin(F, F.mv.p, C, C.mv.p, s);
+            return launch_galerkin(F, F.qv.p, C, C.qv.p, s, c->sym_source) +
+                   launch_galerkin(F, F.mv.p, C, C.mv.p, s, c->sym_source);
         });
     cudaError_t e = cudaStreamSynchronize(s);
     if (!e) e = cudaGetLastError();
@@ -1131,6 +1164,7 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_GAL2")) c->use_gal2 = std::string(m) != "0";
     if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) == "1";
     if (const char* m = getenv("MG_GAL_MAP")) c->use_galg = std::string(m) != "0";
+    if (const char* m = getenv("MG_GAL_MAP_HALF")) c->galg_half = std::string(m) != "0";
     if (const char* m = getenv("MG_GAL_MAP_MAX_MB")) c->galg_max_bytes = (size_t)atoll(m) << 20;
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
@@ -1458,6 +1492,7 @@ static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* ro
 
 int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const double* val,
                   int on_device) {
+    if (c) c->sym_source = false;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (!val) return c->fail(MG_ERR_INVALID_ARG, "null CSR value array");
@@ -1612,6 +1647,7 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
 }
 
 int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double lap_coeff) {
+    if (c) c->sym_source = true;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if ((rc = load_cotan_pattern(c, V))) return rc;
@@ -1643,6 +1679,7 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
 
 // Row f3: A = mass_coeff M + bilap_coeff L M^{-1} L on the 2-ring pattern.
 int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, double bilap_coeff) {
+    if (c) c->sym_source = true;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (!V) return c->fail(MG_ERR_INVALID_ARG, "V is null");
@@ -1709,6 +1746,7 @@ int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, dou
 
 int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col,
                         const double* q_val, const double* m_val) {
+    if (c) c->sym_source = false;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (c->dir || c->dir_all) return c->fail(MG_ERR_STATE, "split operators are not available with Dirichlet constraints");
@@ -1729,6 +1767,7 @@ int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_pt
 }
 
 int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
+    if (c) c->sym_source = true;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (c->dir || c->dir_all) return c->fail(MG_ERR_STATE, "split operators are not available with Dirichlet constraints");

@@ -99,8 +99,11 @@ struct Level {
     // Galerkin as a fixed linear map of the fine values (this level coarse):
     // val[slot] = sum_t gmap_w[t] * fine.val[gmap_e[t]], t in [gmap_ptr[slot], gmap_ptr[slot+1])
     bool galg = false;
+    bool galg_half = false;               // map covers the upper triangle only (symmetric sources)
     DBuf<int32_t> gmap_ptr, gmap_e;
     DBuf<double> gmap_w;
+    DBuf<int32_t> gmap_diag;              // half map: slot of the diagonal per row
+    DBuf<int32_t> gmap_tpos;              // half map: slot of (J, I) for slot (I, J)
     // Galerkin v4 (this level coarse): coarse rows in groups of consecutive
     // gal_order rows; per group the distinct children (fine rows) and, for
     // every children-list entry, the child's index inside its group
@@ -213,7 +216,8 @@ int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, 
                  cudaStream_t s);
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);
 int launch_scatter_vec(const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
-int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s);
+int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s,
+                    bool symmetric);
 int galerkin_max_row();
 int galerkin4_capc();
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);

@@ -1535,17 +1535,21 @@ namespace {
 // lane l takes the slot's entries l, l+4, ... (map entries stream once,
 // evict-first), then a fixed-order shuffle reduction.  Deterministic.
 constexpr int kGmapLanes = 4;
+// HALF: the map holds the upper triangle (slots from the diagonal on); each
+// value is also stored at its transposed slot (symmetric sources).
+template <bool HALF>
 __global__ void __launch_bounds__(256) k_galerkin_map(int nc, const int* __restrict__ order, const int* __restrict__ crp,
                                                       const int* __restrict__ gptr, const int* __restrict__ ge,
                                                       const double* __restrict__ gw, const double* __restrict__ fval,
-                                                      double* __restrict__ cval) {
+                                                      double* __restrict__ cval, const int* __restrict__ diag,
+                                                      const int* __restrict__ tpos) {
     const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
     if (w >= nc) return;
     const int lane = threadIdx.x & 31;
     const int grp = lane / kGmapLanes;
     const int sl = lane & (kGmapLanes - 1);
     const int I = order[w];
-    const int s0 = crp[I], s1 = crp[I + 1];
+    const int s0 = HALF ? diag[I] : crp[I], s1 = crp[I + 1];
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (int sb = s0; sb < s1; sb += 32 / kGmapLanes) {
@@ -1571,16 +1575,26 @@ __global__ void __launch_bounds__(256) k_galerkin_map(int nc, const int* __restr
         }
 #pragma unroll
         for (int off = kGmapLanes / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, kGmapLanes);
-        if (slot < s1 && sl == 0) cval[slot] = acc;
+        if (slot < s1 && sl == 0) {
+            cval[slot] = acc;
+            if (HALF && slot != s0) cval[tpos[slot]] = acc;
+        }
     }
 }
 }  // namespace
 
-int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s) {
+int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s,
+                    bool symmetric) {
     const int nc = coarse.n;
-    if (coarse.galg) {
-        k_galerkin_map<<<(int)(((int64_t)nc * 32 + 255) / 256), 256, 0, s>>>(
-            nc, coarse.gal_order.p, coarse.rp.p, coarse.gmap_ptr.p, coarse.gmap_e.p, coarse.gmap_w.p, fval, cval);
+    if (coarse.galg && (symmetric || !coarse.galg_half)) {
+        const int grid = (int)(((int64_t)nc * 32 + 255) / 256);
+        if (coarse.galg_half)
+            k_galerkin_map<true><<<grid, 256, 0, s>>>(nc, coarse.gal_order.p, coarse.rp.p, coarse.gmap_ptr.p,
+                                                      coarse.gmap_e.p, coarse.gmap_w.p, fval, cval,
+                                                      coarse.gmap_diag.p, coarse.gmap_tpos.p);
+        else
+            k_galerkin_map<false><<<grid, 256, 0, s>>>(nc, coarse.gal_order.p, coarse.rp.p, coarse.gmap_ptr.p,
+                                                       coarse.gmap_e.p, coarse.gmap_w.p, fval, cval, nullptr, nullptr);
         return 1;
     }
     if (coarse.gal4_maxt > 0 && fine.prow_c.p) {

@@ -279,13 +279,15 @@ def test_launch_modes_agree(ora, monkeypatch):
         "nosmall": {"MG_SMALL_ROWS": "0"},
         "nogalmap": {"MG_GAL_MAP": "0"},
         "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
+        "galmap_full": {"MG_GAL_MAP_HALF": "0"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
     }
     out = {}
     for name, env in variants.items():
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
-                  "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB"):
+                  "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB",
+                  "MG_GAL_MAP_HALF"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
