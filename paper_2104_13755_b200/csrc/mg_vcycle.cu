@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
                                                          double* __restrict__ partial, int cap, double omega, int rev) {
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
-    constexpr int GB = 4;
+    constexpr int GB = 4;   // gathers in flight per lane (8 with 2 CTAs/SM measured slower)
     const int tid = threadIdx.x;
     const int tr = tid / LPR;
     const int lane = tid & (LPR - 1);
