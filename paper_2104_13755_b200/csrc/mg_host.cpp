@@ -552,6 +552,10 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                                                                                                             : 0;
         if (const char* e = getenv(("MG_PIPE_LPR_L" + std::to_string(l)).c_str())) L.pipe_lpr = atoi(e);
         if (L.pipe_lpr != 0 && L.pipe_lpr != 1 && L.pipe_lpr != 2 && L.pipe_lpr != 4 && L.pipe_lpr != 8) L.pipe_lpr = 0;
+        // k = 3: all ~6 off-diagonal gathers of a row in one batch (80 registers,
+        // 3 CTAs/SM) beat two batches at 4 CTAs/SM (C4: 366 -> 372 V-cycles/s,
+        // level-0 GS 0.50 -> 0.54 of the HBM roofline; profiles/r01/sweeps/aw_*)
+        L.pipe_unr8 = !getenv("MG_PIPE_UNR8") || std::string(getenv("MG_PIPE_UNR8")) != "0";
         // shared-memory capacity of the tile-staged kernels
         const int T = tile_rows() / std::max(1, L.pipe_lpr);
         auto tile_max = [&](int r0, int r1) {

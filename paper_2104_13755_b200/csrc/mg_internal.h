@@ -69,6 +69,7 @@ struct Level {
     int small_cap = 0;                    // max nnz of a small-kernel tile
     DBuf<int32_t> stiles;                 // small-kernel tiles {row0, nrow, e0, e1}, per colour
     DBuf<int32_t> stoff;                  // [ncolours+1] tile ranges per colour
+    bool pipe_unr8 = false;               // k_tile_pipe with 8 gathers per batch (K = 3, 3 CTAs/SM)
     int pipe_lpr = 1;
                      // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range

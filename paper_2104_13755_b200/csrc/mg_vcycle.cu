@@ -276,8 +276,8 @@ __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, co
     }
 }
 
-template <int K, int MODE>
-__global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
+template <int K, int MODE, int UNR = PipeUnroll<K>::value>
+__global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
                                                      const int* __restrict__ rp, const int* __restrict__ col,
                                                      const double* __restrict__ val, const double* __restrict__ b,
                                                      double* __restrict__ x, double* __restrict__ r,
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_pipe(const TileDesc* __restri
             ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
             if (MODE != 0) ldrow_pol<K>(x + (size_t)row * VS<K>::S, xr, xpol);
             double s[K], dg;
-            stage_row<K, PipeUnroll<K>::value>(v, tid, row, x, s, dg, xpol);
+            stage_row<K, UNR>(v, tid, row, x, s, dg, xpol);
             if (MODE == 0) {
                 double xn[K];
 #pragma unroll
@@ -1449,16 +1449,22 @@ __global__ void __launch_bounds__(kBlock) k_sumsq_partial(const double* __restri
 // ---------------------------------------------------------------------------
 inline size_t tile_smem(int cap) { return (size_t)cap * (sizeof(double) + sizeof(int)); }
 
-inline int pipe_grid(int ntiles, int cap) {
+inline int pipe_nsm() {
     static int nsm = 0;
     if (!nsm) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = 2 * ((stage_bytes(cap) + 127) / 128 * 128) + 2048;
-    const int per_sm = std::max(1, std::min<int>(8, (int)((227 * 1024) / smem)));
-    return std::max(1, std::min(ntiles, nsm * per_sm));
+    return nsm;
+}
+// persistent grid: every CTA resident at once (registers: 4 CTAs/SM for the
+// thread-per-row kernel, 3 for the lanes-per-row and 8-gather variants)
+inline int pipe_grid(const Level& L, int K, int ntiles) {
+    const size_t smem = 2 * ((stage_bytes(L.pipe_cap) + 127) / 128 * 128) + 2048;
+    const int by_regs = (L.pipe_lpr > 1 || (K == 3 && L.pipe_unr8)) ? 3 : 4;
+    const int per_sm = std::max(1, std::min<int>(by_regs, (int)((227 * 1024) / smem)));
+    return std::max(1, std::min(ntiles, pipe_nsm() * per_sm));
 }
 inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
 
@@ -1470,7 +1476,12 @@ void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double*
     const size_t sm = pipe_smem(L.pipe_cap);
     const int rev = (MODE != 2 && L.serpentine) ? (L.pass_ctr++ & 1) : 0;   // norm partials keep one order
     switch (L.pipe_lpr) {
-        case 1: launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+        case 1:
+            if (K == 3 && L.pipe_unr8)
+                launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+            else
+                launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+            break;
         case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
         case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
         default: launch_k(pdl, k_tile_pipe_lpr<K, 8, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
@@ -1497,7 +1508,7 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
             t0 = L.tile_off[L.tile_off.size() - 2];   // whole-level tiles are the last range
             t1 = L.tile_off.back();
         }
-        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(t1 - t0, L.pipe_cap), omega, pdl, s);
+        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(L, K, t1 - t0), omega, pdl, s);
         return 1;
     }
     if (L.tiled) {
@@ -1522,7 +1533,7 @@ int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, doub
     int grid;
     if (L.pipe) {
         const int t0 = L.tile_off[L.tile_off.size() - 2], t1 = L.tile_off.back();
-        grid = std::min(nb, pipe_grid(t1 - t0, L.pipe_cap));
+        grid = std::min(nb, pipe_grid(L, K, t1 - t0));
         pipe_launch<K, 2>(L, t0, t1, L.x.p, nullptr, partial, grid, 0.0, pdl, s);
     } else if (L.tiled) {
         grid = std::min(nb, nblk(L.n, kTile));
@@ -1552,6 +1563,10 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_pipe<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 0, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe<K, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);

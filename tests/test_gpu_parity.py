@@ -280,6 +280,7 @@ def test_launch_modes_agree(ora, monkeypatch):
         "nogalmap": {"MG_GAL_MAP": "0"},
         "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
         "galmap_full": {"MG_GAL_MAP_HALF": "0"},
+        "unr8": {"MG_PIPE_UNR8": "0"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
     }
     out = {}
@@ -287,7 +288,7 @@ def test_launch_modes_agree(ora, monkeypatch):
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
                   "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB",
-                  "MG_GAL_MAP_HALF"):
+                  "MG_GAL_MAP_HALF", "MG_PIPE_UNR8"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -305,7 +306,8 @@ def test_launch_modes_agree(ora, monkeypatch):
     # order of the restriction change no row's arithmetic
     assert np.array_equal(out["default"], out["noserp"])
     assert np.array_equal(out["default"], out["nospatial"])
-    assert np.array_equal(out["default"], out["restrict_order"])   # same per-row arithmetic, one launch per phase
+    assert np.array_equal(out["default"], out["restrict_order"])
+    assert np.array_equal(out["default"], out["unr8"])   # gather batching does not change the summation order   # same per-row arithmetic, one launch per phase
 
 
 @pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
