@@ -1900,12 +1900,21 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
     const int32_t n = L0.n;
     double* dXout = nullptr;
     if ((rc = prep_solve(c, k, B, X, &dXout))) return rc;
-    c->timed(PC_RESNORM, 0, s, [&] {
-        return vc_resnorm(k, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, false, s);
-    });
-    cudaError_t e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
-    if (!e) e = cudaStreamSynchronize(s);
-    if (e) return c->cuda_fail(e, "mg_solve");
+    cudaError_t e;
+    if (c->zero_guess && !c->dir) {
+        // x0 = 0: r0 = b exactly, so rho_0 = ||b|| / ||b|| = 1 (0 for b = 0)
+        e = cudaMemcpyAsync(c->h_rho, c->bnorm.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) return c->cuda_fail(e, "mg_solve");
+        for (int j = 0; j < k; ++j) c->h_rho[j] = c->h_rho[j] > 0.0 ? 1.0 : 0.0;
+    } else {
+        c->timed(PC_RESNORM, 0, s, [&] {
+            return vc_resnorm(k, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, false, s);
+        });
+        e = cudaMemcpyAsync(c->h_rho, c->rho.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) return c->cuda_fail(e, "mg_solve");
+    }
     cudaGraphExec_t exec = nullptr;
     if ((rc = get_vcycle_graph(c, k, &exec))) return rc;
     int32_t cyc = 0;

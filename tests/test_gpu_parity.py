@@ -701,8 +701,10 @@ def test_zero_guess(ora):
     check_x(X0, Xo)
     S.set_zero_guess(True)
     Xg = np.full_like(Bo, 1e30)
-    S.solve(Bo, Xg, rel_tol=0.0, max_cycles=3)
+    _, _, hz = S.solve(Bo, Xg, rel_tol=0.0, max_cycles=3)
     assert np.array_equal(Xg, X0)
+    assert np.all(hz[0] == 1.0)                        # r0 = b exactly: rho_0 = 1 without a residual pass
+    check_history(hz, ho, tau_floor(A.to_scipy(), Xo, Bo))
     Xd = torch.full(Bo.shape, float("nan"), dtype=torch.float64, device="cuda")
     S.solve(torch.from_numpy(Bo).cuda(), Xd, rel_tol=0.0, max_cycles=3)
     assert np.array_equal(Xd.cpu().numpy(), X0)
