@@ -865,6 +865,38 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         cudaError_t e = c->lv[l]->dcoff.upload(c->lv[l]->colour_off, s);
         if (e) return c->cuda_fail(e, "pattern upload");
     }
+    // small levels: all GS sweeps on one thread-block cluster (k_cluster_gs);
+    // CTA r of the cluster owns rows i = r (mod CS)
+    {
+        // opt-in: measured slower than one PDL launch per colour (2.6 vs 2.1 us
+        // per colour step at 16 CTAs; 8, 4, 2 CTAs no better — DESIGN.md §8)
+        const int cl_rows = getenv("MG_CLUSTER_GS_ROWS") ? atoi(getenv("MG_CLUSTER_GS_ROWS")) : 0;
+        int cs = cl_rows > 0 ? cluster_gs_max_cs() : 0;
+        if (const char* m = getenv("MG_CLUSTER_GS_CS")) cs = std::min(cs, atoi(m));
+        for (int l = 0; l < H; ++l) {
+            Level& L = *c->lv[l];
+            L.cl_cs = 0;
+            if (cs <= 0 || L.pipe || L.n > cl_rows || L.n < cs) continue;
+            const int stride = (L.n + cs - 1) / cs + 1;
+            std::vector<int32_t> crp((size_t)cs * stride, 0);
+            int nnz_max = 0;
+            for (int r = 0; r < cs; ++r) {
+                int acc = 0, q = 0;
+                for (int i = r; i < L.n; i += cs, ++q) {
+                    crp[(size_t)r * stride + q] = acc;
+                    acc += L.irp[i + 1] - L.irp[i];
+                }
+                crp[(size_t)r * stride + q] = acc;
+                nnz_max = std::max(nnz_max, acc);
+            }
+            cudaError_t e = L.cl_rp.upload(crp, s);
+            if (e) return c->cuda_fail(e, "pattern upload");
+            L.cl_cs = cs;
+            L.cl_stride = stride;
+            L.cl_nown_max = stride - 1;
+            L.cl_nnz_max = nnz_max;
+        }
+    }
     // coarsest dense factor storage
     const int nH = c->lv[H]->n;
     c->npad = (nH + 31) / 32 * 32;
@@ -975,6 +1007,10 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
     }
     if (L.small && mu > 0) {
         const int nl = vc_small_gs(K, L, mu, reverse, pdl, s);
+        if (nl > 0) return nl;
+    }
+    if (L.cl_cs > 0 && mu > 0) {
+        const int nl = vc_cluster_gs(K, L, mu, reverse, pdl, s);
         if (nl > 0) return nl;
     }
     for (int it = 0; it < mu; ++it)

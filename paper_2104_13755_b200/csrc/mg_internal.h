@@ -65,7 +65,10 @@ struct Level {
     mutable int pass_ctr = 0;             // pipelined launches enqueued on this level (serpentine direction)
     bool serpentine = true;               // alternate the tile walk direction between passes
     bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
-    bool small = false;                   // GS sweeps by the one-CTA shared-memory kernel
+    int cl_cs = 0;                        // cluster GS: CTAs per cluster (0: not used)
+    int cl_stride = 0, cl_nown_max = 0, cl_nnz_max = 0;
+    DBuf<int32_t> cl_rp;                  // [cl_cs][cl_stride] local row pointers of each CTA's own rows
+        bool small = false;                   // GS sweeps by the one-CTA shared-memory kernel
     int small_cap = 0;                    // max nnz of a small-kernel tile
     DBuf<int32_t> stiles;                 // small-kernel tiles {row0, nrow, e0, e1}, per colour
     DBuf<int32_t> stoff;                  // [ncolours+1] tile ranges per colour
@@ -173,6 +176,8 @@ int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long lon
 int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s);   // mu dataflow GS sweeps
 int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one CTA
 int small_rows_per_tile();
+int vc_cluster_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one cluster
+int cluster_gs_max_cs();
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
 int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
 int vc_prolong(int K, const Level& fine, const Level& coarse, bool pdl, cudaStream_t s);   // fine.x += P coarse.x

@@ -812,6 +812,186 @@ int launch_small_gs_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream
 }
 
 // ---------------------------------------------------------------------------
+// Small levels on one thread-block cluster: all mu GS sweeps of the level in
+// ONE launch of CS CTAs (16 where the device allows the non-portable size).
+// Every CTA holds a full replica of the level's iterate in shared memory and
+// the rows i = rank + q CS it owns (their A rows and b) — nothing but the
+// replica is read during the sweeps.  Per colour class each CTA updates its
+// own rows (8 lanes per row, entries l, l+8, ... as k_lpr_sweep<K,8>,
+// fixed-order shuffle reduction), writes the new values into its replica and
+// into every other CTA's replica with distributed-shared-memory stores, then
+// one barrier.cluster (release/acquire) separates colour classes — instead of
+// one dependent kernel launch and an L2 round trip per colour.
+constexpr int kCgThreads = 256;
+constexpr int kCgLPR = 8;
+
+__device__ __forceinline__ unsigned cg_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cg_size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cg_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cg_mapa(const void* p, unsigned cta) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void cg_st_remote(unsigned addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+
+// own rows of CTA r below row X: #{i < X : i = r (mod CS)}
+__device__ __forceinline__ int cg_count(int X, int r, int CS) { return X > r ? (X - r + CS - 1) / CS : 0; }
+
+template <int K>
+__host__ __device__ inline size_t cluster_gs_smem(int n, int nown_max, int nnz_own_max) {
+    size_t o = ((size_t)n * K * 8 + 15) / 16 * 16;               // replica of x
+    o += ((size_t)nnz_own_max * 8 + 15) / 16 * 16;                // own A values
+    o += ((size_t)nown_max * K * 8 + 15) / 16 * 16;               // own b
+    o += ((size_t)nnz_own_max * 4 + 15) / 16 * 16;                // own A columns
+    o += ((size_t)(nown_max + 1) * 4 + 15) / 16 * 16;             // own row pointers
+    return o;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kCgThreads, 1) k_cluster_gs(int n, int ncol, const int* __restrict__ coff,
+                                                              const int* __restrict__ rp, const int* __restrict__ col,
+                                                              const double* __restrict__ val,
+                                                              const double* __restrict__ b, double* __restrict__ x,
+                                                              const int* __restrict__ cl_rp, int cl_stride,
+                                                              int nown_max, int nnz_own_max, int mu, int reverse) {
+    constexpr int S = VS<K>::S;
+    constexpr int G = kCgLPR;
+    extern __shared__ __align__(16) unsigned char smem_cg[];
+    const int CS = (int)cg_size(), r = (int)cg_rank();
+    const int tid = threadIdx.x, grp = tid / G, lane = tid & (G - 1), ngrp = kCgThreads / G;
+    const int nown = cg_count(n, r, CS);
+    double* xs = reinterpret_cast<double*>(smem_cg);
+    size_t o = ((size_t)n * K * 8 + 15) / 16 * 16;
+    double* av = reinterpret_cast<double*>(smem_cg + o);
+    o += ((size_t)nnz_own_max * 8 + 15) / 16 * 16;
+    double* bs = reinterpret_cast<double*>(smem_cg + o);
+    o += ((size_t)nown_max * K * 8 + 15) / 16 * 16;
+    int* ac = reinterpret_cast<int*>(smem_cg + o);
+    o += ((size_t)nnz_own_max * 4 + 15) / 16 * 16;
+    int* lrp = reinterpret_cast<int*>(smem_cg + o);
+    const int* grp_rp = cl_rp + (size_t)r * cl_stride;
+    pdl_launch_dependents();
+    // own rows of A (constant during the solve) before the dependency wait
+    for (int q = tid; q <= nown; q += kCgThreads) lrp[q] = grp_rp[q];
+    for (int q = grp; q < nown; q += ngrp) {
+        const int i = r + q * CS;
+        const int e0 = rp[i], len = rp[i + 1] - e0, base = grp_rp[q];
+        for (int t = lane; t < len; t += G) {
+            ac[base + t] = col[e0 + t];
+            av[base + t] = val[e0 + t];
+        }
+    }
+    pdl_wait();
+    for (int i = tid; i < n; i += kCgThreads) {
+        double v[K];
+        ldrow<K>(x + (size_t)i * S, v);
+#pragma unroll
+        for (int k = 0; k < K; ++k) xs[(size_t)i * K + k] = v[k];
+    }
+    for (int q = tid; q < nown; q += kCgThreads) {
+        double v[K];
+        ldrow<K>(b + (size_t)(r + q * CS) * S, v);
+#pragma unroll
+        for (int k = 0; k < K; ++k) bs[(size_t)q * K + k] = v[k];
+    }
+    cg_sync();   // every replica loaded before any CTA writes into it
+    const unsigned gmask = group_mask(G);
+    for (int step = 0; step < mu * ncol; ++step) {
+        const int c = reverse ? ncol - 1 - step % ncol : step % ncol;
+        const int q0 = cg_count(__ldg(coff + c), r, CS), q1 = cg_count(__ldg(coff + c + 1), r, CS);
+        for (int q = q0 + grp; q < q1; q += ngrp) {
+            const int i = r + q * CS;
+            double sacc[K], dg = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) sacc[k] = 0.0;
+            for (int t = lrp[q] + lane; t < lrp[q + 1]; t += G) {
+                const int j = ac[t];
+                const double a = av[t];
+                if (j == i) {
+                    dg += a;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) sacc[k] = fma(a, xs[(size_t)j * K + k], sacc[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) sacc[k] = group_sum<G>(sacc[k], gmask);
+            dg = group_sum<G>(dg, gmask);
+            double xn[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) xn[k] = (bs[(size_t)q * K + k] - sacc[k]) / dg;
+            // lane l writes the replicas of CTAs l, l + 8 (its own one locally)
+            for (int d = lane; d < CS; d += G) {
+                if (d == r) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) xs[(size_t)i * K + k] = xn[k];
+                } else {
+                    const unsigned ra = cg_mapa(xs + (size_t)i * K, (unsigned)d);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) cg_st_remote(ra + 8u * k, xn[k]);
+                }
+            }
+        }
+        cg_sync();
+    }
+    for (int q = tid; q < nown; q += kCgThreads) {
+        const int i = r + q * CS;
+        double v[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = xs[(size_t)i * K + k];
+        strow<K>(x + (size_t)i * S, v);
+    }
+}
+
+template <int K>
+int launch_cluster_gs_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    const size_t smem = cluster_gs_smem<K>(L.n, L.cl_nown_max, L.cl_nnz_max);
+    if (smem > 220 * 1024 || L.cl_cs <= 0) return -1;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cluster_gs<K>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k_cluster_gs<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.cl_cs);
+    cfg.blockDim = dim3(kCgThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = L.cl_cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cluster_gs<K>, L.n, L.ncolours, (const int*)L.dcoff.p,
+                                             (const int*)L.rp.p, (const int*)L.col.p, (const double*)L.val.p,
+                                             (const double*)L.b.p, L.x.p, (const int*)L.cl_rp.p, L.cl_stride,
+                                             L.cl_nown_max, L.cl_nnz_max, mu, reverse ? 1 : 0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return 1;
+}
+
+// ---------------------------------------------------------------------------
 // LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
 // prefetches up to U = 32/LPR (col, val) of its row in the PDL prologue;
 // after the wait its x gathers go out in batches of GB independent loads.
@@ -1625,6 +1805,37 @@ int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream
     }
 }
 int small_rows_per_tile() { return kSmallRows; }
+int vc_cluster_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (launch_cluster_gs_k<KK>(L, mu, reverse, pdl, s)))
+}
+int cluster_gs_max_cs() {
+    static int cs = -1;
+    if (cs < 0) {
+        cs = 0;
+        cudaFuncSetAttribute(k_cluster_gs<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k_cluster_gs<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        for (int c : {16, 8}) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(c);
+            cfg.blockDim = dim3(kCgThreads);
+            cfg.dynamicSmemBytes = 200 * 1024;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = c;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, k_cluster_gs<3>, &cfg) == cudaSuccess && ncl >= 1) {
+                cs = c;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    return cs;
+}
 int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (launch_small_gs_k<KK>(L, mu, reverse, pdl, s)))
 }

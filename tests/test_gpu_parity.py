@@ -281,6 +281,8 @@ def test_launch_modes_agree(ora, monkeypatch):
         "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
         "galmap_full": {"MG_GAL_MAP_HALF": "0"},
         "unr8": {"MG_PIPE_UNR8": "0"},
+        "cluster_gs": {"MG_CLUSTER_GS_ROWS": "4608"},
+        "cluster_gs8": {"MG_CLUSTER_GS_ROWS": "100000", "MG_CLUSTER_GS_CS": "8"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
     }
     out = {}
@@ -288,7 +290,8 @@ def test_launch_modes_agree(ora, monkeypatch):
         for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
                   "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB",
-                  "MG_GAL_MAP_HALF", "MG_PIPE_UNR8"):
+                  "MG_GAL_MAP_HALF", "MG_PIPE_UNR8", "MG_CLUSTER_GS_ROWS",
+                  "MG_CLUSTER_GS_CS"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
