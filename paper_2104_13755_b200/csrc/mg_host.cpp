@@ -359,6 +359,13 @@ struct mg_ctx {
     cudaGraphExec_t vc_exec[kMaxK + 1] = {};
     int vc_launches[kMaxK + 1] = {};
     cudaGraphExec_t pcg_exec[kMaxK + 1] = {};   // one MG-PCG iteration (row f4)
+    cudaGraphExec_t loop_exec[kMaxK + 1] = {};  // whole solve: conditional WHILE node around the V-cycle
+    int loop_check_launches = 1;
+    bool device_loop = true;                    // MG_DEVICE_LOOP
+    DBuf<LoopState> loop_st;
+    DBuf<double> loop_hist;
+    LoopState* h_loop = nullptr;                // pinned
+    double* h_hist = nullptr;                   // pinned, kLoopHistCycles * kMaxK
     int pcg_launches[kMaxK + 1] = {};
     DBuf<double> pcg_x, pcg_r, pcg_p, pcg_q, pcg_partial, pcg_sc;
     DBuf<int> pcg_first;
@@ -400,6 +407,10 @@ struct mg_ctx {
             if (pcg_exec[k]) {
                 cudaGraphExecDestroy(pcg_exec[k]);
                 pcg_exec[k] = nullptr;
+            }
+            if (loop_exec[k]) {
+                cudaGraphExecDestroy(loop_exec[k]);
+                loop_exec[k] = nullptr;
             }
             for (auto* v : {&graph_ev[k], &pcg_graph_ev[k]}) {
                 for (auto& ev : *v) {
@@ -472,6 +483,8 @@ struct mg_ctx {
         }
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (h_rho) cudaFreeHost(h_rho);
+        if (h_loop) cudaFreeHost(h_loop);
+        if (h_hist) cudaFreeHost(h_hist);
         if (cap) cudaStreamDestroy(cap);
         if (own_stream && stream) cudaStreamDestroy(stream);
     }
@@ -1113,6 +1126,55 @@ int get_vcycle_graph(mg_ctx* c, int K, cudaGraphExec_t* out) {
     return MG_OK;
 }
 
+// Whole solve as one graph: a conditional WHILE node whose body is one
+// V-cycle + residual norm + k_loop_check (which records rho and sets the
+// condition).  The node's condition defaults to 1 at every launch; the host
+// launches it only when at least one cycle is due.
+int get_loop_graph(mg_ctx* c, int K, cudaGraphExec_t* out) {
+    if (c->loop_exec[K]) {
+        *out = c->loop_exec[K];
+        return MG_OK;
+    }
+    cudaError_t e;
+    if ((e = c->loop_st.alloc(1)) || (e = c->loop_hist.alloc((size_t)(kLoopHistCycles + 1) * kMaxK)))
+        return c->cuda_fail(e, "loop graph alloc");
+    cudaGraph_t g;
+    if ((e = cudaGraphCreate(&g, 0))) return c->cuda_fail(e, "loop graph");
+    cudaGraphConditionalHandle h;
+    e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if (!e) e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
+    if (e) {
+        cudaGraphDestroy(g);
+        return c->cuda_fail(e, "loop graph conditional node");
+    }
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(c->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e) {
+        cudaGraphDestroy(g);
+        return c->cuda_fail(e, "loop graph capture");
+    }
+    const int64_t before = c->launches;
+    c->capturing = true;
+    enqueue_vcycle(c, K, c->cap);
+    c->capturing = false;
+    c->launches += vc_loop_check(K, c->rho.p, c->loop_st.p, c->loop_hist.p, h, c->cap);
+    c->vc_launches[K] = (int)(c->launches - before) - 1;
+    c->launches = before;
+    cudaGraph_t body_out = body;
+    e = cudaStreamEndCapture(c->cap, &body_out);
+    if (!e) e = cudaGraphInstantiate(&c->loop_exec[K], g, 0);
+    cudaGraphDestroy(g);
+    if (e) return c->cuda_fail(e, "loop graph instantiate");
+    *out = c->loop_exec[K];
+    return MG_OK;
+}
+
 // One MG-PCG iteration (row f4) on level-0 internal vectors:
 // z = V(0, r) with the symmetric V-cycle, then the PCG direction and step,
 // then rho = |r| / |b| copied to the host.
@@ -1210,9 +1272,12 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     if (const char* m = getenv("MG_FLOW_ROWS")) c->flow_rows = atoll(m);
     if (const char* m = getenv("MG_GS_PERSIST")) c->gs_persist = std::string(m) == "1";
+    if (const char* m = getenv("MG_DEVICE_LOOP")) c->device_loop = std::string(m) != "0";
     c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess) {
+        cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess ||
+        cudaMallocHost(&c->h_loop, sizeof(LoopState)) != cudaSuccess ||
+        cudaMallocHost(&c->h_hist, sizeof(double) * kLoopHistCycles * kMaxK) != cudaSuccess) {
         delete c;
         return MG_ERR_CUDA;
     }
@@ -1951,11 +2016,49 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
         if (!e) e = cudaStreamSynchronize(s);
         if (e) return c->cuda_fail(e, "mg_solve");
     }
-    cudaGraphExec_t exec = nullptr;
-    if ((rc = get_vcycle_graph(c, k, &exec))) return rc;
     int32_t cyc = 0;
     int status = MG_NOT_CONVERGED;
-    while (true) {
+    // device-side loop: one graph launch and one synchronisation per solve
+    // (per-cycle host round trips otherwise; profiling keeps the host loop)
+    const bool dloop = c->device_loop && !c->prof_mask && max_cycles <= kLoopHistCycles;
+    if (dloop) {
+        bool finite = true, done = rel_tol > 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double r = c->h_rho[j];
+            if (res_hist) res_hist[j] = r;
+            finite &= std::isfinite(r);
+            done &= (r <= rel_tol);
+        }
+        if (!finite) {
+            status = MG_ERR_NUMERIC;
+        } else if (done) {
+            status = MG_OK;
+        } else if (max_cycles > 0) {
+            cudaGraphExec_t lexec = nullptr;
+            if ((rc = get_loop_graph(c, k, &lexec))) return rc;
+            c->h_loop->tol = rel_tol;
+            c->h_loop->max_cycles = max_cycles;
+            c->h_loop->cyc = 0;
+            c->h_loop->status = 0;
+            e = cudaMemcpyAsync(c->loop_st.p, c->h_loop, sizeof(LoopState), cudaMemcpyHostToDevice, s);
+            if (!e) e = cudaGraphLaunch(lexec, s);
+            if (!e) e = cudaMemcpyAsync(c->h_loop, c->loop_st.p, sizeof(LoopState), cudaMemcpyDeviceToHost, s);
+            if (!e)
+                e = cudaMemcpyAsync(c->h_hist, c->loop_hist.p + k, sizeof(double) * (size_t)max_cycles * k,
+                                    cudaMemcpyDeviceToHost, s);
+            if (!e) e = cudaStreamSynchronize(s);
+            if (e) return c->cuda_fail(e, "mg_solve V-cycle loop");
+            cyc = c->h_loop->cyc;
+            c->launches += (int64_t)cyc * (c->vc_launches[k] + c->loop_check_launches);
+            if (res_hist)
+                for (int t = 1; t <= cyc; ++t)
+                    for (int j = 0; j < k; ++j) res_hist[(size_t)t * k + j] = c->h_hist[(size_t)(t - 1) * k + j];
+            status = c->h_loop->status == 2 ? MG_ERR_NUMERIC : c->h_loop->status == 1 ? MG_OK : MG_NOT_CONVERGED;
+        }
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (!dloop && (rc = get_vcycle_graph(c, k, &exec))) return rc;
+    while (!dloop) {
         bool finite = true, done = rel_tol > 0.0;
         for (int j = 0; j < k; ++j) {
             const double r = c->h_rho[j];

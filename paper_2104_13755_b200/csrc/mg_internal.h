@@ -166,6 +166,16 @@ struct TailParams {
     TailLevel lv[kTailMaxLevels];
 };
 
+// Device-side state of the V-cycle loop (mg_solve with the conditional graph).
+struct LoopState {
+    double tol;
+    int max_cycles;
+    int cyc;       // cycles run
+    int status;    // 0 running / budget spent, 1 converged, 2 non-finite
+    int pad;
+};
+constexpr int kLoopHistCycles = 4096;   // device history capacity (cycles)
+
 // Launch helpers.  All enqueue on `s` and return the number of kernel
 // launches issued.  `pdl`: launch with programmatic stream serialisation
 // (V-cycle graph).
@@ -176,6 +186,7 @@ int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long lon
 int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s);   // mu dataflow GS sweeps
 int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one CTA
 int small_rows_per_tile();
+int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGraphConditionalHandle h, cudaStream_t s);
 int vc_cluster_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one cluster
 int cluster_gs_max_cs();
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x

@@ -1804,6 +1804,40 @@ int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream
         default: return launch_gs_flow_kk<4>(L, mu, reverse, err, s);
     }
 }
+// Device-side V-cycle loop (conditional WHILE graph node): after each cycle's
+// residual norm this kernel records rho into the history, applies mg_solve's
+// stopping rule (non-finite -> stop; every column rho <= tol -> stop; cycle
+// budget spent -> stop) and sets the loop condition, so a whole solve is one
+// graph launch and one host synchronisation.
+template <int K>
+__global__ void k_loop_check(const double* __restrict__ rho, LoopState* st, double* __restrict__ hist,
+                             cudaGraphConditionalHandle h) {
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    const int cyc = st->cyc + 1;
+    st->cyc = cyc;
+    bool finite = true, done = st->tol > 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const double r = rho[j];
+        hist[(size_t)cyc * K + j] = r;
+        finite &= isfinite(r);
+        done &= r <= st->tol;
+    }
+    st->status = !finite ? 2 : done ? 1 : 0;
+    cudaGraphSetConditional(h, (finite && !done && cyc < st->max_cycles) ? 1u : 0u);
+}
+
+int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGraphConditionalHandle h, cudaStream_t s) {
+    switch (K) {
+        case 1: k_loop_check<1><<<1, 32, 0, s>>>(rho, st, hist, h); break;
+        case 2: k_loop_check<2><<<1, 32, 0, s>>>(rho, st, hist, h); break;
+        case 3: k_loop_check<3><<<1, 32, 0, s>>>(rho, st, hist, h); break;
+        default: k_loop_check<4><<<1, 32, 0, s>>>(rho, st, hist, h); break;
+    }
+    return 1;
+}
+
 int small_rows_per_tile() { return kSmallRows; }
 int vc_cluster_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (launch_cluster_gs_k<KK>(L, mu, reverse, pdl, s)))

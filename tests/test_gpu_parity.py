@@ -281,6 +281,7 @@ def test_launch_modes_agree(ora, monkeypatch):
         "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
         "galmap_full": {"MG_GAL_MAP_HALF": "0"},
         "unr8": {"MG_PIPE_UNR8": "0"},
+        "hostloop": {"MG_DEVICE_LOOP": "0"},
         "cluster_gs": {"MG_CLUSTER_GS_ROWS": "4608"},
         "cluster_gs8": {"MG_CLUSTER_GS_ROWS": "100000", "MG_CLUSTER_GS_CS": "8"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
@@ -291,7 +292,7 @@ def test_launch_modes_agree(ora, monkeypatch):
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
                   "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB",
                   "MG_GAL_MAP_HALF", "MG_PIPE_UNR8", "MG_CLUSTER_GS_ROWS",
-                  "MG_CLUSTER_GS_CS"):
+                  "MG_CLUSTER_GS_CS", "MG_DEVICE_LOOP"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -310,7 +311,8 @@ def test_launch_modes_agree(ora, monkeypatch):
     assert np.array_equal(out["default"], out["noserp"])
     assert np.array_equal(out["default"], out["nospatial"])
     assert np.array_equal(out["default"], out["restrict_order"])
-    assert np.array_equal(out["default"], out["unr8"])   # gather batching does not change the summation order   # same per-row arithmetic, one launch per phase
+    assert np.array_equal(out["default"], out["unr8"])
+    assert np.array_equal(out["default"], out["hostloop"])   # device-side cycle loop == host loop   # gather batching does not change the summation order   # same per-row arithmetic, one launch per phase
 
 
 @pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
@@ -718,3 +720,30 @@ def test_zero_guess(ora):
     S.solve_pcg(Bo, P0, rel_tol=0.0, max_iters=3)
     assert np.array_equal(P1, P0)
     S.close()
+
+
+def test_device_loop_matches_host_loop(ora, monkeypatch):
+    """The device-side cycle loop (conditional graph node, one launch per
+    solve) applies mg_solve's stopping rule exactly like the host loop: same
+    cycle count, bitwise-identical history and iterate, for a tolerance stop,
+    a cycle-budget stop and a zero budget."""
+    p = meshgen.make_config(4, subdiv=5)
+    A, M, mgo = oracle_problem(ora, p)
+    Bo = oracle_rhs(ora, p, M)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MG_DEVICE_LOOP", mode)
+        S = gpu_solver(p)
+        S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+        out = []
+        for tol, mc in ((1e-8, 50), (1e-30, 4), (1e-8, 0)):
+            X = np.zeros_like(Bo)
+            rc, cyc, h = S.solve(Bo, X, rel_tol=tol, max_cycles=mc)
+            out.append((rc, cyc, h.copy(), X.copy()))
+        res[mode] = out
+        S.close()
+    for a, b in zip(res["1"], res["0"]):
+        assert a[0] == b[0] and a[1] == b[1]
+        assert np.array_equal(a[2], b[2])
+        assert np.array_equal(a[3], b[3])
+    assert res["1"][1][1] == 4 and res["1"][2][1] == 0
