@@ -361,7 +361,7 @@ struct mg_ctx {
     cudaGraphExec_t pcg_exec[kMaxK + 1] = {};   // one MG-PCG iteration (row f4)
     cudaGraphExec_t loop_exec[kMaxK + 1] = {};  // whole solve: conditional WHILE node around the V-cycle
     int loop_check_launches = 1;
-    bool device_loop = true;                    // MG_DEVICE_LOOP
+    bool device_loop = false;                   // MG_DEVICE_LOOP=1 (opt-in: ncu does not see kernels inside conditional nodes)
     DBuf<LoopState> loop_st;
     DBuf<double> loop_hist;
     LoopState* h_loop = nullptr;                // pinned

@@ -281,7 +281,7 @@ def test_launch_modes_agree(ora, monkeypatch):
         "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
         "galmap_full": {"MG_GAL_MAP_HALF": "0"},
         "unr8": {"MG_PIPE_UNR8": "0"},
-        "hostloop": {"MG_DEVICE_LOOP": "0"},
+        "deviceloop": {"MG_DEVICE_LOOP": "1"},
         "cluster_gs": {"MG_CLUSTER_GS_ROWS": "4608"},
         "cluster_gs8": {"MG_CLUSTER_GS_ROWS": "100000", "MG_CLUSTER_GS_CS": "8"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
@@ -312,7 +312,7 @@ def test_launch_modes_agree(ora, monkeypatch):
     assert np.array_equal(out["default"], out["nospatial"])
     assert np.array_equal(out["default"], out["restrict_order"])
     assert np.array_equal(out["default"], out["unr8"])
-    assert np.array_equal(out["default"], out["hostloop"])   # device-side cycle loop == host loop   # gather batching does not change the summation order   # same per-row arithmetic, one launch per phase
+    assert np.array_equal(out["default"], out["deviceloop"])   # device-side cycle loop == host loop   # gather batching does not change the summation order   # same per-row arithmetic, one launch per phase
 
 
 @pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])

@@ -25,7 +25,7 @@ def main():
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     per = []
     for r in rows[2:]:
-        if "k_tile_pipe<3, 0>" in r[ik] or "k_tile_pipe<(int)3, (int)0>" in r[ik]:
+        if "k_tile_pipe<3, 0>" in r[ik] or "k_tile_pipe<3, 0, " in r[ik] or "k_tile_pipe<(int)3, (int)0" in r[ik]:
             per.append(float(r[ir].replace(",", "")) * scale[units[ir]] + float(r[iw].replace(",", "")) * scale[units[iw]])
     if not per:
         sys.exit("no k_tile_pipe<3, 0> launch in the report")
@@ -35,7 +35,7 @@ def main():
                   "ncu flushes the caches before every replayed kernel, so these are COLD-cache numbers: the gathered "
                   "iterate x (84 MB) comes from DRAM instead of L2 as it does inside the timed V-cycle; the "
                   "algorithmic bytes per launch are 69.9 MB (config 4)." % os.path.relpath(rep, ROOT),
-        "config4": {"kernel": "k_tile_pipe<3,0> (level-0 GS colour pass)", "per_launch_bytes": per,
+        "config4": {"kernel": "k_tile_pipe<3,0,8> (level-0 GS colour pass)", "per_launch_bytes": per,
                     "gs_sweep_level0_bytes_per_launch": sum(per) / len(per)},
     }
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
