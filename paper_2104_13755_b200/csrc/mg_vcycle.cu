@@ -1248,13 +1248,15 @@ int launch_gs_flow_kk(const Level& L, int mu, bool reverse, int* err, cudaStream
 // vertices (transpose of P): deterministic, no atomics.  G lanes per coarse
 // row; children indices and weights prefetched before the wait.  Zeroes the
 // coarse iterate (the recursive V-cycle starts from 0).
-constexpr int kRestrictG = 16;
-template <int K>
+constexpr int kRestrictG = 8;   // measured: 8 lanes x 4 prefetched children beat 16 x 2 (C4 L0 225 -> 191 us/cycle)
+// G lanes per coarse row, U = 32 / G children per lane prefetched before the
+// PDL wait; after it every lane issues its U residual gathers at once.
+template <int K, int G>
 __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cptr, const int* __restrict__ cidx,
                                                      const double* __restrict__ cw, const double* __restrict__ r,
                                                      double* __restrict__ bc, double* __restrict__ xc, int nc,
                                                      const int* __restrict__ order) {
-    constexpr int G = kRestrictG;
+    constexpr int U = 32 / G;
     const int g = (blockIdx.x * kBlock + threadIdx.x) / G;
     const int lane = threadIdx.x & (G - 1);
     pdl_launch_dependents();
@@ -1262,19 +1264,18 @@ __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cpt
     // coarse rows in locality order (all colours interleaved): the children's
     // residual rows are then gathered from a small spatial window (L2 hits)
     const int I = active ? (order ? order[g] : g) : 0;
-    int t0 = 0, t1 = 0, i0 = -1, i1 = -1;
-    double w0 = 0.0, w1 = 0.0;
+    int t0 = 0, t1 = 0;
+    int ii[U];
+    double ww[U];
     if (active) {
         t0 = cptr[I];
         t1 = cptr[I + 1];
-        if (t0 + lane < t1) {
-            i0 = cidx[t0 + lane];
-            w0 = cw[t0 + lane];
-        }
-        if (t0 + lane + G < t1) {
-            i1 = cidx[t0 + lane + G];
-            w1 = cw[t0 + lane + G];
-        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int t = t0 + lane + u * G;
+        ii[u] = (active && t < t1) ? cidx[t] : -1;
+        ww[u] = (active && t < t1) ? cw[t] : 0.0;
     }
     pdl_wait();
     if (!active) return;
@@ -1282,19 +1283,16 @@ __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cpt
     double s[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = 0.0;
-    if (i0 >= 0) {
-        double rv[K];
-        ldrow<K>(r + (size_t)i0 * VS<K>::S, rv);
+    double rv[U][K];
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = fma(w0, rv[c], s[c]);
-    }
-    if (i1 >= 0) {
-        double rv[K];
-        ldrow<K>(r + (size_t)i1 * VS<K>::S, rv);
+    for (int u = 0; u < U; ++u)
+        if (ii[u] >= 0) ldrow<K>(r + (size_t)ii[u] * VS<K>::S, rv[u]);
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = fma(w1, rv[c], s[c]);
-    }
-    for (int t = t0 + lane + 2 * G; t < t1; t += G) {
+    for (int u = 0; u < U; ++u)
+        if (ii[u] >= 0)
+#pragma unroll
+            for (int c = 0; c < K; ++c) s[c] = fma(ww[u], rv[u][c], s[c]);
+    for (int t = t0 + lane + U * G; t < t1; t += G) {
         const int i = cidx[t];
         const double w = cw[t];
 #pragma unroll
@@ -1880,9 +1878,14 @@ int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 1>(L, 0, L.n, L.r.p, pdl, s)))
 }
 int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s) {
-    MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK>, nblk((int64_t)C.n * kRestrictG, kBlock), kBlock, 0, s, C.cptr.p,
-                             C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n,
-                             C.restrict_ordered ? (const int*)C.gal_order.p : nullptr), 1))
+    static const int G = getenv("MG_RESTRICT_G") ? atoi(getenv("MG_RESTRICT_G")) : kRestrictG;
+    const int* ord = C.restrict_ordered ? (const int*)C.gal_order.p : nullptr;
+    switch (G) {
+        case 4: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 4>, nblk((int64_t)C.n * 4, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 8: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 16: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 16>, nblk((int64_t)C.n * 16, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        default: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+    }
 }
 int vc_prolong(int K, const Level& F, const Level& C, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (launch_k(pdl, k_prolong<KK>, nblk(F.n, kBlock), kBlock, 0, s, F.pc.p, F.pw.p, C.x.p, F.x.p, F.n), 1))

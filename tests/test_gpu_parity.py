@@ -282,6 +282,8 @@ def test_launch_modes_agree(ora, monkeypatch):
         "galmap_full": {"MG_GAL_MAP_HALF": "0"},
         "unr8": {"MG_PIPE_UNR8": "0"},
         "deviceloop": {"MG_DEVICE_LOOP": "1"},
+        "restrict16": {"MG_RESTRICT_G": "16"},
+        "restrict4": {"MG_RESTRICT_G": "4"},
         "cluster_gs": {"MG_CLUSTER_GS_ROWS": "4608"},
         "cluster_gs8": {"MG_CLUSTER_GS_ROWS": "100000", "MG_CLUSTER_GS_CS": "8"},
         "small_all": {"MG_SMALL_ROWS": "100000"},
@@ -292,7 +294,8 @@ def test_launch_modes_agree(ora, monkeypatch):
                   "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
                   "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB",
                   "MG_GAL_MAP_HALF", "MG_PIPE_UNR8", "MG_CLUSTER_GS_ROWS",
-                  "MG_CLUSTER_GS_CS", "MG_DEVICE_LOOP"):
+                  "MG_CLUSTER_GS_CS", "MG_DEVICE_LOOP",
+                  "MG_RESTRICT_G"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
