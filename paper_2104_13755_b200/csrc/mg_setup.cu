@@ -1280,7 +1280,7 @@ __device__ __forceinline__ void cg_trinv32_warp(const double (*S)[33], const dou
     for (int i = 0; i < 32; ++i) Li[i][lane] = xv[i];
 }
 
-__device__ void cg_factor_diag(double (*S)[33], double (*Li)[33], double* Dkk, double* Linvk, double* Wkk, int npad,
+__device__ __noinline__ void cg_factor_diag(double (*S)[33], double (*Li)[33], double* Dkk, double* Linvk, double* Wkk, int npad,
                                int* err) {
     __shared__ double colb[40], rdg[32];
     cg_chol32_warp(S, colb, rdg, err);
