@@ -552,17 +552,37 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         // batches); optionally pipelined tiles with pipe_lpr lanes per row for
         // longer rows (tiles of kTile / pipe_lpr rows); lanes-per-row otherwise
         const double tile_avg = getenv("MG_TILE_MAX_AVG") ? atof(getenv("MG_TILE_MAX_AVG")) : 12.0;
-        // Measured on B200 (profiles/r01, sweep r01ah): 2 lanes per row win on
-        // config 4's level 1 (avg 17.5 nnz/row, 38k rows per colour: GS 3.72 ->
-        // 3.17 ms/step); on smaller colour classes the untiled LPR kernels'
-        // wider grids win, and 4 or 8 lanes lose everywhere.
-        const double plpr_avg = getenv("MG_PIPE_LPR_MAX_AVG") ? atof(getenv("MG_PIPE_LPR_MAX_AVG")) : 20.0;
-        const double plpr_rows = getenv("MG_PIPE_LPR_MIN_ROWS") ? atof(getenv("MG_PIPE_LPR_MIN_ROWS")) : 32768.0;
-        const int plpr = getenv("MG_PIPE_LPR") ? atoi(getenv("MG_PIPE_LPR")) : 2;
+        // Pipelined lanes-per-row tiles (tiles of 256 / LPR rows) for the
+        // Galerkin-fill levels with large colour classes.  Measured on B200
+        // (profiles/r01/sweeps ah_*, bh_*): the most lanes per row that keep
+        // the largest colour pass within one wave of resident CTAs (3 per SM)
+        // win — C4 level 1 (38k rows/colour) LPR 2, C3 level 1 (15k) LPR 4,
+        // C4 level 2 / C5 level 1 (9-10k) LPR 8; below ~6000 rows per colour
+        // the untiled k_lpr_sweep's wider grids win.  MG_PIPE_LPR (+ _MAX_AVG,
+        // _MIN_ROWS) forces one width, MG_PIPE_LPR_L<l> one level.
+        const double plpr_avg = getenv("MG_PIPE_LPR_MAX_AVG") ? atof(getenv("MG_PIPE_LPR_MAX_AVG")) : 40.0;
+        const double plpr_rows = getenv("MG_PIPE_LPR_MIN_ROWS") ? atof(getenv("MG_PIPE_LPR_MIN_ROWS")) : 6000.0;
+        int max_colour = 0;
+        for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k)
+            max_colour = std::max(max_colour, L.colour_off[k + 1] - L.colour_off[k]);
         const double colour_rows = (double)L.n / std::max(1, (int)L.colour_off.size() - 1);
-        L.pipe_lpr = avg <= tile_avg ? 1
-                     : (avg <= plpr_avg && colour_rows >= plpr_rows && (plpr == 2 || plpr == 4 || plpr == 8)) ? plpr
-                                                                                                            : 0;
+        int auto_lpr = 0;
+        if (avg > tile_avg && avg <= plpr_avg && colour_rows >= plpr_rows) {
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+            const int resident = 3 * nsm;
+            for (int w : {8, 4, 2})
+                if ((max_colour + tile_rows() / w - 1) / (tile_rows() / w) <= resident) {
+                    auto_lpr = w;
+                    break;
+                }
+        }
+        if (const char* e = getenv("MG_PIPE_LPR")) {
+            const int plpr = atoi(e);
+            auto_lpr = (avg > tile_avg && avg <= plpr_avg && colour_rows >= plpr_rows &&
+                        (plpr == 2 || plpr == 4 || plpr == 8)) ? plpr : 0;
+        }
+        L.pipe_lpr = avg <= tile_avg ? 1 : auto_lpr;
         if (const char* e = getenv(("MG_PIPE_LPR_L" + std::to_string(l)).c_str())) L.pipe_lpr = atoi(e);
         if (L.pipe_lpr != 0 && L.pipe_lpr != 1 && L.pipe_lpr != 2 && L.pipe_lpr != 4 && L.pipe_lpr != 8) L.pipe_lpr = 0;
         // k = 3: all ~6 off-diagonal gathers of a row in one batch (80 registers,
