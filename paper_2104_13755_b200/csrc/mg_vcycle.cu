@@ -1878,7 +1878,7 @@ int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 1>(L, 0, L.n, L.r.p, pdl, s)))
 }
 int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s) {
-    static const int G = getenv("MG_RESTRICT_G") ? atoi(getenv("MG_RESTRICT_G")) : kRestrictG;
+    const int G = getenv("MG_RESTRICT_G") ? atoi(getenv("MG_RESTRICT_G")) : kRestrictG;
     const int* ord = C.restrict_ordered ? (const int*)C.gal_order.p : nullptr;
     switch (G) {
         case 4: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 4>, nblk((int64_t)C.n * 4, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
