@@ -843,6 +843,27 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             // (measured: C4 level 0 -> 1 +3%, C3 level 0 -> 1 -8%)
             C.restrict_ordered = getenv("MG_RESTRICT_ORDER") ? std::string(getenv("MG_RESTRICT_ORDER")) != "0"
                                                             : L.n >= 1500000;
+            // ordered restriction: children lists laid out in the visiting
+            // order (contiguous list reads, no order[] indirection before them)
+            C.rcptr.release();
+            C.rcidx.release();
+            C.rcw.release();
+            if (C.restrict_ordered) {
+                std::vector<int32_t> optr(C.n + 1, 0), oidx(cidx.size());
+                std::vector<double> ow(cidx.size());
+                for (int32_t g = 0; g < C.n; ++g) {
+                    const int32_t I = order[g];
+                    int32_t o = optr[g];
+                    for (int32_t t = cnt[I]; t < cnt[I + 1]; ++t, ++o) {
+                        oidx[o] = cidx[t];
+                        ow[o] = cw[t];
+                    }
+                    optr[g + 1] = o;
+                }
+                if ((e = C.rcptr.upload(optr, s)) || (e = C.rcidx.upload(oidx, s)) || (e = C.rcw.upload(ow, s)))
+                    return c->cuda_fail(e, "pattern upload");
+                cudaStreamSynchronize(s);
+            }
         }
     }
     // L2 residency of the fine iterate: a persisting access-policy window over

@@ -65,6 +65,8 @@ struct Level {
     mutable int pass_ctr = 0;             // pipelined launches enqueued on this level (serpentine direction)
     bool serpentine = true;               // alternate the tile walk direction between passes
     bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
+    DBuf<int32_t> rcptr, rcidx;           // children lists in gal_order (ordered restriction)
+    DBuf<double> rcw;
     int cl_cs = 0;                        // cluster GS: CTAs per cluster (0: not used)
     int cl_stride = 0, cl_nown_max = 0, cl_nnz_max = 0;
     DBuf<int32_t> cl_rp;                  // [cl_cs][cl_stride] local row pointers of each CTA's own rows

@@ -1263,13 +1263,16 @@ __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cpt
     const bool active = g < nc;
     // coarse rows in locality order (all colours interleaved): the children's
     // residual rows are then gathered from a small spatial window (L2 hits)
+    // ordered mode: the lists (cptr, cidx, cw) are already in visiting order
+    // g; order[g] only names the output row
     const int I = active ? (order ? order[g] : g) : 0;
+    const int L = order ? g : I;
     int t0 = 0, t1 = 0;
     int ii[U];
     double ww[U];
     if (active) {
-        t0 = cptr[I];
-        t1 = cptr[I + 1];
+        t0 = cptr[L];
+        t1 = cptr[L + 1];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1879,12 +1882,16 @@ int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
 }
 int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s) {
     const int G = getenv("MG_RESTRICT_G") ? atoi(getenv("MG_RESTRICT_G")) : kRestrictG;
-    const int* ord = C.restrict_ordered ? (const int*)C.gal_order.p : nullptr;
+    const bool ordered = C.restrict_ordered && C.rcptr.p;
+    const int* ord = ordered ? (const int*)C.gal_order.p : nullptr;
+    const int* cp = ordered ? (const int*)C.rcptr.p : (const int*)C.cptr.p;
+    const int* ci = ordered ? (const int*)C.rcidx.p : (const int*)C.cidx.p;
+    const double* cwp = ordered ? (const double*)C.rcw.p : (const double*)C.cw.p;
     switch (G) {
-        case 4: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 4>, nblk((int64_t)C.n * 4, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
-        case 8: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
-        case 16: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 16>, nblk((int64_t)C.n * 16, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
-        default: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, C.cptr.p, C.cidx.p, C.cw.p, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 4: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 4>, nblk((int64_t)C.n * 4, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 8: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 16: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 16>, nblk((int64_t)C.n * 16, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        default: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
     }
 }
 int vc_prolong(int K, const Level& F, const Level& C, bool pdl, cudaStream_t s) {
