@@ -270,6 +270,12 @@ int mg_set_profiling(mg_ctx* ctx, int class_mask);
 int mg_get_profile(mg_ctx* ctx, double* ms, int64_t* launches);
 /* Device kernel launches issued by this context since creation. */
 int64_t mg_launch_count(const mg_ctx* ctx);
+/* Shape of the loaded problem, for argument checking by bindings: *n_full =
+ * fine vertices of the hierarchy as loaded (the row count of every user-side
+ * B, X, V; Dirichlet constraints do not change it), *device = the CUDA device
+ * the context enqueues on.  Either pointer may be NULL.  MG_ERR_STATE before
+ * mg_hierarchy_load. */
+int mg_problem_size(const mg_ctx* ctx, int32_t* n_full, int32_t* device);
 
 #ifdef __cplusplus
 }

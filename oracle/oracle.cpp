@@ -30,6 +30,7 @@
 // synthetic configs are parity unpinned (the paper prints none).
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -301,7 +302,16 @@ struct MG {
     int symmetric = 0;                            // 1: post-relaxation in reverse colour order
     std::vector<double> Lfac;                     // dense Cholesky factor of A_H
     int status = 0;
+    // wall-clock phase times in seconds (timing only, for bench.py's CPU
+    // baseline: SURVEY §8(d.6)); [0] Galerkin (symbolic + numeric, all
+    // levels), [1] colouring + classes, [2] coarsest Cholesky, [3] V-cycles
+    // and [4] residual norms of the last ora_mg_solve
+    double phase_s[5] = {0, 0, 0, 0, 0};
 };
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 void build_classes(Level& L) {
     L.classes.assign(L.ncolours, {});
@@ -489,17 +499,22 @@ ora_mg* ora_mg_new(int32_t n_levels, const int32_t* n_verts, const int32_t* cons
     mg->mu_post = mu_post;
     mg->lv.resize(n_levels);
     mg->lv[0].A = *A0;
+    double t0 = now_s();
     for (int l = 0; l + 1 < n_levels; ++l) {
         Csr* P = ora_prolongation(n_verts[l], n_verts[l + 1], P_cols[l], P_w[l]);
         mg->lv[l].P = *P;
         delete P;
         mg->lv[l + 1].A = galerkin(mg->lv[l].P, mg->lv[l].A);
     }
+    double t1 = now_s();
+    mg->phase_s[0] = t1 - t0;
     for (auto& L : mg->lv) {
         L.colour.resize(L.A.nrows);
         L.ncolours = greedy_colouring(L.A, L.colour.data());
         build_classes(L);
     }
+    t0 = now_s();
+    mg->phase_s[1] = t0 - t1;
     const Csr& AH = mg->lv.back().A;
     const int32_t nH = AH.nrows;
     std::vector<double> D((size_t)nH * nH, 0.0);
@@ -507,8 +522,10 @@ ora_mg* ora_mg_new(int32_t n_levels, const int32_t* n_verts, const int32_t* cons
         for (int64_t e = AH.rowptr[i]; e < AH.rowptr[i + 1]; ++e) D[(size_t)i * nH + AH.col[e]] = AH.val[e];
     mg->Lfac.assign((size_t)nH * nH, 0.0);
     mg->status = dense_cholesky(nH, D.data(), mg->Lfac.data());
+    mg->phase_s[2] = now_s() - t0;
     return mg;
 }
+void ora_mg_phase_times(const ora_mg* mg, double* out) { std::memcpy(out, mg->phase_s, sizeof(mg->phase_s)); }
 void ora_mg_free(ora_mg* mg) { delete mg; }
 int ora_mg_status(const ora_mg* mg) { return mg->status; }
 int32_t ora_mg_levels(const ora_mg* mg) { return (int32_t)mg->lv.size(); }
@@ -540,7 +557,10 @@ int ora_mg_solve(ora_mg* mg, int32_t k, const double* B, double* X, double rel_t
     for (int32_t i = 0; i < A.nrows; ++i)
         for (int c = 0; c < k; ++c) bnorm[c] += B[(size_t)i * k + c] * B[(size_t)i * k + c];
     for (int c = 0; c < k; ++c) bnorm[c] = std::sqrt(bnorm[c]);
+    double tn = now_s();
     residual_norms(A, k, B, X, bnorm, hist);
+    mg->phase_s[3] = 0.0;
+    mg->phase_s[4] = now_s() - tn;
     int32_t cyc = 0;
     auto done = [&](const double* rho) {
         if (!(rel_tol > 0.0)) return false;
@@ -557,9 +577,13 @@ int ora_mg_solve(ora_mg* mg, int32_t k, const double* B, double* X, double rel_t
     if (bad(hist)) rc = 7;
     else if (done(hist)) rc = 0;
     while (rc == 8 && cyc < max_cycles) {
+        const double tv = now_s();
         vcycle(*mg, 0, k, B, X);
         ++cyc;
+        const double tr = now_s();
         residual_norms(A, k, B, X, bnorm, hist + (size_t)cyc * k);
+        mg->phase_s[3] += tr - tv;
+        mg->phase_s[4] += now_s() - tr;
         if (bad(hist + (size_t)cyc * k)) rc = 7;
         else if (done(hist + (size_t)cyc * k)) rc = 0;
     }
@@ -625,7 +649,7 @@ int ora_mg_pcg(ora_mg* mg, int32_t k, const double* B, double* X, double rel_tol
         for (size_t t = 0; t < nk; ++t) rz_new[t % k] += r[t] * z[t];
         for (size_t t = 0; t < nk; ++t) {
             const int c = (int)(t % k);
-            const double beta = it == 0 ? 0.0 : rz_new[c] / rz[c];
+            const double beta = (it == 0 || rz[c] == 0.0) ? 0.0 : rz_new[c] / rz[c];   // reading A27
             p[t] = z[t] + beta * p[t];
         }
         rz = rz_new;
@@ -637,7 +661,7 @@ int ora_mg_pcg(ora_mg* mg, int32_t k, const double* B, double* X, double rel_tol
             }
         for (size_t t = 0; t < nk; ++t) {
             const int c = (int)(t % k);
-            const double alpha = rz[c] / pq[c];
+            const double alpha = pq[c] == 0.0 ? 0.0 : rz[c] / pq[c];   // reading A27: solved column
             X[t] += alpha * p[t];
             r[t] -= alpha * q[t];
         }

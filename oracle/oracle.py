@@ -20,13 +20,24 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 CXXFLAGS = ["-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
 
+def _src_hash():
+    import hashlib
+    with open(_SRC, "rb") as f:
+        return hashlib.sha256(" ".join(CXXFLAGS).encode() + f.read()).hexdigest()
+
+
 def build(force=False):
-    """Compile the oracle (g++, single-threaded, no FMA contraction; reading A18)."""
-    if not force and os.path.exists(_LIB) and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC):
+    """Compile the oracle (g++, single-threaded, no FMA contraction; reading
+    A18).  Rebuilt whenever the source hash recorded beside the library differs."""
+    hfile = _LIB + ".sha256"
+    h = _src_hash()
+    if not force and os.path.exists(_LIB) and os.path.exists(hfile) and open(hfile).read().strip() == h:
         return _LIB
     tmp = _LIB + f".tmp{os.getpid()}"
     subprocess.check_call(["g++", *CXXFLAGS, _SRC, "-o", tmp])
     os.replace(tmp, _LIB)
+    with open(hfile, "w") as f:
+        f.write(h + "\n")
     return _LIB
 
 
@@ -71,6 +82,7 @@ def lib():
             "ora_mg_solve": (C.c_int, [_vp, C.c_int32, _f64p, _f64p, C.c_double, C.c_int32, _f64p,
                                        C.POINTER(C.c_int32)]),
             "ora_mg_set_smoother": (None, [_vp, C.c_int32, C.c_double, C.c_int32]),
+            "ora_mg_phase_times": (None, [_vp, _f64p]),
             "ora_jacobi_sweep": (None, [_vp, C.c_int32, _f64p, _f64p, C.c_double]),
             "ora_mg_pcg": (C.c_int, [_vp, C.c_int32, _f64p, _f64p, C.c_double, C.c_int32, _f64p,
                                      C.POINTER(C.c_int32)]),
@@ -271,6 +283,14 @@ class MG:
         colour = np.empty(n.value, np.int32)
         lib().ora_mg_level_export(self.h, l, rp, col, val, colour)
         return dict(n=n.value, nnz=nnz.value, ncolours=nc.value, rowptr=rp, col=col, val=val, colour=colour)
+
+    def phase_times(self):
+        """Wall-clock seconds of the setup phases (Galerkin symbolic + numeric,
+        colouring, coarsest Cholesky) and of the last solve (V-cycles, residual
+        norms).  Timing only (bench.py's CPU baseline)."""
+        t = np.zeros(5)
+        lib().ora_mg_phase_times(self.h, t)
+        return dict(zip(("galerkin_s", "colouring_s", "cholesky_s", "vcycles_s", "norms_s"), map(float, t)))
 
     def coarse_factor(self):
         n = self.level(self.n_levels - 1)["n"]

@@ -27,11 +27,28 @@ def _sources():
         [os.path.join(CSRC, "mg_internal.h"), os.path.join(CSRC, "mg_common.cuh"), os.path.join(INC, "mg.h")]
 
 
+def source_hash():
+    """sha256 over every source, header and the compile flags: the library is
+    rebuilt whenever this differs from the hash recorded beside it (file
+    mtimes do not survive the copy to the GPU box reliably)."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(" ".join(NVCC_FLAGS + CU_SOURCES + CPP_SOURCES).encode())
+    for s in _sources():
+        with open(s, "rb") as f:
+            h.update(os.path.basename(s).encode())
+            h.update(f.read())
+    return h.hexdigest()
+
+
+HASH_FILE = LIB + ".sha256"
+
+
 def up_to_date():
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(HASH_FILE)):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(s) <= t for s in _sources())
+    with open(HASH_FILE) as f:
+        return f.read().strip() == source_hash()
 
 
 def build(force=False, verbose=False):
@@ -53,6 +70,8 @@ def build(force=False, verbose=False):
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)
+    with open(HASH_FILE, "w") as f:
+        f.write(source_hash() + "\n")
     return LIB
 
 

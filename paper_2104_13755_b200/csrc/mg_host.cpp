@@ -293,6 +293,7 @@ struct mg_ctx {
 
     bool have_pattern = false;
     uint64_t pattern_hash = 0;
+    std::vector<int32_t> pat_rp, pat_cl;   // the last validated user CSR pattern (pattern_kind 0)
     int pattern_kind = -1;   // 0 user CSR, 1 cotan 1-ring
     bool have_matrix = false;
     bool have_mass = false;
@@ -1607,7 +1608,9 @@ static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* ro
     uint64_t h = fnv1a(1469598103934665603ULL, rp.data(), rp.size() * 4);
     h = fnv1a(h, cl.data(), cl.size() * 4);
     h = fnv1a(h, &c->dir_version, sizeof(c->dir_version));
-    if (c->have_pattern && c->pattern_kind == 0 && c->pattern_hash == h) return MG_OK;
+    // the hash only selects the candidate: the stored pattern is compared in full
+    if (c->have_pattern && c->pattern_kind == 0 && c->pattern_hash == h && rp == c->pat_rp && cl == c->pat_cl)
+        return MG_OK;
     if (rp[0] != 0 || rp[n] != nnz) return c->fail(MG_ERR_INPUT, "row_ptr[0] must be 0 and row_ptr[n] == nnz");
     for (int32_t i = 0; i < n; ++i) {
         if (rp[i + 1] < rp[i]) return c->fail(MG_ERR_INPUT, "row_ptr not monotone at row %d", i);
@@ -1626,12 +1629,14 @@ static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* ro
                 return c->fail(MG_ERR_INPUT, "pattern not structurally symmetric at (%d, %d)", i, j);
         }
     if (c->dir_all) return MG_OK;   // every vertex known: nothing to factor
-    if (!c->have_pattern || c->pattern_kind != 0 || c->pattern_hash != h) {
+    if (!c->have_pattern || c->pattern_kind != 0 || c->pattern_hash != h || rp != c->pat_rp || cl != c->pat_cl) {
         c->have_pattern = false;
         rc = c->dir ? dir_pattern(c, rp, cl) : setup_pattern(c, rp, cl);
         if (rc) return rc;
         c->pattern_hash = h;
         c->pattern_kind = 0;
+        c->pat_rp = std::move(rp);
+        c->pat_cl = std::move(cl);
     }
     return MG_OK;
 }
@@ -2048,7 +2053,10 @@ int mg_solve(mg_ctx* c, int32_t k, const double* B, double* X, double rel_tol, i
         e = cudaMemcpyAsync(c->h_rho, c->bnorm.p, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
         if (!e) e = cudaStreamSynchronize(s);
         if (e) return c->cuda_fail(e, "mg_solve");
-        for (int j = 0; j < k; ++j) c->h_rho[j] = c->h_rho[j] > 0.0 ? 1.0 : 0.0;
+        for (int j = 0; j < k; ++j) {   // a non-finite |b| stays non-finite: MG_ERR_NUMERIC below
+            const double bn = c->h_rho[j];
+            c->h_rho[j] = std::isfinite(bn) ? (bn > 0.0 ? 1.0 : 0.0) : bn;
+        }
     } else {
         c->timed(PC_RESNORM, 0, s, [&] {
             return vc_resnorm(k, L0, c->partial.p, resnorm_blocks(n), c->bnorm.p, c->rho.p, false, s);
@@ -2330,5 +2338,13 @@ int mg_get_profile(mg_ctx* c, double* ms, int64_t* launches) {
 }
 
 int64_t mg_launch_count(const mg_ctx* c) { return c ? c->launches : 0; }
+
+int mg_problem_size(const mg_ctx* c, int32_t* n_full, int32_t* device) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (device) *device = c->device;
+    if (c->H < 0) return MG_ERR_STATE;
+    if (n_full) *n_full = c->n_full;
+    return MG_OK;
+}
 
 }  // extern "C"

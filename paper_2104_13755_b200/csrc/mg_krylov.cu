@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_beta(const double* __restrict__ 
         const bool f = *first != 0;
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-            sc[K + c] = f ? 0.0 : rz[c] / sc[c];
+            sc[K + c] = (f || sc[c] == 0.0) ? 0.0 : rz[c] / sc[c];   // reading A27
             sc[c] = rz[c];
         }
         *first = 0;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_alpha(const double* __restrict__
     finalize_sum<K>(partial, nb, pq);
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int c = 0; c < K; ++c) sc[2 * K + c] = sc[c] / pq[c];
+        for (int c = 0; c < K; ++c) sc[2 * K + c] = pq[c] == 0.0 ? 0.0 : sc[c] / pq[c];   // reading A27: solved column
 }
 
 template <int K>

@@ -71,6 +71,7 @@ def lib():
             "mg_set_profiling": (C.c_int, [_vp, C.c_int]),
             "mg_get_profile": (C.c_int, [_vp, _vp, _vp]),
             "mg_launch_count": (i64, [_vp]),
+            "mg_problem_size": (C.c_int, [_vp, _vp, _vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -94,6 +95,31 @@ def _ptr(a, dtype):
     if a.dtype != tdt or not a.is_contiguous():
         raise TypeError(f"expected contiguous {tdt} tensor, got {a.dtype}")
     return a.data_ptr()
+
+
+def mg_problem_size(ctx):
+    """(n_full, device) of the loaded hierarchy."""
+    n, dev = C.c_int32(), C.c_int32()
+    _check(ctx, lib().mg_problem_size(ctx, C.byref(n), C.byref(dev)))
+    return n.value, dev.value
+
+
+def _check_rows(ctx, a, k, name):
+    """The C side cannot see extents: B / X / V must be (n_full, k) (or (n_full,)
+    for k = 1), and a CUDA tensor must live on the context's device."""
+    if a is None:
+        return
+    n, dev = mg_problem_size(ctx)
+    shape = tuple(a.shape)
+    if not (shape == (n, k) or (k == 1 and shape == (n,))):
+        raise ValueError(f"{name}: expected shape ({n}, {k}), got {shape}")
+    if not isinstance(a, np.ndarray) and getattr(a, "is_cuda", False) and a.device.index != dev:
+        raise ValueError(f"{name}: tensor on cuda:{a.device.index}, context on cuda:{dev}")
+
+
+def _check_len(a, count, name):
+    if a is not None and int(np.prod(a.shape)) < count:
+        raise ValueError(f"{name}: needs at least {count} entries, got {int(np.prod(a.shape))}")
 
 
 def _check(ctx, rc, allow=()):
@@ -150,20 +176,28 @@ def mg_hierarchy_load(ctx, levels, P):
 
 
 def mg_set_matrix(ctx, n, nnz, row_ptr, col, val, on_device=0):
+    _check_len(row_ptr, n + 1, "row_ptr")
+    _check_len(col, nnz, "col")
+    _check_len(val, nnz, "val")
     return _check(ctx, lib().mg_set_matrix(ctx, int(n), int(nnz), _ptr(row_ptr, np.int32), _ptr(col, np.int32),
                                            _ptr(val, np.float64), int(on_device)))
 
 
 def mg_set_matrix_cotan(ctx, V, mass_coeff, lap_coeff):
+    _check_rows(ctx, V, 3, "V")
     return _check(ctx, lib().mg_set_matrix_cotan(ctx, _ptr(V, np.float64), float(mass_coeff), float(lap_coeff)))
 
 
 def mg_set_matrix_split(ctx, n, nnz, row_ptr, col, q_val, m_val):
+    _check_len(row_ptr, n + 1, "row_ptr")
+    for a, nm in ((col, "col"), (q_val, "q_val"), (m_val, "m_val")):
+        _check_len(a, nnz, nm)
     return _check(ctx, lib().mg_set_matrix_split(ctx, int(n), int(nnz), _ptr(row_ptr, np.int32), _ptr(col, np.int32),
                                                  _ptr(q_val, np.float64), _ptr(m_val, np.float64)))
 
 
 def mg_set_matrix_split_cotan(ctx, V):
+    _check_rows(ctx, V, 3, "V")
     return _check(ctx, lib().mg_set_matrix_split_cotan(ctx, _ptr(V, np.float64)))
 
 
@@ -172,12 +206,17 @@ def mg_set_alpha(ctx, alpha):
 
 
 def mg_apply_mass(ctx, k, X, B):
+    _check_rows(ctx, X, k, "X")
+    _check_rows(ctx, B, k, "B")
     return _check(ctx, lib().mg_apply_mass(ctx, int(k), _ptr(X, np.float64), _ptr(B, np.float64)))
 
 
 def mg_solve(ctx, k, B, X, rel_tol, max_cycles, res_hist=None):
     """Returns (status, cycles); status MG_OK or MG_NOT_CONVERGED (others raise).
     res_hist: optional float64 numpy array of (max_cycles+1)*k entries."""
+    _check_rows(ctx, B, k, "B")
+    _check_rows(ctx, X, k, "X")
+    _check_len(res_hist, (int(max_cycles) + 1) * int(k), "res_hist")
     cyc = C.c_int32(0)
     rc = lib().mg_solve(ctx, int(k), _ptr(B, np.float64), _ptr(X, np.float64), float(rel_tol), int(max_cycles),
                         _ptr(res_hist, np.float64), C.byref(cyc))
@@ -186,6 +225,7 @@ def mg_solve(ctx, k, B, X, rel_tol, max_cycles, res_hist=None):
 
 
 def mg_set_matrix_bilaplacian(ctx, V, mass_coeff, bilap_coeff):
+    _check_rows(ctx, V, 3, "V")
     return _check(ctx, lib().mg_set_matrix_bilaplacian(ctx, _ptr(V, np.float64), float(mass_coeff), float(bilap_coeff)))
 
 
@@ -207,6 +247,9 @@ def mg_set_zero_guess(ctx, on=True):
 
 def mg_solve_pcg(ctx, k, B, X, rel_tol, max_iters, res_hist=None):
     """MG-preconditioned CG; returns (status, iterations)."""
+    _check_rows(ctx, B, k, "B")
+    _check_rows(ctx, X, k, "X")
+    _check_len(res_hist, (int(max_iters) + 1) * int(k), "res_hist")
     it = C.c_int32(0)
     rc = lib().mg_solve_pcg(ctx, int(k), _ptr(B, np.float64), _ptr(X, np.float64), float(rel_tol), int(max_iters),
                             _ptr(res_hist, np.float64), C.byref(it))

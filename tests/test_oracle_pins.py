@@ -605,6 +605,26 @@ def test_pcg_special_cases_and_dense_solve(ora):
     assert rc == 0 and hist.shape[0] == 1 and not X.any()
 
 
+def test_pcg_solved_column_stays_solved(ora):
+    """Reading A27: a column whose residual is already zero (b = 0, x0 = 0)
+    has nothing left for CG to do; with alpha = beta = 0 it stays exactly 0
+    and the other columns follow exactly their single-column CG iterates
+    (the columns of CG are independent)."""
+    p = meshgen.make_config(2, subdiv=4)
+    V, F = p.levels[0]
+    A, _ = ora.assemble(V, F, 1.0, 1e-2)
+    n = V.shape[0]
+    b = np.random.default_rng(14).standard_normal((n, 1))
+    mg = ora.MG(p.sizes, p.P, A)
+    B3 = np.ascontiguousarray(np.concatenate([b, np.zeros((n, 1)), 3.0 * b], axis=1))
+    X3, h3, rc = mg.pcg(B3, rel_tol=0.0, max_iters=4)
+    X1, h1, _ = mg.pcg(b, rel_tol=0.0, max_iters=4)
+    assert rc == 0 and np.all(np.isfinite(X3)) and not X3[:, 1].any()
+    assert np.array_equal(X3[:, 0], X1[:, 0])
+    assert np.linalg.norm(X3[:, 2] - 3.0 * X1[:, 0]) <= 1e-13 * np.linalg.norm(3.0 * X1[:, 0])
+    assert np.all(h3[:, 1] == 0.0)
+
+
 def test_pcg_energy_error_decreases(ora):
     """CG theory: the A-norm error decreases monotonically per iteration."""
     p = meshgen.make_config(3, grid=(48, 40))
