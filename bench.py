@@ -89,7 +89,7 @@ def vcycle_bytes(levels, k, mu=4):
     return tot
 
 
-def level_rooflines(breakdown, levels, k, cycles, peak):
+def level_rooflines(breakdown, levels, k, cycles, peak, rebuilds=1):
     """Achieved GB/s and fraction of the HBM peak per level for the GS sweeps
     (4 sweeps per cycle) and the Galerkin product, from the per-class event
     breakdown of one step (bench's separate profiled pass)."""
@@ -107,7 +107,7 @@ def level_rooflines(breakdown, levels, k, cycles, peak):
         if str(l) in gal:
             t = gal[str(l)]["ms"] / 1e3
             nc, nnzc = levels[l + 1]
-            b = level_bytes(n, nnz) + 36 * n + 12 * nnzc + 4 * nc
+            b = rebuilds * (level_bytes(n, nnz) + 36 * n + 12 * nnzc + 4 * nc)
             row["galerkin_GBps"] = round(b / t / 1e9, 1)
             row["galerkin_frac"] = round(b / t / 1e9 / peak, 3)
         out[str(l)] = row
@@ -656,7 +656,7 @@ def run_mg(args):
                             "achieved_GBps": vc_bytes / (mean_solve / mean_cyc / 1e3) / 1e9 if mean_cyc else None,
                             "frac": (vc_bytes / (mean_solve / mean_cyc / 1e3) / 1e9) / peak if mean_cyc else None},
         "galerkin_bytes": galerkin_bytes(levels_nnz),
-        "level_rooflines": level_rooflines(breakdown, levels_nnz, k, mean_cyc, peak),
+        "level_rooflines": level_rooflines(breakdown, levels_nnz, k, mean_cyc, peak, rebuilds=nsub),
         "breakdown_ms": breakdown,
         "setup_s_first_call": t_setup,
     }

@@ -84,6 +84,12 @@ __device__ __forceinline__ void ldrow(const double* p, double (&v)[K]) {
         asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
     }
 }
+// 32-byte read-only load (one sector, 256-bit): packed {w0, w1, w2, 0} P rows
+__device__ __forceinline__ double4 ldg_d4(const double4* p) {
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint64_t evict_last_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));

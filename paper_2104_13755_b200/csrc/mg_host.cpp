@@ -116,113 +116,149 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
     }
 }
 
-// 63-bit Morton key of each vertex in its level's bounding box.
-// Galerkin map (numeric P^T A P as a fixed linear map of the fine values; see
-// load_csr_pattern): for coarse slot (I, J) the entries (e, w_iI w_jJ) over
-// children i of I (children-list order), nonzeros e = (i, j) of fine row i
-// (CSR order) and parents J of j (ELL order).  Built in parallel over coarse
-// rows (count, prefix, fill); false if a level would exceed 2^31 entries.
-bool build_galerkin_map(const Level& L, const Level& C, const std::vector<int32_t>& cptr,
-                        const std::vector<int32_t>& cidx, const std::vector<double>& cw,
-                        const std::vector<int32_t>& pc, const std::vector<double>& pw, bool half,
-                        std::vector<int32_t>& gptr, std::vector<int32_t>& ge, std::vector<double>& gw,
-                        std::vector<int32_t>& diag, std::vector<int32_t>& tpos) {
+// Structure of the numeric Galerkin kernel k_galerkin_t (mg_setup.cu), built
+// once per pattern from integer data only (P's columns, the fine and coarse
+// patterns); every value it multiplies is read at run time.  With
+// T = A_l P_l (fine rows x coarse columns),
+//   (P^T A P)_IJ = sum_{i child of I} w_iI T_iJ,   T_iJ = sum_{j in row i} a_ij w_jJ.
+// * T-pattern of fine row i: the distinct parents J (w_jJ != 0) of the
+//   columns j of row i, in first-occurrence order over (nonzero, parent q);
+//   tlen[i] = its length (<= kGalTMax); per fine nonzero e, tp[e] packs the
+//   T-position of parent q of col[e] in bits 5q..5q+4 (31: w == 0, skip).
+// * groups: consecutive coarse rows of gal_order (locality order) whose
+//   distinct children (fine rows, U) fit one CTA; per group the U list.
+// * per coarse row r (gal_order position) its children entries
+//   (local index in U << 2 | parent slot q of I in the child's P row) in the
+//   children-list order, and per entry the slot in row I of every T-position
+//   of the child (one byte each, rows <= 255 entries).
+struct GalT {
+    int tcap = 0;                         // 16 or 32; 0: structure does not fit (generic kernel)
+    std::vector<uint16_t> tp;             // [fine nnz]
+    std::vector<uint8_t> tlen;            // [fine n]
+    std::vector<int32_t> grows, guoff, U; // groups: gal_order offsets, U offsets, U rows
+    std::vector<int32_t> cptr, soff;      // [nc + 1] in gal_order: children entries, slot-code bytes
+    std::vector<uint16_t> cl;             // children entries
+    std::vector<uint8_t> codes;           // slot codes
+    int max_m = 0;
+};
+constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-bit fields
+constexpr int kGalUCap = 256;             // distinct children per group (one phase-1 thread each)
+constexpr int kGalClCap = 2048;           // children entries per group (staged in shared memory)
+constexpr int kGalCodeCap = 12288;        // slot-code bytes per group (staged in shared memory)
+
+bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>& pc, const std::vector<double>& pw,
+                      const std::vector<int32_t>& cptr, const std::vector<int32_t>& cidx,
+                      const std::vector<int32_t>& order, GalT& G) {
     const int32_t n = L.n, nc = C.n;
-    std::vector<uint8_t> npar(n);
-    for (int32_t j = 0; j < n; ++j)
-        npar[j] = (uint8_t)((pw[j] != 0.0) + (pw[(size_t)n + j] != 0.0) + (pw[2 * (size_t)n + j] != 0.0));
-    std::vector<int64_t> roff((size_t)nc + 1, 0);
-    const unsigned hw = std::thread::hardware_concurrency();
-    const int nth = (int)std::max(1u, std::min(hw ? hw : 1u, 64u));
-    auto parallel_rows = [&](auto&& body) {
-        std::atomic<int32_t> next(0);
-        auto worker = [&]() {
-            for (;;) {
-                const int32_t a = next.fetch_add(2048);
-                if (a >= nc) break;
-                const int32_t b = std::min(nc, a + 2048);
-                for (int32_t I = a; I < b; ++I) body(I);
-            }
-        };
-        std::vector<std::thread> th;
-        for (int t = 1; t < nth; ++t) th.emplace_back(worker);
-        worker();
-        for (auto& t : th) t.join();
-    };
-    parallel_rows([&](int32_t I) {
-        int64_t k = 0;
-        for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
-            const int32_t i = cidx[t];
-            for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
-                const int32_t j = L.icol[e];
-                if (!half) {
-                    k += npar[j];
-                    continue;
-                }
-                for (int q = 0; q < 3; ++q)
-                    if (pw[(size_t)q * n + j] != 0.0 && pc[(size_t)q * n + j] >= I) ++k;
-            }
-        }
-        roff[(size_t)I + 1] = k;
-    });
-    for (int32_t I = 0; I < nc; ++I) roff[(size_t)I + 1] += roff[I];
-    if (roff[nc] > (int64_t)INT32_MAX) return false;
-    gptr.assign((size_t)C.nnz + 1, 0);
-    ge.resize((size_t)roff[nc]);
-    gw.resize((size_t)roff[nc]);
-    struct Q {
-        int32_t slot, e;
-        double w;
-    };
-    parallel_rows([&](int32_t I) {
-        thread_local std::vector<Q> tmp;
-        thread_local std::vector<int32_t> cntl;
-        const int32_t s0 = C.irp[I], s1 = C.irp[I + 1];
-        tmp.clear();
-        for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
-            const int32_t i = cidx[t];
-            const double wI = cw[t];
-            for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
-                const int32_t j = L.icol[e];
-                for (int q = 0; q < 3; ++q) {
-                    const double wJ = pw[(size_t)q * n + j];
-                    if (wJ == 0.0) continue;
+    G = GalT();
+    G.tp.assign((size_t)std::max<int64_t>(L.nnz, 1), 0);
+    G.tlen.assign((size_t)n, 0);
+    // T-patterns of the fine rows (kept on the host for the slot codes)
+    std::vector<int64_t> toff((size_t)n + 1, 0);
+    std::vector<int32_t> tj;
+    tj.reserve((size_t)n * 12);
+    int maxt = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        const size_t t0 = tj.size();
+        for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
+            const int32_t j = L.icol[e];
+            uint32_t code = 0;
+            for (int q = 0; q < 3; ++q) {
+                uint32_t pos = 31;
+                if (pw[(size_t)q * n + j] != 0.0) {
                     const int32_t J = pc[(size_t)q * n + j];
-                    if (half && J < I) continue;
-                    const int32_t* pos = std::lower_bound(C.icol.data() + s0, C.icol.data() + s1, J);
-                    tmp.push_back({(int32_t)(pos - C.icol.data()) - s0, e, wI * wJ});
+                    size_t k = t0;
+                    while (k < tj.size() && tj[k] != J) ++k;
+                    if (k == tj.size()) tj.push_back(J);
+                    pos = (uint32_t)std::min<size_t>(k - t0, 31);
+                }
+                code |= pos << (5 * q);
+            }
+            G.tp[e] = (uint16_t)code;
+        }
+        const int len = (int)(tj.size() - t0);
+        if (len > kGalTMax) return false;
+        maxt = std::max(maxt, len);
+        G.tlen[i] = (uint8_t)len;
+        toff[(size_t)i + 1] = (int64_t)tj.size();
+    }
+    G.tcap = maxt <= 16 ? 16 : 32;
+    // groups of consecutive gal_order rows
+    std::vector<int32_t> loc((size_t)n, -1);
+    std::vector<int32_t> cur;
+    G.grows.assign(1, 0);
+    G.guoff.assign(1, 0);
+    G.cptr.assign((size_t)nc + 1, 0);
+    G.soff.assign((size_t)nc + 1, 0);
+    G.cl.clear();
+    G.codes.clear();
+    int32_t r = 0;
+    while (r < nc) {
+        cur.clear();
+        int32_t r1 = r;
+        size_t ncl = 0, ncode = 0;
+        while (r1 < nc) {
+            const int32_t I = order[r1];
+            int add = 0;
+            size_t rcl = 0, rcode = 0;
+            for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
+                const int32_t i = cidx[t];
+                if (loc[i] == -1) {
+                    loc[i] = -2;         // provisional mark (undone below if the row does not fit)
+                    ++add;
+                }
+                ++rcl;
+                rcode += G.tlen[i];
+            }
+            const bool fits = (int)cur.size() + add <= kGalUCap && ncl + rcl <= kGalClCap && ncode + rcode <= kGalCodeCap;
+            if (!fits) {
+                for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t)
+                    if (loc[cidx[t]] <= -2) loc[cidx[t]] = -1;
+                if (r1 == r) return false;   // one coarse row alone exceeds a cap
+                break;
+            }
+            for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
+                const int32_t i = cidx[t];
+                if (loc[i] <= -2) {
+                    loc[i] = (int32_t)cur.size();
+                    cur.push_back(i);
                 }
             }
+            ncl += rcl;
+            ncode += rcode;
+            ++r1;
         }
-        cntl.assign((size_t)(s1 - s0) + 1, 0);
-        for (const Q& x : tmp) cntl[x.slot + 1]++;
-        for (int32_t k = 0; k < s1 - s0; ++k) cntl[k + 1] += cntl[k];
-        const int64_t base = roff[I];
-        for (int32_t k = 0; k < s1 - s0; ++k) gptr[s0 + k] = (int32_t)(base + cntl[k]);
-        for (const Q& x : tmp) {   // stable: enumeration order inside a slot
-            const int64_t at = base + cntl[x.slot]++;
-            ge[at] = x.e;
-            gw[at] = x.w;
-        }
-    });
-    gptr[C.nnz] = (int32_t)roff[nc];
-    if (half) {
-        diag.assign(nc, 0);
-        tpos.assign((size_t)C.nnz, 0);
-        parallel_rows([&](int32_t I) {
-            for (int32_t q = C.irp[I]; q < C.irp[I + 1]; ++q) {
-                const int32_t J = C.icol[q];
-                if (J == I) diag[I] = q;
-                const int32_t* pos = std::lower_bound(C.icol.data() + C.irp[J], C.icol.data() + C.irp[J + 1], I);
-                tpos[q] = (int32_t)(pos - C.icol.data());
+        // children entries and slot codes of the group's rows, in gal_order
+        for (int32_t q = r; q < r1; ++q) {
+            const int32_t I = order[q];
+            const int32_t s0 = C.irp[I], s1 = C.irp[I + 1];
+            if (s1 - s0 > 255) return false;
+            G.max_m = std::max(G.max_m, s1 - s0);
+            for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
+                const int32_t i = cidx[t];
+                // the parent slot q of I in i's P row: the children list holds one
+                // entry per nonzero (i, q) in ascending q, so the m-th entry of i
+                // in this row is i's m-th slot with column I
+                int seen = 0, cnt = 0, slotq = -1;
+                for (int32_t t2 = cptr[I]; t2 < t; ++t2) seen += cidx[t2] == i;
+                for (int k = 0; k < 3 && slotq < 0; ++k)
+                    if (pw[(size_t)k * n + i] != 0.0 && pc[(size_t)k * n + i] == I && cnt++ == seen) slotq = k;
+                if (slotq < 0) return false;
+                G.cl.push_back((uint16_t)((loc[i] << 2) | slotq));
+                for (int64_t k = toff[i]; k < toff[(size_t)i + 1]; ++k) {
+                    const int32_t* pos = std::lower_bound(C.icol.data() + s0, C.icol.data() + s1, tj[k]);
+                    if (pos == C.icol.data() + s1 || *pos != tj[k]) return false;   // pattern invariant (A9)
+                    G.codes.push_back((uint8_t)(pos - (C.icol.data() + s0)));
+                }
             }
-        });
-        for (int32_t I = 0; I < nc; ++I)   // the half map needs a symmetric pattern with every diagonal stored
-            if (C.icol[diag[I]] != I) return false;
-        for (int64_t q = 0; q < C.nnz; ++q) {
-            const int32_t t = tpos[q];
-            if (t >= C.nnz || tpos[t] != q) return false;
+            G.cptr[(size_t)q + 1] = (int32_t)G.cl.size();
+            G.soff[(size_t)q + 1] = (int32_t)G.codes.size();
         }
+        for (int32_t i : cur) loc[i] = -1;
+        G.U.insert(G.U.end(), cur.begin(), cur.end());
+        G.grows.push_back(r1);
+        G.guoff.push_back((int32_t)G.U.size());
+        r = r1;
     }
     return true;
 }
@@ -334,13 +370,7 @@ struct mg_ctx {
     bool symmetric = false;          // post-relaxation colours reversed (symmetric V-cycle)
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
-    bool use_gal2 = true;            // Galerkin v2 kernel
     bool zero_guess = false;          // mg_set_zero_guess
-    bool galg_half = true;            // upper-triangle map for symmetric sources (cotan, bilaplacian)
-    bool sym_source = false;          // the current matrix source is symmetric by construction
-    bool use_galg = true;            // Galerkin through the precomputed linear map (k_galerkin_map)
-    size_t galg_max_bytes = (size_t)16 << 30;   // device bytes allowed for the maps of all levels
-        bool use_gal4 = false;           // Galerkin v4 kernel (group-of-rows, A P rows once per group; measured slower, opt-in)
     int64_t l2_persist = 0;          // bytes of L2 set aside for the fine iterate (-1: auto, 0: off;
                                      // measured slightly slower than eviction hints alone, so off)
     int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
@@ -683,7 +713,6 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         }
     }
     cudaStream_t s = c->stream;
-    size_t galg_bytes = 0;
     for (int l = 0; l <= H; ++l) {
         Level& L = *c->lv[l];
         cudaError_t e;
@@ -732,110 +761,29 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 const uint64_t ka = key[C.perm[a]], kb = key[C.perm[b]];
                 return ka != kb ? ka < kb : a < b;
             });
-            // Galerkin v2 inputs: packed P rows (fine) and children with row extents (coarse)
-            std::vector<int32_t> prc(4 * (size_t)L.n), cinfo(4 * cidx.size());
-            std::vector<double> prw(4 * (size_t)L.n);
+            // packed P weights {w0, w1, w2, 0} per fine row (Galerkin)
+            std::vector<double> prw(4 * (size_t)L.n, 0.0);
             for (int32_t i = 0; i < L.n; ++i)
-                for (int q = 0; q < 3; ++q) {
-                    prc[4 * (size_t)i + q] = pc[(size_t)q * L.n + i];
-                    prw[4 * (size_t)i + q] = pw[(size_t)q * L.n + i];
-                }
-            for (size_t t = 0; t < cidx.size(); ++t) {
-                const int32_t i = cidx[t];
-                cinfo[4 * t] = i;
-                cinfo[4 * t + 1] = L.irp[i];
-                cinfo[4 * t + 2] = L.irp[i + 1] - L.irp[i];
-            }
-            int maxrow = 0;
-            for (int32_t I = 0; I < C.n; ++I) maxrow = std::max(maxrow, C.irp[I + 1] - C.irp[I]);
-            C.gal2 = c->use_gal2 && maxrow <= galerkin_max_row();
-            // Galerkin v4 structure: T_i = (A P)_i row sizes, groups of coarse rows
-            C.gal4_maxt = 0;
-            if (c->use_gal4) {
-                int maxT = 0;
-                std::vector<int32_t> seen(C.n, -1);
-                for (int32_t i = 0; i < L.n; ++i) {
-                    int cnt_t = 0;
-                    for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
-                        const int32_t j = L.icol[e];
-                        for (int q = 0; q < 3; ++q) {
-                            if (pw[(size_t)q * L.n + j] == 0.0) continue;
-                            const int32_t J = pc[(size_t)q * L.n + j];
-                            if (seen[J] != i) {
-                                seen[J] = i;
-                                ++cnt_t;
-                            }
-                        }
-                    }
-                    maxT = std::max(maxT, cnt_t);
-                }
-                const int capc = galerkin4_capc();
-                int maxch = 0;
-                for (int32_t I = 0; I < C.n; ++I) maxch = std::max(maxch, cnt[I + 1] - cnt[I]);
-                if (maxT <= 24 && maxch <= 32 && maxrow <= 64) {
-                    C.gal4_maxt = maxT <= 12 ? 12 : 24;
-                    std::vector<int32_t> grows(1, 0), gcoff(1, 0), gch, rcl(cidx.size());
-                    std::vector<int32_t> loc(L.n, -1);
-                    std::vector<int32_t> cur;
-                    size_t r = 0;
-                    while (r < order.size()) {
-                        // grow the group while its distinct children fit
-                        cur.clear();
-                        size_t r1 = r;
-                        while (r1 < order.size()) {
-                            const int32_t I = order[r1];
-                            int add = 0;
-                            for (int32_t t = cnt[I]; t < cnt[I + 1]; ++t)
-                                if (loc[cidx[t]] < 0) ++add;
-                            if ((int)cur.size() + add > capc && r1 > r) break;
-                            for (int32_t t = cnt[I]; t < cnt[I + 1]; ++t) {
-                                const int32_t i = cidx[t];
-                                if (loc[i] < 0) {
-                                    loc[i] = (int32_t)cur.size();
-                                    cur.push_back(i);
-                                }
-                                rcl[t] = loc[i];
-                            }
-                            ++r1;
-                        }
-                        for (int32_t i : cur) loc[i] = -1;
-                        gch.insert(gch.end(), cur.begin(), cur.end());
-                        grows.push_back((int32_t)r1);
-                        gcoff.push_back((int32_t)gch.size());
-                        r = r1;
-                    }
-                    C.gal4_ngroups = (int)grows.size() - 1;
-                    if ((e = C.g4_rows.upload(grows, s)) || (e = C.g4_coff.upload(gcoff, s)) ||
-                        (e = C.g4_children.upload(gch, s)) || (e = C.g4_rcl.upload(rcl, s)))
+                for (int q = 0; q < 3; ++q) prw[4 * (size_t)i + q] = pw[(size_t)q * L.n + i];
+            // numeric Galerkin structure (integer only): T-patterns, groups,
+            // children entries, slot codes (build_galerkin_t)
+            C.galt_tcap = 0;
+            {
+                GalT G;
+                if (build_galerkin_t(L, C, pc, pw, cnt, cidx, order, G)) {
+                    if ((e = L.gt_tp.upload(G.tp, s)) || (e = L.gt_tlen.upload(G.tlen, s)) ||
+                        (e = C.gt_rows.upload(G.grows, s)) || (e = C.gt_uoff.upload(G.guoff, s)) ||
+                        (e = C.gt_U.upload(G.U.empty() ? std::vector<int32_t>(1, 0) : G.U, s)) ||
+                        (e = C.gt_cptr.upload(G.cptr, s)) || (e = C.gt_soff.upload(G.soff, s)) ||
+                        (e = C.gt_cl.upload(G.cl.empty() ? std::vector<uint16_t>(1, 0) : G.cl, s)) ||
+                        (e = C.gt_codes.upload(G.codes.empty() ? std::vector<uint8_t>(16, 0) : G.codes, s)) ||
+                        (e = cudaStreamSynchronize(s)))
                         return c->cuda_fail(e, "pattern upload");
+                    C.galt_tcap = G.tcap;
+                    C.galt_ngroups = (int)G.grows.size() - 1;
                 }
             }
-            // Galerkin map: P and the patterns are fixed, so every coarse value is
-            // a fixed linear combination of fine values,
-            //   (P^T A P)_IJ = sum_{i child of I} sum_{j in row i, J parent of j} w_iI w_jJ a_ij,
-            // stored per coarse slot as (fine nonzero index, w_iI w_jJ) in
-            // (child, fine nonzero, parent) order.  The numeric Galerkin is then a
-            // deterministic streaming gather (k_galerkin_map) with no slot search.
-            C.galg = false;
-            if (c->use_galg) {
-                std::vector<int32_t> gptr, ge, gdiag, gtpos;
-                std::vector<double> gwv;
-                const bool ok = build_galerkin_map(L, C, cnt, cidx, cw, pc, pw, c->galg_half, gptr, ge, gwv, gdiag, gtpos);
-                const size_t bytes = ge.size() * 12 + gptr.size() * 4 + gtpos.size() * 4 + gdiag.size() * 4;
-                size_t freeb = 0, totb = 0;
-                cudaMemGetInfo(&freeb, &totb);
-                if (ok && galg_bytes + bytes <= c->galg_max_bytes && bytes * 2 < freeb) {
-                    if ((e = C.gmap_ptr.upload(gptr, s)) || (e = C.gmap_e.upload(ge, s)) || (e = C.gmap_w.upload(gwv, s)) ||
-                        (e = C.gmap_diag.upload(gdiag, s)) || (e = C.gmap_tpos.upload(gtpos, s)))
-                        return c->cuda_fail(e, "pattern upload");
-                    cudaStreamSynchronize(s);   // host staging vectors go out of scope
-                    C.galg = true;
-                    C.galg_half = c->galg_half;
-                    galg_bytes += bytes;
-                }
-            }
-            if ((e = L.prow_c.upload(prc, s)) || (e = L.prow_w.upload(prw, s)) || (e = C.cinfo.upload(cinfo, s)))
-                return c->cuda_fail(e, "pattern upload");
+            if ((e = L.prow_w.upload(prw, s))) return c->cuda_fail(e, "pattern upload");
             if ((e = L.pc.upload(pc, s)) || (e = L.pw.upload(pw, s)) || (e = C.cptr.upload(cnt, s)) ||
                 (e = C.cidx.upload(cidx, s)) || (e = C.cw.upload(cw, s)) || (e = C.gal_order.upload(order, s)))
                 return c->cuda_fail(e, "pattern upload");
@@ -1005,7 +953,7 @@ int rebuild_hierarchy(mg_ctx* c) {
     cudaStream_t s = c->stream;
     for (int l = 0; l < c->H; ++l)
         c->timed(PC_GALERKIN, l, s, [&] {
-            return launch_galerkin(*c->lv[l], c->lv[l]->val.p, *c->lv[l + 1], c->lv[l + 1]->val.p, s, c->sym_source);
+            return launch_galerkin(*c->lv[l], c->lv[l]->val.p, *c->lv[l + 1], c->lv[l + 1]->val.p, s);
         });
     return factor_coarsest(c);
 }
@@ -1025,8 +973,8 @@ int split_hierarchy(mg_ctx* c) {
         c->timed(PC_GALERKIN, l, s, [&] {
             Level& F = *c->lv[l];
             Level& C = *c->lv[l + 1];
-            return launch_galerkin(F, F.qv.p, C, C.qv.p, s, c->sym_source) +
-                   launch_galerkin(F, F.mv.p, C, C.mv.p, s, c->sym_source);
+            return launch_galerkin(F, F.qv.p, C, C.qv.p, s) +
+                   launch_galerkin(F, F.mv.p, C, C.mv.p, s);
         });
     cudaError_t e = cudaStreamSynchronize(s);
     if (!e) e = cudaGetLastError();
@@ -1305,11 +1253,6 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
     if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
     if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
-    if (const char* m = getenv("MG_GAL2")) c->use_gal2 = std::string(m) != "0";
-    if (const char* m = getenv("MG_GAL4")) c->use_gal4 = std::string(m) == "1";
-    if (const char* m = getenv("MG_GAL_MAP")) c->use_galg = std::string(m) != "0";
-    if (const char* m = getenv("MG_GAL_MAP_HALF")) c->galg_half = std::string(m) != "0";
-    if (const char* m = getenv("MG_GAL_MAP_MAX_MB")) c->galg_max_bytes = (size_t)atoll(m) << 20;
     if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
     if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
     if (const char* m = getenv("MG_FLOW_ROWS")) c->flow_rows = atoll(m);
@@ -1643,7 +1586,6 @@ static int load_csr_pattern(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* ro
 
 int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col, const double* val,
                   int on_device) {
-    if (c) c->sym_source = false;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (!val) return c->fail(MG_ERR_INVALID_ARG, "null CSR value array");
@@ -1798,7 +1740,6 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
 }
 
 int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double lap_coeff) {
-    if (c) c->sym_source = true;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if ((rc = load_cotan_pattern(c, V))) return rc;
@@ -1830,7 +1771,6 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
 
 // Row f3: A = mass_coeff M + bilap_coeff L M^{-1} L on the 2-ring pattern.
 int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, double bilap_coeff) {
-    if (c) c->sym_source = true;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (!V) return c->fail(MG_ERR_INVALID_ARG, "V is null");
@@ -1897,7 +1837,6 @@ int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, dou
 
 int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, const int32_t* col,
                         const double* q_val, const double* m_val) {
-    if (c) c->sym_source = false;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (c->dir || c->dir_all) return c->fail(MG_ERR_STATE, "split operators are not available with Dirichlet constraints");
@@ -1918,7 +1857,6 @@ int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_pt
 }
 
 int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
-    if (c) c->sym_source = true;   // Galerkin half map only for sources symmetric by construction
     int rc = check_state(c, false);
     if (rc) return rc;
     if (c->dir || c->dir_all) return c->fail(MG_ERR_STATE, "split operators are not available with Dirichlet constraints");

@@ -101,27 +101,17 @@ struct Level {
     DBuf<int32_t> cptr, cidx;             // transpose of P_{l-1} (this level coarse): children
     DBuf<double> cw;
     DBuf<int32_t> gal_order;              // rows of this level in locality order (Galerkin)
-    bool gal2 = false;                    // Galerkin v2 usable for this (coarse) level
-    // Galerkin as a fixed linear map of the fine values (this level coarse):
-    // val[slot] = sum_t gmap_w[t] * fine.val[gmap_e[t]], t in [gmap_ptr[slot], gmap_ptr[slot+1])
-    bool galg = false;
-    bool galg_half = false;               // map covers the upper triangle only (symmetric sources)
-    DBuf<int32_t> gmap_ptr, gmap_e;
-    DBuf<double> gmap_w;
-    DBuf<int32_t> gmap_diag;              // half map: slot of the diagonal per row
-    DBuf<int32_t> gmap_tpos;              // half map: slot of (J, I) for slot (I, J)
-    // Galerkin v4 (this level coarse): coarse rows in groups of consecutive
-    // gal_order rows; per group the distinct children (fine rows) and, for
-    // every children-list entry, the child's index inside its group
-    int gal4_maxt = 0;                    // 0: v4 not usable; else T-row capacity (12 or 24)
-    int gal4_ngroups = 0;
-    DBuf<int32_t> g4_rows;                // [ngroups+1] offsets into gal_order
-    DBuf<int32_t> g4_coff;                // [ngroups+1] offsets into g4_children
-    DBuf<int32_t> g4_children;            // distinct fine rows per group
-    DBuf<int32_t> g4_rcl;                 // parallel to cidx: local child index within the group
-    DBuf<int32_t> cinfo;                  // children as {i, row start, row length, 0} (this level coarse)
-    DBuf<int32_t> prow_c;                 // P rows packed: {c0, c1, c2, 0} (this level fine)
-    DBuf<double> prow_w;                  //                {w0, w1, w2, 0}
+    // numeric Galerkin k_galerkin_t (this level coarse; structure built by
+    // build_galerkin_t in mg_host.cpp, integer data only)
+    int galt_tcap = 0;                    // 16 / 32: T-positions per fine row; 0: generic kernel
+    int galt_ngroups = 0;
+    DBuf<int32_t> gt_rows, gt_uoff, gt_U; // groups: gal_order offsets, U offsets, distinct children
+    DBuf<int32_t> gt_cptr, gt_soff;       // [n + 1] in gal_order: children-entry / slot-code offsets
+    DBuf<uint16_t> gt_cl;                 // children entries: local index in U << 2 | parent slot q
+    DBuf<uint8_t> gt_codes;               // slot of each T-position of each child in the coarse row
+    DBuf<uint16_t> gt_tp;                 // (this level fine) per nonzero: T-positions of the 3 parents of col
+    DBuf<uint8_t> gt_tlen;                // (this level fine) T-pattern length per row
+    DBuf<double> prow_w;                  // P rows packed: {w0, w1, w2, 0} (this level fine)
     DBuf<int32_t> dperm;                  // perm on device
     DBuf<int32_t> diperm;                 // iperm on device (user -> internal)
     DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
@@ -235,10 +225,7 @@ int launch_axpby(const double* Qv, const double* Mv, double alpha, double beta, 
                  cudaStream_t s);
 int launch_apply_mass(int K, const double* M_user, const double* X, double* B, int n, cudaStream_t s);
 int launch_scatter_vec(const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
-int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s,
-                    bool symmetric);
-int galerkin_max_row();
-int galerkin4_capc();
+int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s);
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
 int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
 int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);

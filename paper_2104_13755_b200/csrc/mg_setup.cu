@@ -318,374 +318,135 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
         for (int s = lane; s < m; s += 32) cval[c0 + s] = acc[w][s];
 }
 
-// K2 v2 (default): same definition, restructured for memory-level
-// parallelism.  Per coarse row (one warp, locality order):
-//   * children come with their fine-row extents {i, start, len} (no
-//     dependent row-pointer load) and weights P[i,I];
-//   * the coarse row's column list is hashed into shared memory (open
-//     addressing, ~2 probes instead of a ~5-step binary search);
-//   * every lane handles two (child, nonzero) pairs per step; for each the
-//     P row of the column j is one packed 48-byte record {c0..c2, w0..w2}
-//     (two vector loads) instead of six scattered scalars;
-//   * rows with <= 32 entries accumulate into LANE-PRIVATE shared-memory
-//     copies acc[lane][slot] (no atomics: fp64 atomicAdd on shared memory is
-//     a CAS spin loop here), summed over lanes in fixed order at the end.
-//     Wider rows fall back to shared atomics on one copy.
-// Deterministic: every sum is taken in a fixed order.
-constexpr int kHash = 256;   // power of two > 2 * kGalMaxM
-constexpr int kGal2Warps = 4;
-constexpr int kPriv = 33;    // padded row of the private accumulators
-constexpr int kCopies = 16;  // accumulator copies per warp: lanes l and l + 16 share copy l (two phases)
+// K2 (default): k_galerkin_t.  With T = A_l P_l (fine rows x coarse columns),
+//   (P^T A P)_IJ = sum_{i child of I} w_iI T_iJ,   T_iJ = sum_{j in row i} a_ij w_jJ
+// (Eq. gca; P's rows hold <= 3 barycentric weights).
+// One CTA per group of consecutive coarse rows in locality order
+// (build_galerkin_t, mg_host.cpp), kGalThreads threads:
+//   stage   the group's children entries and slot codes (coalesced, shared);
+//   phase 1 one thread per distinct child i of the group (the U list):
+//           T_i = sum over row i of a_ij * (the 3 P weights of j), accumulated
+//           at the precomputed T-positions in shared memory Ts[pos][u] --
+//           each fine row is read once per group and its columns' P weights
+//           are gathered once per nonzero, not once per parent;
+//   phase 2 kGalLPR lanes per coarse row I: for every child entry (u, q) in
+//           the children-list order, lane k adds w_{u,q} T_u[k] into the
+//           row's accumulator at the precomputed slot of T-position k (the
+//           positions of one child are distinct coarse columns, so the lanes
+//           of one step never collide); then the row is written, coalesced.
+// Every sum runs in a fixed order (nonzeros, then parents; children in list
+// order): deterministic, no atomics.  Only integer structure is precomputed;
+// every value (a_ij, w) is read here.
+constexpr int kGalThreads = 256;   // = kGalUCap (mg_host.cpp): one phase-1 thread per child
+constexpr int kGalUCapK = 256;
+constexpr int kGalClCapK = 2048;
+constexpr int kGalCodeCapK = 12288;
+constexpr int kGalLPR = 8;         // lanes per coarse row in phase 2
+constexpr int kGalMCap = 64;       // coarse-row entries accumulated in shared memory (wider rows: in place)
 
-__device__ __forceinline__ unsigned hslot(int J) { return ((unsigned)J * 2654435761u) >> (32 - 8); }
-
-__global__ void __launch_bounds__(kGal2Warps * 32) k_galerkin2(
-    int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
-    double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
-    const double* __restrict__ cw, const int* __restrict__ col, const double* __restrict__ val,
-    const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
-    __shared__ double accp[kGal2Warps][kCopies * kPriv];   // copies (m <= 32) or one shared copy (m <= 96)
-    __shared__ int hkey[kGal2Warps][kHash];
-    __shared__ unsigned char hval[kGal2Warps][kHash];
-    __shared__ int ch_start[kGal2Warps][32];
-    __shared__ int ch_scan[kGal2Warps][32];
-    __shared__ double ch_w[kGal2Warps][32];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kGal2Warps + w;
-    if (gw >= nc) return;
-    const int I = order[gw];
-    const int c0 = crp[I];
-    const int m = crp[I + 1] - c0;
-    const bool priv = m <= 32;
-    double* mine = priv ? &accp[w][(lane & (kCopies - 1)) * kPriv] : &accp[w][0];
-    for (int h = lane; h < kHash; h += 32) hkey[w][h] = -1;
-    if (priv) {
-        for (int s2 = 0; s2 < m; ++s2) mine[s2] = 0.0;
-    } else {
-        for (int s2 = lane; s2 < m; s2 += 32) accp[w][s2] = 0.0;
-    }
-    __syncwarp();
-    for (int s2 = lane; s2 < m; s2 += 32) {
-        const int J = ccol[c0 + s2];
-        unsigned h = hslot(J);
-        while (atomicCAS(&hkey[w][h], -1, J) != -1) h = (h + 1) & (kHash - 1);
-        hval[w][h] = (unsigned char)s2;
-    }
-    __syncwarp();
-    const int t0 = cptr[I], t1 = cptr[I + 1];
-    for (int tb = t0; tb < t1; tb += 32) {
-        const int nb = min(32, t1 - tb);
-        int len = 0;
-        if (lane < nb) {
-            const int4 ci = cinfo[tb + lane];
-            ch_w[w][lane] = cw[tb + lane];
-            ch_start[w][lane] = ci.y;
-            len = ci.z;
-        }
-        int incl = len;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += v;
-        }
-        ch_scan[w][lane] = incl;
-        const int total = __shfl_sync(0xffffffffu, incl, nb - 1);
-        __syncwarp();
-        for (int g0 = 0; g0 < total; g0 += 64) {
-            int e[2];
-            double pwt[2];
-            bool ok[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int g = g0 + lane + 32 * u;
-                ok[u] = g < total;
-                int lo = 0, hi = nb - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (ch_scan[w][mid] > g) hi = mid;
-                    else lo = mid + 1;
-                }
-                const int excl = lo ? ch_scan[w][lo - 1] : 0;
-                e[u] = ok[u] ? ch_start[w][lo] + (g - excl) : 0;
-                pwt[u] = ch_w[w][lo];
-            }
-            int j[2];
-            double a[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                j[u] = ok[u] ? col[e[u]] : 0;
-                a[u] = ok[u] ? pwt[u] * val[e[u]] : 0.0;
-            }
-            int4 pc[2];
-            double4 pw[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                pc[u] = prow_c[j[u]];
-                pw[u] = prow_w[j[u]];
-            }
-            int slot[2][3];
-            double tv[2][3];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int Js[3] = {pc[u].x, pc[u].y, pc[u].z};
-                const double ws[3] = {pw[u].x, pw[u].y, pw[u].z};
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    slot[u][q] = -1;
-                    tv[u][q] = a[u] * ws[q];
-                    if (!ok[u] || ws[q] == 0.0) continue;
-                    unsigned h = hslot(Js[q]);
-                    while (hkey[w][h] != Js[q]) h = (h + 1) & (kHash - 1);
-                    slot[u][q] = hval[w][h];
-                }
-            }
-            if (priv) {
-                // lanes l and l + 16 share a copy: they accumulate in two phases
-#pragma unroll
-                for (int ph = 0; ph < 32 / kCopies; ++ph) {
-                    if ((lane / kCopies) == ph) {
-#pragma unroll
-                        for (int u = 0; u < 2; ++u)
-#pragma unroll
-                            for (int q = 0; q < 3; ++q)
-                                if (slot[u][q] >= 0) mine[slot[u][q]] += tv[u][q];
-                    }
-                    __syncwarp();
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < 2; ++u)
-#pragma unroll
-                    for (int q = 0; q < 3; ++q)
-                        if (slot[u][q] >= 0) atomicAdd(&accp[w][slot[u][q]], tv[u][q]);
-            }
-        }
-        __syncwarp();
-    }
-    __syncwarp();
-    if (priv) {
-        if (lane < m) {
-            double sum = 0.0;
-            for (int l = 0; l < kCopies; ++l) sum += accp[w][l * kPriv + lane];
-            cval[c0 + lane] = sum;
-        }
-    } else {
-        for (int s2 = lane; s2 < m; s2 += 32) cval[c0 + s2] = accp[w][s2];
-    }
+template <int TCAP>
+constexpr size_t galt_smem() {
+    return (size_t)TCAP * kGalUCapK * 8 + 3 * (size_t)kGalUCapK * 8 +
+           (size_t)(kGalThreads / kGalLPR) * kGalMCap * 8 + (size_t)kGalUCapK + (size_t)kGalClCapK * 2 +
+           (size_t)kGalCodeCapK;
 }
 
-// K2 v4 (default where it applies): A_c = P^T (A P), one CTA per group of
-// consecutive coarse rows (locality order).
-//   phase 1: every distinct child i of the group (fine row with P[i,I] != 0
-//            for a row I of the group) computes its row T_i = (A P)_i ONCE, in
-//            registers: the row's stored entries in ascending order, the three
-//            barycentric parents of each neighbour, accumulated into a small
-//            key/value map (<= MAXT distinct coarse columns, checked at
-//            pattern setup), then staged in shared memory;
-//   phase 2: owner computes: one thread per stored coarse entry (I, J) sums
-//            P[i,I] T_i[J] over the children list of I in its fixed order.
-// No atomics, every sum in a fixed order: deterministic.  Versus v2 the
-// triple-product terms per fine row drop from 3 x (|row| x 3) (recomputed for
-// each parent) to |row| x 3, and the P-row gathers by the same factor 3.
-constexpr int kGal4Threads = 256;
-constexpr int kGal4Capc = 256;   // distinct children per group (= threads: one child per thread)
-
-template <int MAXT>
-__global__ void __launch_bounds__(kGal4Threads, MAXT <= 12 ? 3 : 2) k_galerkin4(
-    const int* __restrict__ order, const int* __restrict__ grows, const int* __restrict__ gcoff,
-    const int* __restrict__ gch, const int* __restrict__ crp, const int* __restrict__ ccol, double* __restrict__ cval,
-    const int* __restrict__ cptr, const int* __restrict__ rcl, const double* __restrict__ cw,
-    const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
-    const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
-    extern __shared__ __align__(16) unsigned char g4_smem[];
-    double* Tv = reinterpret_cast<double*>(g4_smem);                          // [capc][MAXT]
-    int* Tk = reinterpret_cast<int*>(Tv + (size_t)kGal4Capc * MAXT);         // [capc][MAXT], ascending keys
-    unsigned char* Tn = reinterpret_cast<unsigned char*>(Tk + (size_t)kGal4Capc * MAXT);   // [capc]
-    constexpr int EB = 4;   // row entries fetched per batch (independent loads in flight)
+template <int TCAP>
+__global__ void __launch_bounds__(kGalThreads) k_galerkin_t(
+    const int* __restrict__ grows, const int* __restrict__ guoff, const int* __restrict__ U,
+    const int* __restrict__ order, const int* __restrict__ gcptr, const int* __restrict__ gsoff,
+    const uint16_t* __restrict__ gcl, const uint8_t* __restrict__ gcodes, const int* __restrict__ crp,
+    double* __restrict__ cval, const int* __restrict__ rp, const int* __restrict__ col,
+    const double* __restrict__ val, const uint16_t* __restrict__ tp, const uint8_t* __restrict__ tlen,
+    const double4* __restrict__ prow_w) {
+    extern __shared__ __align__(16) unsigned char galt_sm[];
+    double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][kGalUCapK]
+    double* Ws = Ts + (size_t)TCAP * kGalUCapK;                            // [3][kGalUCapK]
+    double* Acc = Ws + 3 * kGalUCapK;                                      // [groups][kGalMCap]
+    uint8_t* Ls = reinterpret_cast<uint8_t*>(Acc + (kGalThreads / kGalLPR) * kGalMCap);
+    uint16_t* Cl = reinterpret_cast<uint16_t*>(Ls + kGalUCapK);
+    uint8_t* Codes = reinterpret_cast<uint8_t*>(Cl + kGalClCapK);
     const int g = blockIdx.x;
-    const int c0 = gcoff[g], nch = gcoff[g + 1] - c0;
-    // ---- phase 1: T rows of the group's children (one child per thread)
-    for (int c = threadIdx.x; c < nch; c += kGal4Threads) {
-        const int i = gch[c0 + c];
-        int key[MAXT];
-        double v[MAXT];
+    const int tid = threadIdx.x;
+    const int r0 = grows[g], r1 = grows[g + 1];
+    const int u0 = guoff[g], nu = guoff[g + 1] - u0;
+    const int cbase = gcptr[r0], sbase = gsoff[r0];
+    // ---- stage the group's children entries and slot codes (coalesced)
+    {
+        const int nclr = gcptr[r1] - cbase;
+        for (int t = tid; t < nclr; t += kGalThreads) Cl[t] = __ldcs(gcl + cbase + t);
+        const int ncode = gsoff[r1] - sbase;
+        for (int t = tid; t < ncode; t += kGalThreads) Codes[t] = __ldcs(gcodes + sbase + t);
+    }
+    // ---- phase 1: T_u for every distinct child u of the group
+    if (tid < nu) {
+        const int i = __ldg(U + u0 + tid);
+        const int L = tlen[i];
+        const double4 wi = ldg_d4(prow_w + i);
+        Ws[tid] = wi.x;
+        Ws[kGalUCapK + tid] = wi.y;
+        Ws[2 * kGalUCapK + tid] = wi.z;
+        Ls[tid] = (uint8_t)L;
 #pragma unroll
-        for (int q = 0; q < MAXT; ++q) {
-            key[q] = 0x7fffffff;
-            v[q] = 0.0;
-        }
-        int cnt = 0;
-        const int e0 = rp[i], e1 = rp[i + 1];
-        for (int eb = e0; eb < e1; eb += EB) {
-            int jj[EB];
-            double aa[EB];
+        for (int k = 0; k < TCAP; ++k)
+            if (k < L) Ts[k * kGalUCapK + tid] = 0.0;
+        const int e0 = __ldg(rp + i), e1 = __ldg(rp + i + 1);
+        for (int e = e0; e < e1; e += 4) {
+            int j[4];
+            double a[4];
+            unsigned c[4];
+            double4 w[4];
 #pragma unroll
-            for (int u = 0; u < EB; ++u) {
-                const bool ok = eb + u < e1;
-                jj[u] = ok ? __ldcs(col + eb + u) : -1;
-                aa[u] = ok ? __ldcs(val + eb + u) : 0.0;
+            for (int u = 0; u < 4; ++u) {
+                const bool ok = e + u < e1;
+                j[u] = ok ? __ldcs(col + e + u) : i;
+                a[u] = ok ? __ldcs(val + e + u) : 0.0;
+                c[u] = ok ? (unsigned)__ldcs(tp + e + u) : 0x7fffu;
             }
-            int4 pcs[EB];
-            double4 pws[EB];
 #pragma unroll
-            for (int u = 0; u < EB; ++u) {
-                if (jj[u] >= 0) {
-                    pcs[u] = prow_c[jj[u]];
-                    pws[u] = prow_w[jj[u]];
-                } else {
-                    pcs[u] = make_int4(0, 0, 0, 0);
-                    pws[u] = make_double4(0.0, 0.0, 0.0, 0.0);
-                }
-            }
+            for (int u = 0; u < 4; ++u) w[u] = ldg_d4(prow_w + j[u]);
 #pragma unroll
-            for (int u = 0; u < EB; ++u) {
-                const int Js[3] = {pcs[u].x, pcs[u].y, pcs[u].z};
-                const double ws[3] = {pws[u].x, pws[u].y, pws[u].z};
-#pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    if (ws[r] == 0.0) continue;   // padding carries no structure (reading A9)
-                    const int J = Js[r];
-                    const double t = aa[u] * ws[r];
-                    bool found = false;
-#pragma unroll
-                    for (int q = 0; q < MAXT; ++q)
-                        if (key[q] == J) {
-                            v[q] += t;
-                            found = true;
-                        }
-                    if (!found) {
-#pragma unroll
-                        for (int q = 0; q < MAXT; ++q)
-                            if (q == cnt) {
-                                key[q] = J;
-                                v[q] = t;
-                            }
-                        ++cnt;
-                    }
-                }
+            for (int u = 0; u < 4; ++u) {
+                const unsigned p0 = c[u] & 31u, p1 = (c[u] >> 5) & 31u, p2 = (c[u] >> 10) & 31u;
+                if (p0 != 31u) Ts[p0 * kGalUCapK + tid] += a[u] * w[u].x;
+                if (p1 != 31u) Ts[p1 * kGalUCapK + tid] += a[u] * w[u].y;
+                if (p2 != 31u) Ts[p2 * kGalUCapK + tid] += a[u] * w[u].z;
             }
         }
-        // store sorted by key (rank = number of smaller keys; unused slots hold INT_MAX)
-#pragma unroll
-        for (int q = 0; q < MAXT; ++q) {
-            int rk = 0;
-#pragma unroll
-            for (int q2 = 0; q2 < MAXT; ++q2) rk += (key[q2] < key[q]) ? 1 : 0;
-            if (q < cnt) {
-                Tk[(size_t)c * MAXT + rk] = key[q];
-                Tv[(size_t)c * MAXT + rk] = v[q];
-            }
-        }
-        Tn[c] = (unsigned char)cnt;
     }
     __syncthreads();
-    // ---- phase 2: one warp per coarse row.  The row's columns go into a
-    // per-warp hash (column -> slot); the children are visited in their fixed
-    // order and, for each child, one lane per entry of its T row adds
-    // P[i,I] T_i[J] into the slot of J.  The keys of one T row are distinct,
-    // so the lanes of one step never hit the same slot: no atomics, and every
-    // entry sums its contributions in the children's order (deterministic).
-    constexpr int kH = 128;   // hash slots per warp (rows have <= 64 entries)
-    __shared__ int hk[kGal4Threads / 32][kH];
-    __shared__ unsigned char hv[kGal4Threads / 32][kH];
-    __shared__ double acc2[kGal4Threads / 32][64];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r0 = grows[g], r1 = grows[g + 1];
-    for (int rr = r0 + warp; rr < r1; rr += kGal4Threads / 32) {
-        const int I = order[rr];
-        const int a0 = crp[I], m = crp[I + 1] - a0;
-        const int t0 = cptr[I], nt = cptr[I + 1] - t0;
-        for (int h = lane; h < kH; h += 32) hk[warp][h] = -1;
-        for (int q = lane; q < m; q += 32) acc2[warp][q] = 0.0;
-        __syncwarp();
-        for (int q = lane; q < m; q += 32) {
-            const int J = ccol[a0 + q];
-            unsigned h = ((unsigned)J * 2654435761u) >> 25;
-            while (atomicCAS(&hk[warp][h], -1, J) != -1) h = (h + 1) & (kH - 1);
-            hv[warp][h] = (unsigned char)q;
-        }
-        const int cl = lane < nt ? rcl[t0 + lane] : 0;
-        const double wl = lane < nt ? cw[t0 + lane] : 0.0;
-        __syncwarp();
-        for (int t = 0; t < nt; ++t) {
-            const int c = __shfl_sync(0xffffffffu, cl, t);
-            const double w = __shfl_sync(0xffffffffu, wl, t);
-            if (lane < Tn[c]) {
-                const int J = Tk[(size_t)c * MAXT + lane];
-                const double v = Tv[(size_t)c * MAXT + lane];
-                unsigned h = ((unsigned)J * 2654435761u) >> 25;
-                while (hk[warp][h] != J) h = (h + 1) & (kH - 1);
-                const int slot = hv[warp][h];
-                acc2[warp][slot] = fma(w, v, acc2[warp][slot]);
-            }
-            __syncwarp();
-        }
-        for (int q = lane; q < m; q += 32) cval[a0 + q] = acc2[warp][q];
-        __syncwarp();
-    }
-}
-
-// K2 v3 (MG_GAL_V3=1, measured slower): slot-owner formulation, atomic-free and deterministic.
-// One warp per coarse row I; lane l owns coarse columns J_l = col(I, l) and
-// J_l' = col(I, l + 32).  The warp walks every (child i, neighbour j) pair of
-// the row in lockstep: (j, p_iI a_ij) is broadcast from the lane that loaded
-// it, the packed P_j record {c0..c2, w0..w2} is a warp-uniform load, and each
-// lane adds p_iI a_ij P[j, J_l] into registers (P[j, J] = sum of the record's
-// weights whose column is J; padding weights are exactly 0).  Rows wider
-// than 64 entries use k_galerkin.
-__global__ void __launch_bounds__(kGalWarps * 32) k_galerkin3(
-    int nc, const int* __restrict__ order, const int* __restrict__ crp, const int* __restrict__ ccol,
-    double* __restrict__ cval, const int* __restrict__ cptr, const int4* __restrict__ cinfo,
-    const double* __restrict__ cw, const int* __restrict__ col, const double* __restrict__ val,
-    const int4* __restrict__ prow_c, const double4* __restrict__ prow_w) {
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * kGalWarps + w;
-    if (gw >= nc) return;
-    const int I = order[gw];
-    const int c0 = crp[I];
-    const int m = crp[I + 1] - c0;
-    const int J0 = lane < m ? ccol[c0 + lane] : -1;
-    const int J1 = lane + 32 < m ? ccol[c0 + 32 + lane] : -1;
-    double acc0 = 0.0, acc1 = 0.0;
-    const int t0 = cptr[I], t1 = cptr[I + 1];
-    for (int tb = t0; tb < t1; tb += 32) {
-        const int nb = min(32, t1 - tb);
-        int4 ci = make_int4(0, 0, 0, 0);
-        double cwv = 0.0;
-        if (lane < nb) {
-            ci = cinfo[tb + lane];
-            cwv = cw[tb + lane];
-        }
-        for (int k = 0; k < nb; ++k) {
-            const int start = __shfl_sync(0xffffffffu, ci.y, k);
-            const int len = __shfl_sync(0xffffffffu, ci.z, k);
-            const double pI = __shfl_sync(0xffffffffu, cwv, k);
-            for (int e0 = start; e0 < start + len; e0 += 32) {
-                const int cnt = min(32, start + len - e0);
-                int jl = 0;
-                double al = 0.0;
-                if (lane < cnt) {
-                    jl = col[e0 + lane];
-                    al = pI * val[e0 + lane];
-                }
-#pragma unroll 4
-                for (int q = 0; q < cnt; ++q) {
-                    const int j = __shfl_sync(0xffffffffu, jl, q);
-                    const double a = __shfl_sync(0xffffffffu, al, q);
-                    const int4 pc = prow_c[j];
-                    const double4 pw = prow_w[j];
-                    const double w0 = (pc.x == J0 ? pw.x : 0.0) + (pc.y == J0 ? pw.y : 0.0) + (pc.z == J0 ? pw.z : 0.0);
-                    acc0 = fma(a, w0, acc0);
-                    if (m > 32) {
-                        const double w1 = (pc.x == J1 ? pw.x : 0.0) + (pc.y == J1 ? pw.y : 0.0) + (pc.z == J1 ? pw.z : 0.0);
-                        acc1 = fma(a, w1, acc1);
-                    }
+    // ---- phase 2: kGalLPR lanes per coarse row
+    constexpr int PPL = (TCAP + kGalLPR - 1) / kGalLPR;   // T-positions per lane
+    const int lg = tid / kGalLPR, lane = tid % kGalLPR;
+    const unsigned mask = group_mask(kGalLPR);
+    for (int r = r0 + lg; r < r1; r += kGalThreads / kGalLPR) {
+        const int I = __ldg(order + r);
+        const int s0 = __ldg(crp + I), m = __ldg(crp + I + 1) - s0;
+        double* acc = m <= kGalMCap ? Acc + lg * kGalMCap : cval + s0;
+        for (int q = lane; q < m; q += kGalLPR) acc[q] = 0.0;
+        __syncwarp(mask);
+        const int c0 = __ldg(gcptr + r) - cbase, c1 = __ldg(gcptr + r + 1) - cbase;
+        int off = __ldg(gsoff + r) - sbase;
+        for (int t = c0; t < c1; ++t) {
+            const unsigned code = Cl[t];
+            const int u = (int)(code >> 2);
+            const double w = Ws[(code & 3u) * kGalUCapK + u];
+            const int L = Ls[u];
+#pragma unroll
+            for (int pp = 0; pp < PPL; ++pp) {
+                const int k = lane + pp * kGalLPR;
+                if (k < L) {
+                    const int slot = Codes[off + k];
+                    acc[slot] += w * Ts[k * kGalUCapK + u];
                 }
             }
+            off += L;
+            __syncwarp(mask);   // the next child's lanes may update the slots written here
         }
+        if (m <= kGalMCap)
+            for (int q = lane; q < m; q += kGalLPR) cval[s0 + q] = acc[q];
+        __syncwarp(mask);
     }
-    if (lane < m) cval[c0 + lane] = acc0;
-    if (lane + 32 < m) cval[c0 + 32 + lane] = acc1;
 }
 
 // ---------------------------------------------------------------------------
@@ -1471,15 +1232,12 @@ void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* 
 
 }  // namespace
 
-size_t galerkin4_smem(int maxt) { return (size_t)kGal4Capc * maxt * 12 + kGal4Capc; }
-int galerkin4_capc() { return kGal4Capc; }
-int galerkin_max_row() { return 64; }   // v2 private rows <= 32, shared copy <= 96; v3 <= 64
 
 void init_setup_attributes() {
     const int big = 200 * 1024;
     cudaFuncSetAttribute(k_chol_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_galerkin4<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galerkin4_smem(12));
-    cudaFuncSetAttribute(k_galerkin4<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galerkin4_smem(24));
+    cudaFuncSetAttribute(k_galerkin_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galt_smem<16>());
+    cudaFuncSetAttribute(k_galerkin_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galt_smem<32>());
 }
 
 int launch_gather_rows(int K, const int32_t* perm, const double* src_user, double* dst_int, int n, cudaStream_t s,
@@ -1530,102 +1288,20 @@ int launch_scatter_vec(const int32_t* perm, const double* src_int, double* dst_u
     k_scatter_vec<<<nblk(n, kBlock), kBlock, 0, s>>>(perm, src_int, dst_user, n);
     return 1;
 }
-namespace {
-// Numeric Galerkin through the precomputed map (see mg_host.cpp, "Galerkin
-// map"): one warp per coarse row (locality order, so the fine values the rows
-// gather are shared in L2 by neighbouring warps), 4 lanes per coarse slot;
-// lane l takes the slot's entries l, l+4, ... with plain cached loads (an L2
-// evict-first hint on the map measured 13% slower: the partial-sector reads
-// of neighbouring lanes then re-fetch from DRAM), then a fixed-order shuffle
-// reduction.  Deterministic.
-constexpr int kGmapLanes = 4;
-// HALF: the map holds the upper triangle (slots from the diagonal on); each
-// value is also stored at its transposed slot (symmetric sources).
-template <bool HALF>
-__global__ void __launch_bounds__(256) k_galerkin_map(int nc, const int* __restrict__ order, const int* __restrict__ crp,
-                                                      const int* __restrict__ gptr, const int* __restrict__ ge,
-                                                      const double* __restrict__ gw, const double* __restrict__ fval,
-                                                      double* __restrict__ cval, const int* __restrict__ diag,
-                                                      const int* __restrict__ tpos) {
-    const int w = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
-    if (w >= nc) return;
-    const int lane = threadIdx.x & 31;
-    const int grp = lane / kGmapLanes;
-    const int sl = lane & (kGmapLanes - 1);
-    const int I = order[w];
-    const int s0 = HALF ? diag[I] : crp[I], s1 = crp[I + 1];
-    for (int sb = s0; sb < s1; sb += 32 / kGmapLanes) {
-        const int slot = sb + grp;
-        double acc = 0.0;
-        if (slot < s1) {
-            const int t0 = gptr[slot], t1 = gptr[slot + 1];
-            int t = t0 + sl;
-            for (; t + 3 * kGmapLanes < t1; t += 4 * kGmapLanes) {
-                int e[4];
-                double g[4], a[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    e[u] = __ldg(ge + t + u * kGmapLanes);
-                    g[u] = __ldg(gw + t + u * kGmapLanes);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) a[u] = __ldg(fval + e[u]);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) acc = fma(g[u], a[u], acc);
-            }
-            for (; t < t1; t += kGmapLanes) acc = fma(__ldg(gw + t), __ldg(fval + __ldg(ge + t)), acc);
-        }
-#pragma unroll
-        for (int off = kGmapLanes / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, kGmapLanes);
-        if (slot < s1 && sl == 0) {
-            cval[slot] = acc;
-            if (HALF && slot != s0) cval[tpos[slot]] = acc;
-        }
-    }
-}
-}  // namespace
-
-int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s,
-                    bool symmetric) {
+int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s) {
     const int nc = coarse.n;
-    if (coarse.galg && (symmetric || !coarse.galg_half)) {
-        const int grid = (int)(((int64_t)nc * 32 + 255) / 256);
-        if (coarse.galg_half)
-            k_galerkin_map<true><<<grid, 256, 0, s>>>(nc, coarse.gal_order.p, coarse.rp.p, coarse.gmap_ptr.p,
-                                                      coarse.gmap_e.p, coarse.gmap_w.p, fval, cval,
-                                                      coarse.gmap_diag.p, coarse.gmap_tpos.p);
-        else
-            k_galerkin_map<false><<<grid, 256, 0, s>>>(nc, coarse.gal_order.p, coarse.rp.p, coarse.gmap_ptr.p,
-                                                       coarse.gmap_e.p, coarse.gmap_w.p, fval, cval, nullptr, nullptr);
+    if (coarse.galt_tcap > 0 && coarse.galt_ngroups > 0) {
+        auto go = [&](auto kern, size_t smem) {
+            kern<<<coarse.galt_ngroups, kGalThreads, smem, s>>>(
+                coarse.gt_rows.p, coarse.gt_uoff.p, coarse.gt_U.p, coarse.gal_order.p, coarse.gt_cptr.p,
+                coarse.gt_soff.p, coarse.gt_cl.p, coarse.gt_codes.p, coarse.rp.p, cval, fine.rp.p, fine.col.p, fval,
+                fine.gt_tp.p, fine.gt_tlen.p, reinterpret_cast<const double4*>(fine.prow_w.p));
+        };
+        if (coarse.galt_tcap <= 16) go(k_galerkin_t<16>, galt_smem<16>());
+        else go(k_galerkin_t<32>, galt_smem<32>());
         return 1;
     }
-    if (coarse.gal4_maxt > 0 && fine.prow_c.p) {
-        if (coarse.gal4_maxt <= 12)
-            k_galerkin4<12><<<coarse.gal4_ngroups, kGal4Threads, galerkin4_smem(12), s>>>(
-                coarse.gal_order.p, coarse.g4_rows.p, coarse.g4_coff.p, coarse.g4_children.p, coarse.rp.p, coarse.col.p,
-                cval, coarse.cptr.p, coarse.g4_rcl.p, coarse.cw.p, fine.rp.p, fine.col.p, fval,
-                reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
-        else
-            k_galerkin4<24><<<coarse.gal4_ngroups, kGal4Threads, galerkin4_smem(24), s>>>(
-                coarse.gal_order.p, coarse.g4_rows.p, coarse.g4_coff.p, coarse.g4_children.p, coarse.rp.p, coarse.col.p,
-                cval, coarse.cptr.p, coarse.g4_rcl.p, coarse.cw.p, fine.rp.p, fine.col.p, fval,
-                reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
-        return 1;
-    }
-    if (coarse.gal2 && fine.prow_c.p && getenv("MG_GAL_V3")) {
-        k_galerkin3<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
-            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p,
-            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fval,
-            reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
-        return 1;
-    }
-    if (coarse.gal2 && fine.prow_c.p) {
-        k_galerkin2<<<nblk(nc, kGal2Warps), kGal2Warps * 32, 0, s>>>(
-            nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p,
-            reinterpret_cast<const int4*>(coarse.cinfo.p), coarse.cw.p, fine.col.p, fval,
-            reinterpret_cast<const int4*>(fine.prow_c.p), reinterpret_cast<const double4*>(fine.prow_w.p));
-        return 1;
-    }
+    // generic fallback (T-patterns wider than 30 or rows wider than 255 entries)
     k_galerkin<<<nblk(nc, kGalWarps), kGalWarps * 32, 0, s>>>(
         nc, coarse.gal_order.p, coarse.rp.p, coarse.col.p, cval, coarse.cptr.p, coarse.cidx.p, coarse.cw.p,
         fine.rp.p, fine.col.p, fval, fine.pc.p, fine.pw.p, fine.n);
