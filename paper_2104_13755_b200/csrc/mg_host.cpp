@@ -126,25 +126,27 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
 //   tlen[i] = its length (<= kGalTMax); per fine nonzero e, tp[e] packs the
 //   T-position of parent q of col[e] in bits 5q..5q+4 (31: w == 0, skip).
 // * groups: consecutive coarse rows of gal_order (locality order) whose
-//   distinct children (fine rows, U) fit one CTA; per group the U list.
-// * per coarse row r (gal_order position) its children entries
-//   (local index in U << 2 | parent slot q of I in the child's P row) in the
-//   children-list order, and per entry the slot in row I of every T-position
-//   of the child (one byte each, rows <= 255 entries).
+//   distinct children (fine rows, the U list) fit one CTA.
+// * per coarse entry (I, J) of a group (rows in gal_order, columns
+//   ascending): its contributions (child u, T-position k, parent slot q of I
+//   in u's P row) packed u | k << 8 | q << 13, in children-list order (the
+//   summation order); eoff = offsets relative to the group's first
+//   contribution (one sentinel per group); rowidx = local row of the entry.
 struct GalT {
-    int tcap = 0;                         // 16 or 32; 0: structure does not fit (generic kernel)
+    int tcap = 0;                         // 16 or 32
     std::vector<uint16_t> tp;             // [fine nnz]
     std::vector<uint8_t> tlen;            // [fine n]
     std::vector<int32_t> grows, guoff, U; // groups: gal_order offsets, U offsets, U rows
-    std::vector<int32_t> cptr, soff;      // [nc + 1] in gal_order: children entries, slot-code bytes
-    std::vector<uint16_t> cl;             // children entries
-    std::vector<uint8_t> codes;           // slot codes
-    int max_m = 0;
+    std::vector<int32_t> gent, gcon;      // groups: entry offsets, contribution offsets
+    std::vector<uint16_t> eoff;           // [entries + groups]
+    std::vector<uint8_t> rowidx;          // [entries]
+    std::vector<uint16_t> con;            // contributions
 };
 constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-bit fields
 constexpr int kGalUCap = 256;             // distinct children per group (one phase-1 thread each)
-constexpr int kGalClCap = 2048;           // children entries per group (staged in shared memory)
-constexpr int kGalCodeCap = 12288;        // slot-code bytes per group (staged in shared memory)
+constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index)
+constexpr int kGalEntCap = 2048;          // coarse entries per group (staged in shared memory)
+constexpr int kGalConCap = 8192;          // contributions per group (staged in shared memory)
 
 bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>& pc, const std::vector<double>& pw,
                       const std::vector<int32_t>& cptr, const std::vector<int32_t>& cidx,
@@ -153,7 +155,7 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
     G = GalT();
     G.tp.assign((size_t)std::max<int64_t>(L.nnz, 1), 0);
     G.tlen.assign((size_t)n, 0);
-    // T-patterns of the fine rows (kept on the host for the slot codes)
+    // T-patterns of the fine rows
     std::vector<int64_t> toff((size_t)n + 1, 0);
     std::vector<int32_t> tj;
     tj.reserve((size_t)n * 12);
@@ -183,81 +185,107 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
         toff[(size_t)i + 1] = (int64_t)tj.size();
     }
     G.tcap = maxt <= 16 ? 16 : 32;
-    // groups of consecutive gal_order rows
+    // the contributions of coarse row I: per slot, (child, T-position, parent slot)
+    // in children-list order; returns false if a cap is exceeded
     std::vector<int32_t> loc((size_t)n, -1);
-    std::vector<int32_t> cur;
+    std::vector<int32_t> cnt;
+    std::vector<std::pair<int32_t, uint32_t>> tmp;   // (slot, code without the local child index)
+    auto row_contribs = [&](int32_t I, std::vector<std::pair<int32_t, uint32_t>>& out, std::vector<int32_t>& kids) {
+        out.clear();
+        kids.clear();
+        const int32_t s0 = C.irp[I], s1 = C.irp[I + 1];
+        for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
+            const int32_t i = cidx[t];
+            // parent slot q of I in i's P row: the children list holds one entry
+            // per nonzero (i, q) in ascending q, so the m-th entry of i in this
+            // row is i's m-th slot with column I
+            int seen = 0, c = 0, slotq = -1;
+            for (int32_t t2 = cptr[I]; t2 < t; ++t2) seen += cidx[t2] == i;
+            for (int k = 0; k < 3 && slotq < 0; ++k)
+                if (pw[(size_t)k * n + i] != 0.0 && pc[(size_t)k * n + i] == I && c++ == seen) slotq = k;
+            if (slotq < 0) return false;
+            kids.push_back(i);
+            if (kids.size() > 256) return false;
+            for (int64_t k = toff[i]; k < toff[(size_t)i + 1]; ++k) {
+                const int32_t* pos = std::lower_bound(C.icol.data() + s0, C.icol.data() + s1, tj[k]);
+                if (pos == C.icol.data() + s1 || *pos != tj[k]) return false;   // pattern invariant (A9)
+                out.push_back({(int32_t)(pos - (C.icol.data() + s0)),
+                               (uint32_t)((int)(kids.size() - 1)) | (uint32_t)(k - toff[i]) << 8 | (uint32_t)slotq << 13});
+            }
+        }
+        return true;
+    };
+    std::vector<std::pair<int32_t, uint32_t>> rc;
+    std::vector<int32_t> kids, cur;
     G.grows.assign(1, 0);
     G.guoff.assign(1, 0);
-    G.cptr.assign((size_t)nc + 1, 0);
-    G.soff.assign((size_t)nc + 1, 0);
-    G.cl.clear();
-    G.codes.clear();
+    G.gent.assign(1, 0);
+    G.gcon.assign(1, 0);
     int32_t r = 0;
     while (r < nc) {
         cur.clear();
         int32_t r1 = r;
-        size_t ncl = 0, ncode = 0;
-        while (r1 < nc) {
+        size_t nent = 0, ncon = 0;
+        // grow the group while its distinct children, entries and contributions fit
+        while (r1 < nc && r1 - r < kGalRowCap) {
             const int32_t I = order[r1];
             int add = 0;
-            size_t rcl = 0, rcode = 0;
+            size_t rcon = 0;
             for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
                 const int32_t i = cidx[t];
                 if (loc[i] == -1) {
-                    loc[i] = -2;         // provisional mark (undone below if the row does not fit)
+                    loc[i] = -2;         // provisional mark (undone if the row does not fit)
                     ++add;
                 }
-                ++rcl;
-                rcode += G.tlen[i];
+                rcon += G.tlen[i];
             }
-            const bool fits = (int)cur.size() + add <= kGalUCap && ncl + rcl <= kGalClCap && ncode + rcode <= kGalCodeCap;
+            const size_t rent = (size_t)(C.irp[I + 1] - C.irp[I]);
+            const bool fits = (int)cur.size() + add <= kGalUCap && nent + rent <= kGalEntCap && ncon + rcon <= kGalConCap;
             if (!fits) {
                 for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t)
-                    if (loc[cidx[t]] <= -2) loc[cidx[t]] = -1;
+                    if (loc[cidx[t]] == -2) loc[cidx[t]] = -1;
                 if (r1 == r) return false;   // one coarse row alone exceeds a cap
                 break;
             }
             for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
                 const int32_t i = cidx[t];
-                if (loc[i] <= -2) {
+                if (loc[i] == -2) {
                     loc[i] = (int32_t)cur.size();
                     cur.push_back(i);
                 }
             }
-            ncl += rcl;
-            ncode += rcode;
+            nent += rent;
+            ncon += rcon;
             ++r1;
         }
-        // children entries and slot codes of the group's rows, in gal_order
+        // entries and contributions of the group's rows
+        const size_t con0 = G.con.size();
         for (int32_t q = r; q < r1; ++q) {
             const int32_t I = order[q];
-            const int32_t s0 = C.irp[I], s1 = C.irp[I + 1];
-            if (s1 - s0 > 255) return false;
-            G.max_m = std::max(G.max_m, s1 - s0);
-            for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
-                const int32_t i = cidx[t];
-                // the parent slot q of I in i's P row: the children list holds one
-                // entry per nonzero (i, q) in ascending q, so the m-th entry of i
-                // in this row is i's m-th slot with column I
-                int seen = 0, cnt = 0, slotq = -1;
-                for (int32_t t2 = cptr[I]; t2 < t; ++t2) seen += cidx[t2] == i;
-                for (int k = 0; k < 3 && slotq < 0; ++k)
-                    if (pw[(size_t)k * n + i] != 0.0 && pc[(size_t)k * n + i] == I && cnt++ == seen) slotq = k;
-                if (slotq < 0) return false;
-                G.cl.push_back((uint16_t)((loc[i] << 2) | slotq));
-                for (int64_t k = toff[i]; k < toff[(size_t)i + 1]; ++k) {
-                    const int32_t* pos = std::lower_bound(C.icol.data() + s0, C.icol.data() + s1, tj[k]);
-                    if (pos == C.icol.data() + s1 || *pos != tj[k]) return false;   // pattern invariant (A9)
-                    G.codes.push_back((uint8_t)(pos - (C.icol.data() + s0)));
-                }
+            const int32_t m = C.irp[I + 1] - C.irp[I];
+            if (!row_contribs(I, rc, kids)) return false;
+            cnt.assign((size_t)m + 1, 0);
+            for (const auto& x : rc) cnt[(size_t)x.first + 1]++;
+            for (int32_t k = 0; k < m; ++k) cnt[(size_t)k + 1] += cnt[k];
+            const size_t base = G.con.size();
+            G.con.resize(base + rc.size());
+            std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+            for (const auto& x : rc) {   // stable: children-list order inside a slot
+                const uint32_t u = (uint32_t)loc[kids[x.second & 255u]];
+                G.con[base + fill[x.first]++] = (uint16_t)((x.second & ~255u) | u);
             }
-            G.cptr[(size_t)q + 1] = (int32_t)G.cl.size();
-            G.soff[(size_t)q + 1] = (int32_t)G.codes.size();
+            for (int32_t k = 0; k < m; ++k) {
+                G.eoff.push_back((uint16_t)(base - con0 + cnt[k]));
+                G.rowidx.push_back((uint8_t)(q - r));
+            }
         }
+        G.eoff.push_back((uint16_t)(G.con.size() - con0));   // group sentinel
         for (int32_t i : cur) loc[i] = -1;
         G.U.insert(G.U.end(), cur.begin(), cur.end());
         G.grows.push_back(r1);
         G.guoff.push_back((int32_t)G.U.size());
+        G.gent.push_back((int32_t)G.rowidx.size());
+        G.gcon.push_back((int32_t)G.con.size());
         r = r1;
     }
     return true;
@@ -771,13 +799,15 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             {
                 GalT G;
                 if (build_galerkin_t(L, C, pc, pw, cnt, cidx, order, G)) {
+                    G.con.resize(G.con.size() + 8, 0);       // 16-byte staging loads may read past the ends
+                    G.eoff.resize(G.eoff.size() + 8, 0);
+                    G.rowidx.resize(G.rowidx.size() + 16, 0);
                     if ((e = L.gt_tp.upload(G.tp, s)) || (e = L.gt_tlen.upload(G.tlen, s)) ||
                         (e = C.gt_rows.upload(G.grows, s)) || (e = C.gt_uoff.upload(G.guoff, s)) ||
                         (e = C.gt_U.upload(G.U.empty() ? std::vector<int32_t>(1, 0) : G.U, s)) ||
-                        (e = C.gt_cptr.upload(G.cptr, s)) || (e = C.gt_soff.upload(G.soff, s)) ||
-                        (e = C.gt_cl.upload(G.cl.empty() ? std::vector<uint16_t>(1, 0) : G.cl, s)) ||
-                        (e = C.gt_codes.upload(G.codes.empty() ? std::vector<uint8_t>(16, 0) : G.codes, s)) ||
-                        (e = cudaStreamSynchronize(s)))
+                        (e = C.gt_ent.upload(G.gent, s)) || (e = C.gt_con.upload(G.gcon, s)) ||
+                        (e = C.gt_eoff.upload(G.eoff, s)) || (e = C.gt_rowidx.upload(G.rowidx, s)) ||
+                        (e = C.gt_codes.upload(G.con, s)) || (e = cudaStreamSynchronize(s)))
                         return c->cuda_fail(e, "pattern upload");
                     C.galt_tcap = G.tcap;
                     C.galt_ngroups = (int)G.grows.size() - 1;

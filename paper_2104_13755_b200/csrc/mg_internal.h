@@ -106,9 +106,10 @@ struct Level {
     int galt_tcap = 0;                    // 16 / 32: T-positions per fine row; 0: generic kernel
     int galt_ngroups = 0;
     DBuf<int32_t> gt_rows, gt_uoff, gt_U; // groups: gal_order offsets, U offsets, distinct children
-    DBuf<int32_t> gt_cptr, gt_soff;       // [n + 1] in gal_order: children-entry / slot-code offsets
-    DBuf<uint16_t> gt_cl;                 // children entries: local index in U << 2 | parent slot q
-    DBuf<uint8_t> gt_codes;               // slot of each T-position of each child in the coarse row
+    DBuf<int32_t> gt_ent, gt_con;         // groups: coarse-entry offsets, contribution offsets
+    DBuf<uint16_t> gt_eoff;               // per entry (+1 sentinel per group): contribution offset in the group
+    DBuf<uint8_t> gt_rowidx;              // per entry: local row in the group
+    DBuf<uint16_t> gt_codes;              // contributions: child u | T-position k << 8 | parent slot q << 13
     DBuf<uint16_t> gt_tp;                 // (this level fine) per nonzero: T-positions of the 3 parents of col
     DBuf<uint8_t> gt_tlen;                // (this level fine) T-pattern length per row
     DBuf<double> prow_w;                  // P rows packed: {w0, w1, w2, 0} (this level fine)

@@ -322,130 +322,148 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 //   (P^T A P)_IJ = sum_{i child of I} w_iI T_iJ,   T_iJ = sum_{j in row i} a_ij w_jJ
 // (Eq. gca; P's rows hold <= 3 barycentric weights).
 // One CTA per group of consecutive coarse rows in locality order
-// (build_galerkin_t, mg_host.cpp), kGalThreads threads:
-//   stage   the group's children entries and slot codes (coalesced, shared);
+// (build_galerkin_t, mg_host.cpp):
+//   stage   the group's contribution lists (coalesced 16-byte loads, issued
+//           before phase 1, stored to shared memory after it);
 //   phase 1 one thread per distinct child i of the group (the U list):
 //           T_i = sum over row i of a_ij * (the 3 P weights of j), accumulated
 //           at the precomputed T-positions in shared memory Ts[pos][u] --
 //           each fine row is read once per group and its columns' P weights
 //           are gathered once per nonzero, not once per parent;
-//   phase 2 kGalLPR lanes per coarse row I: for every child entry (u, q) in
-//           the children-list order, lane k adds w_{u,q} T_u[k] into the
-//           row's accumulator at the precomputed slot of T-position k (the
-//           positions of one child are distinct coarse columns, so the lanes
-//           of one step never collide); then the row is written, coalesced.
-// Every sum runs in a fixed order (nonzeros, then parents; children in list
-// order): deterministic, no atomics.  Only integer structure is precomputed;
-// every value (a_ij, w) is read here.
+//   phase 2 one thread per coarse entry (I, J) of the group: the sum of
+//           w_{u,q} T_u[k] over the entry's contribution list (children-list
+//           order), in a register; one coalesced store.
+// Every sum runs in a fixed order: deterministic, no atomics.  Only integer
+// structure is precomputed; every value (a_ij, w) is read here.
 constexpr int kGalThreads = 256;   // = kGalUCap (mg_host.cpp): one phase-1 thread per child
 constexpr int kGalUCapK = 256;
-constexpr int kGalClCapK = 2048;
-constexpr int kGalCodeCapK = 12288;
-constexpr int kGalLPR = 8;         // lanes per coarse row in phase 2
-constexpr int kGalMCap = 64;       // coarse-row entries accumulated in shared memory (wider rows: in place)
+constexpr int kGalTStr = kGalUCapK + 1;   // odd stride: spreads the T reads of phase 2 over banks
+constexpr int kGalRowCapK = 255;
+constexpr int kGalEntCapK = 2048;
+constexpr int kGalConCapK = 8192;
+// staged bytes (+16 per array for the aligned-down start): contributions, entry offsets, local rows
+constexpr int kGalStageBytes = (kGalConCapK * 2 + 16) + ((kGalEntCapK + 1) * 2 + 16 + 14) + (kGalEntCapK + 16 + 16);
+constexpr int kGalStageV = kGalStageBytes / 16 / kGalThreads + 1;   // uint4 per thread
 
 template <int TCAP>
 constexpr size_t galt_smem() {
-    return (size_t)TCAP * kGalUCapK * 8 + 3 * (size_t)kGalUCapK * 8 +
-           (size_t)(kGalThreads / kGalLPR) * kGalMCap * 8 + (size_t)kGalUCapK + (size_t)kGalClCapK * 2 +
-           (size_t)kGalCodeCapK;
+    return (size_t)TCAP * kGalTStr * 8 + 3 * (size_t)kGalUCapK * 8 + 2 * 256 * 4 + (size_t)kGalStageV * kGalThreads * 16;
+}
+
+// 16-byte-aligned window [base & ~15, end) of a byte array, in uint4 units
+struct Win {
+    const uint4* src;
+    int head;   // bytes before the first wanted byte
+    int n16;
+};
+__device__ __forceinline__ Win win16(const void* first, int bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(first);
+    Win w;
+    w.src = reinterpret_cast<const uint4*>(a & ~(uintptr_t)15);
+    w.head = (int)(a & 15);
+    w.n16 = (w.head + bytes + 15) / 16;
+    return w;
 }
 
 template <int TCAP>
-__global__ void __launch_bounds__(kGalThreads) k_galerkin_t(
+__global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
     const int* __restrict__ grows, const int* __restrict__ guoff, const int* __restrict__ U,
-    const int* __restrict__ order, const int* __restrict__ gcptr, const int* __restrict__ gsoff,
-    const uint16_t* __restrict__ gcl, const uint8_t* __restrict__ gcodes, const int* __restrict__ crp,
-    double* __restrict__ cval, const int* __restrict__ rp, const int* __restrict__ col,
+    const int* __restrict__ order, const int* __restrict__ gent, const int* __restrict__ gcon,
+    const uint16_t* __restrict__ geoff, const uint8_t* __restrict__ growidx, const uint16_t* __restrict__ gcodes,
+    const int* __restrict__ crp, double* __restrict__ cval, const int* __restrict__ rp, const int* __restrict__ col,
     const double* __restrict__ val, const uint16_t* __restrict__ tp, const uint8_t* __restrict__ tlen,
     const double4* __restrict__ prow_w) {
     extern __shared__ __align__(16) unsigned char galt_sm[];
-    double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][kGalUCapK]
-    double* Ws = Ts + (size_t)TCAP * kGalUCapK;                            // [3][kGalUCapK]
-    double* Acc = Ws + 3 * kGalUCapK;                                      // [groups][kGalMCap]
-    uint8_t* Ls = reinterpret_cast<uint8_t*>(Acc + (kGalThreads / kGalLPR) * kGalMCap);
-    uint16_t* Cl = reinterpret_cast<uint16_t*>(Ls + kGalUCapK);
-    uint8_t* Codes = reinterpret_cast<uint8_t*>(Cl + kGalClCapK);
+    double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][kGalTStr]
+    double* Ws = Ts + (size_t)TCAP * kGalTStr;                             // [3][kGalUCapK]
+    int* RowStart = reinterpret_cast<int*>(Ws + 3 * kGalUCapK);            // [256] crp of the group's rows
+    int* RowFirst = RowStart + 256;                                        // [256] first local entry of each row
+    uint4* Stage = reinterpret_cast<uint4*>(RowFirst + 256);
     const int g = blockIdx.x;
     const int tid = threadIdx.x;
-    const int r0 = grows[g], r1 = grows[g + 1];
+    const int r0 = grows[g], nr = grows[g + 1] - r0;
     const int u0 = guoff[g], nu = guoff[g + 1] - u0;
-    const int cbase = gcptr[r0], sbase = gsoff[r0];
-    // ---- stage the group's children entries and slot codes (coalesced)
-    {
-        const int nclr = gcptr[r1] - cbase;
-        for (int t = tid; t < nclr; t += kGalThreads) Cl[t] = __ldcs(gcl + cbase + t);
-        const int ncode = gsoff[r1] - sbase;
-        for (int t = tid; t < ncode; t += kGalThreads) Codes[t] = __ldcs(gcodes + sbase + t);
+    const int e0g = gent[g], nent = gent[g + 1] - e0g;
+    const int c0g = gcon[g], ncon = gcon[g + 1] - c0g;
+    // ---- stage: contributions, entry offsets (with the group sentinel), local rows
+    const Win wc = win16(gcodes + c0g, ncon * 2);
+    const Win we = win16(geoff + e0g + g, (nent + 1) * 2);
+    const Win wr = win16(growidx + e0g, nent);
+    const int ntot = wc.n16 + we.n16 + wr.n16;
+    uint4 stv[kGalStageV];
+#pragma unroll
+    for (int v = 0; v < kGalStageV; ++v) {
+        const int t = tid + v * kGalThreads;
+        stv[v] = make_uint4(0, 0, 0, 0);
+        if (t < wc.n16) stv[v] = __ldcs(wc.src + t);
+        else if (t < wc.n16 + we.n16) stv[v] = __ldcs(we.src + (t - wc.n16));
+        else if (t < ntot) stv[v] = __ldcs(wr.src + (t - wc.n16 - we.n16));
+    }
+    // row table: output start and first local entry of each row
+    if (tid < nr) {
+        const int I = __ldg(order + r0 + tid);
+        RowStart[tid] = __ldg(crp + I);
     }
     // ---- phase 1: T_u for every distinct child u of the group
     if (tid < nu) {
         const int i = __ldg(U + u0 + tid);
+        const int e0 = __ldg(rp + i), e1 = __ldg(rp + i + 1);
         const int L = tlen[i];
         const double4 wi = ldg_d4(prow_w + i);
         Ws[tid] = wi.x;
         Ws[kGalUCapK + tid] = wi.y;
         Ws[2 * kGalUCapK + tid] = wi.z;
-        Ls[tid] = (uint8_t)L;
 #pragma unroll
         for (int k = 0; k < TCAP; ++k)
-            if (k < L) Ts[k * kGalUCapK + tid] = 0.0;
-        const int e0 = __ldg(rp + i), e1 = __ldg(rp + i + 1);
-        for (int e = e0; e < e1; e += 4) {
-            int j[4];
-            double a[4];
-            unsigned c[4];
-            double4 w[4];
+            if (k < L) Ts[k * kGalTStr + tid] = 0.0;
+        constexpr int B = 8;
+        for (int e = e0; e < e1; e += B) {
+            int j[B];
+            double a[B];
+            unsigned c[B];
+            double4 w[B];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < B; ++u) {
                 const bool ok = e + u < e1;
                 j[u] = ok ? __ldcs(col + e + u) : i;
                 a[u] = ok ? __ldcs(val + e + u) : 0.0;
                 c[u] = ok ? (unsigned)__ldcs(tp + e + u) : 0x7fffu;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) w[u] = ldg_d4(prow_w + j[u]);
+            for (int u = 0; u < B; ++u) w[u] = ldg_d4(prow_w + j[u]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < B; ++u) {
                 const unsigned p0 = c[u] & 31u, p1 = (c[u] >> 5) & 31u, p2 = (c[u] >> 10) & 31u;
-                if (p0 != 31u) Ts[p0 * kGalUCapK + tid] += a[u] * w[u].x;
-                if (p1 != 31u) Ts[p1 * kGalUCapK + tid] += a[u] * w[u].y;
-                if (p2 != 31u) Ts[p2 * kGalUCapK + tid] += a[u] * w[u].z;
+                if (p0 != 31u) Ts[p0 * kGalTStr + tid] += a[u] * w[u].x;
+                if (p1 != 31u) Ts[p1 * kGalTStr + tid] += a[u] * w[u].y;
+                if (p2 != 31u) Ts[p2 * kGalTStr + tid] += a[u] * w[u].z;
             }
         }
     }
-    __syncthreads();
-    // ---- phase 2: kGalLPR lanes per coarse row
-    constexpr int PPL = (TCAP + kGalLPR - 1) / kGalLPR;   // T-positions per lane
-    const int lg = tid / kGalLPR, lane = tid % kGalLPR;
-    const unsigned mask = group_mask(kGalLPR);
-    for (int r = r0 + lg; r < r1; r += kGalThreads / kGalLPR) {
-        const int I = __ldg(order + r);
-        const int s0 = __ldg(crp + I), m = __ldg(crp + I + 1) - s0;
-        double* acc = m <= kGalMCap ? Acc + lg * kGalMCap : cval + s0;
-        for (int q = lane; q < m; q += kGalLPR) acc[q] = 0.0;
-        __syncwarp(mask);
-        const int c0 = __ldg(gcptr + r) - cbase, c1 = __ldg(gcptr + r + 1) - cbase;
-        int off = __ldg(gsoff + r) - sbase;
-        for (int t = c0; t < c1; ++t) {
-            const unsigned code = Cl[t];
-            const int u = (int)(code >> 2);
-            const double w = Ws[(code & 3u) * kGalUCapK + u];
-            const int L = Ls[u];
 #pragma unroll
-            for (int pp = 0; pp < PPL; ++pp) {
-                const int k = lane + pp * kGalLPR;
-                if (k < L) {
-                    const int slot = Codes[off + k];
-                    acc[slot] += w * Ts[k * kGalUCapK + u];
-                }
-            }
-            off += L;
-            __syncwarp(mask);   // the next child's lanes may update the slots written here
+    for (int v = 0; v < kGalStageV; ++v) {
+        const int t = tid + v * kGalThreads;
+        if (t < ntot) Stage[t] = stv[v];
+    }
+    __syncthreads();
+    const uint16_t* Con = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(Stage) + wc.head);
+    const uint16_t* Eoff =
+        reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(Stage + wc.n16) + we.head);
+    const uint8_t* Rowi = reinterpret_cast<const uint8_t*>(Stage + wc.n16 + we.n16) + wr.head;
+    for (int e = tid; e < nent; e += kGalThreads)   // first local entry of every row
+        if (e == 0 || Rowi[e] != Rowi[e - 1]) RowFirst[Rowi[e]] = e;
+    __syncthreads();
+    // ---- phase 2: one thread per coarse entry
+    for (int e = tid; e < nent; e += kGalThreads) {
+        const int p0 = Eoff[e], p1 = Eoff[e + 1];
+        double acc = 0.0;
+        for (int p = p0; p < p1; ++p) {
+            const unsigned c = Con[p];
+            const unsigned u = c & 255u, k = (c >> 8) & 31u, q = c >> 13;
+            acc = fma(Ws[q * kGalUCapK + u], Ts[k * kGalTStr + u], acc);
         }
-        if (m <= kGalMCap)
-            for (int q = lane; q < m; q += kGalLPR) cval[s0 + q] = acc[q];
-        __syncwarp(mask);
+        const int r = Rowi[e];
+        cval[RowStart[r] + (e - RowFirst[r])] = acc;
     }
 }
 
@@ -1293,9 +1311,10 @@ int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, 
     if (coarse.galt_tcap > 0 && coarse.galt_ngroups > 0) {
         auto go = [&](auto kern, size_t smem) {
             kern<<<coarse.galt_ngroups, kGalThreads, smem, s>>>(
-                coarse.gt_rows.p, coarse.gt_uoff.p, coarse.gt_U.p, coarse.gal_order.p, coarse.gt_cptr.p,
-                coarse.gt_soff.p, coarse.gt_cl.p, coarse.gt_codes.p, coarse.rp.p, cval, fine.rp.p, fine.col.p, fval,
-                fine.gt_tp.p, fine.gt_tlen.p, reinterpret_cast<const double4*>(fine.prow_w.p));
+                coarse.gt_rows.p, coarse.gt_uoff.p, coarse.gt_U.p, coarse.gal_order.p, coarse.gt_ent.p,
+                coarse.gt_con.p, coarse.gt_eoff.p, coarse.gt_rowidx.p, coarse.gt_codes.p, coarse.rp.p, cval,
+                fine.rp.p, fine.col.p, fval, fine.gt_tp.p, fine.gt_tlen.p,
+                reinterpret_cast<const double4*>(fine.prow_w.p));
         };
         if (coarse.galt_tcap <= 16) go(k_galerkin_t<16>, galt_smem<16>());
         else go(k_galerkin_t<32>, galt_smem<32>());
