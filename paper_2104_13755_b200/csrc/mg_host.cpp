@@ -130,8 +130,10 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
 // * per coarse entry (I, J) of a group (rows in gal_order, columns
 //   ascending): its contributions (child u, T-position k, parent slot q of I
 //   in u's P row) packed u | k << 8 | q << 13, in children-list order (the
-//   summation order); eoff = offsets relative to the group's first
-//   contribution (one sentinel per group); rowidx = local row of the entry.
+//   summation order); entries in descending order of contribution count
+//   inside a group, each with its local row (rowidx) and column slot (slot);
+//   eoff = offsets relative to the group's first contribution (one sentinel
+//   per group).
 struct GalT {
     int tcap = 0;                         // 16 or 32
     std::vector<uint16_t> tp;             // [fine nnz]
@@ -139,12 +141,12 @@ struct GalT {
     std::vector<int32_t> grows, guoff, U; // groups: gal_order offsets, U offsets, U rows
     std::vector<int32_t> gent, gcon;      // groups: entry offsets, contribution offsets
     std::vector<uint16_t> eoff;           // [entries + groups]
-    std::vector<uint8_t> rowidx;          // [entries]
+    std::vector<uint8_t> rowidx, slot;    // [entries]: local row, column slot in the row
     std::vector<uint16_t> con;            // contributions
 };
 constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-bit fields
 constexpr int kGalUCap = 256;             // distinct children per group (one phase-1 thread each)
-constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index)
+constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index; rows <= 256 entries)
 constexpr int kGalEntCap = 2048;          // coarse entries per group (staged in shared memory)
 constexpr int kGalConCap = 8192;          // contributions per group (staged in shared memory)
 
@@ -240,6 +242,7 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
                 rcon += G.tlen[i];
             }
             const size_t rent = (size_t)(C.irp[I + 1] - C.irp[I]);
+            if (rent > 256) return false;   // uint8 slot index
             const bool fits = (int)cur.size() + add <= kGalUCap && nent + rent <= kGalEntCap && ncon + rcon <= kGalConCap;
             if (!fits) {
                 for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t)
@@ -258,8 +261,16 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
             ncon += rcon;
             ++r1;
         }
-        // entries and contributions of the group's rows
+        // entries and contributions of the group's rows; the entries are
+        // emitted in descending order of their contribution count (stable), so
+        // that the lanes of a warp in phase 2 run loops of similar length
         const size_t con0 = G.con.size();
+        struct Ent {
+            uint8_t row, slot;
+            uint32_t c0, c1;   // range in gcon
+        };
+        std::vector<Ent> ents;
+        std::vector<uint16_t> gcon;
         for (int32_t q = r; q < r1; ++q) {
             const int32_t I = order[q];
             const int32_t m = C.irp[I + 1] - C.irp[I];
@@ -267,17 +278,23 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
             cnt.assign((size_t)m + 1, 0);
             for (const auto& x : rc) cnt[(size_t)x.first + 1]++;
             for (int32_t k = 0; k < m; ++k) cnt[(size_t)k + 1] += cnt[k];
-            const size_t base = G.con.size();
-            G.con.resize(base + rc.size());
+            const size_t base = gcon.size();
+            gcon.resize(base + rc.size());
             std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
             for (const auto& x : rc) {   // stable: children-list order inside a slot
                 const uint32_t u = (uint32_t)loc[kids[x.second & 255u]];
-                G.con[base + fill[x.first]++] = (uint16_t)((x.second & ~255u) | u);
+                gcon[base + fill[x.first]++] = (uint16_t)((x.second & ~255u) | u);
             }
-            for (int32_t k = 0; k < m; ++k) {
-                G.eoff.push_back((uint16_t)(base - con0 + cnt[k]));
-                G.rowidx.push_back((uint8_t)(q - r));
-            }
+            for (int32_t k = 0; k < m; ++k)
+                ents.push_back({(uint8_t)(q - r), (uint8_t)k, (uint32_t)(base + cnt[k]), (uint32_t)(base + cnt[k + 1])});
+        }
+        std::stable_sort(ents.begin(), ents.end(),
+                         [](const Ent& a, const Ent& b) { return a.c1 - a.c0 > b.c1 - b.c0; });
+        for (const Ent& x : ents) {
+            G.eoff.push_back((uint16_t)(G.con.size() - con0));
+            G.con.insert(G.con.end(), gcon.begin() + x.c0, gcon.begin() + x.c1);
+            G.rowidx.push_back(x.row);
+            G.slot.push_back(x.slot);
         }
         G.eoff.push_back((uint16_t)(G.con.size() - con0));   // group sentinel
         for (int32_t i : cur) loc[i] = -1;
@@ -802,11 +819,13 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     G.con.resize(G.con.size() + 8, 0);       // 16-byte staging loads may read past the ends
                     G.eoff.resize(G.eoff.size() + 8, 0);
                     G.rowidx.resize(G.rowidx.size() + 16, 0);
+                    G.slot.resize(G.slot.size() + 16, 0);
                     if ((e = L.gt_tp.upload(G.tp, s)) || (e = L.gt_tlen.upload(G.tlen, s)) ||
                         (e = C.gt_rows.upload(G.grows, s)) || (e = C.gt_uoff.upload(G.guoff, s)) ||
                         (e = C.gt_U.upload(G.U.empty() ? std::vector<int32_t>(1, 0) : G.U, s)) ||
                         (e = C.gt_ent.upload(G.gent, s)) || (e = C.gt_con.upload(G.gcon, s)) ||
                         (e = C.gt_eoff.upload(G.eoff, s)) || (e = C.gt_rowidx.upload(G.rowidx, s)) ||
+                        (e = C.gt_slot.upload(G.slot, s)) ||
                         (e = C.gt_codes.upload(G.con, s)) || (e = cudaStreamSynchronize(s)))
                         return c->cuda_fail(e, "pattern upload");
                     C.galt_tcap = G.tcap;

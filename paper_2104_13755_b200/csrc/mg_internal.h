@@ -108,7 +108,7 @@ struct Level {
     DBuf<int32_t> gt_rows, gt_uoff, gt_U; // groups: gal_order offsets, U offsets, distinct children
     DBuf<int32_t> gt_ent, gt_con;         // groups: coarse-entry offsets, contribution offsets
     DBuf<uint16_t> gt_eoff;               // per entry (+1 sentinel per group): contribution offset in the group
-    DBuf<uint8_t> gt_rowidx;              // per entry: local row in the group
+    DBuf<uint8_t> gt_rowidx, gt_slot;     // per entry: local row in the group, column slot in the row
     DBuf<uint16_t> gt_codes;              // contributions: child u | T-position k << 8 | parent slot q << 13
     DBuf<uint16_t> gt_tp;                 // (this level fine) per nonzero: T-positions of the 3 parents of col
     DBuf<uint8_t> gt_tlen;                // (this level fine) T-pattern length per row

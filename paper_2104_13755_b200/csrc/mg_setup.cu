@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 // (Eq. gca; P's rows hold <= 3 barycentric weights).
 // One CTA per group of consecutive coarse rows in locality order
 // (build_galerkin_t, mg_host.cpp):
-//   stage   the group's contribution lists (coalesced 16-byte loads, issued
-//           before phase 1, stored to shared memory after it);
+//   stage   the group's contribution lists into shared memory with 16-byte
+//           cp.async copies (no registers held), overlapping phase 1;
 //   phase 1 one thread per distinct child i of the group (the U list):
 //           T_i = sum over row i of a_ij * (the 3 P weights of j), accumulated
 //           at the precomputed T-positions in shared memory Ts[pos][u] --
@@ -332,25 +332,25 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 //           are gathered once per nonzero, not once per parent;
 //   phase 2 one thread per coarse entry (I, J) of the group: the sum of
 //           w_{u,q} T_u[k] over the entry's contribution list (children-list
-//           order), in a register; one coalesced store.
+//           order), in a register; entries come sorted by list length, so the
+//           lanes of a warp loop alike.
 // Every sum runs in a fixed order: deterministic, no atomics.  Only integer
 // structure is precomputed; every value (a_ij, w) is read here.
 constexpr int kGalThreads = 256;   // = kGalUCap (mg_host.cpp): one phase-1 thread per child
 constexpr int kGalUCapK = 256;
 constexpr int kGalTStr = kGalUCapK + 1;   // odd stride: spreads the T reads of phase 2 over banks
-constexpr int kGalRowCapK = 255;
 constexpr int kGalEntCapK = 2048;
 constexpr int kGalConCapK = 8192;
-// staged bytes (+16 per array for the aligned-down start): contributions, entry offsets, local rows
-constexpr int kGalStageBytes = (kGalConCapK * 2 + 16) + ((kGalEntCapK + 1) * 2 + 16 + 14) + (kGalEntCapK + 16 + 16);
-constexpr int kGalStageV = kGalStageBytes / 16 / kGalThreads + 1;   // uint4 per thread
+// staged bytes (each array from its 16-byte aligned-down start): contributions,
+// entry offsets (+ sentinel), local rows, slots
+constexpr int kGalStageBytes = (kGalConCapK * 2 + 16) + ((kGalEntCapK + 1) * 2 + 32) + 2 * (kGalEntCapK + 32);
 
 template <int TCAP>
 constexpr size_t galt_smem() {
-    return (size_t)TCAP * kGalTStr * 8 + 3 * (size_t)kGalUCapK * 8 + 2 * 256 * 4 + (size_t)kGalStageV * kGalThreads * 16;
+    return (size_t)TCAP * kGalTStr * 8 + 3 * (size_t)kGalUCapK * 8 + 256 * 4 + (size_t)kGalStageBytes + 64;
 }
 
-// 16-byte-aligned window [base & ~15, end) of a byte array, in uint4 units
+// 16-byte-aligned window [first & ~15, first + bytes) in uint4 units
 struct Win {
     const uint4* src;
     int head;   // bytes before the first wanted byte
@@ -364,46 +364,45 @@ __device__ __forceinline__ Win win16(const void* first, int bytes) {
     w.n16 = (w.head + bytes + 15) / 16;
     return w;
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int TCAP>
 __global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
     const int* __restrict__ grows, const int* __restrict__ guoff, const int* __restrict__ U,
     const int* __restrict__ order, const int* __restrict__ gent, const int* __restrict__ gcon,
-    const uint16_t* __restrict__ geoff, const uint8_t* __restrict__ growidx, const uint16_t* __restrict__ gcodes,
-    const int* __restrict__ crp, double* __restrict__ cval, const int* __restrict__ rp, const int* __restrict__ col,
-    const double* __restrict__ val, const uint16_t* __restrict__ tp, const uint8_t* __restrict__ tlen,
-    const double4* __restrict__ prow_w) {
+    const uint16_t* __restrict__ geoff, const uint8_t* __restrict__ growidx, const uint8_t* __restrict__ gslot,
+    const uint16_t* __restrict__ gcodes, const int* __restrict__ crp, double* __restrict__ cval,
+    const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
+    const uint16_t* __restrict__ tp, const uint8_t* __restrict__ tlen, const double4* __restrict__ prow_w) {
     extern __shared__ __align__(16) unsigned char galt_sm[];
     double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][kGalTStr]
     double* Ws = Ts + (size_t)TCAP * kGalTStr;                             // [3][kGalUCapK]
     int* RowStart = reinterpret_cast<int*>(Ws + 3 * kGalUCapK);            // [256] crp of the group's rows
-    int* RowFirst = RowStart + 256;                                        // [256] first local entry of each row
-    uint4* Stage = reinterpret_cast<uint4*>(RowFirst + 256);
+    uint4* Stage = reinterpret_cast<uint4*>(RowStart + 256);
     const int g = blockIdx.x;
     const int tid = threadIdx.x;
     const int r0 = grows[g], nr = grows[g + 1] - r0;
     const int u0 = guoff[g], nu = guoff[g + 1] - u0;
     const int e0g = gent[g], nent = gent[g + 1] - e0g;
     const int c0g = gcon[g], ncon = gcon[g + 1] - c0g;
-    // ---- stage: contributions, entry offsets (with the group sentinel), local rows
+    // ---- stage (asynchronous): contributions, entry offsets with the group sentinel, rows, slots
     const Win wc = win16(gcodes + c0g, ncon * 2);
     const Win we = win16(geoff + e0g + g, (nent + 1) * 2);
     const Win wr = win16(growidx + e0g, nent);
-    const int ntot = wc.n16 + we.n16 + wr.n16;
-    uint4 stv[kGalStageV];
-#pragma unroll
-    for (int v = 0; v < kGalStageV; ++v) {
-        const int t = tid + v * kGalThreads;
-        stv[v] = make_uint4(0, 0, 0, 0);
-        if (t < wc.n16) stv[v] = __ldcs(wc.src + t);
-        else if (t < wc.n16 + we.n16) stv[v] = __ldcs(we.src + (t - wc.n16));
-        else if (t < ntot) stv[v] = __ldcs(wr.src + (t - wc.n16 - we.n16));
+    const Win ws = win16(gslot + e0g, nent);
+    {
+        const int o1 = wc.n16, o2 = o1 + we.n16, o3 = o2 + wr.n16, ntot = o3 + ws.n16;
+        for (int t = tid; t < ntot; t += kGalThreads) {
+            const uint4* src = t < o1 ? wc.src + t : t < o2 ? we.src + (t - o1) : t < o3 ? wr.src + (t - o2)
+                                                                                   : ws.src + (t - o3);
+            cp_async16(Stage + t, src);
+        }
     }
-    // row table: output start and first local entry of each row
-    if (tid < nr) {
-        const int I = __ldg(order + r0 + tid);
-        RowStart[tid] = __ldg(crp + I);
-    }
+    if (tid < nr) RowStart[tid] = __ldg(crp + __ldg(order + r0 + tid));
     // ---- phase 1: T_u for every distinct child u of the group
     if (tid < nu) {
         const int i = __ldg(U + u0 + tid);
@@ -416,7 +415,7 @@ __global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
 #pragma unroll
         for (int k = 0; k < TCAP; ++k)
             if (k < L) Ts[k * kGalTStr + tid] = 0.0;
-        constexpr int B = 8;
+        constexpr int B = 4;
         for (int e = e0; e < e1; e += B) {
             int j[B];
             double a[B];
@@ -440,19 +439,13 @@ __global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
             }
         }
     }
-#pragma unroll
-    for (int v = 0; v < kGalStageV; ++v) {
-        const int t = tid + v * kGalThreads;
-        if (t < ntot) Stage[t] = stv[v];
-    }
+    cp_async_wait_all();
     __syncthreads();
-    const uint16_t* Con = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(Stage) + wc.head);
-    const uint16_t* Eoff =
-        reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(Stage + wc.n16) + we.head);
-    const uint8_t* Rowi = reinterpret_cast<const uint8_t*>(Stage + wc.n16 + we.n16) + wr.head;
-    for (int e = tid; e < nent; e += kGalThreads)   // first local entry of every row
-        if (e == 0 || Rowi[e] != Rowi[e - 1]) RowFirst[Rowi[e]] = e;
-    __syncthreads();
+    const uint8_t* sb = reinterpret_cast<const uint8_t*>(Stage);
+    const uint16_t* Con = reinterpret_cast<const uint16_t*>(sb + wc.head);
+    const uint16_t* Eoff = reinterpret_cast<const uint16_t*>(sb + 16 * wc.n16 + we.head);
+    const uint8_t* Rowi = sb + 16 * (wc.n16 + we.n16) + wr.head;
+    const uint8_t* Slot = sb + 16 * (wc.n16 + we.n16 + wr.n16) + ws.head;
     // ---- phase 2: one thread per coarse entry
     for (int e = tid; e < nent; e += kGalThreads) {
         const int p0 = Eoff[e], p1 = Eoff[e + 1];
@@ -462,8 +455,7 @@ __global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
             const unsigned u = c & 255u, k = (c >> 8) & 31u, q = c >> 13;
             acc = fma(Ws[q * kGalUCapK + u], Ts[k * kGalTStr + u], acc);
         }
-        const int r = Rowi[e];
-        cval[RowStart[r] + (e - RowFirst[r])] = acc;
+        cval[RowStart[Rowi[e]] + Slot[e]] = acc;
     }
 }
 
@@ -1312,7 +1304,8 @@ int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, 
         auto go = [&](auto kern, size_t smem) {
             kern<<<coarse.galt_ngroups, kGalThreads, smem, s>>>(
                 coarse.gt_rows.p, coarse.gt_uoff.p, coarse.gt_U.p, coarse.gal_order.p, coarse.gt_ent.p,
-                coarse.gt_con.p, coarse.gt_eoff.p, coarse.gt_rowidx.p, coarse.gt_codes.p, coarse.rp.p, cval,
+                coarse.gt_con.p, coarse.gt_eoff.p, coarse.gt_rowidx.p, coarse.gt_slot.p, coarse.gt_codes.p,
+                coarse.rp.p, cval,
                 fine.rp.p, fine.col.p, fval, fine.gt_tp.p, fine.gt_tlen.p,
                 reinterpret_cast<const double4*>(fine.prow_w.p));
         };
