@@ -145,10 +145,10 @@ struct GalT {
     std::vector<uint16_t> con;            // contributions
 };
 constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-bit fields
-constexpr int kGalUCap = 256;             // distinct children per group (one phase-1 thread each)
+// caps shared with k_galerkin_t (mg_setup.cu)
 constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index; rows <= 256 entries)
-constexpr int kGalEntCap = 2048;          // coarse entries per group (staged in shared memory)
-constexpr int kGalConCap = 8192;          // contributions per group (staged in shared memory)
+constexpr int kGalEntCap = 1024;          // coarse entries per group (staged in shared memory)
+constexpr int kGalConCap = 4096;          // contributions per group (staged in shared memory)
 
 bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>& pc, const std::vector<double>& pw,
                       const std::vector<int32_t>& cptr, const std::vector<int32_t>& cidx,
@@ -187,6 +187,7 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
         toff[(size_t)i + 1] = (int64_t)tj.size();
     }
     G.tcap = maxt <= 16 ? 16 : 32;
+    const int ucap = 4096 / G.tcap;       // distinct children per group (one phase-1 thread each)
     // the contributions of coarse row I: per slot, (child, T-position, parent slot)
     // in children-list order; returns false if a cap is exceeded
     std::vector<int32_t> loc((size_t)n, -1);
@@ -243,7 +244,7 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
             }
             const size_t rent = (size_t)(C.irp[I + 1] - C.irp[I]);
             if (rent > 256) return false;   // uint8 slot index
-            const bool fits = (int)cur.size() + add <= kGalUCap && nent + rent <= kGalEntCap && ncon + rcon <= kGalConCap;
+            const bool fits = (int)cur.size() + add <= ucap && nent + rent <= kGalEntCap && ncon + rcon <= kGalConCap;
             if (!fits) {
                 for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t)
                     if (loc[cidx[t]] == -2) loc[cidx[t]] = -1;

@@ -336,18 +336,23 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 //           lanes of a warp loop alike.
 // Every sum runs in a fixed order: deterministic, no atomics.  Only integer
 // structure is precomputed; every value (a_ij, w) is read here.
-constexpr int kGalThreads = 256;   // = kGalUCap (mg_host.cpp): one phase-1 thread per child
-constexpr int kGalUCapK = 256;
-constexpr int kGalTStr = kGalUCapK + 1;   // odd stride: spreads the T reads of phase 2 over banks
-constexpr int kGalEntCapK = 2048;
-constexpr int kGalConCapK = 8192;
+// Caps shared with build_galerkin_t (mg_host.cpp): distinct children per
+// group 4096 / TCAP (one phase-1 thread each: 256 for TCAP 16, 128 for 32),
+// coarse entries 1024 and contributions 4096 per group -- about 53 KB of
+// shared memory for TCAP 16, four CTAs per SM.
+constexpr int kGalThreads = 256;
+template <int TCAP>
+__host__ __device__ constexpr int galt_ucap() { return 4096 / TCAP; }
+constexpr int kGalEntCapK = 1024;
+constexpr int kGalConCapK = 4096;
 // staged bytes (each array from its 16-byte aligned-down start): contributions,
 // entry offsets (+ sentinel), local rows, slots
 constexpr int kGalStageBytes = (kGalConCapK * 2 + 16) + ((kGalEntCapK + 1) * 2 + 32) + 2 * (kGalEntCapK + 32);
 
 template <int TCAP>
 constexpr size_t galt_smem() {
-    return (size_t)TCAP * kGalTStr * 8 + 3 * (size_t)kGalUCapK * 8 + 256 * 4 + (size_t)kGalStageBytes + 64;
+    return (size_t)TCAP * (galt_ucap<TCAP>() + 1) * 8 + 3 * (size_t)galt_ucap<TCAP>() * 8 + 256 * 4 +
+           (size_t)kGalStageBytes + 64;
 }
 
 // 16-byte-aligned window [first & ~15, first + bytes) in uint4 units
@@ -371,13 +376,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int TCAP>
-__global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
+__global__ void __launch_bounds__(kGalThreads, 4) k_galerkin_t(
     const int* __restrict__ grows, const int* __restrict__ guoff, const int* __restrict__ U,
     const int* __restrict__ order, const int* __restrict__ gent, const int* __restrict__ gcon,
     const uint16_t* __restrict__ geoff, const uint8_t* __restrict__ growidx, const uint8_t* __restrict__ gslot,
     const uint16_t* __restrict__ gcodes, const int* __restrict__ crp, double* __restrict__ cval,
     const int* __restrict__ rp, const int* __restrict__ col, const double* __restrict__ val,
     const uint16_t* __restrict__ tp, const uint8_t* __restrict__ tlen, const double4* __restrict__ prow_w) {
+    constexpr int kGalUCapK = galt_ucap<TCAP>();
+    constexpr int kGalTStr = kGalUCapK + 1;   // odd stride: spreads the T reads of phase 2 over banks
     extern __shared__ __align__(16) unsigned char galt_sm[];
     double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][kGalTStr]
     double* Ws = Ts + (size_t)TCAP * kGalTStr;                             // [3][kGalUCapK]
@@ -424,9 +431,9 @@ __global__ void __launch_bounds__(kGalThreads, 3) k_galerkin_t(
 #pragma unroll
             for (int u = 0; u < B; ++u) {
                 const bool ok = e + u < e1;
-                j[u] = ok ? __ldcs(col + e + u) : i;
-                a[u] = ok ? __ldcs(val + e + u) : 0.0;
-                c[u] = ok ? (unsigned)__ldcs(tp + e + u) : 0x7fffu;
+                j[u] = ok ? __ldg(col + e + u) : i;   // cached: rows shared by neighbouring groups
+                a[u] = ok ? __ldg(val + e + u) : 0.0;
+                c[u] = ok ? (unsigned)__ldg(tp + e + u) : 0x7fffu;
             }
 #pragma unroll
             for (int u = 0; u < B; ++u) w[u] = ldg_d4(prow_w + j[u]);
