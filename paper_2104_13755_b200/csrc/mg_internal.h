@@ -110,6 +110,8 @@ struct Level {
     DBuf<uint16_t> gt_eoff;               // per entry (+1 sentinel per group): contribution offset in the group
     DBuf<uint8_t> gt_rowidx, gt_slot;     // per entry: local row in the group, column slot in the row
     DBuf<uint16_t> gt_codes;              // contributions: child u | T-position k << 8 | parent slot q << 13
+    DBuf<uint32_t> gt_umeta;              // per U row: staged offset | length << 16 | T length << 24
+    DBuf<int32_t> gt_roff, gt_runs;       // groups: run offsets; runs {first nonzero, staged base} + sentinel
     DBuf<uint16_t> gt_tp;                 // (this level fine) per nonzero: T-positions of the 3 parents of col
     DBuf<uint8_t> gt_tlen;                // (this level fine) T-pattern length per row
     DBuf<double> prow_w;                  // P rows packed: {w0, w1, w2, 0} (this level fine)
