@@ -253,6 +253,20 @@ int mg_util_galerkin_pattern(int32_t n_fine, const int32_t* row_ptr, const int32
                              const int32_t* P_cols, const double* P_w, int32_t* c_row_ptr, int64_t* c_nnz,
                              int32_t* c_col);
 
+/* ---- execution options ----------------------------------------------------- */
+
+/* How the same arithmetic is scheduled (results are bitwise identical except
+ * MG_EXEC_COARSE_TRSV, which changes the coarsest solve's rounding only).
+ * flags: OR of the bits below; 0 = defaults.  Must be followed by
+ * mg_set_matrix* (the pattern setup builds the tile and cluster structures),
+ * drops captured graphs.  MG_ERR_INVALID_ARG on unknown bits. */
+#define MG_EXEC_NO_PDL 1          /* no programmatic dependent launch inside the V-cycle graph */
+#define MG_EXEC_NO_PIPE 2         /* plain tile kernels instead of the TMA-bulk pipelined ones */
+#define MG_EXEC_COARSE_TRSV 4     /* coarsest solve by two triangular solves (one CTA), not A_H^{-1} GEMV */
+#define MG_EXEC_DEVICE_LOOP 8     /* Alg. 1 loop on the device (conditional WHILE graph node) */
+#define MG_EXEC_NO_CLUSTER 16     /* per-colour launches instead of the cluster-resident small-level smoother */
+int mg_set_execution(mg_ctx* ctx, int flags);
+
 /* ---- instrumentation (bench.py) ----------------------------------------- */
 
 /* Per-kernel-class timing with CUDA events on the context stream.  Bit c of

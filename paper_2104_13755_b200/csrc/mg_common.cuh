@@ -165,8 +165,7 @@ __device__ __forceinline__ void strow(double* p, const double (&v)[K]) {
 template <typename... KArgs, typename... Args>
 inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args... args) {
-    const cudaAccessPolicyWindow* win = current_window();
-    if (!pdl && !win) {
+    if (!pdl) {
         kern<<<grid, block, smem, s>>>(args...);
         return;
     }
@@ -175,20 +174,11 @@ inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    int na = 0;
-    if (pdl) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    if (win) {
-        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
-        at[na].val.accessPolicyWindow = *win;
-        ++na;
-    }
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = na;
+    cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -147,6 +148,7 @@ struct GalT {
     std::vector<uint8_t> rowidx, slot;    // [entries]: local row, column slot in the row
     std::vector<uint16_t> con;            // contributions
 };
+constexpr int32_t kClusterMaxRows = 65536;   // levels smoothed by one cluster (larger: per-colour launches)
 constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-bit fields
 // caps shared with k_galerkin_t (mg_setup.cu)
 constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index; rows <= 256 entries)
@@ -370,6 +372,111 @@ std::vector<uint64_t> morton_keys(const std::vector<double>& V, int32_t n) {
     return key;
 }
 
+// Cluster-resident smoother structure of one level (see ClusterSmoother in
+// mg_internal.h).  Integer structure only; false if the level does not
+// qualify (the per-colour launches then smooth it).
+bool setup_cluster_smoother(Level& L, int cs, cudaStream_t s) {
+    ClusterSmoother& Q = L.cls;
+    Q.cs = 0;
+    const int32_t n = L.n, C = L.ncolours;
+    if (cs <= 1 || n < 4 * cs || L.tiled || L.pipe || C < 1) return false;
+    // spatial parts: rank in (Morton key, user index) order -- the order inside each colour
+    const std::vector<uint64_t> key = morton_keys(L.V, n);
+    std::vector<int32_t> ord(n);
+    std::iota(ord.begin(), ord.end(), 0);
+    auto less = [&](int32_t a, int32_t b) {
+        const int32_t ua = L.perm[a], ub = L.perm[b];
+        return key[ua] != key[ub] ? key[ua] < key[ub] : ua < ub;
+    };
+    std::sort(ord.begin(), ord.end(), less);
+    std::vector<int32_t> part(n);
+    for (int32_t r = 0; r < n; ++r) part[ord[r]] = (int32_t)((int64_t)r * cs / n);
+    std::vector<int32_t> rowa((size_t)C * (cs + 1));
+    for (int32_t c = 0; c < C; ++c) {
+        const int32_t a = L.colour_off[c], b = L.colour_off[c + 1];
+        int32_t i = a;
+        for (int p = 0; p <= cs; ++p) {
+            while (i < b && part[i] < p) ++i;
+            rowa[(size_t)c * (cs + 1) + p] = i;
+        }
+        for (int32_t t = a + 1; t < b; ++t)
+            if (part[t] < part[t - 1]) return false;   // parts must be contiguous inside a colour
+    }
+    std::vector<int32_t> lbase((size_t)cs * C), nown(cs, 0), loc(n);
+    for (int p = 0; p < cs; ++p)
+        for (int32_t c = 0; c < C; ++c) {
+            lbase[(size_t)p * C + c] = nown[p];
+            const int32_t a = rowa[(size_t)c * (cs + 1) + p], b = rowa[(size_t)c * (cs + 1) + p + 1];
+            for (int32_t i = a; i < b; ++i) loc[i] = nown[p] + (i - a);
+            nown[p] += b - a;
+        }
+    // halos, local columns
+    std::vector<int32_t> hoff(1, 0), hrow;
+    std::vector<uint16_t> lcol((size_t)std::max<int64_t>(L.nnz, 1) + 8, 0);
+    std::vector<std::vector<std::array<int32_t, 3>>> sends((size_t)cs * C);   // per (owner, colour): {src, dst, dst local}
+    int rmax = 0, emax = 0, nloc_max = 0;
+    std::vector<int32_t> hidx(n, -1);
+    for (int p = 0; p < cs; ++p) {
+        std::vector<int32_t> h;
+        for (int32_t c = 0; c < C; ++c) {
+            const int32_t a = rowa[(size_t)c * (cs + 1) + p], b = rowa[(size_t)c * (cs + 1) + p + 1];
+            rmax = std::max(rmax, b - a);
+            emax = std::max(emax, L.irp[b] - L.irp[a]);
+            for (int32_t e = L.irp[a]; e < L.irp[b]; ++e) {
+                const int32_t j = L.icol[e];
+                if (part[j] != p && hidx[j] < 0) {
+                    hidx[j] = 0;
+                    h.push_back(j);
+                }
+            }
+        }
+        std::sort(h.begin(), h.end());
+        for (size_t k = 0; k < h.size(); ++k) hidx[h[k]] = nown[p] + (int32_t)k;
+        const int64_t nl = (int64_t)nown[p] + (int64_t)h.size();
+        if (nl > 65535) return false;
+        nloc_max = std::max<int>(nloc_max, (int)nl);
+        for (int32_t c = 0; c < C; ++c) {
+            const int32_t a = rowa[(size_t)c * (cs + 1) + p], b = rowa[(size_t)c * (cs + 1) + p + 1];
+            for (int32_t i = a; i < b; ++i)
+                for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
+                    const int32_t j = L.icol[e];
+                    lcol[e] = (uint16_t)(part[j] == p ? loc[j] : hidx[j]);
+                }
+        }
+        for (int32_t j : h) {
+            const int32_t q = part[j];
+            int32_t cj = 0;
+            while (L.colour_off[cj + 1] <= j) ++cj;
+            sends[(size_t)q * C + cj].push_back({loc[j], p, hidx[j]});
+            hidx[j] = -1;
+        }
+        hrow.insert(hrow.end(), h.begin(), h.end());
+        hoff.push_back((int32_t)hrow.size());
+    }
+    std::vector<int32_t> soff;
+    std::vector<int2> send;
+    for (int p = 0; p < cs; ++p)
+        for (int32_t c = 0; c < C; ++c) {
+            auto& v = sends[(size_t)p * C + c];
+            std::sort(v.begin(), v.end());
+            soff.push_back((int32_t)send.size());
+            for (const auto& x : v) send.push_back(make_int2(x[0], x[1] << 16 | x[2]));
+            if (c == C - 1) soff.push_back((int32_t)send.size());
+        }
+    if (hrow.empty()) hrow.push_back(0);
+    if (send.empty()) send.push_back(make_int2(0, 0));
+    cudaError_t e;
+    if ((e = Q.rowa.upload(rowa, s)) || (e = Q.lbase.upload(lbase, s)) || (e = Q.hoff.upload(hoff, s)) ||
+        (e = Q.hrow.upload(hrow, s)) || (e = Q.lcol.upload(lcol, s)) || (e = Q.soff.upload(soff, s)) ||
+        (e = Q.send.upload(send, s)) || (e = cudaStreamSynchronize(s)))
+        return false;
+    Q.rmax = rmax;
+    Q.emax = emax;
+    Q.nloc_max = nloc_max;
+    Q.cs = cs;
+    return true;
+}
+
 uint64_t fnv1a(uint64_t h, const void* data, size_t bytes) {
     const unsigned char* p = (const unsigned char*)data;
     for (size_t i = 0; i < bytes; ++i) {
@@ -449,16 +556,7 @@ struct mg_ctx {
     bool pdl = true;                 // programmatic dependent launch inside the V-cycle graph
     bool use_pipe = true;            // persistent TMA-bulk pipelined tile kernels
     bool zero_guess = false;          // mg_set_zero_guess
-    int64_t l2_persist = 0;          // bytes of L2 set aside for the fine iterate (-1: auto, 0: off;
-                                     // measured slightly slower than eviction hints alone, so off)
-    int tail_start = -1;             // first level run by the cluster tail kernel (-1: none)
-    int64_t tail_rows = 0;           // levels with at most this many rows join the cluster tail (0: off)
-    int tail_cs = 0;                 // cluster size of the tail kernel
     DBuf<int> errflag;
-    DBuf<int> flow_err;              // set by a dataflow GS kernel whose wait timed out
-    bool gs_persist = false;         // tiled levels: all colour passes of a smoothing phase in one launch
-    DBuf<unsigned long long> persist_ctr;   // its grid-barrier counter (monotone)
-    int64_t flow_rows = 0;           // levels 1.. with at most this many rows use dataflow GS (0: off)
 
     DBuf<double> partial, bnorm, rho;
     double* h_rho = nullptr;         // pinned, kMaxK
@@ -470,7 +568,8 @@ struct mg_ctx {
     cudaGraphExec_t pcg_exec[kMaxK + 1] = {};   // one MG-PCG iteration (row f4)
     cudaGraphExec_t loop_exec[kMaxK + 1] = {};  // whole solve: conditional WHILE node around the V-cycle
     int loop_check_launches = 1;
-    bool device_loop = false;                   // MG_DEVICE_LOOP=1 (opt-in: ncu does not see kernels inside conditional nodes)
+    bool device_loop = false;                   // MG_EXEC_DEVICE_LOOP (opt-in: ncu does not see kernels inside conditional nodes)
+    bool use_cluster = true;                    // cluster-resident smoothing of the small levels (MG_EXEC_NO_CLUSTER: off)
     DBuf<LoopState> loop_st;
     DBuf<double> loop_hist;
     LoopState* h_loop = nullptr;                // pinned
@@ -660,7 +759,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         // tile-staged kernels for short rows (a thread per row, few gather
         // batches); optionally pipelined tiles with pipe_lpr lanes per row for
         // longer rows (tiles of kTile / pipe_lpr rows); lanes-per-row otherwise
-        const double tile_avg = getenv("MG_TILE_MAX_AVG") ? atof(getenv("MG_TILE_MAX_AVG")) : 12.0;
+        const double tile_avg = 12.0;
         // Pipelined lanes-per-row tiles (tiles of 256 / LPR rows) for the
         // Galerkin-fill levels with large colour classes.  Measured on B200
         // (profiles/r01/sweeps ah_*, bh_*): the most lanes per row that keep
@@ -669,8 +768,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         // C4 level 2 / C5 level 1 (9-10k) LPR 8; below ~6000 rows per colour
         // the untiled k_lpr_sweep's wider grids win.  MG_PIPE_LPR (+ _MAX_AVG,
         // _MIN_ROWS) forces one width, MG_PIPE_LPR_L<l> one level.
-        const double plpr_avg = getenv("MG_PIPE_LPR_MAX_AVG") ? atof(getenv("MG_PIPE_LPR_MAX_AVG")) : 40.0;
-        const double plpr_rows = getenv("MG_PIPE_LPR_MIN_ROWS") ? atof(getenv("MG_PIPE_LPR_MIN_ROWS")) : 6000.0;
+        const double plpr_avg = 40.0, plpr_rows = 6000.0;
         int max_colour = 0;
         for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k)
             max_colour = std::max(max_colour, L.colour_off[k + 1] - L.colour_off[k]);
@@ -686,18 +784,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     break;
                 }
         }
-        if (const char* e = getenv("MG_PIPE_LPR")) {
-            const int plpr = atoi(e);
-            auto_lpr = (avg > tile_avg && avg <= plpr_avg && colour_rows >= plpr_rows &&
-                        (plpr == 2 || plpr == 4 || plpr == 8)) ? plpr : 0;
-        }
         L.pipe_lpr = avg <= tile_avg ? 1 : auto_lpr;
-        if (const char* e = getenv(("MG_PIPE_LPR_L" + std::to_string(l)).c_str())) L.pipe_lpr = atoi(e);
         if (L.pipe_lpr != 0 && L.pipe_lpr != 1 && L.pipe_lpr != 2 && L.pipe_lpr != 4 && L.pipe_lpr != 8) L.pipe_lpr = 0;
         // k = 3: all ~6 off-diagonal gathers of a row in one batch (80 registers,
         // 3 CTAs/SM) beat two batches at 4 CTAs/SM (C4: 366 -> 372 V-cycles/s,
         // level-0 GS 0.50 -> 0.54 of the HBM roofline; profiles/r01/sweeps/aw_*)
-        L.pipe_unr8 = !getenv("MG_PIPE_UNR8") || std::string(getenv("MG_PIPE_UNR8")) != "0";
+        L.pipe_unr8 = true;
         // shared-memory capacity of the tile-staged kernels
         const int T = tile_rows() / std::max(1, L.pipe_lpr);
         auto tile_max = [&](int r0, int r1) {
@@ -726,8 +818,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 L.tile_off.push_back((int32_t)(td.size() / 4));
             };
             for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k) add_tiles(L.colour_off[k], L.colour_off[k + 1]);
-            const bool spatial = !getenv("MG_TILE_SPATIAL") || std::string(getenv("MG_TILE_SPATIAL")) != "0";
-            if (spatial) {
+            {
                 // whole-level passes (residual, norm) walk the colour tiles in
                 // Morton order of their middle row: all colours of one spatial
                 // window are processed together, so the neighbours' x gathered
@@ -743,36 +834,11 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     td.insert(td.end(), {d0, d1, d2, d3});
                 }
                 L.tile_off.push_back((int32_t)(td.size() / 4));
-            } else {
-                add_tiles(0, L.n);
             }
-            L.serpentine = !getenv("MG_SERPENTINE") || std::string(getenv("MG_SERPENTINE")) != "0";
+            L.serpentine = true;
             L.pass_ctr = 0;
             L.pipe_cap = std::max(L.cap_gs, L.cap_all);
             cudaError_t e = L.tiles.upload(td, c->stream);
-            if (!e) e = L.dtoff.upload(L.tile_off, c->stream);
-            if (e) return c->cuda_fail(e, "tile upload");
-        }
-        // small levels: all GS sweeps in one CTA with x in shared memory
-        // (opt-in: measured 2x slower than one PDL launch per colour — one SM
-        // issues ~430 warp-instructions per 128-row tile at ~1.6 IPC, 4.3 us
-        // per tile against ~2.2 us per colour launch; profiles/r01/sweeps/al_*)
-        const int small_max = getenv("MG_SMALL_ROWS") ? atoi(getenv("MG_SMALL_ROWS")) : 0;
-        L.small = !L.pipe && L.n > 0 && L.n <= small_max;
-        if (L.small) {
-            const int TS = small_rows_per_tile();
-            std::vector<int32_t> td, toff(1, 0);
-            L.small_cap = 1;
-            for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k) {
-                for (int a = L.colour_off[k]; a < L.colour_off[k + 1]; a += TS) {
-                    const int nr = std::min(TS, L.colour_off[k + 1] - a);
-                    td.insert(td.end(), {a, nr, L.irp[a], L.irp[a + nr]});
-                    L.small_cap = std::max(L.small_cap, L.irp[a + nr] - L.irp[a]);
-                }
-                toff.push_back((int32_t)(td.size() / 4));
-            }
-            cudaError_t e = L.stiles.upload(td, c->stream);
-            if (!e) e = L.stoff.upload(toff, c->stream);
             if (e) return c->cuda_fail(e, "tile upload");
         }
         if (!L.tiled) {
@@ -785,9 +851,6 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             // whole-level passes (residual, norm) have C times the rows of a
             // colour pass: a few entries per lane instead of one wave
             L.lpr_all = avg <= 24.0 ? 4 : 8;
-            const std::string lv = std::to_string(l);
-            if (const char* e = getenv(("MG_LPR_L" + lv).c_str())) L.lpr = atoi(e);
-            if (const char* e = getenv(("MG_LPR_ALL_L" + lv).c_str())) L.lpr_all = atoi(e);
         }
     }
     cudaStream_t s = c->stream;
@@ -875,8 +938,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             // restriction in coarse locality order pays once the fine residual
             // (32 B/row) no longer sits in L2 next to the streamed lists
             // (measured: C4 level 0 -> 1 +3%, C3 level 0 -> 1 -8%)
-            C.restrict_ordered = getenv("MG_RESTRICT_ORDER") ? std::string(getenv("MG_RESTRICT_ORDER")) != "0"
-                                                            : L.n >= 1500000;
+            C.restrict_ordered = L.n >= 1500000;
             // ordered restriction: children lists laid out in the visiting
             // order (contiguous list reads, no order[] indirection before them)
             C.rcptr.release();
@@ -900,91 +962,6 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             }
         }
     }
-    // L2 residency of the fine iterate: a persisting access-policy window over
-    // level 0's x (re-gathered by every colour pass of every sweep).
-    {
-        Level& L0 = *c->lv[0];
-        L0.has_win = false;
-        int maxp = 0, maxw = 0;
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
-        const size_t xbytes = (size_t)L0.n * kMaxK * sizeof(double);
-        const int64_t want = c->l2_persist < 0 ? (int64_t)std::min<size_t>(xbytes, (size_t)maxp) : c->l2_persist;
-        if (want > 0 && maxp > 0 && maxw > 0 && H > 0) {
-            const size_t lim = std::min<size_t>((size_t)want, (size_t)maxp);
-            if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim) == cudaSuccess) {
-                L0.win.base_ptr = L0.x.p;
-                L0.win.num_bytes = std::min<size_t>(xbytes, (size_t)maxw);
-                L0.win.hitRatio = (float)std::min(1.0, (double)lim / (double)L0.win.num_bytes);
-                L0.win.hitProp = cudaAccessPropertyPersisting;
-                L0.win.missProp = cudaAccessPropertyStreaming;
-                L0.has_win = true;
-            }
-            cudaGetLastError();
-        }
-    }
-    // dataflow GS levels (coarse, latency-bound colour passes)
-    {
-        cudaError_t e = c->flow_err.alloc(1);
-        if (!e) e = cudaMemsetAsync(c->flow_err.p, 0, sizeof(int), c->stream);
-        if (!e && !c->persist_ctr.p) {
-            e = c->persist_ctr.alloc(1);
-            if (!e) e = cudaMemsetAsync(c->persist_ctr.p, 0, sizeof(unsigned long long), c->stream);
-        }
-        if (e) return c->cuda_fail(e, "flow setup");
-        for (int l = 0; l < H; ++l) {
-            Level& L = *c->lv[l];
-            L.flow = l >= 1 && c->flow_rows > 0 && L.n <= c->flow_rows && !L.tiled && !L.pipe;
-            if (L.flow) {
-                if ((e = L.done.alloc(L.n)) || (e = cudaMemsetAsync(L.done.p, 0, sizeof(int) * L.n, c->stream)))
-                    return c->cuda_fail(e, "flow setup");
-            }
-        }
-    }
-    // levels run by the cluster tail: the coarsest ones with <= tail_rows rows.
-    // Off by default: measured slower than per-launch PDL kernels.
-    c->tail_start = -1;
-    if (c->tail_cs > 0 && c->coarse_mode == 1) {
-        int lt = H;
-        while (lt > 0 && c->lv[lt - 1]->n <= c->tail_rows && H - (lt - 1) < kTailMaxLevels) --lt;
-        if (lt < H) c->tail_start = lt;
-    }
-    for (int l = 0; l <= H; ++l) {
-        cudaError_t e = c->lv[l]->dcoff.upload(c->lv[l]->colour_off, s);
-        if (e) return c->cuda_fail(e, "pattern upload");
-    }
-    // small levels: all GS sweeps on one thread-block cluster (k_cluster_gs);
-    // CTA r of the cluster owns rows i = r (mod CS)
-    {
-        // opt-in: measured slower than one PDL launch per colour (2.6 vs 2.1 us
-        // per colour step at 16 CTAs; 8, 4, 2 CTAs no better — DESIGN.md §8)
-        const int cl_rows = getenv("MG_CLUSTER_GS_ROWS") ? atoi(getenv("MG_CLUSTER_GS_ROWS")) : 0;
-        int cs = cl_rows > 0 ? cluster_gs_max_cs() : 0;
-        if (const char* m = getenv("MG_CLUSTER_GS_CS")) cs = std::min(cs, atoi(m));
-        for (int l = 0; l < H; ++l) {
-            Level& L = *c->lv[l];
-            L.cl_cs = 0;
-            if (cs <= 0 || L.pipe || L.n > cl_rows || L.n < cs) continue;
-            const int stride = (L.n + cs - 1) / cs + 1;
-            std::vector<int32_t> crp((size_t)cs * stride, 0);
-            int nnz_max = 0;
-            for (int r = 0; r < cs; ++r) {
-                int acc = 0, q = 0;
-                for (int i = r; i < L.n; i += cs, ++q) {
-                    crp[(size_t)r * stride + q] = acc;
-                    acc += L.irp[i + 1] - L.irp[i];
-                }
-                crp[(size_t)r * stride + q] = acc;
-                nnz_max = std::max(nnz_max, acc);
-            }
-            cudaError_t e = L.cl_rp.upload(crp, s);
-            if (e) return c->cuda_fail(e, "pattern upload");
-            L.cl_cs = cs;
-            L.cl_stride = stride;
-            L.cl_nown_max = stride - 1;
-            L.cl_nnz_max = nnz_max;
-        }
-    }
     // coarsest dense factor storage
     const int nH = c->lv[H]->n;
     c->npad = (nH + 31) / 32 * 32;
@@ -995,6 +972,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         (e = c->bnorm.alloc(kMaxK)) || (e = c->rho.alloc(kMaxK)))
         return c->cuda_fail(e, "pattern alloc");
     if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "pattern upload");
+    // cluster-resident smoothing of the levels whose colour passes are launch-bound
+    const int ccs = c->use_cluster ? cluster_smooth_max_cs() : 0;
+    for (int l = 0; l < H; ++l) {
+        Level& L = *c->lv[l];
+        if (!(ccs > 0 && L.n <= kClusterMaxRows && setup_cluster_smoother(L, ccs, s))) L.cls.cs = 0;
+    }
     c->have_pattern = true;
     return MG_OK;
 }
@@ -1005,22 +988,13 @@ int factor_coarsest(mg_ctx* c) {
     Level& LH = *c->lv[c->H];
     cudaError_t e = cudaMemsetAsync(c->errflag.p, 0, sizeof(int), s);
     if (e) return c->cuda_fail(e, "factor");
+    int nl = 0;
     c->timed(PC_FACTOR, c->H, s, [&] {
-        int n = launch_densify(LH, c->D.p, c->npad, s);
-        // default: one cooperative launch (factor + inverse); MG_CHOL=cluster
-        // selects the single-cluster kernel, MG_CHOL_LAUNCHES per-panel launches
-        const char* mode = getenv("MG_CHOL");
-        int nc = -1;
-        if (c->coarse_mode == 1 && !getenv("MG_CHOL_LAUNCHES")) {
-            if (!mode || std::string(mode) == "grid")
-                nc = launch_chol_grid(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s);
-            if (nc < 0) nc = launch_chol_cluster(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s);
-        }
-        if (nc > 0) return n + nc;
-        n += launch_chol_factor(c->D.p, c->Linv.p, c->npad, c->errflag.p, s);
-        if (c->coarse_mode == 1) n += launch_chol_inverse(c->D.p, c->Linv.p, c->npad, c->Ainv.p, s);
-        return n;
+        const int nd = launch_densify(LH, c->D.p, c->npad, s);
+        nl = launch_chol_grid(c->D.p, c->Linv.p, c->Wbuf.p, c->Ainv.p, c->npad, c->errflag.p, s);
+        return nd + std::max(nl, 0);
     });
+    if (nl < 0) return c->fail(MG_ERR_CUDA, "coarsest factor: cooperative launch unavailable");
     int flag = 0;
     if ((e = cudaMemcpyAsync(&flag, c->errflag.p, sizeof(int), cudaMemcpyDeviceToHost, s)) ||
         (e = cudaStreamSynchronize(s)))
@@ -1077,6 +1051,10 @@ int split_hierarchy(mg_ctx* c) {
 // V-cycle), or damped Jacobi (App. E) alternating x -> r -> x.
 int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
     int n = 0;
+    if (c->smoother == 0 && L.cls.cs > 0 && mu > 0) {
+        const int nl = vc_cluster_smooth(K, L, mu, reverse, pdl, s);
+        if (nl > 0) return nl;
+    }
     if (c->smoother == 1) {
         for (int it = 0; it < mu; ++it)
             n += (it & 1) ? vc_jacobi(K, L, L.r.p, L.x.p, c->omega, pdl, s) : vc_jacobi(K, L, L.x.p, L.r.p, c->omega, pdl, s);
@@ -1084,22 +1062,6 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
             cudaMemcpyAsync(L.x.p, L.r.p, sizeof(double) * (size_t)L.n * kMaxK, cudaMemcpyDeviceToDevice, s);
         }
         return n;
-    }
-    if (L.flow && mu > 0) {
-        const int nl = vc_gs_flow(K, L, mu, reverse, c->flow_err.p, s);
-        if (nl > 0) return nl;
-    }
-    if (c->gs_persist && L.pipe && L.pipe_lpr == 1 && mu > 0 && c->persist_ctr.p) {
-        const int nl = vc_gs_persist(K, L, mu, reverse, c->persist_ctr.p, s);
-        if (nl > 0) return nl;
-    }
-    if (L.small && mu > 0) {
-        const int nl = vc_small_gs(K, L, mu, reverse, pdl, s);
-        if (nl > 0) return nl;
-    }
-    if (L.cl_cs > 0 && mu > 0) {
-        const int nl = vc_cluster_gs(K, L, mu, reverse, pdl, s);
-        if (nl > 0) return nl;
     }
     for (int it = 0; it < mu; ++it)
         for (int q = 0; q < L.ncolours; ++q) {
@@ -1114,53 +1076,20 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
 void enqueue_vcycle_body(mg_ctx* c, int K, cudaStream_t s, bool symmetric) {
     const int H = c->H;
     const bool pdl = c->pdl;
-    // the cluster tail implements forward multicolour GS only
-    const bool tail_ok = c->smoother == 0 && !symmetric;
-    const int lt = (tail_ok && c->tail_start >= 0) ? c->tail_start : H;   // levels >= lt: tail (or coarsest solve)
-    for (int l = 0; l < lt; ++l) {
+    for (int l = 0; l < H; ++l) {
         Level& L = *c->lv[l];
-        WindowScope ws(L.has_win ? &L.win : nullptr);
         c->timed(PC_GS, l, s, [&] { return relax(c, K, L, c->mu_pre, false, pdl, s); });
         c->timed(PC_RESTRICT, l, s, [&] {
             return vc_residual(K, L, pdl, s) + vc_restrict(K, *c->lv[l + 1], L, pdl, s);
         });
     }
     Level& LH = *c->lv[H];
-    if (lt < H) {
-        TailParams p = {};
-        p.nl = H - lt + 1;
-        p.mu_pre = c->mu_pre;
-        p.mu_post = c->mu_post;
-        p.npad = c->npad;
-        p.Z = c->Ainv.p;
-        for (int i = 0; i < p.nl; ++i) {
-            Level& L = *c->lv[lt + i];
-            TailLevel& t = p.lv[i];
-            t.n = L.n;
-            t.ncol = L.ncolours;
-            t.coff = L.dcoff.p;
-            t.rp = L.rp.p;
-            t.col = L.col.p;
-            t.val = L.val.p;
-            t.x = L.x.p;
-            t.b = L.b.p;
-            t.r = L.r.p;
-            t.pc = L.pc.p;
-            t.pw = L.pw.p;
-            t.cptr = L.cptr.p;
-            t.cidx = L.cidx.p;
-            t.cw = L.cw.p;
-        }
-        c->timed(PC_TAIL, lt, s, [&] { return std::max(0, vc_tail(K, p, c->tail_cs, pdl, s)); });
-    } else {
-        c->timed(PC_COARSE, H, s, [&] {
-            return c->coarse_mode == 1 ? vc_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s)
-                                       : vc_coarse_trsv(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s);
-        });
-    }
-    for (int l = lt - 1; l >= 0; --l) {
+    c->timed(PC_COARSE, H, s, [&] {
+        return c->coarse_mode == 1 ? vc_coarse_gemv(K, c->Ainv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s)
+                                   : vc_coarse_trsv(K, c->D.p, c->Linv.p, c->npad, LH.n, LH.b.p, LH.x.p, pdl, s);
+    });
+    for (int l = H - 1; l >= 0; --l) {
         Level& L = *c->lv[l];
-        WindowScope ws(L.has_win ? &L.win : nullptr);
         c->timed(PC_PROLONG, l, s, [&] { return vc_prolong(K, L, *c->lv[l + 1], pdl, s); });
         c->timed(PC_GS, l, s, [&] { return relax(c, K, L, c->mu_post, symmetric, pdl, s); });
     }
@@ -1169,7 +1098,6 @@ void enqueue_vcycle_body(mg_ctx* c, int K, cudaStream_t s, bool symmetric) {
 // One V-cycle and the residual norm of the new iterate into c->rho.
 void enqueue_vcycle(mg_ctx* c, int K, cudaStream_t s) {
     enqueue_vcycle_body(c, K, s, c->symmetric);
-    WindowScope ws(c->lv[0]->has_win ? &c->lv[0]->win : nullptr);
     c->timed(PC_RESNORM, 0, s, [&] {
         return vc_resnorm(K, *c->lv[0], c->partial.p, resnorm_blocks(c->lv[0]->n), c->bnorm.p, c->rho.p, c->pdl, s);
     });
@@ -1335,15 +1263,6 @@ int mg_create(mg_ctx** out, int device, void* cuda_stream) {
     }
     init_vcycle_attributes();
     init_setup_attributes();
-    if (const char* m = getenv("MG_COARSE_SOLVE")) c->coarse_mode = (std::string(m) == "trsv") ? 0 : 1;
-    if (const char* m = getenv("MG_PDL")) c->pdl = std::string(m) != "0";
-    if (const char* m = getenv("MG_PIPE")) c->use_pipe = std::string(m) != "0";
-    if (const char* m = getenv("MG_L2_PERSIST_MB")) c->l2_persist = atoll(m) * 1024 * 1024;
-    if (const char* m = getenv("MG_TAIL_ROWS")) c->tail_rows = atoll(m);
-    if (const char* m = getenv("MG_FLOW_ROWS")) c->flow_rows = atoll(m);
-    if (const char* m = getenv("MG_GS_PERSIST")) c->gs_persist = std::string(m) == "1";
-    if (const char* m = getenv("MG_DEVICE_LOOP")) c->device_loop = std::string(m) != "0";
-    c->tail_cs = tail_cluster_size();
     if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&c->h_rho, sizeof(double) * kMaxK) != cudaSuccess ||
         cudaMallocHost(&c->h_loop, sizeof(LoopState)) != cudaSuccess ||
@@ -1362,6 +1281,22 @@ void mg_destroy(mg_ctx* c) {
 }
 
 const char* mg_last_error(const mg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int mg_set_execution(mg_ctx* c, int flags) {
+    if (!c) return MG_ERR_INVALID_ARG;
+    if (flags & ~(MG_EXEC_NO_PDL | MG_EXEC_NO_PIPE | MG_EXEC_COARSE_TRSV | MG_EXEC_DEVICE_LOOP | MG_EXEC_NO_CLUSTER))
+        return c->fail(MG_ERR_INVALID_ARG, "unknown execution flag");
+    cudaStreamSynchronize(c->stream);
+    c->pdl = !(flags & MG_EXEC_NO_PDL);
+    c->use_pipe = !(flags & MG_EXEC_NO_PIPE);
+    c->coarse_mode = (flags & MG_EXEC_COARSE_TRSV) ? 0 : 1;
+    c->device_loop = (flags & MG_EXEC_DEVICE_LOOP) != 0;
+    c->use_cluster = !(flags & MG_EXEC_NO_CLUSTER);
+    c->drop_graphs();
+    c->have_pattern = false;   // tile / cluster structures are built by the next pattern setup
+    c->have_matrix = false;
+    return MG_OK;
+}
 
 int mg_set_options(mg_ctx* c, int mu_pre, int mu_post) {
     if (!c) return MG_ERR_INVALID_ARG;
@@ -2039,11 +1974,6 @@ static int finish_solve(mg_ctx* c, int32_t k, const double* xint, double* X, dou
         return c->cuda_fail(e, "solve");
     if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "solve");
     if ((e = cudaGetLastError())) return c->cuda_fail(e, "solve kernels");
-    if (c->flow_rows > 0 && c->flow_err.p) {
-        int fe = 0;
-        if ((e = cudaMemcpy(&fe, c->flow_err.p, sizeof(int), cudaMemcpyDeviceToHost))) return c->cuda_fail(e, "solve");
-        if (fe) return c->fail(MG_ERR_CUDA, "dataflow Gauss-Seidel: dependency wait timed out");
-    }
     return MG_OK;
 }
 

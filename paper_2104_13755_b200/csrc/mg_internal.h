@@ -48,6 +48,26 @@ struct DBuf {
     }
 };
 
+// Cluster-resident multicolour GS of one level (k_cluster_smooth): the rows
+// are split into cs spatially contiguous parts (Morton order), CTA p of the
+// cluster owns part p.  Inside the colour-grouped internal order the rows of
+// colour c owned by CTA p are the contiguous range [rowa[c*(cs+1)+p],
+// rowa[c*(cs+1)+p+1]).  Every CTA keeps x of its own rows and of its halo
+// (columns of its rows owned elsewhere) in shared memory; after each colour
+// step it pushes its updated rows to the CTAs whose halo holds them.
+struct ClusterSmoother {
+    int cs = 0;                           // CTAs per cluster (0: level not cluster-smoothed)
+    int smem = 0;                         // dynamic shared memory per CTA (bytes)
+    int rmax = 0, emax = 0;               // most rows / entries of one (CTA, colour) step
+    int nloc_max = 0;                     // most local rows (own + halo) of a CTA
+    DBuf<int32_t> rowa;                   // [ncolours][cs+1] internal row boundaries
+    DBuf<int32_t> lbase;                  // [cs][ncolours] local index of the first own row of colour c
+    DBuf<int32_t> hoff, hrow;             // [cs+1] halo offsets; internal rows of each CTA's halo
+    DBuf<uint16_t> lcol;                  // [nnz] local column index of every entry (in its owner CTA)
+    DBuf<int32_t> soff;                   // [cs][ncolours+1] send-list offsets
+    DBuf<int2> send;                      // {own local row, dst CTA << 16 | dst local row}
+};
+
 // One grid of the hierarchy.  "internal" order = rows grouped by Alg. 3
 // colour (ascending), locality (Morton) order inside a colour; the coarsest
 // level keeps the user order (it has no smoother).
@@ -67,21 +87,15 @@ struct Level {
     bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
     DBuf<int32_t> rcptr, rcidx;           // children lists in gal_order (ordered restriction)
     DBuf<double> rcw;
-    int cl_cs = 0;                        // cluster GS: CTAs per cluster (0: not used)
-    int cl_stride = 0, cl_nown_max = 0, cl_nnz_max = 0;
-    DBuf<int32_t> cl_rp;                  // [cl_cs][cl_stride] local row pointers of each CTA's own rows
-        bool small = false;                   // GS sweeps by the one-CTA shared-memory kernel
-    int small_cap = 0;                    // max nnz of a small-kernel tile
-    DBuf<int32_t> stiles;                 // small-kernel tiles {row0, nrow, e0, e1}, per colour
-    DBuf<int32_t> stoff;                  // [ncolours+1] tile ranges per colour
     bool pipe_unr8 = false;               // k_tile_pipe with 8 gathers per batch (K = 3, 3 CTAs/SM)
     int pipe_lpr = 1;
                      // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
+    // cluster-resident smoothing (k_cluster_smooth, mg_vcycle.cu): all mu sweeps
+    // of this level in one launch of one thread-block cluster; set up by
+    // setup_cluster_smoother (mg_host.cpp)
+    ClusterSmoother cls;
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
-    DBuf<int32_t> dtoff;                  // tile_off on device (persistent GS)
-    bool has_win = false;                 // L2 persisting window over this level's iterate x
-    cudaAccessPolicyWindow win = {};
     std::vector<double> V;                // user-order positions [n][3]
     std::vector<int32_t> colour;          // user order
     std::vector<int32_t> colour_off;      // internal row ranges per colour [ncolours+1]
@@ -117,49 +131,10 @@ struct Level {
     DBuf<double> prow_w;                  // P rows packed: {w0, w1, w2, 0} (this level fine)
     DBuf<int32_t> dperm;                  // perm on device
     DBuf<int32_t> diperm;                 // iperm on device (user -> internal)
-    DBuf<int32_t> dcoff;                  // colour_off on device (coarse tail)
     DBuf<int64_t> di2u;                   // level 0: internal nnz -> user nnz
     DBuf<double> x, b, r;                 // [n][kMaxK] work vectors
-    bool flow = false;                    // GS by the dataflow kernel (per-row sweep counters)
-    DBuf<int> done;                       // [n] completed sweeps per row (monotone, dataflow GS)
 };
 
-// L2 access-policy window applied to the next launches issued by this host
-// thread (set around the fine-level kernels to keep the iterate resident).
-inline const cudaAccessPolicyWindow*& current_window() {
-    static thread_local const cudaAccessPolicyWindow* w = nullptr;
-    return w;
-}
-struct WindowScope {
-    const cudaAccessPolicyWindow* prev;
-    explicit WindowScope(const cudaAccessPolicyWindow* w) : prev(current_window()) { current_window() = w; }
-    ~WindowScope() { current_window() = prev; }
-};
-
-// Device view of one level for the coarse-tail kernel (mg_tail.cu).
-struct TailLevel {
-    int n, ncol;
-    const int32_t* coff;                          // colour ranges [ncol+1]
-    const int32_t* rp;
-    const int32_t* col;
-    const double* val;
-    double* x;
-    double* b;
-    double* r;
-    const int32_t* pc;                            // P of this level (fine) -> next, SoA [3][n]
-    const double* pw;
-    const int32_t* cptr;                          // children of this level's rows (as coarse)
-    const int32_t* cidx;
-    const double* cw;
-};
-constexpr int kTailMaxLevels = 12;
-struct TailParams {
-    int nl;                                       // levels lt..H; lv[nl-1] is the coarsest
-    int mu_pre, mu_post;
-    int npad;
-    const double* Z;                              // explicit inverse of A_H
-    TailLevel lv[kTailMaxLevels];
-};
 
 // Device-side state of the V-cycle loop (mg_solve with the conditional graph).
 struct LoopState {
@@ -176,14 +151,11 @@ constexpr int kLoopHistCycles = 4096;   // device history capacity (cycles)
 // (V-cycle graph).
 // mg_vcycle.cu
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
+int vc_cluster_smooth(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);   // all mu sweeps
+int cluster_smooth_max_cs();              // CTAs per cluster the device supports for k_cluster_smooth (0: none)
+int cluster_smooth_smem(int K, int nloc, int rmax, int emax, int nbuf);   // dynamic shared memory of one CTA
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
-int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s);  // all colours of mu sweeps
-int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s);   // mu dataflow GS sweeps
-int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one CTA
-int small_rows_per_tile();
 int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGraphConditionalHandle h, cudaStream_t s);
-int vc_cluster_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);  // all mu sweeps, one cluster
-int cluster_gs_max_cs();
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
 int vc_restrict(int K, const Level& coarse, const Level& fine, bool pdl, cudaStream_t s);  // coarse.b = P^T fine.r, coarse.x = 0
 int vc_prolong(int K, const Level& fine, const Level& coarse, bool pdl, cudaStream_t s);   // fine.x += P coarse.x
@@ -207,9 +179,6 @@ int pcg_direction(int K, const double* r, const double* z, double* p, int n, dou
                   bool pdl, cudaStream_t s);
 int pcg_step(int K, const Level& L0, double* x, double* r, const double* p, double* q, double* partial, double* sc,
              bool pdl, cudaStream_t s);
-// mg_tail.cu
-int tail_cluster_size();
-int vc_tail(int K, const TailParams& p, int cs, bool pdl, cudaStream_t s);
 // mg_setup.cu
 void init_setup_attributes();
 int launch_gather_rows(int K, const int32_t* iperm, const double* src_user, double* dst_int, int n, cudaStream_t s,
@@ -230,9 +199,6 @@ int launch_apply_mass(int K, const double* M_user, const double* X, double* B, i
 int launch_scatter_vec(const int32_t* iperm, const double* src_int, double* dst_user, int n, cudaStream_t s);
 int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, double* cval, cudaStream_t s);
 int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s);
-int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s);
-int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s);
 int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s);
-int launch_chol_cluster(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s);
 
 }  // namespace mg

@@ -532,439 +532,6 @@ __global__ void k_densify(const int* __restrict__ rp, const int* __restrict__ co
     for (int e = rp[i]; e < rp[i + 1]; ++e) D[(size_t)i * npad + col[e]] = val[e];
 }
 
-__global__ void __launch_bounds__(1024) k_chol_diag(double* __restrict__ D, int npad, int kb, int* err) {
-    __shared__ double Ld[32][33];
-    const int tid = threadIdx.x, r = tid >> 5, c = tid & 31;
-    const int base = kb * 32;
-    Ld[r][c] = D[(size_t)(base + r) * npad + base + c];
-    __syncthreads();
-    for (int p = 0; p < 32; ++p) {
-        if (tid == 0) {
-            double d = Ld[p][p];
-            if (!(d > 0.0)) {
-                atomicExch(err, 1);
-                d = 1.0;
-            }
-            Ld[p][p] = sqrt(d);
-        }
-        __syncthreads();
-        if (tid > p && tid < 32) Ld[tid][p] /= Ld[p][p];
-        __syncthreads();
-        if (r > p && c > p && c <= r) Ld[r][c] -= Ld[r][p] * Ld[c][p];
-        __syncthreads();
-    }
-    D[(size_t)(base + r) * npad + base + c] = (c <= r) ? Ld[r][c] : 0.0;
-}
-
-// panel below the diagonal block: l = a L_kk^{-T}, one thread per row
-constexpr int kTrsmThreads = 64;
-__global__ void __launch_bounds__(kTrsmThreads) k_chol_trsm(double* __restrict__ D, int npad, int kb) {
-    __shared__ double Ld[32][33];
-    const int base = kb * 32;
-    for (int s = threadIdx.x; s < 1024; s += kTrsmThreads) Ld[s >> 5][s & 31] = D[(size_t)(base + (s >> 5)) * npad + base + (s & 31)];
-    __syncthreads();
-    const int i = base + 32 + blockIdx.x * kTrsmThreads + threadIdx.x;
-    if (i >= npad) return;
-    double a[32];
-    double* Di = D + (size_t)i * npad + base;
-#pragma unroll
-    for (int p = 0; p < 32; ++p) a[p] = Di[p];
-#pragma unroll
-    for (int p = 0; p < 32; ++p) {
-        double s = a[p];
-#pragma unroll
-        for (int q = 0; q < p; ++q) s -= a[q] * Ld[p][q];
-        a[p] = s / Ld[p][p];
-    }
-#pragma unroll
-    for (int p = 0; p < 32; ++p) Di[p] = a[p];
-}
-
-__global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ D, int npad, int kb) {
-    __shared__ double Pi[32][33];
-    __shared__ double Pj[32][33];
-    const int t = blockIdx.x;
-    int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    while (ti * (ti + 1) / 2 > t) --ti;
-    const int tj = t - ti * (ti + 1) / 2;
-    const int bi = kb + 1 + ti, bj = kb + 1 + tj;
-    const int base = kb * 32;
-    for (int s = threadIdx.x; s < 1024; s += 256) {
-        const int r = s >> 5, c = s & 31;
-        Pi[r][c] = D[(size_t)(bi * 32 + r) * npad + base + c];
-        Pj[r][c] = D[(size_t)(bj * 32 + r) * npad + base + c];
-    }
-    __syncthreads();
-    for (int s = threadIdx.x; s < 1024; s += 256) {
-        const int r = s >> 5, c = s & 31;
-        if (bi == bj && c > r) continue;
-        double acc = 0.0;
-#pragma unroll
-        for (int p = 0; p < 32; ++p) acc = fma(Pi[r][p], Pj[c][p], acc);
-        D[(size_t)(bi * 32 + r) * npad + bj * 32 + c] -= acc;
-    }
-}
-
-// Cooperative single-launch factorisation (default): the same blocked
-// right-looking algorithm, all phases in one kernel separated by a software
-// grid barrier (co-residency guaranteed by the cooperative launch).
-//   for each 32-wide panel kb:
-//     phase 1: every CTA factors the diagonal block in shared memory (cheap,
-//              redundant) and solves its share of the 32-row blocks below it;
-//              CTA 0 writes L_kk back;
-//     phase 2: the trailing lower triangle gets the rank-32 update, 32x32
-//              tiles distributed over the CTAs.
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        target += gridDim.x;
-        __threadfence();
-        atomicAdd(ctr, 1u);
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-        } while (v < target);
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ void factor_diag_smem(double (*Ld)[33], int* err) {
-    // 32x32 Cholesky in shared memory by 256 threads (rows r = tid >> 3, 8 threads per row)
-    const int tid = threadIdx.x;
-    for (int p = 0; p < 32; ++p) {
-        if (tid == 0) {
-            double d = Ld[p][p];
-            if (!(d > 0.0)) {
-                if (err) atomicExch(err, 1);
-                d = 1.0;
-            }
-            Ld[p][p] = sqrt(d);
-        }
-        __syncthreads();
-        if (tid > p && tid < 32) Ld[tid][p] /= Ld[p][p];
-        __syncthreads();
-        for (int t = tid; t < 1024; t += blockDim.x) {
-            const int r = t >> 5, c = t & 31;
-            if (r > p && c > p && c <= r) Ld[r][c] -= Ld[r][p] * Ld[c][p];
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(256) k_chol_coop(double* __restrict__ D, int npad, int* err, unsigned* ctr) {
-    __shared__ double Ld[32][33];
-    __shared__ double Pi[32][33];
-    __shared__ double Pj[32][33];
-    const int nb = npad / 32;
-    const int tid = threadIdx.x;
-    unsigned target = 0;
-    for (int kb = 0; kb < nb; ++kb) {
-        const int base = kb * 32;
-        // ---- phase 1: diagonal factor + panel solve
-        const int m = nb - kb - 1;   // row blocks below the diagonal
-        const bool busy = (int)blockIdx.x <= m;
-        if (busy) {
-            for (int t = tid; t < 1024; t += 256) Ld[t >> 5][t & 31] = D[(size_t)(base + (t >> 5)) * npad + base + (t & 31)];
-            __syncthreads();
-            factor_diag_smem(Ld, blockIdx.x == 0 ? err : nullptr);
-            for (int ib = kb + 1 + blockIdx.x; ib < nb; ib += gridDim.x) {
-                // rows of block ib: L_ib = A_ib L_kk^{-T}, in shared memory, thread r = row r
-                __syncthreads();
-                for (int t = tid; t < 1024; t += 256)
-                    Pi[t >> 5][t & 31] = D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)];
-                __syncthreads();
-                if (tid < 32) {
-                    for (int p = 0; p < 32; ++p) {
-                        double sum = Pi[tid][p];
-                        for (int q = 0; q < p; ++q) sum -= Pi[tid][q] * Ld[p][q];
-                        Pi[tid][p] = sum / Ld[p][p];
-                    }
-                }
-                __syncthreads();
-                for (int t = tid; t < 1024; t += 256)
-                    D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)] = Pi[t >> 5][t & 31];
-            }
-        }
-        grid_barrier(ctr, target);
-        // L_kk written back only now: every CTA has read A_kk in phase 1
-        if (blockIdx.x == 0) {
-            for (int t = tid; t < 1024; t += 256) {
-                const int r = t >> 5, c = t & 31;
-                D[(size_t)(base + r) * npad + base + c] = (c <= r) ? Ld[r][c] : 0.0;
-            }
-        }
-        // ---- phase 2: trailing update A_ij -= L_ik L_jk^T, kb < j <= i
-        const int ntile = m * (m + 1) / 2;
-        for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
-            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-            while (ti * (ti + 1) / 2 > t) --ti;
-            const int tj = t - ti * (ti + 1) / 2;
-            const int bi = kb + 1 + ti, bj = kb + 1 + tj;
-            __syncthreads();
-            for (int q = tid; q < 1024; q += 256) {
-                const int r = q >> 5, c = q & 31;
-                Pi[r][c] = D[(size_t)(bi * 32 + r) * npad + base + c];
-                Pj[r][c] = D[(size_t)(bj * 32 + r) * npad + base + c];
-            }
-            __syncthreads();
-            for (int q = tid; q < 1024; q += 256) {
-                const int r = q >> 5, c = q & 31;
-                if (bi == bj && c > r) continue;
-                double acc = 0.0;
-#pragma unroll
-                for (int p = 0; p < 32; ++p) acc = fma(Pi[r][p], Pj[c][p], acc);
-                D[(size_t)(bi * 32 + r) * npad + bj * 32 + c] -= acc;
-            }
-        }
-        grid_barrier(ctr, target);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K7a (default): factor AND explicit inverse of the coarsest operator in ONE
-// launch of a thread-block cluster (up to 16 CTAs x 512 threads), phases
-// separated by barrier.cluster:
-//   1. blocked right-looking Cholesky A_H = L L^T (32-wide panels: redundant
-//      diagonal factor per CTA, panel solve, rank-32 trailing update);
-//   2. inverses of the diagonal blocks;
-//   3. W = L^{-1} by block diagonals: W_ij = -inv(L_ii) sum_{k=j}^{i-1} L_ik W_kj;
-//   4. Z = A_H^{-1} = W^T W (both triangles written, for the per-cycle GEMV).
-// All block products are 32x32 shared-memory tile GEMMs.
-constexpr int kCholThreads = 512;
-
-__device__ __forceinline__ void csync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ unsigned crank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned csize() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-
-// acc[e] (e = 0,1) for output (r, c0 + e) of a 32x32 tile, r = tid >> 4, c0 = 2 (tid & 15):
-// acc += op(A) op(B), A/B 32x32 blocks at global row-major addresses with leading dim ld.
-__device__ __forceinline__ void tile_mac(double (&acc)[2], const double* __restrict__ A, bool tA,
-                                         const double* __restrict__ B, bool tB, int ld, double (*As)[33],
-                                         double (*Bs)[33]) {
-    const int tid = threadIdx.x;
-    __syncthreads();
-    for (int q = tid; q < 1024; q += kCholThreads) {
-        const int r = q >> 5, c = q & 31;
-        const double av = A[(size_t)r * ld + c];
-        const double bv = B[(size_t)r * ld + c];
-        if (tA) As[c][r] = av; else As[r][c] = av;
-        if (tB) Bs[c][r] = bv; else Bs[r][c] = bv;
-    }
-    __syncthreads();
-    const int r = tid >> 4, c0 = 2 * (tid & 15);
-#pragma unroll 8
-    for (int p = 0; p < 32; ++p) {
-        const double a = As[r][p];
-        acc[0] = fma(a, Bs[p][c0], acc[0]);
-        acc[1] = fma(a, Bs[p][c0 + 1], acc[1]);
-    }
-}
-
-__global__ void __launch_bounds__(kCholThreads, 1) k_chol_cluster(double* __restrict__ D, double* __restrict__ Linv,
-                                                                  double* __restrict__ W, double* __restrict__ Z,
-                                                                  int npad, int* err) {
-    __shared__ double Ld[32][33];
-    __shared__ double As[32][33];
-    __shared__ double Bs[32][33];
-    const int nb = npad / 32;
-    const int tid = threadIdx.x;
-    const int rank = (int)crank(), ncta = (int)csize();
-    const int r = tid >> 4, c0 = 2 * (tid & 15);
-    // ---- 1. Cholesky
-    for (int kb = 0; kb < nb; ++kb) {
-        const int base = kb * 32;
-        for (int t = tid; t < 1024; t += kCholThreads) Ld[t >> 5][t & 31] = D[(size_t)(base + (t >> 5)) * npad + base + (t & 31)];
-        __syncthreads();
-        for (int p = 0; p < 32; ++p) {
-            if (tid == 0) {
-                double d = Ld[p][p];
-                if (!(d > 0.0)) {
-                    if (rank == 0) atomicExch(err, 1);
-                    d = 1.0;
-                }
-                Ld[p][p] = sqrt(d);
-            }
-            __syncthreads();
-            if (tid > p && tid < 32) Ld[tid][p] /= Ld[p][p];
-            __syncthreads();
-            for (int t = tid; t < 1024; t += kCholThreads) {
-                const int rr = t >> 5, cc = t & 31;
-                if (rr > p && cc > p && cc <= rr) Ld[rr][cc] -= Ld[rr][p] * Ld[cc][p];
-            }
-            __syncthreads();
-        }
-        for (int ib = kb + 1 + rank; ib < nb; ib += ncta) {
-            __syncthreads();
-            for (int t = tid; t < 1024; t += kCholThreads) As[t >> 5][t & 31] = D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)];
-            __syncthreads();
-            if (tid < 32) {
-                for (int p = 0; p < 32; ++p) {
-                    double sum = As[tid][p];
-                    for (int q = 0; q < p; ++q) sum -= As[tid][q] * Ld[p][q];
-                    As[tid][p] = sum / Ld[p][p];
-                }
-            }
-            __syncthreads();
-            for (int t = tid; t < 1024; t += kCholThreads) D[(size_t)(ib * 32 + (t >> 5)) * npad + base + (t & 31)] = As[t >> 5][t & 31];
-        }
-        csync();
-        if (rank == 0)
-            for (int t = tid; t < 1024; t += kCholThreads) {
-                const int rr = t >> 5, cc = t & 31;
-                D[(size_t)(base + rr) * npad + base + cc] = (cc <= rr) ? Ld[rr][cc] : 0.0;
-            }
-        const int m = nb - kb - 1;
-        const int ntile = m * (m + 1) / 2;
-        for (int t = rank; t < ntile; t += ncta) {
-            int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-            while (ti * (ti + 1) / 2 > t) --ti;
-            const int tj = t - ti * (ti + 1) / 2;
-            const int bi = kb + 1 + ti, bj = kb + 1 + tj;
-            double acc[2] = {0.0, 0.0};
-            tile_mac(acc, D + (size_t)(bi * 32) * npad + base, false, D + (size_t)(bj * 32) * npad + base, true, npad, As, Bs);
-            double* out = D + (size_t)(bi * 32 + r) * npad + bj * 32 + c0;
-            if (!(bi == bj && c0 > r)) out[0] -= acc[0];
-            if (!(bi == bj && c0 + 1 > r)) out[1] -= acc[1];
-        }
-        csync();
-    }
-    // ---- 2. inverses of the diagonal blocks (thread t < 32 solves column t)
-    for (int I = rank; I < nb; I += ncta) {
-        __syncthreads();
-        for (int t = tid; t < 1024; t += kCholThreads) Ld[t >> 5][t & 31] = D[(size_t)(I * 32 + (t >> 5)) * npad + I * 32 + (t & 31)];
-        __syncthreads();
-        if (tid < 32) {
-            for (int rr = 0; rr < 32; ++rr) {
-                double sum = (rr == tid) ? 1.0 : 0.0;
-                for (int q = tid; q < rr; ++q) sum -= Ld[rr][q] * As[q][tid];
-                As[rr][tid] = (rr >= tid) ? sum / Ld[rr][rr] : 0.0;
-            }
-        }
-        __syncthreads();
-        for (int t = tid; t < 1024; t += kCholThreads) {
-            const double v = As[t >> 5][t & 31];
-            Linv[(size_t)I * 1024 + t] = v;
-            W[(size_t)(I * 32 + (t >> 5)) * npad + I * 32 + (t & 31)] = v;
-        }
-    }
-    csync();
-    // ---- 3. W = L^{-1}, block diagonals d = 1 .. nb-1
-    for (int dd = 1; dd < nb; ++dd) {
-        for (int j = rank; j + dd < nb; j += ncta) {
-            const int i = j + dd;
-            double acc[2] = {0.0, 0.0};
-            for (int k = j; k < i; ++k)
-                tile_mac(acc, D + (size_t)(i * 32) * npad + k * 32, false, W + (size_t)(k * 32) * npad + j * 32, false,
-                         npad, As, Bs);
-            // T = acc (the tile sum_k L_ik W_kj) -> Bs, then W_ij = -inv(L_ii) T
-            __syncthreads();
-            Bs[r][c0] = acc[0];
-            Bs[r][c0 + 1] = acc[1];
-            for (int q = tid; q < 1024; q += kCholThreads) As[q >> 5][q & 31] = Linv[(size_t)i * 1024 + q];
-            __syncthreads();
-            double o0 = 0.0, o1 = 0.0;
-#pragma unroll 8
-            for (int p = 0; p < 32; ++p) {
-                o0 = fma(As[r][p], Bs[p][c0], o0);
-                o1 = fma(As[r][p], Bs[p][c0 + 1], o1);
-            }
-            double* out = W + (size_t)(i * 32 + r) * npad + j * 32 + c0;
-            out[0] = -o0;
-            out[1] = -o1;
-        }
-        csync();
-    }
-    // ---- 4. Z = W^T W, lower tiles I >= J, mirrored
-    const int ntz = nb * (nb + 1) / 2;
-    for (int t = rank; t < ntz; t += ncta) {
-        int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-        while ((I + 1) * (I + 2) / 2 <= t) ++I;
-        while (I * (I + 1) / 2 > t) --I;
-        const int J = t - I * (I + 1) / 2;
-        double acc[2] = {0.0, 0.0};
-        for (int k = I; k < nb; ++k)
-            tile_mac(acc, W + (size_t)(k * 32) * npad + I * 32, true, W + (size_t)(k * 32) * npad + J * 32, false, npad,
-                     As, Bs);
-        Z[(size_t)(I * 32 + r) * npad + J * 32 + c0] = acc[0];
-        Z[(size_t)(I * 32 + r) * npad + J * 32 + c0 + 1] = acc[1];
-        Z[(size_t)(J * 32 + c0) * npad + I * 32 + r] = acc[0];
-        Z[(size_t)(J * 32 + c0 + 1) * npad + I * 32 + r] = acc[1];
-    }
-}
-
-// Inverse of every 32x32 diagonal block of L (for the solve); thread t
-// computes column t by forward substitution.
-__global__ void __launch_bounds__(32) k_chol_diaginv(const double* __restrict__ D, int npad, double* __restrict__ Linv) {
-    __shared__ double Ld[32][33];
-    const int I = blockIdx.x, t = threadIdx.x;
-    for (int r = 0; r < 32; ++r) Ld[r][t] = D[(size_t)(I * 32 + r) * npad + I * 32 + t];
-    __syncwarp();
-    double z[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-        double s = (r == t) ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = 0; q < r; ++q) s -= Ld[r][q] * z[q];
-        z[r] = (r >= t) ? s / Ld[r][r] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r) Linv[(size_t)I * 1024 + r * 32 + t] = z[r];
-}
-
-// Explicit inverse A_H^{-1} = L^{-T} L^{-1} from the factor: CTA b solves
-// L L^T Z = I for columns [16b, 16b+16) by blocked forward/backward
-// substitution (off-diagonal blocks streamed from L2 as warp-broadcast
-// loads, diagonal blocks applied through their inverses).  Computed once per
-// rebuild; afterwards every coarsest solve is one GEMV (k_coarse_gemv).
-constexpr int kInvCols = 16;
-__global__ void __launch_bounds__(512) k_chol_inverse(const double* __restrict__ L, const double* __restrict__ Linv,
-                                                      int npad, double* __restrict__ Z) {
-    extern __shared__ double sm[];
-    double* Y = sm;                          // [npad][16]
-    double* T = sm + (size_t)npad * kInvCols; // [32][16]
-    const int tid = threadIdx.x, r = tid >> 4, c = tid & 15;
-    const int c0 = blockIdx.x * kInvCols;
-    const int nb = npad / 32;
-    for (int I = 0; I < nb; ++I) {
-        double acc = 0.0;
-        const double* Lr = L + (size_t)(32 * I + r) * npad;
-        for (int j = 0; j < 32 * I; ++j) acc = fma(Lr[j], Y[j * kInvCols + c], acc);
-        T[r * kInvCols + c] = ((32 * I + r) == (c0 + c) ? 1.0 : 0.0) - acc;
-        __syncthreads();
-        double v = 0.0;
-        const double* Li = Linv + (size_t)I * 1024 + r * 32;
-#pragma unroll 8
-        for (int q = 0; q < 32; ++q) v = fma(Li[q], T[q * kInvCols + c], v);
-        Y[(32 * I + r) * kInvCols + c] = v;
-        __syncthreads();
-    }
-    for (int I = nb - 1; I >= 0; --I) {
-        double acc = 0.0;
-        for (int j = 32 * (I + 1); j < npad; ++j) acc = fma(L[(size_t)j * npad + 32 * I + r], Y[j * kInvCols + c], acc);
-        T[r * kInvCols + c] = Y[(32 * I + r) * kInvCols + c] - acc;
-        __syncthreads();
-        double v = 0.0;
-#pragma unroll 8
-        for (int q = 0; q < 32; ++q) v = fma(Linv[(size_t)I * 1024 + q * 32 + r], T[q * kInvCols + c], v);
-        Y[(32 * I + r) * kInvCols + c] = v;
-        __syncthreads();
-    }
-    for (int i = tid; i < npad * kInvCols; i += 512) Z[(size_t)(i / kInvCols) * npad + c0 + (i % kInvCols)] = Y[i];
-}
-
 // ---------------------------------------------------------------------------
 // K7a v3 (default): Cholesky factor AND explicit inverse of A_H in ONE
 // cooperative launch over up to one CTA per SM; dependent phases are
@@ -1298,8 +865,6 @@ void rows_k(int K, bool gather, const int32_t* perm, const double* src, double* 
 
 
 void init_setup_attributes() {
-    const int big = 200 * 1024;
-    cudaFuncSetAttribute(k_chol_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_galerkin_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galt_smem<16>());
     cudaFuncSetAttribute(k_galerkin_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)galt_smem<32>());
 }
@@ -1394,84 +959,6 @@ int launch_densify(const Level& LH, double* D, int npad, cudaStream_t s) {
     k_densify<<<nblk(npad, kBlock), kBlock, 0, s>>>(LH.rp.p, LH.col.p, LH.val.p, LH.n, npad, D);
     return 2;
 }
-int launch_chol_factor(double* D, double* Linv, int npad, int* err, cudaStream_t s) {
-    const int nb = npad / 32;
-    int launches = 0;
-    static unsigned* ctr = nullptr;
-    static int coop_blocks = -1;
-    if (coop_blocks < 0) {
-        int dev = 0, nsm = 0, per = 0, coop = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_coop, 256, 0);
-        coop_blocks = (coop && per > 0 && cudaMalloc(&ctr, sizeof(unsigned)) == cudaSuccess) ? nsm * std::min(per, 1) : 0;
-        cudaGetLastError();
-    }
-    if (coop_blocks > 0 && !getenv("MG_CHOL_LAUNCHES")) {
-        const int grid = std::max(1, std::min(coop_blocks, nb * (nb - 1) / 2 + 1));
-        cudaMemsetAsync(ctr, 0, sizeof(unsigned), s);
-        void* args[] = {&D, &npad, &err, &ctr};
-        cudaLaunchCooperativeKernel((const void*)k_chol_coop, dim3(grid), dim3(256), args, 0, s);
-        k_chol_diaginv<<<nb, 32, 0, s>>>(D, npad, Linv);
-        return 2;
-    }
-    for (int kb = 0; kb < nb; ++kb) {
-        k_chol_diag<<<1, 1024, 0, s>>>(D, npad, kb, err);
-        ++launches;
-        const int m = nb - kb - 1;
-        if (m > 0) {
-            k_chol_trsm<<<nblk(32 * m, kTrsmThreads), kTrsmThreads, 0, s>>>(D, npad, kb);
-            k_chol_update<<<m * (m + 1) / 2, 256, 0, s>>>(D, npad, kb);
-            launches += 2;
-        }
-    }
-    k_chol_diaginv<<<nb, 32, 0, s>>>(D, npad, Linv);
-    return launches + 1;
-}
-int chol_cluster_size() {
-    static int cs = -1;
-    if (cs >= 0) return cs;
-    cudaFuncSetAttribute(k_chol_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cs = 0;
-    for (int c : {16, 8, 4}) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(c);
-        cfg.blockDim = dim3(kCholThreads);
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = c;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, k_chol_cluster, &cfg) == cudaSuccess && ncl >= 1) {
-            cs = c;
-            break;
-        }
-        cudaGetLastError();
-    }
-    return cs;
-}
-
-int launch_chol_cluster(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s) {
-    const int cs = chol_cluster_size();
-    if (cs <= 0) return -1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kCholThreads);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_chol_cluster, D, Linv, W, Z, npad, err) == cudaSuccess ? 1 : -1;
-}
-
 int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, int* err, cudaStream_t s) {
     static unsigned* ctr = nullptr;
     static int grid_max = -1;
@@ -1489,39 +976,12 @@ int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, in
     const int grid = std::max(2, std::min(grid_max, nb * (nb + 1) / 2 + 1));   // CTA 0 + >= 1 worker
     if (grid_max < 2) return -1;
     if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess) return -1;
-    // MG_CHOL_TRACE: CTA 0 phase timestamps (%globaltimer), printed to stderr
-    static unsigned long long* tr = nullptr;
-    const bool trace = getenv("MG_CHOL_TRACE") != nullptr;
-    if (trace && !tr && cudaMalloc(&tr, 256 * sizeof(unsigned long long)) != cudaSuccess) tr = nullptr;
-    unsigned long long* trp = trace ? tr : nullptr;
-    if (trp) cudaMemsetAsync(trp, 0, 256 * sizeof(unsigned long long), s);
+    unsigned long long* trp = nullptr;   // phase timestamps of CTA 0 (debug builds pass a buffer)
     void* args[] = {&D, &Linv, &W, &Z, &npad, &err, &ctr, &trp};
     const bool ok = cudaLaunchCooperativeKernel((const void*)k_chol_grid, dim3(grid), dim3(kCgThreads), args, 0, s) ==
                     cudaSuccess;
-    if (ok && trp) {
-        // one ZERO-sized extra slot marks the end of Z: the kernel's completion
-        unsigned long long h[256];
-        cudaStreamSynchronize(s);
-        cudaMemcpy(h, trp, sizeof(h), cudaMemcpyDeviceToHost);
-        double p1 = 0, b1 = 0, p2 = 0, b2 = 0;
-        for (int k = 0; k + 1 < nb; ++k) {
-            p1 += (h[3 + 4 * k] - (k ? h[6 + 4 * (k - 1)] : h[2])) * 1e-3;
-            b1 += (h[4 + 4 * k] - h[3 + 4 * k]) * 1e-3;
-            p2 += (h[5 + 4 * k] - h[4 + 4 * k]) * 1e-3;
-            b2 += (h[6 + 4 * k] - h[5 + 4 * k]) * 1e-3;
-        }
-        fprintf(stderr, "[chol trace] prelude: load %.1f chol32 %.1f trinv32 %.1f\n", (h[200] - h[0]) * 1e-3,
-                (h[201] - h[200]) * 1e-3, (h[202] - h[201]) * 1e-3);
-        fprintf(stderr, "[chol trace] prelude %.1f us, P1 %.1f, bar1 %.1f, P2 %.1f, bar2 %.1f, tail %.1f us (npad %d)\n",
-                (h[2] - h[0]) * 1e-3, p1, b1, p2, b2, (h[101] - h[100]) * 1e-3, npad);
-    }
     return ok ? 1 : -1;
 }
 
-int launch_chol_inverse(const double* D, const double* Linv, int npad, double* Z, cudaStream_t s) {
-    const size_t smem = sizeof(double) * ((size_t)npad * kInvCols + 32 * kInvCols);
-    k_chol_inverse<<<npad / kInvCols, 512, smem, s>>>(D, Linv, npad, Z);
-    return 1;
-}
 
 }  // namespace mg

@@ -493,505 +493,6 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
 }
 
 // ---------------------------------------------------------------------------
-// Persistent multicolour GS for the tiled levels (level 0): ALL colour passes
-// of mu sweeps in ONE cooperative launch.  Each CTA walks its tiles of
-// colour c (t = off[c] + blockIdx.x + i * G), colour after colour, sweep
-// after sweep, through the same double-buffered TMA-bulk stage ring as
-// k_tile_pipe; the matrix part of the next tiles is streamed ACROSS colour
-// boundaries (A never changes during the solve), so HBM stays busy while the
-// CTAs meet at the grid barrier that separates colour classes (multicolour GS
-// semantics: colour c reads the x written by colours < c of this sweep).
-// The barrier is a monotone 64-bit counter (base taken modulo G at entry);
-// its acquire fence also invalidates L1, so gathers after it see the
-// neighbours' new x.  Same arithmetic per row as k_tile_pipe<K, 0>.
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-template <int K>
-__global__ void __launch_bounds__(kTile, 4) k_gs_persist(const TileDesc* __restrict__ tiles,
-                                                         const int* __restrict__ toff, int ncol, int mu, int reverse,
-                                                         const int* __restrict__ rp, const int* __restrict__ col,
-                                                         const double* __restrict__ val, const double* __restrict__ b,
-                                                         double* __restrict__ x, int cap,
-                                                         unsigned long long* __restrict__ ctr) {
-    extern __shared__ __align__(128) unsigned char smem_pipe[];
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ unsigned long long s_base;
-    const int tid = threadIdx.x;
-    const int G = gridDim.x;
-    const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
-    unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
-    uint64_t pol = 0;
-    if (tid == 0) {
-        pol = evict_first_policy();
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_base = ld_acquire_u64(ctr) / (unsigned long long)G * (unsigned long long)G;
-    }
-    __syncthreads();
-    unsigned long long target = s_base;
-    // task cursor over (sweep, colour step, i); ntask(c) = this CTA's tiles of colour c
-    auto colour_of = [&](int q) { return reverse ? ncol - 1 - q : q; };
-    auto ntask = [&](int c) {
-        const int nt = __ldg(toff + c + 1) - __ldg(toff + c);
-        return nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + G - 1) / G : 0;
-    };
-    const int nsteps = mu * ncol;
-    // prefetch cursor: (step ps, index pi) of the next task whose A data is issued
-    int ps = 0, pi = 0, issued = 0;
-    auto issue_next = [&]() {   // thread 0 only
-        while (ps < nsteps && pi >= ntask(colour_of(ps % ncol))) {
-            ++ps;
-            pi = 0;
-        }
-        if (ps >= nsteps) return;
-        const int c = colour_of(ps % ncol);
-        const TileDesc d = tiles[__ldg(toff + c) + blockIdx.x + pi * G];
-        issue_tile(d, stage[issued & 1], cap, &bar[issued & 1], rp, col, val, pol);
-        ++pi;
-        ++issued;
-    };
-    if (tid == 0) {
-        issue_next();
-        issue_next();
-    }
-    const uint64_t xpol = evict_last_policy();
-    const uint64_t spol = evict_first_policy();
-    int done = 0;   // tasks consumed by this CTA
-    for (int step = 0; step < nsteps; ++step) {
-        const int c = colour_of(step % ncol);
-        const int mine = ntask(c);
-        const int t0 = __ldg(toff + c);
-        for (int i = 0; i < mine; ++i) {
-            const int sidx = done & 1;
-            const TileDesc d = tiles[t0 + blockIdx.x + i * G];
-            mbar_wait(&bar[sidx], (unsigned)((done >> 1) & 1));
-            const StageView v = view_tile(d, stage[sidx], cap);
-            if (tid < d.nrow) {
-                const int row = d.row0 + tid;
-                double bv[K];
-                ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
-                double sacc[K], dg;
-                stage_row<K, PipeUnroll<K>::value>(v, tid, row, x, sacc, dg, xpol);
-                double xn[K];
-#pragma unroll
-                for (int k = 0; k < K; ++k) xn[k] = (bv[k] - sacc[k]) / dg;
-                strow_pol<K>(x + (size_t)row * VS<K>::S, xn, xpol);
-            }
-            __syncthreads();   // stage consumed
-            ++done;
-            if (tid == 0) issue_next();
-        }
-        if (step + 1 < nsteps) {   // colour boundary: grid barrier
-            target += (unsigned long long)G;
-            __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(ctr, 1ull);
-                while (ld_acquire_u64(ctr) < target) {
-                }
-                __threadfence();
-            }
-            __syncthreads();
-        }
-    }
-}
-
-template <int K>
-int launch_gs_persist_k(const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s) {
-    static int per_sm = -2, nsm = 0;
-    const size_t smem = 2 * ((stage_bytes(L.pipe_cap) + 127) / 128 * 128);
-    if (per_sm == -2) {
-        int dev = 0, coop = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        cudaFuncSetAttribute(k_gs_persist<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        per_sm = coop ? 0 : -1;
-        cudaGetLastError();
-    }
-    if (per_sm == -1) return -1;
-    int per = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gs_persist<K>, kTile, smem) != cudaSuccess || per <= 0) {
-        cudaGetLastError();
-        return -1;
-    }
-    int maxt = 1;
-    for (int c = 0; c < L.ncolours; ++c) maxt = std::max(maxt, L.tile_off[c + 1] - L.tile_off[c]);
-    const int grid = std::max(1, std::min(per * nsm, maxt));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kTile);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_gs_persist<K>, reinterpret_cast<const TileDesc*>(L.tiles.p),
-                              (const int*)L.dtoff.p, L.ncolours, mu, reverse ? 1 : 0, (const int*)L.rp.p,
-                              (const int*)L.col.p, (const double*)L.val.p, (const double*)L.b.p, L.x.p, L.pipe_cap,
-                              ctr) == cudaSuccess
-               ? 1
-               : -1;
-}
-
-// ---------------------------------------------------------------------------
-// Small levels (a few thousand rows): all mu GS sweeps of the level in ONE
-// CTA.  The level's iterate lives in shared memory (compact [n][K]); the
-// matrix rows and right-hand side of each 128-row tile of a colour class are
-// streamed into a double-buffered stage with TMA bulk copies while the
-// previous tile is computed, so a colour step costs a __syncthreads instead
-// of a dependent launch + L2 round trips (the per-launch floor measured
-// ~2.2 us per colour pass on these levels).  LPR = 8 lanes per row take
-// entries l, l+8, ... (the order of k_lpr_sweep<K,8>), fixed-order shuffle
-// reduction; tiles of one colour are independent, colours run in order
-// (reversed for the symmetric cycle's post-smoothing).
-constexpr int kSmallThreads = 1024;
-constexpr int kSmallLPR = 8;
-constexpr int kSmallRows = kSmallThreads / kSmallLPR;
-
-template <int K>
-__host__ __device__ inline size_t small_stage_bytes(int cap) {
-    const size_t a = (stage_bytes(cap) + 15) / 16 * 16;
-    return (a + (size_t)(kSmallRows + 2) * VS<K>::S * 8 + 127) / 128 * 128;
-}
-template <int K>
-__host__ __device__ inline size_t small_smem_bytes(int n, int cap) {
-    return ((size_t)n * K * 8 + 127) / 128 * 128 + 2 * small_stage_bytes<K>(cap);
-}
-
-template <int K>
-__device__ __forceinline__ void small_issue(const TileDesc& d, unsigned char* stage, int cap, uint64_t* bar,
-                                            const int* rp, const int* col, const double* val, const double* b,
-                                            uint64_t pol) {
-    constexpr int S = VS<K>::S;
-    const int ra = d.row0 & ~3;
-    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
-    const int ca = d.e0 & ~3;
-    const int ccnt = (d.e1 - ca + 3) & ~3;
-    const int va = d.e0 & ~1;
-    const int vcnt = (d.e1 - va + 1) & ~1;
-    // b rows [row0, row0 + nrow) of S doubles, 16-byte aligned and padded
-    const int ba = S >= 2 ? d.row0 : (d.row0 & ~1);
-    const int bcnt = S >= 2 ? d.nrow * S : ((d.row0 + d.nrow - ba + 1) & ~1);
-    int* rps = reinterpret_cast<int*>(stage);
-    int* cs = rps + (kTile + 8);
-    double* vs = reinterpret_cast<double*>(stage + ((size_t)stage_ints(cap) * 4 + 15) / 16 * 16);
-    double* bs = reinterpret_cast<double*>(stage + (stage_bytes(cap) + 15) / 16 * 16);
-    const unsigned bytes = (unsigned)(rcnt * 4 + ccnt * 4 + vcnt * 8 + bcnt * 8);
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(rps, rp + ra, rcnt * 4, bar, pol);
-    if (ccnt > 0) bulk_g2s(cs, col + ca, ccnt * 4, bar, pol);
-    if (vcnt > 0) bulk_g2s(vs, val + va, vcnt * 8, bar, pol);
-    bulk_g2s(bs, b + (size_t)ba * S, bcnt * 8, bar, pol);
-}
-
-template <int K>
-__global__ void __launch_bounds__(kSmallThreads, 1) k_small_gs(const TileDesc* __restrict__ tiles,
-                                                               const int* __restrict__ toff, int ncol, int mu,
-                                                               int reverse, const int* __restrict__ rp,
-                                                               const int* __restrict__ col,
-                                                               const double* __restrict__ val,
-                                                               const double* __restrict__ b, double* __restrict__ x,
-                                                               int n, int cap) {
-    constexpr int S = VS<K>::S;
-    constexpr int G = kSmallLPR;
-    extern __shared__ __align__(128) unsigned char smem_small[];
-    __shared__ __align__(8) uint64_t bar[2];
-    double* xs = reinterpret_cast<double*>(smem_small);
-    const size_t xoff = ((size_t)n * K * 8 + 127) / 128 * 128;
-    const size_t sb = small_stage_bytes<K>(cap);
-    unsigned char* stage[2] = {smem_small + xoff, smem_small + xoff + sb};
-    const int tid = threadIdx.x;
-    const int grp = tid / G;
-    const int lane = tid & (G - 1);
-    pdl_launch_dependents();
-    uint64_t pol = 0;
-    if (tid == 0) {
-        pol = evict_first_policy();
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // task cursor over (sweep, colour step, tile of the colour)
-    const int nsteps = mu * ncol;
-    int ps = 0, pt = 0, issued = 0;
-    auto colour_of = [&](int q) { return reverse ? ncol - 1 - q : q; };
-    auto issue_next = [&]() {   // thread 0 only
-        while (ps < nsteps) {
-            const int c = colour_of(ps % ncol);
-            if (__ldg(toff + c) + pt < __ldg(toff + c + 1)) break;
-            ++ps;
-            pt = 0;
-        }
-        if (ps >= nsteps) return;
-        const int c = colour_of(ps % ncol);
-        const TileDesc d = tiles[__ldg(toff + c) + pt];
-        small_issue<K>(d, stage[issued & 1], cap, &bar[issued & 1], rp, col, val, b, pol);
-        ++pt;
-        ++issued;
-    };
-    pdl_wait();   // x and b come from the previous kernels
-    if (tid == 0) {
-        issue_next();
-        issue_next();
-    }
-    for (int i = tid; i < n; i += kSmallThreads) {
-        double v[K];
-        ldrow<K>(x + (size_t)i * S, v);
-#pragma unroll
-        for (int c = 0; c < K; ++c) xs[(size_t)i * K + c] = v[c];
-    }
-    __syncthreads();
-    int done = 0;
-    for (int step = 0; step < nsteps; ++step) {
-        const int c = colour_of(step % ncol);
-        const int t0 = __ldg(toff + c), t1 = __ldg(toff + c + 1);
-        for (int t = t0; t < t1; ++t) {
-            const int sidx = done & 1;
-            const TileDesc d = tiles[t];
-            mbar_wait(&bar[sidx], (unsigned)((done >> 1) & 1));
-            const StageView v = view_tile(d, stage[sidx], cap);
-            const double* bs = reinterpret_cast<const double*>(stage[sidx] + (stage_bytes(cap) + 15) / 16 * 16) +
-                               (S >= 2 ? 0 : (d.row0 & 1));
-            const bool valid = grp < d.nrow;
-            const int row = d.row0 + grp;
-            const int qb = valid ? v.rps[grp] : 0, qe = valid ? v.rps[grp + 1] : 0;
-            double sacc[K], dg = 0.0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) sacc[k] = 0.0;
-            for (int q = qb + lane; q < qe; q += G) {
-                const int j = v.cs[q];
-                const double a = v.vs[q];
-                if (j == row) {
-                    dg += a;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) sacc[k] = fma(a, xs[(size_t)j * K + k], sacc[k]);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) sacc[k] = group_sum<G>(sacc[k], 0xffffffffu);
-            dg = group_sum<G>(dg, 0xffffffffu);
-            if (valid && lane == 0) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) xs[(size_t)row * K + k] = (bs[(size_t)grp * S + k] - sacc[k]) / dg;
-            }
-            __syncthreads();   // stage consumed; this tile's x visible to the next colour
-            ++done;
-            if (tid == 0) issue_next();
-        }
-    }
-    for (int i = tid; i < n; i += kSmallThreads) {
-        double v[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) v[c] = xs[(size_t)i * K + c];
-        strow<K>(x + (size_t)i * S, v);
-    }
-}
-
-template <int K>
-int launch_small_gs_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    const size_t smem = small_smem_bytes<K>(L.n, L.small_cap);
-    if (smem > 220 * 1024) return -1;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_small_gs<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr = true;
-    }
-    launch_k(pdl, k_small_gs<K>, 1, kSmallThreads, smem, s, reinterpret_cast<const TileDesc*>(L.stiles.p),
-             (const int*)L.stoff.p, L.ncolours, mu, reverse ? 1 : 0, (const int*)L.rp.p, (const int*)L.col.p,
-             (const double*)L.val.p, (const double*)L.b.p, L.x.p, L.n, L.small_cap);
-    return 1;
-}
-
-// ---------------------------------------------------------------------------
-// Small levels on one thread-block cluster: all mu GS sweeps of the level in
-// ONE launch of CS CTAs (16 where the device allows the non-portable size).
-// Every CTA holds a full replica of the level's iterate in shared memory and
-// the rows i = rank + q CS it owns (their A rows and b) — nothing but the
-// replica is read during the sweeps.  Per colour class each CTA updates its
-// own rows (8 lanes per row, entries l, l+8, ... as k_lpr_sweep<K,8>,
-// fixed-order shuffle reduction), writes the new values into its replica and
-// into every other CTA's replica with distributed-shared-memory stores, then
-// one barrier.cluster (release/acquire) separates colour classes — instead of
-// one dependent kernel launch and an L2 round trip per colour.
-constexpr int kCgThreads = 256;
-constexpr int kCgLPR = 8;
-
-__device__ __forceinline__ unsigned cg_rank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned cg_size() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cg_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ unsigned cg_mapa(const void* p, unsigned cta) {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(cta));
-    return r;
-}
-__device__ __forceinline__ void cg_st_remote(unsigned addr, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-
-// own rows of CTA r below row X: #{i < X : i = r (mod CS)}
-__device__ __forceinline__ int cg_count(int X, int r, int CS) { return X > r ? (X - r + CS - 1) / CS : 0; }
-
-template <int K>
-__host__ __device__ inline size_t cluster_gs_smem(int n, int nown_max, int nnz_own_max) {
-    size_t o = ((size_t)n * K * 8 + 15) / 16 * 16;               // replica of x
-    o += ((size_t)nnz_own_max * 8 + 15) / 16 * 16;                // own A values
-    o += ((size_t)nown_max * K * 8 + 15) / 16 * 16;               // own b
-    o += ((size_t)nnz_own_max * 4 + 15) / 16 * 16;                // own A columns
-    o += ((size_t)(nown_max + 1) * 4 + 15) / 16 * 16;             // own row pointers
-    return o;
-}
-
-template <int K>
-__global__ void __launch_bounds__(kCgThreads, 1) k_cluster_gs(int n, int ncol, const int* __restrict__ coff,
-                                                              const int* __restrict__ rp, const int* __restrict__ col,
-                                                              const double* __restrict__ val,
-                                                              const double* __restrict__ b, double* __restrict__ x,
-                                                              const int* __restrict__ cl_rp, int cl_stride,
-                                                              int nown_max, int nnz_own_max, int mu, int reverse) {
-    constexpr int S = VS<K>::S;
-    constexpr int G = kCgLPR;
-    extern __shared__ __align__(16) unsigned char smem_cg[];
-    const int CS = (int)cg_size(), r = (int)cg_rank();
-    const int tid = threadIdx.x, grp = tid / G, lane = tid & (G - 1), ngrp = kCgThreads / G;
-    const int nown = cg_count(n, r, CS);
-    double* xs = reinterpret_cast<double*>(smem_cg);
-    size_t o = ((size_t)n * K * 8 + 15) / 16 * 16;
-    double* av = reinterpret_cast<double*>(smem_cg + o);
-    o += ((size_t)nnz_own_max * 8 + 15) / 16 * 16;
-    double* bs = reinterpret_cast<double*>(smem_cg + o);
-    o += ((size_t)nown_max * K * 8 + 15) / 16 * 16;
-    int* ac = reinterpret_cast<int*>(smem_cg + o);
-    o += ((size_t)nnz_own_max * 4 + 15) / 16 * 16;
-    int* lrp = reinterpret_cast<int*>(smem_cg + o);
-    const int* grp_rp = cl_rp + (size_t)r * cl_stride;
-    pdl_launch_dependents();
-    // own rows of A (constant during the solve) before the dependency wait
-    for (int q = tid; q <= nown; q += kCgThreads) lrp[q] = grp_rp[q];
-    for (int q = grp; q < nown; q += ngrp) {
-        const int i = r + q * CS;
-        const int e0 = rp[i], len = rp[i + 1] - e0, base = grp_rp[q];
-        for (int t = lane; t < len; t += G) {
-            ac[base + t] = col[e0 + t];
-            av[base + t] = val[e0 + t];
-        }
-    }
-    pdl_wait();
-    for (int i = tid; i < n; i += kCgThreads) {
-        double v[K];
-        ldrow<K>(x + (size_t)i * S, v);
-#pragma unroll
-        for (int k = 0; k < K; ++k) xs[(size_t)i * K + k] = v[k];
-    }
-    for (int q = tid; q < nown; q += kCgThreads) {
-        double v[K];
-        ldrow<K>(b + (size_t)(r + q * CS) * S, v);
-#pragma unroll
-        for (int k = 0; k < K; ++k) bs[(size_t)q * K + k] = v[k];
-    }
-    cg_sync();   // every replica loaded before any CTA writes into it
-    const unsigned gmask = group_mask(G);
-    for (int step = 0; step < mu * ncol; ++step) {
-        const int c = reverse ? ncol - 1 - step % ncol : step % ncol;
-        const int q0 = cg_count(__ldg(coff + c), r, CS), q1 = cg_count(__ldg(coff + c + 1), r, CS);
-        for (int q = q0 + grp; q < q1; q += ngrp) {
-            const int i = r + q * CS;
-            double sacc[K], dg = 0.0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) sacc[k] = 0.0;
-            for (int t = lrp[q] + lane; t < lrp[q + 1]; t += G) {
-                const int j = ac[t];
-                const double a = av[t];
-                if (j == i) {
-                    dg += a;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) sacc[k] = fma(a, xs[(size_t)j * K + k], sacc[k]);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) sacc[k] = group_sum<G>(sacc[k], gmask);
-            dg = group_sum<G>(dg, gmask);
-            double xn[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) xn[k] = (bs[(size_t)q * K + k] - sacc[k]) / dg;
-            // lane l writes the replicas of CTAs l, l + 8 (its own one locally)
-            for (int d = lane; d < CS; d += G) {
-                if (d == r) {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) xs[(size_t)i * K + k] = xn[k];
-                } else {
-                    const unsigned ra = cg_mapa(xs + (size_t)i * K, (unsigned)d);
-#pragma unroll
-                    for (int k = 0; k < K; ++k) cg_st_remote(ra + 8u * k, xn[k]);
-                }
-            }
-        }
-        cg_sync();
-    }
-    for (int q = tid; q < nown; q += kCgThreads) {
-        const int i = r + q * CS;
-        double v[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) v[k] = xs[(size_t)i * K + k];
-        strow<K>(x + (size_t)i * S, v);
-    }
-}
-
-template <int K>
-int launch_cluster_gs_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    const size_t smem = cluster_gs_smem<K>(L.n, L.cl_nown_max, L.cl_nnz_max);
-    if (smem > 220 * 1024 || L.cl_cs <= 0) return -1;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_cluster_gs<K>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(k_cluster_gs<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(L.cl_cs);
-    cfg.blockDim = dim3(kCgThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = L.cl_cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 2 : 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cluster_gs<K>, L.n, L.ncolours, (const int*)L.dcoff.p,
-                                             (const int*)L.rp.p, (const int*)L.col.p, (const double*)L.val.p,
-                                             (const double*)L.b.p, L.x.p, (const int*)L.cl_rp.p, L.cl_stride,
-                                             L.cl_nown_max, L.cl_nnz_max, mu, reverse ? 1 : 0);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return -1;
-    }
-    return 1;
-}
-
-// ---------------------------------------------------------------------------
 // LPR lanes per row (levels with long rows: Galerkin fill).  Each lane
 // prefetches up to U = 32/LPR (col, val) of its row in the PDL prologue;
 // after the wait its x gathers go out in batches of GB independent loads.
@@ -1096,150 +597,266 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
 }
 
 // ---------------------------------------------------------------------------
-// Dataflow multicolour Gauss-Seidel (all mu sweeps of one level in ONE
-// cooperative launch).  The colour classes are dependency levels, not global
-// barriers: row i of colour c in sweep s needs its neighbours of colours
-// processed before c to have finished sweep s and its other neighbours to
-// have finished sweep s-1 (and, by the same rule applied to them, not sweep s:
-// they wait for i).  Every row carries a monotone counter done[i] of completed
-// sweeps (release store after its x is written; neighbours poll it with
-// acquire loads and read x through L2), so each colour step costs a flag
-// round trip instead of a kernel launch + drain.  The arithmetic of a row is
-// exactly the per-launch kernel's (same entries, same order).  Groups walk
-// their rows in (sweep, colour) order and every dependency points to an
-// earlier step, so with all CTAs co-resident (cooperative launch) the
-// earliest pending row can always run; a bounded spin sets *err instead of
-// hanging if that is ever violated.
-__device__ __forceinline__ int ld_acquire_i32(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+// Cluster-resident multicolour Gauss-Seidel (levels whose colour passes are
+// launch-bound; structure: ClusterSmoother, mg_internal.h).  All mu sweeps of
+// a level run in ONE launch of one thread-block cluster: CTA p owns a
+// spatially contiguous part of the rows and keeps x of its own rows and of
+// its halo in shared memory.  A colour step is
+//   * the step's rows, entries, local columns and right-hand sides arrive by
+//     16-byte cp.async, issued one step ahead (double buffer): A does not
+//     change during the solve, so nothing of it is on the step's critical
+//     path;
+//   * LPR lanes per row, lane l takes the entries l, l+LPR, ... in order and a
+//     fixed xor-butterfly sums the lanes -- exactly the arithmetic of
+//     k_lpr_sweep<K, LPR, 0>, so the iterate is bitwise the per-colour-launch
+//     one (tested);
+//   * updated rows are pushed into the shared memory of the CTAs whose halo
+//     holds them (st.shared::cluster), then barrier.cluster (release /
+//     acquire) ends the step.
+// Per colour step this costs one cluster barrier and a few shared-memory
+// round trips instead of a kernel launch and an L2 round trip.
+constexpr int kClsThreads = 256;
+
+__device__ __forceinline__ void cls_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ int ld_relaxed_i32(const int* p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ unsigned cls_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
 }
-__device__ __forceinline__ void st_release_i32(int* p, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ unsigned cls_mapa(const void* p, unsigned cta) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void cls_st_remote(unsigned addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cls_cp16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ int al16(int bytes) { return (bytes + 15) & ~15; }
+
+// bytes of one step buffer: row pointers, values, local columns, right-hand sides
+__host__ __device__ inline int cls_buf_bytes(int S, int rmax, int emax) {
+    return ((rmax + 1 + 4) * 4 + 15) / 16 * 16 + ((emax + 2) * 8 + 15) / 16 * 16 + ((emax + 8) * 2 + 15) / 16 * 16 +
+           ((rmax * S + 2) * 8 + 15) / 16 * 16;
 }
 
 template <int K, int LPR>
-__global__ void __launch_bounds__(kBlock) k_gs_flow(const int* __restrict__ rp, const int* __restrict__ col,
-                                                    const double* __restrict__ val, const double* __restrict__ b,
-                                                    double* __restrict__ x, int* __restrict__ done,
-                                                    const int* __restrict__ coff, int ncol, int mu, int reverse,
-                                                    int* __restrict__ err) {
-    const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
-    const int lane = threadIdx.x & (LPR - 1);
-    const int ngroups = gridDim.x * (kBlock / LPR);
-    const unsigned mask = group_mask(LPR);
-    const int base = ld_acquire_i32(done);   // every row holds the same count at launch
-    for (int sw = 0; sw < mu; ++sw) {
-        for (int q = 0; q < ncol; ++q) {
-            const int c = reverse ? ncol - 1 - q : q;
-            const int r0 = __ldg(coff + c), r1 = __ldg(coff + c + 1);
-            for (int row = r0 + g; row < r1; row += ngroups) {   // whole groups iterate together
-                const int e0 = __ldg(rp + row), e1 = __ldg(rp + row + 1);
-                double sacc[K];
+__global__ void __launch_bounds__(kClsThreads, 1) k_cluster_smooth(
+    int ncol, int mu, int rev, int rmax, int emax, const int* __restrict__ rowa, const int* __restrict__ lbase,
+    const int* __restrict__ hoff, const int* __restrict__ hrow, const uint16_t* __restrict__ lcol,
+    const int* __restrict__ soff, const int2* __restrict__ send, const int* __restrict__ rp,
+    const double* __restrict__ val, const double* __restrict__ b, double* __restrict__ x, int nloc_max, int nbuf) {
+    constexpr int S = VS<K>::S;
+    extern __shared__ __align__(16) unsigned char cls_sm[];
+    const int cs = (int)gridDim.x;   // one cluster
+    const int p = (int)cls_rank();
+    const int tid = threadIdx.x;
+    double* xs = reinterpret_cast<double*>(cls_sm);   // [nloc][K]
+    const int bufb = cls_buf_bytes(S, rmax, emax);
+    unsigned char* buf0 = cls_sm + al16(nloc_max * K * 8);
+    pdl_launch_dependents();
+    // the step's windows: rows [a, bb) of colour c owned by this CTA
+    auto rows_of = [&](int c, int& a, int& bb) {
+        a = __ldg(rowa + c * (cs + 1) + p);
+        bb = __ldg(rowa + c * (cs + 1) + p + 1);
+    };
+    auto colour_of = [&](int t) {
+        const int q = t % ncol;
+        return rev ? ncol - 1 - q : q;
+    };
+    struct View {
+        const int* rps;
+        const double* vs;
+        const uint16_t* ls;
+        const double* bs;
+    };
+    // issue the cp.async copies of step t into buffer t & 1
+    auto issue = [&](int t) {
+        if (t >= mu * ncol) return;
+        int a, bb;
+        rows_of(colour_of(t), a, bb);
+        if (bb <= a) return;
+        unsigned char* base = buf0 + (size_t)((t & 1) & (nbuf - 1)) * bufb;
+        const int e0 = __ldg(rp + a), e1 = __ldg(rp + bb);
+        const uintptr_t w[4] = {reinterpret_cast<uintptr_t>(rp + a), reinterpret_cast<uintptr_t>(val + e0),
+                                reinterpret_cast<uintptr_t>(lcol + e0), reinterpret_cast<uintptr_t>(b + (size_t)a * S)};
+        const int bytes[4] = {(bb - a + 1) * 4, (e1 - e0) * 8, (e1 - e0) * 2, (bb - a) * S * 8};
+        const int cap[4] = {al16((rmax + 1 + 4) * 4), al16((emax + 2) * 8), al16((emax + 8) * 2),
+                            al16((rmax * S + 2) * 8)};
+        int off = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uintptr_t lo = w[k] & ~(uintptr_t)15;
+            const int n16 = (int)((w[k] - lo) + bytes[k] + 15) / 16;
+            for (int q = tid; q < n16; q += kClsThreads) cls_cp16(base + off + 16 * q, reinterpret_cast<const void*>(lo + 16 * (uintptr_t)q));
+            off += cap[k];
+        }
+    };
+    auto view = [&](int t, int a, int e0) {
+        unsigned char* base = buf0 + (size_t)((t & 1) & (nbuf - 1)) * bufb;
+        const uintptr_t hr = reinterpret_cast<uintptr_t>(rp + a) & 15, hv = reinterpret_cast<uintptr_t>(val + e0) & 15,
+                        hl = reinterpret_cast<uintptr_t>(lcol + e0) & 15, hb = reinterpret_cast<uintptr_t>(b + (size_t)a * S) & 15;
+        View v;
+        int off = 0;
+        v.rps = reinterpret_cast<const int*>(base + off + hr);
+        off += al16((rmax + 1 + 4) * 4);
+        v.vs = reinterpret_cast<const double*>(base + off + hv);
+        off += al16((emax + 2) * 8);
+        v.ls = reinterpret_cast<const uint16_t*>(base + off + hl);
+        off += al16((emax + 8) * 2);
+        v.bs = reinterpret_cast<const double*>(base + off + hb);
+        return v;
+    };
+    pdl_wait();
+    // x of own rows (colour by colour) and of the halo
+    for (int c = 0; c < ncol; ++c) {
+        int a, bb;
+        rows_of(c, a, bb);
+        const int lb = __ldg(lbase + p * ncol + c);
+        for (int r = tid; r < bb - a; r += kClsThreads) {
+            double v[K];
+            ldrow<K>(x + (size_t)(a + r) * S, v);
+#pragma unroll
+            for (int k = 0; k < K; ++k) xs[(lb + r) * K + k] = v[k];
+        }
+    }
+    const int h0 = __ldg(hoff + p), h1 = __ldg(hoff + p + 1);
+    int nown = 0;
+    for (int c = 0; c < ncol; ++c) {
+        int a, bb;
+        rows_of(c, a, bb);
+        nown += bb - a;
+    }
+    for (int q = tid; q < h1 - h0; q += kClsThreads) {
+        double v[K];
+        ldrow<K>(x + (size_t)__ldg(hrow + h0 + q) * S, v);
+#pragma unroll
+        for (int k = 0; k < K; ++k) xs[(nown + q) * K + k] = v[k];
+    }
+    issue(0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    cls_sync();   // every halo slot loaded before any CTA pushes into it
+    const int grp = tid / LPR, lane = tid & (LPR - 1), ngrp = kClsThreads / LPR;
+    const unsigned gmask = group_mask(LPR);
+    for (int t = 0; t < mu * ncol; ++t) {
+        if (nbuf == 2) {   // next step's copies in flight during this one
+            issue(t + 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const int c = colour_of(t);
+        int a, bb;
+        rows_of(c, a, bb);
+        if (bb > a) {
+            const int e0 = __ldg(rp + a);
+            const View v = view(t, a, e0);
+            const int lb = __ldg(lbase + p * ncol + c);
+            for (int r = grp; r < bb - a; r += ngrp) {
+                const int li = lb + r;
+                const int qb = v.rps[r] - e0, qe = v.rps[r + 1] - e0;
+                double sacc[K], d = 0.0;
 #pragma unroll
                 for (int k = 0; k < K; ++k) sacc[k] = 0.0;
-                double d = 0.0;
-                constexpr int U = 32 / LPR;
-                for (int eb = e0; eb < e1; eb += U * LPR) {
-                    int j[U], need[U];
-                    double a[U];
+                for (int q = qb + lane; q < qe; q += LPR) {
+                    const int j = v.ls[q];
+                    const double av = v.vs[q];
+                    if (j == li) {
+                        d += av;
+                    } else {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int e = eb + lane + u * LPR;
-                        const bool ok = e < e1;
-                        j[u] = ok ? __ldg(col + e) : -1;
-                        a[u] = ok ? __ldg(val + e) : 0.0;
-                        const bool before = reverse ? (j[u] >= r1) : (j[u] < r0);
-                        need[u] = base + sw + (before ? 1 : 0);
-                    }
-                    // poll every neighbour flag of the chunk with independent relaxed
-                    // loads, then one acquire fence before the x gathers
-                    int spins = 0;
-                    bool ready;
-                    do {
-                        ready = true;
-#pragma unroll
-                        for (int u = 0; u < U; ++u)
-                            if (j[u] >= 0 && j[u] != row) ready &= ld_relaxed_i32(done + j[u]) >= need[u];
-                    } while (!ready && ++spins < (1 << 22));
-                    if (!ready) atomicExch(err, 1);
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    double xv[U][K];
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (j[u] >= 0 && j[u] != row) ldrow_cg<K>(x + (size_t)j[u] * VS<K>::S, xv[u]);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        if (j[u] < 0) continue;
-                        if (j[u] == row) {
-                            d += a[u];
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < K; ++k) sacc[k] = fma(a[u], xv[u][k], sacc[k]);
-                        }
+                        for (int k = 0; k < K; ++k) sacc[k] = fma(av, xs[j * K + k], sacc[k]);
                     }
                 }
 #pragma unroll
-                for (int k = 0; k < K; ++k) sacc[k] = group_sum<LPR>(sacc[k], mask);
-                d = group_sum<LPR>(d, mask);
-                if (lane == 0) {
-                    double bv[K], xn[K];
-                    ldrow<K>(b + (size_t)row * VS<K>::S, bv);
+                for (int k = 0; k < K; ++k) sacc[k] = group_sum<LPR>(sacc[k], gmask);
+                d = group_sum<LPR>(d, gmask);
+                if (lane == 0)
 #pragma unroll
-                    for (int k = 0; k < K; ++k) xn[k] = (bv[k] - sacc[k]) / d;
-                    strow<K>(x + (size_t)row * VS<K>::S, xn);
-                    st_release_i32(done + row, base + sw + 1);
-                }
-                __syncwarp(mask);
+                    for (int k = 0; k < K; ++k) xs[li * K + k] = (v.bs[r * S + k] - sacc[k]) / d;
             }
+        }
+        __syncthreads();
+        if (nbuf == 1) {   // one buffer: the next step's copies overlap the pushes and the barrier
+            issue(t + 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // push the step's updated rows into the halos that hold them
+        const int s0 = __ldg(soff + p * (ncol + 1) + c), s1 = __ldg(soff + p * (ncol + 1) + c + 1);
+        for (int q = s0 + tid; q < s1; q += kClsThreads) {
+            const int2 m = __ldg(send + q);
+            const unsigned ra = cls_mapa(xs + (size_t)(m.y & 0xffff) * K, (unsigned)(m.y >> 16));
+#pragma unroll
+            for (int k = 0; k < K; ++k) cls_st_remote(ra + 8u * k, xs[m.x * K + k]);
+        }
+        cls_sync();
+    }
+    // own rows back to x
+    for (int c = 0; c < ncol; ++c) {
+        int a, bb;
+        rows_of(c, a, bb);
+        const int lb = __ldg(lbase + p * ncol + c);
+        for (int r = tid; r < bb - a; r += kClsThreads) {
+            double v[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) v[k] = xs[(lb + r) * K + k];
+            strow<K>(x + (size_t)(a + r) * S, v);
         }
     }
 }
 
 template <int K, int LPR>
-int launch_gs_flow_k(const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
-    static int per_sm = -1, nsm = 0;
-    if (per_sm < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_flow<K, LPR>, kBlock, 0);
-        cudaGetLastError();
+int launch_cluster_smooth_kl(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    const ClusterSmoother& Q = L.cls;
+    int nbuf = 2;
+    int smem = cluster_smooth_smem(K, Q.nloc_max, Q.rmax, Q.emax, 2);
+    if (smem > 227 * 1024) {
+        nbuf = 1;
+        smem = cluster_smooth_smem(K, Q.nloc_max, Q.rmax, Q.emax, 1);
     }
-    if (per_sm <= 0) return -1;
-    int maxrows = 0;
-    for (int c = 0; c < L.ncolours; ++c) maxrows = std::max(maxrows, L.colour_off[c + 1] - L.colour_off[c]);
-    const int grid = std::max(1, std::min(per_sm * nsm, nblk((int64_t)maxrows * LPR, kBlock)));
+    if (smem > 227 * 1024) return -1;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cluster_smooth<K, LPR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k_cluster_smooth<K, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kBlock);
+    cfg.gridDim = dim3(Q.cs);
+    cfg.blockDim = dim3(kClsThreads);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = Q.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const int rev = reverse ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_gs_flow<K, LPR>, (const int*)L.rp.p, (const int*)L.col.p, (const double*)L.val.p,
-                              (const double*)L.b.p, L.x.p, L.done.p, (const int*)L.dcoff.p, L.ncolours, mu, rev,
-                              err) == cudaSuccess
-               ? 1
-               : -1;
+    cfg.numAttrs = pdl ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cluster_smooth<K, LPR>, L.ncolours, mu, reverse ? 1 : 0, Q.rmax,
+                                             Q.emax, (const int*)Q.rowa.p, (const int*)Q.lbase.p, (const int*)Q.hoff.p,
+                                             (const int*)Q.hrow.p, (const uint16_t*)Q.lcol.p, (const int*)Q.soff.p,
+                                             (const int2*)Q.send.p, (const int*)L.rp.p, (const double*)L.val.p,
+                                             (const double*)L.b.p, L.x.p, Q.nloc_max, nbuf);
+    return e == cudaSuccess ? 1 : -1;
 }
-
 template <int K>
-int launch_gs_flow_kk(const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
+int launch_cluster_smooth_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
     switch (L.lpr) {
-        case 4: return launch_gs_flow_k<K, 4>(L, mu, reverse, err, s);
-        case 8: return launch_gs_flow_k<K, 8>(L, mu, reverse, err, s);
-        case 16: return launch_gs_flow_k<K, 16>(L, mu, reverse, err, s);
-        default: return launch_gs_flow_k<K, 32>(L, mu, reverse, err, s);
+        case 4: return launch_cluster_smooth_kl<K, 4>(L, mu, reverse, pdl, s);
+        case 8: return launch_cluster_smooth_kl<K, 8>(L, mu, reverse, pdl, s);
+        case 16: return launch_cluster_smooth_kl<K, 16>(L, mu, reverse, pdl, s);
+        default: return launch_cluster_smooth_kl<K, 32>(L, mu, reverse, pdl, s);
     }
 }
 
@@ -1788,23 +1405,6 @@ void init_vcycle_attributes() {
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
 }
-int vc_gs_persist(int K, const Level& L, int mu, bool reverse, unsigned long long* ctr, cudaStream_t s) {
-    if (!L.pipe || !L.dtoff.p) return -1;
-    switch (K) {
-        case 1: return launch_gs_persist_k<1>(L, mu, reverse, ctr, s);
-        case 2: return launch_gs_persist_k<2>(L, mu, reverse, ctr, s);
-        case 3: return launch_gs_persist_k<3>(L, mu, reverse, ctr, s);
-        default: return launch_gs_persist_k<4>(L, mu, reverse, ctr, s);
-    }
-}
-int vc_gs_flow(int K, const Level& L, int mu, bool reverse, int* err, cudaStream_t s) {
-    switch (K) {
-        case 1: return launch_gs_flow_kk<1>(L, mu, reverse, err, s);
-        case 2: return launch_gs_flow_kk<2>(L, mu, reverse, err, s);
-        case 3: return launch_gs_flow_kk<3>(L, mu, reverse, err, s);
-        default: return launch_gs_flow_kk<4>(L, mu, reverse, err, s);
-    }
-}
 // Device-side V-cycle loop (conditional WHILE graph node): after each cycle's
 // residual norm this kernel records rho into the history, applies mg_solve's
 // stopping rule (non-finite -> stop; every column rho <= tol -> stop; cycle
@@ -1839,20 +1439,24 @@ int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGra
     return 1;
 }
 
-int small_rows_per_tile() { return kSmallRows; }
-int vc_cluster_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    MG_K_SWITCH(K, (launch_cluster_gs_k<KK>(L, mu, reverse, pdl, s)))
+int cluster_smooth_smem(int K, int nloc, int rmax, int emax, int nbuf) {
+    const int S = K == 3 ? 4 : K;
+    return (nloc * K * 8 + 15) / 16 * 16 + nbuf * cls_buf_bytes(S, rmax, emax);
 }
-int cluster_gs_max_cs() {
+int vc_cluster_smooth(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
+    if (L.cls.cs <= 0) return -1;
+    MG_K_SWITCH(K, (launch_cluster_smooth_k<KK>(L, mu, reverse, pdl, s)))
+}
+int cluster_smooth_max_cs() {
     static int cs = -1;
     if (cs < 0) {
         cs = 0;
-        cudaFuncSetAttribute(k_cluster_gs<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(k_cluster_gs<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_cluster_smooth<3, 32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k_cluster_smooth<3, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         for (int c : {16, 8}) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(c);
-            cfg.blockDim = dim3(kCgThreads);
+            cfg.blockDim = dim3(kClsThreads);
             cfg.dynamicSmemBytes = 200 * 1024;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1862,7 +1466,7 @@ int cluster_gs_max_cs() {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             int ncl = 0;
-            if (cudaOccupancyMaxActiveClusters(&ncl, k_cluster_gs<3>, &cfg) == cudaSuccess && ncl >= 1) {
+            if (cudaOccupancyMaxActiveClusters(&ncl, k_cluster_smooth<3, 32>, &cfg) == cudaSuccess && ncl >= 1) {
                 cs = c;
                 break;
             }
@@ -1871,9 +1475,6 @@ int cluster_gs_max_cs() {
     }
     return cs;
 }
-int vc_small_gs(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    MG_K_SWITCH(K, (launch_small_gs_k<KK>(L, mu, reverse, pdl, s)))
-}
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 3>(L, 0, L.n, xout, pdl, s, xin, omega)))
 }
@@ -1881,7 +1482,7 @@ int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 1>(L, 0, L.n, L.r.p, pdl, s)))
 }
 int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s) {
-    const int G = getenv("MG_RESTRICT_G") ? atoi(getenv("MG_RESTRICT_G")) : kRestrictG;
+    const int G = kRestrictG;
     const bool ordered = C.restrict_ordered && C.rcptr.p;
     const int* ord = ordered ? (const int*)C.gal_order.p : nullptr;
     const int* cp = ordered ? (const int*)C.rcptr.p : (const int*)C.cptr.p;

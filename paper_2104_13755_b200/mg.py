@@ -72,6 +72,7 @@ def lib():
             "mg_get_profile": (C.c_int, [_vp, _vp, _vp]),
             "mg_launch_count": (i64, [_vp]),
             "mg_problem_size": (C.c_int, [_vp, _vp, _vp]),
+            "mg_set_execution": (C.c_int, [_vp, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -149,6 +150,14 @@ def mg_destroy(ctx):
 
 def mg_last_error(ctx):
     return lib().mg_last_error(ctx).decode()
+
+
+MG_EXEC_NO_PDL, MG_EXEC_NO_PIPE, MG_EXEC_COARSE_TRSV, MG_EXEC_DEVICE_LOOP, MG_EXEC_NO_CLUSTER = 1, 2, 4, 8, 16
+
+
+def mg_set_execution(ctx, flags=0):
+    """Scheduling options (include/mg.h MG_EXEC_*); call before mg_set_matrix*."""
+    return _check(ctx, lib().mg_set_execution(ctx, int(flags)))
 
 
 def mg_set_options(ctx, mu_pre=2, mu_post=2):
@@ -364,13 +373,15 @@ def mg_launch_count(ctx):
 class Solver:
     """RAII wrapper: hierarchy + matrix + solve on one context."""
 
-    def __init__(self, levels, P, device=0, stream=None, mu_pre=2, mu_post=2):
+    def __init__(self, levels, P, device=0, stream=None, mu_pre=2, mu_post=2, execution=0):
         self.ctx = mg_create(device, stream)
         self.levels = levels
         self.n = levels[0][0].shape[0]
         self.sizes = [V.shape[0] for V, _ in levels]
         mg_hierarchy_load(self.ctx, levels, P)
         mg_set_options(self.ctx, mu_pre, mu_post)
+        if execution:
+            mg_set_execution(self.ctx, execution)
 
     def close(self):
         if getattr(self, "ctx", None) is not None:

@@ -24,9 +24,9 @@ def oracle_problem(ora, p, mu=(2, 2)):
     return A, M, mg
 
 
-def gpu_solver(p, mu=(2, 2)):
+def gpu_solver(p, mu=(2, 2), execution=0):
     from paper_2104_13755_b200 import mg
-    return mg.Solver(p.levels, p.P, mu_pre=mu[0], mu_post=mu[1])
+    return mg.Solver(p.levels, p.P, mu_pre=mu[0], mu_post=mu[1], execution=execution)
 
 
 def tau_floor(A_scipy, X, B):

@@ -262,76 +262,48 @@ def test_full_size_parity(ora, cid):
     check_history(hg, ho, tauo)
 
 
-def test_launch_modes_agree(ora, monkeypatch):
-    """Scheduling variants must not change the arithmetic: PDL on/off and the
-    pipelined (TMA bulk) vs plain tile kernels give bitwise-identical
-    iterates.  The one-CTA triangular coarsest solve vs the explicit-inverse
-    GEMV (both Alg. 2's direct solve, reading A12) and the cluster coarse tail
-    vs per-launch kernels agree with the oracle to the X tolerance."""
-    p = meshgen.make_config(4, subdiv=5)
-    A, M, mgo = oracle_problem(ora, p)
-    Bo = oracle_rhs(ora, p, M)
-    Xo, ho, _, tauo = oracle_solve_tau(mgo, A.to_scipy(), Bo, rel_tol=0.0, max_cycles=5)
-    variants = {
-        "default": {},
-        "nopdl": {"MG_PDL": "0"},
-        "nopipe": {"MG_PIPE": "0"},
-        "trsv": {"MG_COARSE_SOLVE": "trsv"},
-        "tail": {"MG_TAIL_ROWS": "20000"},
-        "gal1": {"MG_GAL2": "0"},
-        "gal4": {"MG_GAL4": "1"},
-        "gal3": {"MG_GAL_V3": "1"},
-        "chol_launches": {"MG_CHOL_LAUNCHES": "1"},
-        "chol_cluster": {"MG_CHOL": "cluster"},
-        "gs_persist": {"MG_GS_PERSIST": "1"},
-        "pipe_lpr4": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "4"},
-        "pipe_lpr8": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "8"},
-        "pipe_lpr2_nopdl": {"MG_PIPE_LPR_MAX_AVG": "64", "MG_PIPE_LPR_MIN_ROWS": "0", "MG_PIPE_LPR": "2",
-                            "MG_PDL": "0"},
-        "pipe_lpr2_l0": {"MG_PIPE_LPR_L0": "2"},
-        "noserp": {"MG_SERPENTINE": "0"},
-        "nospatial": {"MG_TILE_SPATIAL": "0", "MG_RESTRICT_ORDER": "0"},
-        "restrict_order": {"MG_RESTRICT_ORDER": "1"},
-        "nosmall": {"MG_SMALL_ROWS": "0"},
-        "nogalmap": {"MG_GAL_MAP": "0"},
-        "galmap_capped": {"MG_GAL_MAP_MAX_MB": "1"},
-        "galmap_full": {"MG_GAL_MAP_HALF": "0"},
-        "unr8": {"MG_PIPE_UNR8": "0"},
-        "deviceloop": {"MG_DEVICE_LOOP": "1"},
-        "restrict16": {"MG_RESTRICT_G": "16"},
-        "restrict4": {"MG_RESTRICT_G": "4"},
-        "cluster_gs": {"MG_CLUSTER_GS_ROWS": "4608"},
-        "cluster_gs8": {"MG_CLUSTER_GS_ROWS": "100000", "MG_CLUSTER_GS_CS": "8"},
-        "small_all": {"MG_SMALL_ROWS": "100000"},
-    }
-    out = {}
-    for name, env in variants.items():
-        for k in ("MG_PDL", "MG_PIPE", "MG_COARSE_SOLVE", "MG_TAIL_ROWS", "MG_GAL2", "MG_GAL_V3", "MG_CHOL_LAUNCHES",
-                  "MG_CHOL", "MG_GAL4", "MG_GS_PERSIST", "MG_PIPE_LPR_MAX_AVG", "MG_PIPE_LPR", "MG_PIPE_LPR_MIN_ROWS", "MG_PIPE_LPR_L0", "MG_SERPENTINE", "MG_TILE_SPATIAL",
-                  "MG_RESTRICT_ORDER", "MG_SMALL_ROWS", "MG_GAL_MAP", "MG_GAL_MAP_MAX_MB",
-                  "MG_GAL_MAP_HALF", "MG_PIPE_UNR8", "MG_CLUSTER_GS_ROWS",
-                  "MG_CLUSTER_GS_CS", "MG_DEVICE_LOOP",
-                  "MG_RESTRICT_G"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        S = gpu_solver(p)
-        S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
-        X = np.zeros_like(Bo)
-        S.solve(Bo, X, rel_tol=0.0, max_cycles=5)
-        check_x(X, Xo)
-        out[name] = X
-        S.close()
-    assert np.array_equal(out["default"], out["nopdl"])
-    assert np.array_equal(out["default"], out["nopipe"])
-    assert np.array_equal(out["default"], out["gs_persist"])
-    # tile walk direction, spatial tile order of the residual and the coarse-row
-    # order of the restriction change no row's arithmetic
-    assert np.array_equal(out["default"], out["noserp"])
-    assert np.array_equal(out["default"], out["nospatial"])
-    assert np.array_equal(out["default"], out["restrict_order"])
-    assert np.array_equal(out["default"], out["unr8"])
-    assert np.array_equal(out["default"], out["deviceloop"])   # device-side cycle loop == host loop   # gather batching does not change the summation order   # same per-row arithmetic, one launch per phase
+def test_launch_modes_agree(ora):
+    """Scheduling variants (mg_set_execution) must not change the arithmetic:
+    PDL on/off, the pipelined (TMA bulk) vs plain tile kernels, the cluster-
+    resident small-level smoother vs one launch per colour, and the device-side
+    cycle loop give bitwise-identical iterates.  The one-CTA triangular
+    coarsest solve vs the explicit-inverse GEMV (both Alg. 2's direct solve,
+    reading A12) agree with the oracle to the X tolerance."""
+    from paper_2104_13755_b200 import mg
+    for cid, kw in ((4, {"subdiv": 6}), (3, {"grid": (160, 128)})):
+        p = meshgen.make_config(cid, **kw)
+        A, M, mgo = oracle_problem(ora, p)
+        Bo = oracle_rhs(ora, p, M)
+        Xo, ho, _ = mgo.solve(Bo, rel_tol=0.0, max_cycles=5)
+        variants = {
+            "default": 0,
+            "nopdl": mg.MG_EXEC_NO_PDL,
+            "nopipe": mg.MG_EXEC_NO_PIPE,
+            "nocluster": mg.MG_EXEC_NO_CLUSTER,
+            "nocluster_nopdl": mg.MG_EXEC_NO_CLUSTER | mg.MG_EXEC_NO_PDL,
+            "deviceloop": mg.MG_EXEC_DEVICE_LOOP,
+            "trsv": mg.MG_EXEC_COARSE_TRSV,
+        }
+        out = {}
+        for name, flags in variants.items():
+            S = gpu_solver(p)
+            mg.mg_set_execution(S.ctx, flags)
+            S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
+            X = np.zeros_like(Bo)
+            S.solve(Bo, X, rel_tol=0.0, max_cycles=5)
+            check_x(X, Xo)
+            out[name] = X
+            # symmetric V-cycle (reversed post colours) through the same kernels
+            S.set_smoother(0, 0.8, True)
+            Xs = np.zeros_like(Bo)
+            S.solve(Bo, Xs, rel_tol=0.0, max_cycles=3)
+            out[name + "_sym"] = Xs
+            S.close()
+        for name in variants:
+            if name == "trsv":
+                continue
+            assert np.array_equal(out["default"], out[name]), name
+            assert np.array_equal(out["default_sym"], out[name + "_sym"]), name
 
 
 @pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)})])
@@ -398,16 +370,12 @@ def test_split_csr_equals_split_cotan(ora):
         gpu_solver(p).set_alpha(0.5)                          # MG_ERR_STATE: no split operators
 
 
-@pytest.mark.parametrize("cid,kw,pipe_lpr", [(4, {"subdiv": 5}, None), (3, {"grid": (96, 80)}, None),
-                                             (4, {"subdiv": 5}, "4")])
-def test_smoother_variants_parity(ora, cid, kw, pipe_lpr, monkeypatch):
+@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 5}), (3, {"grid": (96, 80)}), (4, {"subdiv": 8})])
+def test_smoother_variants_parity(ora, cid, kw):
     """Row f4: damped-Jacobi smoothing (App. E) and the symmetric
-    (reversed post colours) V-cycle match the oracle's same variants (also
-    with the pipelined lanes-per-row tiles on the coarse levels)."""
-    if pipe_lpr:
-        monkeypatch.setenv("MG_PIPE_LPR_MAX_AVG", "64")
-        monkeypatch.setenv("MG_PIPE_LPR_MIN_ROWS", "0")
-        monkeypatch.setenv("MG_PIPE_LPR", pipe_lpr)
+    (reversed post colours) V-cycle match the oracle's same variants (the
+    655k-row case runs level 1 through the pipelined lanes-per-row tiles and
+    the small levels through the cluster-resident smoother)."""
     p = meshgen.make_config(cid, **kw)
     A, M, _ = oracle_problem(ora, p)
     Bo = oracle_rhs(ora, p, M)
@@ -715,30 +683,6 @@ def test_new_api_errors():
     S.close()
 
 
-@pytest.mark.parametrize("cid,kw", [(4, {"subdiv": 6}), (3, {"grid": (128, 96)})])
-def test_dataflow_gs_parity(ora, cid, kw, monkeypatch):
-    """Dataflow multicolour GS (per-row sweep counters instead of one launch
-    per colour, MG_FLOW_ROWS) reproduces multicolour GS: same V-cycle iterate
-    as the per-colour launches to rounding, forward and symmetric (PCG)."""
-    p = meshgen.make_config(cid, **kw)
-    A, M, mgo = oracle_problem(ora, p)
-    Bo = oracle_rhs(ora, p, M)
-    Xo, ho, _, tauo = oracle_solve_tau(mgo, A.to_scipy(), Bo, rel_tol=0.0, max_cycles=4)
-    Xp, hp, _ = ora.MG(p.sizes, p.P, A).pcg(Bo, rel_tol=0.0, max_iters=4)
-    monkeypatch.setenv("MG_FLOW_ROWS", "100000000")
-    S = gpu_solver(p)
-    S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
-    for _ in range(2):                                   # counters keep increasing across solves
-        Xg = np.zeros_like(Bo)
-        rc, cyc, hg = S.solve(Bo, Xg, rel_tol=0.0, max_cycles=4)
-        check_x(Xg, Xo)
-        check_history(hg, ho, tauo)
-    Xg = np.zeros_like(Bo)
-    rc, it, hg = S.solve_pcg(Bo, Xg, rel_tol=0.0, max_iters=4)
-    check_x(Xg, Xp)
-    S.close()
-
-
 def test_zero_guess(ora):
     """mg_set_zero_guess: X is output only — garbage on input gives the same
     iterate (bitwise) as an explicit zero guess, for host and device X, for
@@ -771,7 +715,7 @@ def test_zero_guess(ora):
     S.close()
 
 
-def test_device_loop_matches_host_loop(ora, monkeypatch):
+def test_device_loop_matches_host_loop(ora):
     """The device-side cycle loop (conditional graph node, one launch per
     solve) applies mg_solve's stopping rule exactly like the host loop: same
     cycle count, bitwise-identical history and iterate, for a tolerance stop,
@@ -780,9 +724,9 @@ def test_device_loop_matches_host_loop(ora, monkeypatch):
     A, M, mgo = oracle_problem(ora, p)
     Bo = oracle_rhs(ora, p, M)
     res = {}
+    from paper_2104_13755_b200 import mg
     for mode in ("1", "0"):
-        monkeypatch.setenv("MG_DEVICE_LOOP", mode)
-        S = gpu_solver(p)
+        S = gpu_solver(p, execution=mg.MG_EXEC_DEVICE_LOOP if mode == "1" else 0)
         S.set_matrix_cotan(p.levels[0][0], p.mass_coeff, p.lap_coeff)
         out = []
         for tol, mc in ((1e-8, 50), (1e-30, 4), (1e-8, 0)):
