@@ -264,7 +264,6 @@ int mg_util_galerkin_pattern(int32_t n_fine, const int32_t* row_ptr, const int32
 #define MG_EXEC_NO_PIPE 2         /* plain tile kernels instead of the TMA-bulk pipelined ones */
 #define MG_EXEC_COARSE_TRSV 4     /* coarsest solve by two triangular solves (one CTA), not A_H^{-1} GEMV */
 #define MG_EXEC_DEVICE_LOOP 8     /* Alg. 1 loop on the device (conditional WHILE graph node) */
-#define MG_EXEC_NO_CLUSTER 16     /* per-colour launches instead of the cluster-resident small-level smoother */
 int mg_set_execution(mg_ctx* ctx, int flags);
 
 /* ---- instrumentation (bench.py) ----------------------------------------- */

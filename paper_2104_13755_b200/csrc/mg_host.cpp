@@ -6,7 +6,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -148,7 +147,6 @@ struct GalT {
     std::vector<uint8_t> rowidx, slot;    // [entries]: local row, column slot in the row
     std::vector<uint16_t> con;            // contributions
 };
-constexpr int32_t kClusterMaxRows = 65536;   // levels smoothed by one cluster (larger: per-colour launches)
 constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-bit fields
 // caps shared with k_galerkin_t (mg_setup.cu)
 constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index; rows <= 256 entries)
@@ -372,111 +370,6 @@ std::vector<uint64_t> morton_keys(const std::vector<double>& V, int32_t n) {
     return key;
 }
 
-// Cluster-resident smoother structure of one level (see ClusterSmoother in
-// mg_internal.h).  Integer structure only; false if the level does not
-// qualify (the per-colour launches then smooth it).
-bool setup_cluster_smoother(Level& L, int cs, cudaStream_t s) {
-    ClusterSmoother& Q = L.cls;
-    Q.cs = 0;
-    const int32_t n = L.n, C = L.ncolours;
-    if (cs <= 1 || n < 4 * cs || L.tiled || L.pipe || C < 1) return false;
-    // spatial parts: rank in (Morton key, user index) order -- the order inside each colour
-    const std::vector<uint64_t> key = morton_keys(L.V, n);
-    std::vector<int32_t> ord(n);
-    std::iota(ord.begin(), ord.end(), 0);
-    auto less = [&](int32_t a, int32_t b) {
-        const int32_t ua = L.perm[a], ub = L.perm[b];
-        return key[ua] != key[ub] ? key[ua] < key[ub] : ua < ub;
-    };
-    std::sort(ord.begin(), ord.end(), less);
-    std::vector<int32_t> part(n);
-    for (int32_t r = 0; r < n; ++r) part[ord[r]] = (int32_t)((int64_t)r * cs / n);
-    std::vector<int32_t> rowa((size_t)C * (cs + 1));
-    for (int32_t c = 0; c < C; ++c) {
-        const int32_t a = L.colour_off[c], b = L.colour_off[c + 1];
-        int32_t i = a;
-        for (int p = 0; p <= cs; ++p) {
-            while (i < b && part[i] < p) ++i;
-            rowa[(size_t)c * (cs + 1) + p] = i;
-        }
-        for (int32_t t = a + 1; t < b; ++t)
-            if (part[t] < part[t - 1]) return false;   // parts must be contiguous inside a colour
-    }
-    std::vector<int32_t> lbase((size_t)cs * C), nown(cs, 0), loc(n);
-    for (int p = 0; p < cs; ++p)
-        for (int32_t c = 0; c < C; ++c) {
-            lbase[(size_t)p * C + c] = nown[p];
-            const int32_t a = rowa[(size_t)c * (cs + 1) + p], b = rowa[(size_t)c * (cs + 1) + p + 1];
-            for (int32_t i = a; i < b; ++i) loc[i] = nown[p] + (i - a);
-            nown[p] += b - a;
-        }
-    // halos, local columns
-    std::vector<int32_t> hoff(1, 0), hrow;
-    std::vector<uint16_t> lcol((size_t)std::max<int64_t>(L.nnz, 1) + 8, 0);
-    std::vector<std::vector<std::array<int32_t, 3>>> sends((size_t)cs * C);   // per (owner, colour): {src, dst, dst local}
-    int rmax = 0, emax = 0, nloc_max = 0;
-    std::vector<int32_t> hidx(n, -1);
-    for (int p = 0; p < cs; ++p) {
-        std::vector<int32_t> h;
-        for (int32_t c = 0; c < C; ++c) {
-            const int32_t a = rowa[(size_t)c * (cs + 1) + p], b = rowa[(size_t)c * (cs + 1) + p + 1];
-            rmax = std::max(rmax, b - a);
-            emax = std::max(emax, L.irp[b] - L.irp[a]);
-            for (int32_t e = L.irp[a]; e < L.irp[b]; ++e) {
-                const int32_t j = L.icol[e];
-                if (part[j] != p && hidx[j] < 0) {
-                    hidx[j] = 0;
-                    h.push_back(j);
-                }
-            }
-        }
-        std::sort(h.begin(), h.end());
-        for (size_t k = 0; k < h.size(); ++k) hidx[h[k]] = nown[p] + (int32_t)k;
-        const int64_t nl = (int64_t)nown[p] + (int64_t)h.size();
-        if (nl > 65535) return false;
-        nloc_max = std::max<int>(nloc_max, (int)nl);
-        for (int32_t c = 0; c < C; ++c) {
-            const int32_t a = rowa[(size_t)c * (cs + 1) + p], b = rowa[(size_t)c * (cs + 1) + p + 1];
-            for (int32_t i = a; i < b; ++i)
-                for (int32_t e = L.irp[i]; e < L.irp[i + 1]; ++e) {
-                    const int32_t j = L.icol[e];
-                    lcol[e] = (uint16_t)(part[j] == p ? loc[j] : hidx[j]);
-                }
-        }
-        for (int32_t j : h) {
-            const int32_t q = part[j];
-            int32_t cj = 0;
-            while (L.colour_off[cj + 1] <= j) ++cj;
-            sends[(size_t)q * C + cj].push_back({loc[j], p, hidx[j]});
-            hidx[j] = -1;
-        }
-        hrow.insert(hrow.end(), h.begin(), h.end());
-        hoff.push_back((int32_t)hrow.size());
-    }
-    std::vector<int32_t> soff;
-    std::vector<int2> send;
-    for (int p = 0; p < cs; ++p)
-        for (int32_t c = 0; c < C; ++c) {
-            auto& v = sends[(size_t)p * C + c];
-            std::sort(v.begin(), v.end());
-            soff.push_back((int32_t)send.size());
-            for (const auto& x : v) send.push_back(make_int2(x[0], x[1] << 16 | x[2]));
-            if (c == C - 1) soff.push_back((int32_t)send.size());
-        }
-    if (hrow.empty()) hrow.push_back(0);
-    if (send.empty()) send.push_back(make_int2(0, 0));
-    cudaError_t e;
-    if ((e = Q.rowa.upload(rowa, s)) || (e = Q.lbase.upload(lbase, s)) || (e = Q.hoff.upload(hoff, s)) ||
-        (e = Q.hrow.upload(hrow, s)) || (e = Q.lcol.upload(lcol, s)) || (e = Q.soff.upload(soff, s)) ||
-        (e = Q.send.upload(send, s)) || (e = cudaStreamSynchronize(s)))
-        return false;
-    Q.rmax = rmax;
-    Q.emax = emax;
-    Q.nloc_max = nloc_max;
-    Q.cs = cs;
-    return true;
-}
-
 uint64_t fnv1a(uint64_t h, const void* data, size_t bytes) {
     const unsigned char* p = (const unsigned char*)data;
     for (size_t i = 0; i < bytes; ++i) {
@@ -569,7 +462,6 @@ struct mg_ctx {
     cudaGraphExec_t loop_exec[kMaxK + 1] = {};  // whole solve: conditional WHILE node around the V-cycle
     int loop_check_launches = 1;
     bool device_loop = false;                   // MG_EXEC_DEVICE_LOOP (opt-in: ncu does not see kernels inside conditional nodes)
-    bool use_cluster = true;                    // cluster-resident smoothing of the small levels (MG_EXEC_NO_CLUSTER: off)
     DBuf<LoopState> loop_st;
     DBuf<double> loop_hist;
     LoopState* h_loop = nullptr;                // pinned
@@ -972,12 +864,6 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         (e = c->bnorm.alloc(kMaxK)) || (e = c->rho.alloc(kMaxK)))
         return c->cuda_fail(e, "pattern alloc");
     if ((e = cudaStreamSynchronize(s))) return c->cuda_fail(e, "pattern upload");
-    // cluster-resident smoothing of the levels whose colour passes are launch-bound
-    const int ccs = c->use_cluster ? cluster_smooth_max_cs() : 0;
-    for (int l = 0; l < H; ++l) {
-        Level& L = *c->lv[l];
-        if (!(ccs > 0 && L.n <= kClusterMaxRows && setup_cluster_smoother(L, ccs, s))) L.cls.cs = 0;
-    }
     c->have_pattern = true;
     return MG_OK;
 }
@@ -1051,10 +937,6 @@ int split_hierarchy(mg_ctx* c) {
 // V-cycle), or damped Jacobi (App. E) alternating x -> r -> x.
 int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
     int n = 0;
-    if (c->smoother == 0 && L.cls.cs > 0 && mu > 0) {
-        const int nl = vc_cluster_smooth(K, L, mu, reverse, pdl, s);
-        if (nl > 0) return nl;
-    }
     if (c->smoother == 1) {
         for (int it = 0; it < mu; ++it)
             n += (it & 1) ? vc_jacobi(K, L, L.r.p, L.x.p, c->omega, pdl, s) : vc_jacobi(K, L, L.x.p, L.r.p, c->omega, pdl, s);
@@ -1284,14 +1166,13 @@ const char* mg_last_error(const mg_ctx* c) { return c ? c->err.c_str() : "null c
 
 int mg_set_execution(mg_ctx* c, int flags) {
     if (!c) return MG_ERR_INVALID_ARG;
-    if (flags & ~(MG_EXEC_NO_PDL | MG_EXEC_NO_PIPE | MG_EXEC_COARSE_TRSV | MG_EXEC_DEVICE_LOOP | MG_EXEC_NO_CLUSTER))
+    if (flags & ~(MG_EXEC_NO_PDL | MG_EXEC_NO_PIPE | MG_EXEC_COARSE_TRSV | MG_EXEC_DEVICE_LOOP))
         return c->fail(MG_ERR_INVALID_ARG, "unknown execution flag");
     cudaStreamSynchronize(c->stream);
     c->pdl = !(flags & MG_EXEC_NO_PDL);
     c->use_pipe = !(flags & MG_EXEC_NO_PIPE);
     c->coarse_mode = (flags & MG_EXEC_COARSE_TRSV) ? 0 : 1;
     c->device_loop = (flags & MG_EXEC_DEVICE_LOOP) != 0;
-    c->use_cluster = !(flags & MG_EXEC_NO_CLUSTER);
     c->drop_graphs();
     c->have_pattern = false;   // tile / cluster structures are built by the next pattern setup
     c->have_matrix = false;

@@ -48,26 +48,6 @@ struct DBuf {
     }
 };
 
-// Cluster-resident multicolour GS of one level (k_cluster_smooth): the rows
-// are split into cs spatially contiguous parts (Morton order), CTA p of the
-// cluster owns part p.  Inside the colour-grouped internal order the rows of
-// colour c owned by CTA p are the contiguous range [rowa[c*(cs+1)+p],
-// rowa[c*(cs+1)+p+1]).  Every CTA keeps x of its own rows and of its halo
-// (columns of its rows owned elsewhere) in shared memory; after each colour
-// step it pushes its updated rows to the CTAs whose halo holds them.
-struct ClusterSmoother {
-    int cs = 0;                           // CTAs per cluster (0: level not cluster-smoothed)
-    int smem = 0;                         // dynamic shared memory per CTA (bytes)
-    int rmax = 0, emax = 0;               // most rows / entries of one (CTA, colour) step
-    int nloc_max = 0;                     // most local rows (own + halo) of a CTA
-    DBuf<int32_t> rowa;                   // [ncolours][cs+1] internal row boundaries
-    DBuf<int32_t> lbase;                  // [cs][ncolours] local index of the first own row of colour c
-    DBuf<int32_t> hoff, hrow;             // [cs+1] halo offsets; internal rows of each CTA's halo
-    DBuf<uint16_t> lcol;                  // [nnz] local column index of every entry (in its owner CTA)
-    DBuf<int32_t> soff;                   // [cs][ncolours+1] send-list offsets
-    DBuf<int2> send;                      // {own local row, dst CTA << 16 | dst local row}
-};
-
 // One grid of the hierarchy.  "internal" order = rows grouped by Alg. 3
 // colour (ascending), locality (Morton) order inside a colour; the coarsest
 // level keeps the user order (it has no smoother).
@@ -90,10 +70,6 @@ struct Level {
     bool pipe_unr8 = false;               // k_tile_pipe with 8 gathers per batch (K = 3, 3 CTAs/SM)
     int pipe_lpr = 1;
                      // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
-    // cluster-resident smoothing (k_cluster_smooth, mg_vcycle.cu): all mu sweeps
-    // of this level in one launch of one thread-block cluster; set up by
-    // setup_cluster_smoother (mg_host.cpp)
-    ClusterSmoother cls;
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
     std::vector<double> V;                // user-order positions [n][3]
@@ -151,9 +127,6 @@ constexpr int kLoopHistCycles = 4096;   // device history capacity (cycles)
 // (V-cycle graph).
 // mg_vcycle.cu
 int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
-int vc_cluster_smooth(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s);   // all mu sweeps
-int cluster_smooth_max_cs();              // CTAs per cluster the device supports for k_cluster_smooth (0: none)
-int cluster_smooth_smem(int K, int nloc, int rmax, int emax, int nbuf);   // dynamic shared memory of one CTA
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
 int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGraphConditionalHandle h, cudaStream_t s);
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x

@@ -597,270 +597,6 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
 }
 
 // ---------------------------------------------------------------------------
-// Cluster-resident multicolour Gauss-Seidel (levels whose colour passes are
-// launch-bound; structure: ClusterSmoother, mg_internal.h).  All mu sweeps of
-// a level run in ONE launch of one thread-block cluster: CTA p owns a
-// spatially contiguous part of the rows and keeps x of its own rows and of
-// its halo in shared memory.  A colour step is
-//   * the step's rows, entries, local columns and right-hand sides arrive by
-//     16-byte cp.async, issued one step ahead (double buffer): A does not
-//     change during the solve, so nothing of it is on the step's critical
-//     path;
-//   * LPR lanes per row, lane l takes the entries l, l+LPR, ... in order and a
-//     fixed xor-butterfly sums the lanes -- exactly the arithmetic of
-//     k_lpr_sweep<K, LPR, 0>, so the iterate is bitwise the per-colour-launch
-//     one (tested);
-//   * updated rows are pushed into the shared memory of the CTAs whose halo
-//     holds them (st.shared::cluster), then barrier.cluster (release /
-//     acquire) ends the step.
-// Per colour step this costs one cluster barrier and a few shared-memory
-// round trips instead of a kernel launch and an L2 round trip.
-constexpr int kClsThreads = 256;
-
-__device__ __forceinline__ void cls_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ unsigned cls_rank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned cls_mapa(const void* p, unsigned cta) {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(cta));
-    return r;
-}
-__device__ __forceinline__ void cls_st_remote(unsigned addr, double v) {
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-__device__ __forceinline__ void cls_cp16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ int al16(int bytes) { return (bytes + 15) & ~15; }
-
-// bytes of one step buffer: row pointers, values, local columns, right-hand sides
-__host__ __device__ inline int cls_buf_bytes(int S, int rmax, int emax) {
-    return ((rmax + 1 + 4) * 4 + 15) / 16 * 16 + ((emax + 2) * 8 + 15) / 16 * 16 + ((emax + 8) * 2 + 15) / 16 * 16 +
-           ((rmax * S + 2) * 8 + 15) / 16 * 16;
-}
-
-template <int K, int LPR>
-__global__ void __launch_bounds__(kClsThreads, 1) k_cluster_smooth(
-    int ncol, int mu, int rev, int rmax, int emax, const int* __restrict__ rowa, const int* __restrict__ lbase,
-    const int* __restrict__ hoff, const int* __restrict__ hrow, const uint16_t* __restrict__ lcol,
-    const int* __restrict__ soff, const int2* __restrict__ send, const int* __restrict__ rp,
-    const double* __restrict__ val, const double* __restrict__ b, double* __restrict__ x, int nloc_max, int nbuf) {
-    constexpr int S = VS<K>::S;
-    extern __shared__ __align__(16) unsigned char cls_sm[];
-    const int cs = (int)gridDim.x;   // one cluster
-    const int p = (int)cls_rank();
-    const int tid = threadIdx.x;
-    double* xs = reinterpret_cast<double*>(cls_sm);   // [nloc][K]
-    const int bufb = cls_buf_bytes(S, rmax, emax);
-    unsigned char* buf0 = cls_sm + al16(nloc_max * K * 8);
-    pdl_launch_dependents();
-    // the step's windows: rows [a, bb) of colour c owned by this CTA
-    auto rows_of = [&](int c, int& a, int& bb) {
-        a = __ldg(rowa + c * (cs + 1) + p);
-        bb = __ldg(rowa + c * (cs + 1) + p + 1);
-    };
-    auto colour_of = [&](int t) {
-        const int q = t % ncol;
-        return rev ? ncol - 1 - q : q;
-    };
-    struct View {
-        const int* rps;
-        const double* vs;
-        const uint16_t* ls;
-        const double* bs;
-    };
-    // issue the cp.async copies of step t into buffer t & 1
-    auto issue = [&](int t) {
-        if (t >= mu * ncol) return;
-        int a, bb;
-        rows_of(colour_of(t), a, bb);
-        if (bb <= a) return;
-        unsigned char* base = buf0 + (size_t)((t & 1) & (nbuf - 1)) * bufb;
-        const int e0 = __ldg(rp + a), e1 = __ldg(rp + bb);
-        const uintptr_t w[4] = {reinterpret_cast<uintptr_t>(rp + a), reinterpret_cast<uintptr_t>(val + e0),
-                                reinterpret_cast<uintptr_t>(lcol + e0), reinterpret_cast<uintptr_t>(b + (size_t)a * S)};
-        const int bytes[4] = {(bb - a + 1) * 4, (e1 - e0) * 8, (e1 - e0) * 2, (bb - a) * S * 8};
-        const int cap[4] = {al16((rmax + 1 + 4) * 4), al16((emax + 2) * 8), al16((emax + 8) * 2),
-                            al16((rmax * S + 2) * 8)};
-        int off = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uintptr_t lo = w[k] & ~(uintptr_t)15;
-            const int n16 = (int)((w[k] - lo) + bytes[k] + 15) / 16;
-            for (int q = tid; q < n16; q += kClsThreads) cls_cp16(base + off + 16 * q, reinterpret_cast<const void*>(lo + 16 * (uintptr_t)q));
-            off += cap[k];
-        }
-    };
-    auto view = [&](int t, int a, int e0) {
-        unsigned char* base = buf0 + (size_t)((t & 1) & (nbuf - 1)) * bufb;
-        const uintptr_t hr = reinterpret_cast<uintptr_t>(rp + a) & 15, hv = reinterpret_cast<uintptr_t>(val + e0) & 15,
-                        hl = reinterpret_cast<uintptr_t>(lcol + e0) & 15, hb = reinterpret_cast<uintptr_t>(b + (size_t)a * S) & 15;
-        View v;
-        int off = 0;
-        v.rps = reinterpret_cast<const int*>(base + off + hr);
-        off += al16((rmax + 1 + 4) * 4);
-        v.vs = reinterpret_cast<const double*>(base + off + hv);
-        off += al16((emax + 2) * 8);
-        v.ls = reinterpret_cast<const uint16_t*>(base + off + hl);
-        off += al16((emax + 8) * 2);
-        v.bs = reinterpret_cast<const double*>(base + off + hb);
-        return v;
-    };
-    pdl_wait();
-    // x of own rows (colour by colour) and of the halo
-    for (int c = 0; c < ncol; ++c) {
-        int a, bb;
-        rows_of(c, a, bb);
-        const int lb = __ldg(lbase + p * ncol + c);
-        for (int r = tid; r < bb - a; r += kClsThreads) {
-            double v[K];
-            ldrow<K>(x + (size_t)(a + r) * S, v);
-#pragma unroll
-            for (int k = 0; k < K; ++k) xs[(lb + r) * K + k] = v[k];
-        }
-    }
-    const int h0 = __ldg(hoff + p), h1 = __ldg(hoff + p + 1);
-    int nown = 0;
-    for (int c = 0; c < ncol; ++c) {
-        int a, bb;
-        rows_of(c, a, bb);
-        nown += bb - a;
-    }
-    for (int q = tid; q < h1 - h0; q += kClsThreads) {
-        double v[K];
-        ldrow<K>(x + (size_t)__ldg(hrow + h0 + q) * S, v);
-#pragma unroll
-        for (int k = 0; k < K; ++k) xs[(nown + q) * K + k] = v[k];
-    }
-    issue(0);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    cls_sync();   // every halo slot loaded before any CTA pushes into it
-    const int grp = tid / LPR, lane = tid & (LPR - 1), ngrp = kClsThreads / LPR;
-    const unsigned gmask = group_mask(LPR);
-    for (int t = 0; t < mu * ncol; ++t) {
-        if (nbuf == 2) {   // next step's copies in flight during this one
-            issue(t + 1);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncthreads();
-        const int c = colour_of(t);
-        int a, bb;
-        rows_of(c, a, bb);
-        if (bb > a) {
-            const int e0 = __ldg(rp + a);
-            const View v = view(t, a, e0);
-            const int lb = __ldg(lbase + p * ncol + c);
-            for (int r = grp; r < bb - a; r += ngrp) {
-                const int li = lb + r;
-                const int qb = v.rps[r] - e0, qe = v.rps[r + 1] - e0;
-                double sacc[K], d = 0.0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) sacc[k] = 0.0;
-                for (int q = qb + lane; q < qe; q += LPR) {
-                    const int j = v.ls[q];
-                    const double av = v.vs[q];
-                    if (j == li) {
-                        d += av;
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < K; ++k) sacc[k] = fma(av, xs[j * K + k], sacc[k]);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < K; ++k) sacc[k] = group_sum<LPR>(sacc[k], gmask);
-                d = group_sum<LPR>(d, gmask);
-                if (lane == 0)
-#pragma unroll
-                    for (int k = 0; k < K; ++k) xs[li * K + k] = (v.bs[r * S + k] - sacc[k]) / d;
-            }
-        }
-        __syncthreads();
-        if (nbuf == 1) {   // one buffer: the next step's copies overlap the pushes and the barrier
-            issue(t + 1);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        // push the step's updated rows into the halos that hold them
-        const int s0 = __ldg(soff + p * (ncol + 1) + c), s1 = __ldg(soff + p * (ncol + 1) + c + 1);
-        for (int q = s0 + tid; q < s1; q += kClsThreads) {
-            const int2 m = __ldg(send + q);
-            const unsigned ra = cls_mapa(xs + (size_t)(m.y & 0xffff) * K, (unsigned)(m.y >> 16));
-#pragma unroll
-            for (int k = 0; k < K; ++k) cls_st_remote(ra + 8u * k, xs[m.x * K + k]);
-        }
-        cls_sync();
-    }
-    // own rows back to x
-    for (int c = 0; c < ncol; ++c) {
-        int a, bb;
-        rows_of(c, a, bb);
-        const int lb = __ldg(lbase + p * ncol + c);
-        for (int r = tid; r < bb - a; r += kClsThreads) {
-            double v[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) v[k] = xs[(lb + r) * K + k];
-            strow<K>(x + (size_t)(a + r) * S, v);
-        }
-    }
-}
-
-template <int K, int LPR>
-int launch_cluster_smooth_kl(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    const ClusterSmoother& Q = L.cls;
-    int nbuf = 2;
-    int smem = cluster_smooth_smem(K, Q.nloc_max, Q.rmax, Q.emax, 2);
-    if (smem > 227 * 1024) {
-        nbuf = 1;
-        smem = cluster_smooth_smem(K, Q.nloc_max, Q.rmax, Q.emax, 1);
-    }
-    if (smem > 227 * 1024) return -1;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_cluster_smooth<K, LPR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(k_cluster_smooth<K, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(Q.cs);
-    cfg.blockDim = dim3(kClsThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = Q.cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 2 : 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cluster_smooth<K, LPR>, L.ncolours, mu, reverse ? 1 : 0, Q.rmax,
-                                             Q.emax, (const int*)Q.rowa.p, (const int*)Q.lbase.p, (const int*)Q.hoff.p,
-                                             (const int*)Q.hrow.p, (const uint16_t*)Q.lcol.p, (const int*)Q.soff.p,
-                                             (const int2*)Q.send.p, (const int*)L.rp.p, (const double*)L.val.p,
-                                             (const double*)L.b.p, L.x.p, Q.nloc_max, nbuf);
-    return e == cudaSuccess ? 1 : -1;
-}
-template <int K>
-int launch_cluster_smooth_k(const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    switch (L.lpr) {
-        case 4: return launch_cluster_smooth_kl<K, 4>(L, mu, reverse, pdl, s);
-        case 8: return launch_cluster_smooth_kl<K, 8>(L, mu, reverse, pdl, s);
-        case 16: return launch_cluster_smooth_kl<K, 16>(L, mu, reverse, pdl, s);
-        default: return launch_cluster_smooth_kl<K, 32>(L, mu, reverse, pdl, s);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // K5b: r_c = P^T r gathered through the children lists of the coarse
 // vertices (transpose of P): deterministic, no atomics.  G lanes per coarse
 // row; children indices and weights prefetched before the wait.  Zeroes the
@@ -1439,42 +1175,6 @@ int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGra
     return 1;
 }
 
-int cluster_smooth_smem(int K, int nloc, int rmax, int emax, int nbuf) {
-    const int S = K == 3 ? 4 : K;
-    return (nloc * K * 8 + 15) / 16 * 16 + nbuf * cls_buf_bytes(S, rmax, emax);
-}
-int vc_cluster_smooth(int K, const Level& L, int mu, bool reverse, bool pdl, cudaStream_t s) {
-    if (L.cls.cs <= 0) return -1;
-    MG_K_SWITCH(K, (launch_cluster_smooth_k<KK>(L, mu, reverse, pdl, s)))
-}
-int cluster_smooth_max_cs() {
-    static int cs = -1;
-    if (cs < 0) {
-        cs = 0;
-        cudaFuncSetAttribute(k_cluster_smooth<3, 32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(k_cluster_smooth<3, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        for (int c : {16, 8}) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(c);
-            cfg.blockDim = dim3(kClsThreads);
-            cfg.dynamicSmemBytes = 200 * 1024;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = c;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            int ncl = 0;
-            if (cudaOccupancyMaxActiveClusters(&ncl, k_cluster_smooth<3, 32>, &cfg) == cudaSuccess && ncl >= 1) {
-                cs = c;
-                break;
-            }
-            cudaGetLastError();
-        }
-    }
-    return cs;
-}
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s) {
     MG_K_SWITCH(K, (sweep_k<KK, 3>(L, 0, L.n, xout, pdl, s, xin, omega)))
 }

@@ -152,7 +152,7 @@ def mg_last_error(ctx):
     return lib().mg_last_error(ctx).decode()
 
 
-MG_EXEC_NO_PDL, MG_EXEC_NO_PIPE, MG_EXEC_COARSE_TRSV, MG_EXEC_DEVICE_LOOP, MG_EXEC_NO_CLUSTER = 1, 2, 4, 8, 16
+MG_EXEC_NO_PDL, MG_EXEC_NO_PIPE, MG_EXEC_COARSE_TRSV, MG_EXEC_DEVICE_LOOP = 1, 2, 4, 8
 
 
 def mg_set_execution(ctx, flags=0):

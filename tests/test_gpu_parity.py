@@ -264,9 +264,8 @@ def test_full_size_parity(ora, cid):
 
 def test_launch_modes_agree(ora):
     """Scheduling variants (mg_set_execution) must not change the arithmetic:
-    PDL on/off, the pipelined (TMA bulk) vs plain tile kernels, the cluster-
-    resident small-level smoother vs one launch per colour, and the device-side
-    cycle loop give bitwise-identical iterates.  The one-CTA triangular
+    PDL on/off, the pipelined (TMA bulk) vs plain tile kernels and the
+    device-side cycle loop give bitwise-identical iterates.  The one-CTA triangular
     coarsest solve vs the explicit-inverse GEMV (both Alg. 2's direct solve,
     reading A12) agree with the oracle to the X tolerance."""
     from paper_2104_13755_b200 import mg
@@ -279,8 +278,7 @@ def test_launch_modes_agree(ora):
             "default": 0,
             "nopdl": mg.MG_EXEC_NO_PDL,
             "nopipe": mg.MG_EXEC_NO_PIPE,
-            "nocluster": mg.MG_EXEC_NO_CLUSTER,
-            "nocluster_nopdl": mg.MG_EXEC_NO_CLUSTER | mg.MG_EXEC_NO_PDL,
+            "nopdl_nopipe": mg.MG_EXEC_NO_PDL | mg.MG_EXEC_NO_PIPE,
             "deviceloop": mg.MG_EXEC_DEVICE_LOOP,
             "trsv": mg.MG_EXEC_COARSE_TRSV,
         }
@@ -374,8 +372,7 @@ def test_split_csr_equals_split_cotan(ora):
 def test_smoother_variants_parity(ora, cid, kw):
     """Row f4: damped-Jacobi smoothing (App. E) and the symmetric
     (reversed post colours) V-cycle match the oracle's same variants (the
-    655k-row case runs level 1 through the pipelined lanes-per-row tiles and
-    the small levels through the cluster-resident smoother)."""
+    655k-row case runs level 1 through the pipelined lanes-per-row tiles)."""
     p = meshgen.make_config(cid, **kw)
     A, M, _ = oracle_problem(ora, p)
     Bo = oracle_rhs(ora, p, M)
