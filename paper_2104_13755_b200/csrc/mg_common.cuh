@@ -42,6 +42,19 @@ __device__ __forceinline__ int ld_stream(const int* p, uint64_t pol) {
     return v;
 }
 
+// ---- GS / Jacobi quotient ---------------------------------------------------
+// num / d for the K right-hand sides of a row with ONE division: q = num *
+// (1/d), refined by one residual step q + (num - q d)(1/d).  Within an ulp of
+// IEEE division (round-off level, like the FMA contraction of reading A18),
+// and the same arithmetic for every K, so a column's iterate does not depend
+// on how many columns are solved together.  Measured on B200: K = 3 fp64
+// divisions on a row's critical path cost ~340 cycles more than one
+// (tools/cluster_step_bench.cu).
+__device__ __forceinline__ double div_by(double num, double d, double inv) {
+    const double q = num * inv;
+    return fma(fma(-q, d, num), inv, q);
+}
+
 // ---- sub-warp groups ----------------------------------------------------
 __device__ __forceinline__ unsigned group_mask(int lpr) {
     if (lpr >= 32) return 0xffffffffu;

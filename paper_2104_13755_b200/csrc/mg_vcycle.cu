@@ -129,18 +129,19 @@ __global__ void __launch_bounds__(kTile) k_tile_sweep(const int* __restrict__ rp
     const int row = row0 + t;
     double s[K], d;
     tile_row<K, Unroll<K>::value>(cs, vs, rps[t] - e0, rps[t + 1] - e0, row, x, s, d);
+    const double inv = (MODE == 0 || MODE == 3) ? 1.0 / d : 0.0;
     if (MODE == 0) {
         double bv[K], xn[K];
         ldrow<K>(b + (size_t)row * VS<K>::S, bv);
 #pragma unroll
-        for (int c = 0; c < K; ++c) xn[c] = (bv[c] - s[c]) / d;
+        for (int c = 0; c < K; ++c) xn[c] = div_by(bv[c] - s[c], d, inv);
         strow<K>(x + (size_t)row * VS<K>::S, xn);
     } else {
 #pragma unroll
         for (int c = 0; c < K; ++c) {
             const double xi = x[(size_t)row * VS<K>::S + c];
             const double rr = b[(size_t)row * VS<K>::S + c] - fma(d, xi, s[c]);
-            r[(size_t)row * VS<K>::S + c] = MODE == 3 ? xi + omega * rr / d : rr;
+            r[(size_t)row * VS<K>::S + c] = MODE == 3 ? xi + div_by(omega * rr, d, inv) : rr;
         }
     }
 }
@@ -324,10 +325,11 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
             if (MODE != 0) ldrow_pol<K>(x + (size_t)row * VS<K>::S, xr, xpol);
             double s[K], dg;
             stage_row<K, UNR>(v, tid, row, x, s, dg, xpol);
+            const double inv = (MODE == 0 || MODE == 3) ? 1.0 / dg : 0.0;
             if (MODE == 0) {
                 double xn[K];
 #pragma unroll
-                for (int c = 0; c < K; ++c) xn[c] = (bv[c] - s[c]) / dg;
+                for (int c = 0; c < K; ++c) xn[c] = div_by(bv[c] - s[c], dg, inv);
                 strow_pol<K>(x + (size_t)row * VS<K>::S, xn, xpol);
             } else {
                 double rr[K];
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
                 } else if (MODE == 3) {
                     double xo[K];
 #pragma unroll
-                    for (int c = 0; c < K; ++c) xo[c] = xr[c] + omega * rr[c] / dg;
+                    for (int c = 0; c < K; ++c) xo[c] = xr[c] + div_by(omega * rr[c], dg, inv);
                     strow_pol<K>(r + (size_t)row * VS<K>::S, xo, xpol);
                 } else {
 #pragma unroll
@@ -461,9 +463,11 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
             for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], 0xffffffffu);
         if (valid && lane == 0) {
             double out[K];
+            const double inv = (MODE == 0 || MODE == 3) ? 1.0 / dg : 0.0;
 #pragma unroll
             for (int c = 0; c < K; ++c)
-                out[c] = MODE == 0 ? (bv[c] - s[c]) / dg : MODE == 3 ? xi[c] + omega * (bv[c] - s[c]) / dg : bv[c] - s[c];
+                out[c] = MODE == 0 ? div_by(bv[c] - s[c], dg, inv)
+                                   : MODE == 3 ? xi[c] + div_by(omega * (bv[c] - s[c]), dg, inv) : bv[c] - s[c];
             if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
             else if (MODE != 2) strow_pol<K>(r + (size_t)row * VS<K>::S, out, xpol);
             else
@@ -588,9 +592,11 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
         for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], mask);   // only the diagonal's lane holds x_i
     if (lane == 0) {
         double out[K];
+        const double inv = (MODE == 0 || MODE == 3) ? 1.0 / d : 0.0;
 #pragma unroll
         for (int c = 0; c < K; ++c)
-            out[c] = MODE == 0 ? (bv[c] - s[c]) / d : MODE == 3 ? xi[c] + omega * (bv[c] - s[c]) / d : bv[c] - s[c];
+            out[c] = MODE == 0 ? div_by(bv[c] - s[c], d, inv)
+                               : MODE == 3 ? xi[c] + div_by(omega * (bv[c] - s[c]), d, inv) : bv[c] - s[c];
         if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
         else strow<K>(r + (size_t)row * VS<K>::S, out);
     }

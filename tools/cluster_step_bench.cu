@@ -5,6 +5,7 @@
 //   mode 2: + row compute from shared memory (ROWS rows / CTA, NNZ entries,
 //           LPR lanes per row, fp64 division)
 //   mode 3: mode 2 with reciprocal multiply instead of division
+//   mode 4: mode 2 with a multiply by a constant (no division at all)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/cluster_step_bench tools/cluster_step_bench.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -65,7 +66,10 @@ __global__ void __launch_bounds__(512, 1) kbench(int steps, int rows, int nnz, i
                     d += __shfl_xor_sync(0xffffffffu, d, off, LPR);
                 }
                 if (lane == 0) {
-                    if (MODE == 3) {
+                    if (MODE == 4) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k) xs[li * K + k] = (1.0 - sacc[k]) * 0.25;
+                    } else if (MODE == 3) {
                         const double id = 1.0 / d;
 #pragma unroll
                         for (int k = 0; k < K; ++k) xs[li * K + k] = (1.0 - sacc[k]) * id;
@@ -132,10 +136,13 @@ int main() {
     run<32, 1>(0, 0, 512, 512);
     for (int rows : {8, 32, 64}) {
         run<32, 2>(rows, 30, 64, 512);
+        run<32, 3>(rows, 30, 64, 512);
+        run<32, 4>(rows, 30, 64, 512);
         run<8, 2>(rows, 30, 64, 512);
+        run<8, 4>(rows, 30, 64, 512);
         run<4, 2>(rows, 30, 64, 512);
         run<4, 3>(rows, 30, 64, 512);
-        run<4, 2>(rows, 30, 64, 256);
+        run<4, 4>(rows, 30, 64, 512);
     }
     return 0;
 }
