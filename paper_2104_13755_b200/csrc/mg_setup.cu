@@ -593,6 +593,20 @@ __device__ __forceinline__ void cg_mma(double (&acc)[4], const double (*As)[33],
     }
 }
 
+// acc[2x2 block of thread] += A A^T  (A[r][p])
+__device__ __forceinline__ void cg_mma_aat(double (&acc)[4], const double (*A)[33]) {
+    const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+#pragma unroll 8
+    for (int p = 0; p < 32; ++p) {
+        const double a0 = A[r0][p], a1 = A[r0 + 1][p];
+        const double b0 = A[c0][p], b1 = A[c0 + 1][p];
+        acc[0] = fma(a0, b0, acc[0]);
+        acc[1] = fma(a0, b1, acc[1]);
+        acc[2] = fma(a1, b0, acc[2]);
+        acc[3] = fma(a1, b1, acc[3]);
+    }
+}
+
 __device__ __forceinline__ void cg_store(double* G, int ld, const double (&v)[4]) {
     const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
     G[(size_t)r0 * ld + c0] = v[0];
@@ -616,7 +630,8 @@ __device__ __forceinline__ void cg_fetch(const double* G, int ld, double (&v)[4]
 // step); L is written back to S and 1/L_pp to rdg.  Shuffles behind the
 // thread-index branch made ptxas emit WARPSYNC.COLLECTIVE sequences, and
 // fp64 sqrt + division on the pivot chain cost ~250 cycles per step.
-__device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, double* rdg, int* err) {
+__device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, double* rdg, int* err,
+                                               volatile int* ready) {
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     double a[32];
@@ -633,7 +648,14 @@ __device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, do
         const double r = rsqrt_nr(piv);
         a[p] = lane == p ? piv * r : (lane > p ? a[p] * r : a[p]);
         colb[lane] = a[p];
-        if (lane == p) rdg[p] = r;
+        if (lane == p) {   // row p of L is final: publish it for the inverse (warp 1)
+            rdg[p] = r;
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+                if (c <= p) S[p][c] = a[c];
+            __threadfence_block();
+            ready[p] = 1;
+        }
         __syncwarp();
         const double lp = a[p];
 #pragma unroll
@@ -649,14 +671,20 @@ __device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, do
     __syncwarp();
 }
 
-// Warp 0: column `lane` of L^{-1} (L lower in S, 1/L_ii in rdg) into Li,
-// forward substitution with four independent partial sums per row.
-__device__ __forceinline__ void cg_trinv32_warp(const double (*S)[33], const double* rdg, double (*Li)[33]) {
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
+// Warp 1: column `lane` of L^{-1} (L lower in S, 1/L_ii in rdg) into Li,
+// forward substitution with four independent partial sums per row; row i is
+// computed as soon as warp 0 has published row i of L, so the inverse runs
+// one pivot behind the factor instead of after it.
+__device__ __forceinline__ void cg_trinv32_warp(const double (*S)[33], const double* rdg, double (*Li)[33],
+                                                const volatile int* ready) {
+    if (threadIdx.x < 32 || threadIdx.x >= 64) return;
+    const int lane = threadIdx.x - 32;
     double xv[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
+        while (ready[i] == 0) {
+        }
+        __threadfence_block();
         double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
         for (int q = 0; q < i; ++q) {
@@ -675,8 +703,11 @@ __device__ __forceinline__ void cg_trinv32_warp(const double (*S)[33], const dou
 __device__ __noinline__ void cg_factor_diag(double (*S)[33], double (*Li)[33], double* Dkk, double* Linvk, double* Wkk, int npad,
                                int* err) {
     __shared__ double colb[40], rdg[32];
-    cg_chol32_warp(S, colb, rdg, err);
-    cg_trinv32_warp(S, rdg, Li);
+    __shared__ int ready[32];
+    if (threadIdx.x < 32) ready[threadIdx.x] = 0;
+    __syncthreads();
+    cg_chol32_warp(S, colb, rdg, err, ready);   // warp 0
+    cg_trinv32_warp(S, rdg, Li, ready);         // warp 1, one row behind
     __syncthreads();
     for (int q = threadIdx.x; q < 1024; q += kCgThreads) {
         const int r = q >> 5, c = q & 31;
@@ -699,6 +730,7 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
                                                           int* err, unsigned* ctr, unsigned long long* tr) {
     __shared__ double As[32][33];
     __shared__ double Bs[32][33];
+    __shared__ double Lk1[32][33];   // CTA 0: its panel tile L_{k+1,k} of P1(k), reused in P2(k)
     const int nb = npad / 32;
     unsigned target = 0;
     // W lower off-diagonal tiles start at 0 (they accumulate T_ij)
@@ -731,6 +763,10 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
     const int G = gridDim.x;
     for (int k = 0; k < nb; ++k) {
         const int m = nb - k - 1;
+        // CTA 0 takes tile (k+1, k+1) in P2(k): its value before panel k's
+        // update is final since the last barrier -- fetch it now, off the path
+        double cpre[4] = {0.0, 0.0, 0.0, 0.0};
+        if (blockIdx.x == 0 && m > 0) cg_fetch(D + (size_t)((k + 1) * 32) * npad + (k + 1) * 32, npad, cpre);
         for (int t = blockIdx.x; t < m + k; t += G) {   // P1
             __syncthreads();
             if (t < m) {   // panel solve
@@ -741,6 +777,13 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
                 double acc[4] = {0.0, 0.0, 0.0, 0.0};
                 cg_mma(acc, As, Bs);
                 cg_store(D + (size_t)(i * 32) * npad + k * 32, npad, acc);
+                if (t == 0) {   // CTA 0: keep L_{k+1,k} for P2(k)
+                    const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
+                    Lk1[r0][c0] = acc[0];
+                    Lk1[r0][c0 + 1] = acc[1];
+                    Lk1[r0 + 1][c0] = acc[2];
+                    Lk1[r0 + 1][c0 + 1] = acc[3];
+                }
             } else {       // W_kj = -Linv_k T_kj
                 const int j = t - m;
                 double* Tkj = W + (size_t)(k * 32) * npad + j * 32;
@@ -762,13 +805,9 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
         if (blockIdx.x == 0) {   // tile (k+1, k+1): update and factor it for panel k+1
             const int kk = k + 1;
             __syncthreads();
-            cg_load<false>(As, D + (size_t)(kk * 32) * npad + k * 32, npad);
-            cg_load<true>(Bs, D + (size_t)(kk * 32) * npad + k * 32, npad);
-            __syncthreads();
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            cg_mma(acc, As, Bs);
-            double cv[4];
-            cg_fetch(D + (size_t)(kk * 32) * npad + kk * 32, npad, cv);
+            cg_mma_aat(acc, Lk1);   // L_{k+1,k} L_{k+1,k}^T from CTA 0's own panel tile
+            const double cv[4] = {cpre[0], cpre[1], cpre[2], cpre[3]};
             __syncthreads();
             const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
             As[r0][c0] = cv[0] - acc[0];
