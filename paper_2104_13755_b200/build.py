@@ -18,6 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INC}", f"-I{CSRC}"]
+# experiment builds only (tools/): extra -D flags; part of the source hash
+NVCC_FLAGS += os.environ.get("MG_NVCC_DEFINES", "").split()
 CU_SOURCES = ["mg_vcycle.cu", "mg_setup.cu", "mg_krylov.cu"]
 CPP_SOURCES = ["mg_host.cpp"]
 

@@ -126,7 +126,9 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
 //   tlen[i] = its length (<= kGalTMax); per fine nonzero e, tp[e] packs the
 //   T-position of parent q of col[e] in bits 5q..5q+4 (31: w == 0, skip).
 // * groups: consecutive coarse rows of gal_order (locality order) whose
-//   distinct children (fine rows, the U list) fit one CTA.
+//   distinct children (fine rows, the U list, ascending) fit one CTA; per U
+//   row umeta = {first nonzero, row, length, T length}; per group row
+//   crp = the coarse row's first slot.
 // * per coarse entry (I, J) of a group (rows in gal_order, columns
 //   ascending): its contributions (child u, T-position k, parent slot q of I
 //   in u's P row) packed u | k << 8 | q << 13, in children-list order (the
@@ -138,10 +140,9 @@ struct GalT {
     int tcap = 0;                         // 16 or 32
     std::vector<uint16_t> tp;             // [fine nnz]
     std::vector<uint8_t> tlen;            // [fine n]
-    std::vector<int32_t> grows, guoff, U; // groups: gal_order offsets, U offsets, U rows (ascending)
-    std::vector<uint32_t> umeta;          // per U row: staged offset | row length << 16 | tlen << 24
-    std::vector<int32_t> groff;           // groups: run offsets
-    std::vector<int32_t> runs;            // per run of consecutive U rows {first nonzero, staged base}; + sentinel {0, total}
+    std::vector<int32_t> grows, guoff;    // groups: gal_order offsets, U offsets
+    std::vector<int32_t> umeta;           // per U row (ascending in a group): {first nonzero, row, length, T length}
+    std::vector<int32_t> gcrp;            // per gal_order row: its first coarse slot
     std::vector<int32_t> gent, gcon;      // groups: entry offsets, contribution offsets
     std::vector<uint16_t> eoff;           // [entries + groups]
     std::vector<uint8_t> rowidx, slot;    // [entries]: local row, column slot in the row
@@ -152,7 +153,6 @@ constexpr int kGalTMax = 30;              // T-positions 0..30 (31 = skip) in 5-
 constexpr int kGalRowCap = 255;           // coarse rows per group (uint8 local row index; rows <= 256 entries)
 constexpr int kGalEntCap = 1024;          // coarse entries per group (staged in shared memory)
 constexpr int kGalConCap = 4096;          // contributions per group (staged in shared memory)
-constexpr int kGalNnzCap = 2048;          // fine nonzeros of the U rows per group (staged in shared memory)
 
 bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>& pc, const std::vector<double>& pw,
                       const std::vector<int32_t>& cptr, const std::vector<int32_t>& cidx,
@@ -226,34 +226,32 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
     std::vector<int32_t> kids, cur;
     G.grows.assign(1, 0);
     G.guoff.assign(1, 0);
-    G.groff.assign(1, 0);
-    for (int32_t i = 0; i < n; ++i)   // a row longer than 255 does not fit the 8-bit length field
-        if (L.irp[i + 1] - L.irp[i] > 255) return false;
+    G.gcrp.resize((size_t)nc);
+    for (int32_t r = 0; r < nc; ++r) G.gcrp[(size_t)r] = C.irp[order[r]];
     G.gent.assign(1, 0);
     G.gcon.assign(1, 0);
     int32_t r = 0;
     while (r < nc) {
         cur.clear();
         int32_t r1 = r;
-        size_t nent = 0, ncon = 0, gnnz = 0;
+        size_t nent = 0, ncon = 0;
         // grow the group while its distinct children, entries and contributions fit
         while (r1 < nc && r1 - r < kGalRowCap) {
             const int32_t I = order[r1];
             int add = 0;
-            size_t rcon = 0, rnnz = 0;
+            size_t rcon = 0;
             for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t) {
                 const int32_t i = cidx[t];
                 if (loc[i] == -1) {
                     loc[i] = -2;         // provisional mark (undone if the row does not fit)
                     ++add;
-                    rnnz += (size_t)(L.irp[i + 1] - L.irp[i]);
                 }
                 rcon += G.tlen[i];
             }
             const size_t rent = (size_t)(C.irp[I + 1] - C.irp[I]);
             if (rent > 256) return false;   // uint8 slot index
             const bool fits = (int)cur.size() + add <= ucap && nent + rent <= kGalEntCap &&
-                              ncon + rcon <= kGalConCap && gnnz + rnnz <= kGalNnzCap;
+                              ncon + rcon <= kGalConCap;
             if (!fits) {
                 for (int32_t t = cptr[I]; t < cptr[I + 1]; ++t)
                     if (loc[cidx[t]] == -2) loc[cidx[t]] = -1;
@@ -269,30 +267,15 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
             }
             nent += rent;
             ncon += rcon;
-            gnnz += rnnz;
             ++r1;
         }
-        // U in ascending fine order (runs of consecutive rows are staged with
-        // contiguous, coalesced copies); local indices follow that order
+        // U in ascending fine order (neighbouring phase-1 threads read
+        // neighbouring rows); local indices follow that order
         std::sort(cur.begin(), cur.end());
-        for (size_t x = 0; x < cur.size(); ++x) loc[cur[x]] = (int32_t)x;
-        {
-            int32_t sb = 0;
-            for (size_t x = 0; x < cur.size();) {
-                size_t y = x + 1;
-                while (y < cur.size() && cur[y] == cur[y - 1] + 1) ++y;
-                const int32_t e0 = L.irp[cur[x]], e1 = L.irp[cur[y - 1] + 1];
-                G.runs.insert(G.runs.end(), {e0, sb});
-                for (size_t z = x; z < y; ++z) {
-                    const int32_t i = cur[z];
-                    G.umeta.push_back((uint32_t)(sb + L.irp[i] - e0) | (uint32_t)(L.irp[i + 1] - L.irp[i]) << 16 |
-                                      (uint32_t)G.tlen[i] << 24);
-                }
-                sb += e1 - e0;
-                x = y;
-            }
-            G.runs.insert(G.runs.end(), {0, sb});   // sentinel: staged total
-            G.groff.push_back((int32_t)(G.runs.size() / 2));
+        for (size_t x = 0; x < cur.size(); ++x) {
+            const int32_t i = cur[x];
+            loc[i] = (int32_t)x;
+            G.umeta.insert(G.umeta.end(), {L.irp[i], i, L.irp[i + 1] - L.irp[i], (int32_t)G.tlen[i]});
         }
         // entries and contributions of the group's rows; the entries are
         // emitted in descending order of their contribution count (stable), so
@@ -331,9 +314,8 @@ bool build_galerkin_t(const Level& L, const Level& C, const std::vector<int32_t>
         }
         G.eoff.push_back((uint16_t)(G.con.size() - con0));   // group sentinel
         for (int32_t i : cur) loc[i] = -1;
-        G.U.insert(G.U.end(), cur.begin(), cur.end());
         G.grows.push_back(r1);
-        G.guoff.push_back((int32_t)G.U.size());
+        G.guoff.push_back((int32_t)(G.umeta.size() / 4));
         G.gent.push_back((int32_t)G.rowidx.size());
         G.gcon.push_back((int32_t)G.con.size());
         r = r1;
@@ -810,13 +792,11 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     G.slot.resize(G.slot.size() + 16, 0);
                     if ((e = L.gt_tp.upload(G.tp, s)) || (e = L.gt_tlen.upload(G.tlen, s)) ||
                         (e = C.gt_rows.upload(G.grows, s)) || (e = C.gt_uoff.upload(G.guoff, s)) ||
-                        (e = C.gt_U.upload(G.U.empty() ? std::vector<int32_t>(1, 0) : G.U, s)) ||
+                        (e = C.gt_umeta.upload(G.umeta.empty() ? std::vector<int32_t>(4, 0) : G.umeta, s)) ||
+                        (e = C.gt_crp.upload(G.gcrp.empty() ? std::vector<int32_t>(1, 0) : G.gcrp, s)) ||
                         (e = C.gt_ent.upload(G.gent, s)) || (e = C.gt_con.upload(G.gcon, s)) ||
                         (e = C.gt_eoff.upload(G.eoff, s)) || (e = C.gt_rowidx.upload(G.rowidx, s)) ||
-                        (e = C.gt_slot.upload(G.slot, s)) ||
-                        (e = C.gt_codes.upload(G.con, s)) || (e = C.gt_umeta.upload(G.umeta, s)) ||
-                        (e = C.gt_roff.upload(G.groff, s)) ||
-                        (e = C.gt_runs.upload(G.runs.empty() ? std::vector<int32_t>(2, 0) : G.runs, s)) ||
+                        (e = C.gt_slot.upload(G.slot, s)) || (e = C.gt_codes.upload(G.con, s)) ||
                         (e = cudaStreamSynchronize(s)))
                         return c->cuda_fail(e, "pattern upload");
                     C.galt_tcap = G.tcap;

@@ -95,13 +95,13 @@ struct Level {
     // build_galerkin_t in mg_host.cpp, integer data only)
     int galt_tcap = 0;                    // 16 / 32: T-positions per fine row; 0: generic kernel
     int galt_ngroups = 0;
-    DBuf<int32_t> gt_rows, gt_uoff, gt_U; // groups: gal_order offsets, U offsets, distinct children
+    DBuf<int32_t> gt_rows, gt_uoff;       // groups: gal_order offsets, offsets into the distinct children (U)
     DBuf<int32_t> gt_ent, gt_con;         // groups: coarse-entry offsets, contribution offsets
     DBuf<uint16_t> gt_eoff;               // per entry (+1 sentinel per group): contribution offset in the group
     DBuf<uint8_t> gt_rowidx, gt_slot;     // per entry: local row in the group, column slot in the row
     DBuf<uint16_t> gt_codes;              // contributions: child u | T-position k << 8 | parent slot q << 13
-    DBuf<uint32_t> gt_umeta;              // per U row: staged offset | length << 16 | T length << 24
-    DBuf<int32_t> gt_roff, gt_runs;       // groups: run offsets; runs {first nonzero, staged base} + sentinel
+    DBuf<int32_t> gt_umeta;               // per U row: {first nonzero, fine row, length, T length}
+    DBuf<int32_t> gt_crp;                 // per gal_order row: first slot of the coarse row
     DBuf<uint16_t> gt_tp;                 // (this level fine) per nonzero: T-positions of the 3 parents of col
     DBuf<uint8_t> gt_tlen;                // (this level fine) T-pattern length per row
     DBuf<double> prow_w;                  // P rows packed: {w0, w1, w2, 0} (this level fine)

@@ -322,42 +322,35 @@ __global__ void __launch_bounds__(kGalWarps * 32) k_galerkin(
 //   (P^T A P)_IJ = sum_{i child of I} w_iI T_iJ,   T_iJ = sum_{j in row i} a_ij w_jJ
 // (Eq. gca; P's rows hold <= 3 barycentric weights).
 // One CTA per group of consecutive coarse rows in locality order
-// (build_galerkin_t, mg_host.cpp).  Every global access of a phase is issued
-// before the first one is consumed (the kernel is latency-bound per CTA):
-//   stage 2 (issued first, asynchronous) the group's contribution lists,
-//           16-byte cp.async into their own shared region;
-//   stage 1 the fine rows of the group's distinct children (the U list, in
-//           ascending order: runs of consecutive rows are contiguous) into
-//           shared memory: each thread takes up to kGalSlots nonzeros of the
-//           flattened runs, coalesced -- a fine row leaves L2 once per group;
-//   phase 1 one thread per child i: T_i = sum over row i of a_ij * (the 3 P
-//           weights of j), accumulated at the precomputed T-positions in
-//           Ts[pos][u]; the P weights of a row's columns are gathered at once;
+// (build_galerkin_t, mg_host.cpp); the kernel is latency-bound per CTA:
+//   stage   (issued first, asynchronous) the group's contribution lists,
+//           16-byte cp.async into shared memory;
+//   phase 1 one thread per distinct child i of the group (the U list, fine
+//           rows ascending, so neighbouring threads read neighbouring rows):
+//           its row of A_l read straight from global memory in batches of GB
+//           nonzeros, then the P rows of those columns gathered at once;
+//           T_i = sum over row i of a_ij * (the 3 P weights of j),
+//           accumulated at the precomputed T-positions in Ts[pos][u];
 //   phase 2 one thread per coarse entry (I, J): the sum of w_{u,q} T_u[k]
 //           over the entry's contribution list (children-list order), in a
 //           register; entries come sorted by list length.
 // Every sum runs in a fixed order: deterministic, no atomics.  Only integer
 // structure is precomputed; every value (a_ij, w) is read here.
 // Caps shared with build_galerkin_t: distinct children per group 4096 / TCAP
-// (256 for TCAP 16, 128 for 32), coarse entries 1024, contributions 4096,
-// staged fine nonzeros 2048, runs 256.
+// (256 for TCAP 16, 128 for 32), coarse entries 1024, contributions 4096.
 constexpr int kGalThreads = 256;
 template <int TCAP>
 __host__ __device__ constexpr int galt_ucap() { return 4096 / TCAP; }
 constexpr int kGalEntCapK = 1024;
 constexpr int kGalConCapK = 4096;
-constexpr int kGalNnzCapK = 2048;
-constexpr int kGalRunCapK = 264;   // runs per group + the sentinel {0, staged total}
-constexpr int kGalSlots = kGalNnzCapK / kGalThreads;   // staged nonzeros per thread
-// stage 2 bytes (each array from its 16-byte aligned-down start): contributions,
+// stage bytes (each array from its 16-byte aligned-down start): contributions,
 // entry offsets (+ sentinel), local rows, slots
 constexpr int kGalStage2 = (kGalConCapK * 2 + 16) + ((kGalEntCapK + 1) * 2 + 32) + 2 * (kGalEntCapK + 32);
-constexpr int kGalStage1 = kGalNnzCapK * (8 + 4 + 2);
 
 template <int TCAP>
 constexpr size_t galt_smem() {
     return (size_t)TCAP * (galt_ucap<TCAP>() + 1) * 8 + 3 * (size_t)galt_ucap<TCAP>() * 8 + 256 * 4 +
-           kGalRunCapK * 8 + (size_t)kGalStage1 + (size_t)kGalStage2 + 64;
+           (size_t)kGalStage2 + 64;
 }
 
 // 16-byte-aligned window [first & ~15, first + bytes) in uint4 units
@@ -380,34 +373,42 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// measured on C4 (all levels, ms): 2 CTAs/SM x 8-nonzero batches 0.95,
+// 3 x 4 1.22, 4 x 4 1.26 (64 registers: 8-wide batches spill)
+#ifndef MG_GALT_MINB
+#define MG_GALT_MINB 2
+#endif
+#ifndef MG_GALT_GB
+#define MG_GALT_GB 8
+#endif
 template <int TCAP>
-__global__ void __launch_bounds__(kGalThreads, 2) k_galerkin_t(
-    const int* __restrict__ grows, const int* __restrict__ guoff, const int* __restrict__ U,
-    const uint32_t* __restrict__ umeta, const int* __restrict__ groff, const int2* __restrict__ runs,
-    const int* __restrict__ order, const int* __restrict__ gent, const int* __restrict__ gcon,
+struct GalTCfg {
+    static constexpr int kMinBlocks = MG_GALT_MINB;   // CTAs per SM
+    static constexpr int kBatch = MG_GALT_GB;         // nonzeros per phase-1 batch
+};
+
+template <int TCAP>
+__global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_galerkin_t(
+    const int* __restrict__ grows, const int* __restrict__ guoff, const int4* __restrict__ umeta,
+    const int* __restrict__ gcrp, const int* __restrict__ gent, const int* __restrict__ gcon,
     const uint16_t* __restrict__ geoff, const uint8_t* __restrict__ growidx, const uint8_t* __restrict__ gslot,
-    const uint16_t* __restrict__ gcodes, const int* __restrict__ crp, double* __restrict__ cval,
-    const int* __restrict__ col, const double* __restrict__ val, const uint16_t* __restrict__ tp,
-    const double4* __restrict__ prow_w) {
+    const uint16_t* __restrict__ gcodes, double* __restrict__ cval, const int* __restrict__ col,
+    const double* __restrict__ val, const uint16_t* __restrict__ tp, const double4* __restrict__ prow_w) {
     constexpr int UCAP = galt_ucap<TCAP>();
     constexpr int TSTR = UCAP + 1;   // odd stride: spreads the T reads of phase 2 over banks
+    constexpr int GB = GalTCfg<TCAP>::kBatch;
     extern __shared__ __align__(16) unsigned char galt_sm[];
     double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][TSTR]
     double* Ws = Ts + (size_t)TCAP * TSTR;                                 // [3][UCAP]
-    double* Sval = Ws + 3 * UCAP;                                          // stage 1: [kGalNnzCapK]
-    int* Scol = reinterpret_cast<int*>(Sval + kGalNnzCapK);
-    int* RowStart = Scol + kGalNnzCapK;                                    // [256] crp of the group's rows
-    int2* RunS = reinterpret_cast<int2*>(RowStart + 256);                  // [kGalRunCapK] {first nonzero, staged base}
-    uint16_t* Stp = reinterpret_cast<uint16_t*>(RunS + kGalRunCapK);       // [kGalNnzCapK]
-    unsigned char* Stage2 = reinterpret_cast<unsigned char*>(Stp + kGalNnzCapK);   // 16-byte aligned
+    int* RowStart = reinterpret_cast<int*>(Ws + 3 * UCAP);                 // [256] crp of the group's rows
+    unsigned char* Stage2 = reinterpret_cast<unsigned char*>(RowStart + 256);   // 16-byte aligned
     const int g = blockIdx.x;
     const int tid = threadIdx.x;
     const int r0 = grows[g], nr = grows[g + 1] - r0;
     const int u0 = guoff[g], nu = guoff[g + 1] - u0;
     const int e0g = gent[g], nent = gent[g + 1] - e0g;
     const int c0g = gcon[g], ncon = gcon[g + 1] - c0g;
-    const int ra = groff[g], nrun = groff[g + 1] - ra - 1;   // the last entry is the sentinel
-    // ---- stage 2 (asynchronous): contributions, entry offsets with the group sentinel, rows, slots
+    // ---- stage (asynchronous): contributions, entry offsets with the group sentinel, rows, slots
     const Win wc = win16(gcodes + c0g, ncon * 2);
     const Win we = win16(geoff + e0g + g, (nent + 1) * 2);
     const Win wr = win16(growidx + e0g, nent);
@@ -421,73 +422,35 @@ __global__ void __launch_bounds__(kGalThreads, 2) k_galerkin_t(
             cp_async16(St + t, src);
         }
     }
-    // ---- stage 1: run descriptors, then every thread's slots of the flattened runs
-    if (tid <= nrun) RunS[tid] = __ldg(runs + ra + tid);
-    if (tid < nr) RowStart[tid] = __ldg(crp + __ldg(order + r0 + tid));
-    int i = 0;
-    uint32_t meta = 0;
-    if (tid < nu) {
-        i = __ldg(U + u0 + tid);
-        meta = __ldg(umeta + u0 + tid);
-    }
-    __syncthreads();
-    const int tot = RunS[nrun].y;   // staged nonzeros of the group
-    {
-        int ga[kGalSlots];
-#pragma unroll
-        for (int v = 0; v < kGalSlots; ++v) {
-            const int x = tid + v * kGalThreads;
-            int lo = 0, hi = nrun - 1;
-            while (lo < hi) {   // last run with staged base <= x
-                const int mid = (lo + hi + 1) >> 1;
-                if (RunS[mid].y <= x) lo = mid;
-                else hi = mid - 1;
-            }
-            ga[v] = x < tot ? RunS[lo].x + (x - RunS[lo].y) : -1;
-        }
-        int cv[kGalSlots];
-        double av[kGalSlots];
-        unsigned short tv[kGalSlots];
-#pragma unroll
-        for (int v = 0; v < kGalSlots; ++v) {
-            if (ga[v] >= 0) {
-                cv[v] = __ldg(col + ga[v]);
-                av[v] = __ldg(val + ga[v]);
-                tv[v] = __ldg(tp + ga[v]);
-            }
-        }
-#pragma unroll
-        for (int v = 0; v < kGalSlots; ++v) {
-            const int x = tid + v * kGalThreads;
-            if (ga[v] >= 0) {
-                Scol[x] = cv[v];
-                Sval[x] = av[v];
-                Stp[x] = tv[v];
-            }
-        }
-    }
-    __syncthreads();
+    if (tid < nr) RowStart[tid] = __ldg(gcrp + r0 + tid);
     // ---- phase 1: T_u for every distinct child u of the group
     if (tid < nu) {
-        const int so = (int)(meta & 0xffffu), len = (int)((meta >> 16) & 255u), L = (int)(meta >> 24);
-        const double4 wi = ldg_d4(prow_w + i);
+        const int4 m = __ldg(umeta + u0 + tid);   // {first nonzero, fine row, length, T length}
+        const int e0 = m.x, len = m.z, L = m.w;
+        const double4 wi = ldg_d4(prow_w + m.y);
 #pragma unroll
         for (int k = 0; k < TCAP; ++k)
             if (k < L) Ts[k * TSTR + tid] = 0.0;
-        constexpr int B = 8;
-        for (int x = 0; x < len; x += B) {
-            double4 w[B];
+        for (int x = 0; x < len; x += GB) {
+            int c[GB];
+            double a[GB];
+            unsigned t[GB];
 #pragma unroll
-            for (int u = 0; u < B; ++u) w[u] = ldg_d4(prow_w + (x + u < len ? Scol[so + x + u] : i));
+            for (int u = 0; u < GB; ++u) {
+                const bool ok = x + u < len;
+                c[u] = ok ? __ldg(col + e0 + x + u) : m.y;
+                a[u] = ok ? __ldg(val + e0 + x + u) : 0.0;
+                t[u] = ok ? (unsigned)__ldg(tp + e0 + x + u) : 0x7fffu;
+            }
+            double4 w[GB];
 #pragma unroll
-            for (int u = 0; u < B; ++u) {
-                if (x + u >= len) break;
-                const double a = Sval[so + x + u];
-                const unsigned c = Stp[so + x + u];
-                const unsigned p0 = c & 31u, p1 = (c >> 5) & 31u, p2 = (c >> 10) & 31u;
-                if (p0 != 31u) Ts[p0 * TSTR + tid] += a * w[u].x;
-                if (p1 != 31u) Ts[p1 * TSTR + tid] += a * w[u].y;
-                if (p2 != 31u) Ts[p2 * TSTR + tid] += a * w[u].z;
+            for (int u = 0; u < GB; ++u) w[u] = ldg_d4(prow_w + c[u]);
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                const unsigned p0 = t[u] & 31u, p1 = (t[u] >> 5) & 31u, p2 = (t[u] >> 10) & 31u;
+                if (p0 != 31u) Ts[p0 * TSTR + tid] += a[u] * w[u].x;
+                if (p1 != 31u) Ts[p1 * TSTR + tid] += a[u] * w[u].y;
+                if (p2 != 31u) Ts[p2 * TSTR + tid] += a[u] * w[u].z;
             }
         }
         Ws[tid] = wi.x;
@@ -961,10 +924,10 @@ int launch_galerkin(const Level& fine, const double* fval, const Level& coarse, 
     if (coarse.galt_tcap > 0 && coarse.galt_ngroups > 0) {
         auto go = [&](auto kern, size_t smem) {
             kern<<<coarse.galt_ngroups, kGalThreads, smem, s>>>(
-                coarse.gt_rows.p, coarse.gt_uoff.p, coarse.gt_U.p, coarse.gt_umeta.p, coarse.gt_roff.p,
-                reinterpret_cast<const int2*>(coarse.gt_runs.p), coarse.gal_order.p, coarse.gt_ent.p,
-                coarse.gt_con.p, coarse.gt_eoff.p, coarse.gt_rowidx.p, coarse.gt_slot.p, coarse.gt_codes.p,
-                coarse.rp.p, cval, fine.col.p, fval, fine.gt_tp.p, reinterpret_cast<const double4*>(fine.prow_w.p));
+                coarse.gt_rows.p, coarse.gt_uoff.p, reinterpret_cast<const int4*>(coarse.gt_umeta.p),
+                coarse.gt_crp.p, coarse.gt_ent.p, coarse.gt_con.p, coarse.gt_eoff.p, coarse.gt_rowidx.p,
+                coarse.gt_slot.p, coarse.gt_codes.p, cval, fine.col.p, fval, fine.gt_tp.p,
+                reinterpret_cast<const double4*>(fine.prow_w.p));
         };
         if (coarse.galt_tcap <= 16) go(k_galerkin_t<16>, galt_smem<16>());
         else go(k_galerkin_t<32>, galt_smem<32>());
