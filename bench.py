@@ -546,7 +546,7 @@ def run_mg(args):
 
     # roofline of the dominant kernel: fine-level multicolour GS sweep
     gs_ms, gs_launches = prof.get("gs_sweep", {}).get(0, (0.0, 0))
-    sweeps = gs_launches / nc0 if nc0 else 0
+    sweeps = 4 * sum(cycles)                   # V(2,2): mu_pre + mu_post sweeps on level 0 per cycle
     sweep_bytes = gs_sweep_bytes(n0, nnz0, k)
     achieved = sweeps * sweep_bytes / (gs_ms / 1e3) / 1e9 if gs_ms > 0 else 0.0
     traffic = None
@@ -555,13 +555,13 @@ def run_mg(args):
         traffic = tr.get(f"config{args.config}", {}).get("gs_sweep_level0_bytes_per_launch")
     except Exception:
         pass
-    kname = "k_tile_pipe<K,0>" if nnz0 / max(n0, 1) <= 12 else "k_lpr_sweep<K,LPR,0>"
+    kname = ("k_tile_pipe<K,0>" if nnz0 / max(n0, 1) <= 12 else "k_lpr_sweep<K,LPR,0>") + \
+        f": level-0 multicolour GS sweep ({nc0} colour launches per sweep)"
     roofline = {"bound": "hbm",
-                "kernel": f"{kname}: level-0 multicolour GS sweep ({nc0} colour launches per sweep; "
-                          f"algorithmic bytes per sweep = 12 nnz + 4 n + 24 k n, DESIGN.md §5)",
+                "kernel": kname + "; algorithmic bytes per sweep = 12 nnz + 4 n + 24 k n, DESIGN.md §5",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind, "traffic": traffic,
-                "algorithmic_bytes_per_launch": sweep_bytes / nc0 if nc0 else None,
+                "algorithmic_bytes_per_launch": sweeps * sweep_bytes / gs_launches if gs_launches else None,
                 "avg_launch_us": gs_ms * 1e3 / gs_launches if gs_launches else None}
 
     # ---- per-class breakdown (separate, untimed pass with every class timed)
