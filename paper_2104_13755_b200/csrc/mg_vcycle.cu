@@ -607,15 +607,26 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
 // vertices (transpose of P): deterministic, no atomics.  G lanes per coarse
 // row; children indices and weights prefetched before the wait.  Zeroes the
 // coarse iterate (the recursive V-cycle starts from 0).
-constexpr int kRestrictG = 8;   // measured: 8 lanes x 4 prefetched children beat 16 x 2 (C4 L0 225 -> 191 us/cycle)
-// G lanes per coarse row, U = 32 / G children per lane prefetched before the
-// PDL wait; after it every lane issues its U residual gathers at once.
-template <int K, int G>
+// G lanes per coarse row, U children per lane prefetched before the PDL wait;
+// after it every lane issues its U residual gathers at once (children beyond
+// G * U in a tail loop).  The kernel is latency-bound: ~30 waves of a 3-deep
+// dependent chain (children offsets -> children -> residual rows), so fewer
+// lanes per row (fewer waves) win while G * U still covers a typical coarse
+// row (~12 children).  Measured on B200 (C4, residual + restriction ms/step,
+// level 0 / level 1): 16 x 2 1.57 / -, 8 x 4 1.30 / 0.634, 8 x 2 1.13 / 0.601,
+// 4 x 8 1.41 / 0.644, 4 x 4 1.06 / 0.614 (profiles/r02/restrict_ab.txt).
+#ifndef MG_RESTRICT_G
+#define MG_RESTRICT_G 4
+#endif
+#ifndef MG_RESTRICT_U
+#define MG_RESTRICT_U 4
+#endif
+constexpr int kRestrictG = MG_RESTRICT_G;
+template <int K, int G, int U = 32 / G>
 __global__ void __launch_bounds__(kBlock) k_restrict(const int* __restrict__ cptr, const int* __restrict__ cidx,
                                                      const double* __restrict__ cw, const double* __restrict__ r,
                                                      double* __restrict__ bc, double* __restrict__ xc, int nc,
                                                      const int* __restrict__ order) {
-    constexpr int U = 32 / G;
     const int g = (blockIdx.x * kBlock + threadIdx.x) / G;
     const int lane = threadIdx.x & (G - 1);
     pdl_launch_dependents();
@@ -1195,8 +1206,8 @@ int vc_restrict(int K, const Level& C, const Level& F, bool pdl, cudaStream_t s)
     const int* ci = ordered ? (const int*)C.rcidx.p : (const int*)C.cidx.p;
     const double* cwp = ordered ? (const double*)C.rcw.p : (const double*)C.cw.p;
     switch (G) {
-        case 4: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 4>, nblk((int64_t)C.n * 4, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
-        case 8: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 4: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 4, MG_RESTRICT_U>, nblk((int64_t)C.n * 4, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
+        case 8: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8, MG_RESTRICT_U>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
         case 16: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 16>, nblk((int64_t)C.n * 16, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
         default: MG_K_SWITCH(K, (launch_k(pdl, k_restrict<KK, 8>, nblk((int64_t)C.n * 8, kBlock), kBlock, 0, s, cp, ci, cwp, F.r.p, C.b.p, C.x.p, C.n, ord), 1))
     }
