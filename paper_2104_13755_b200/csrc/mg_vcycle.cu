@@ -613,8 +613,9 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
 // dependent chain (children offsets -> children -> residual rows), so fewer
 // lanes per row (fewer waves) win while G * U still covers a typical coarse
 // row (~12 children).  Measured on B200 (C4, residual + restriction ms/step,
-// level 0 / level 1): 16 x 2 1.57 / -, 8 x 4 1.30 / 0.634, 8 x 2 1.13 / 0.601,
-// 4 x 8 1.41 / 0.644, 4 x 4 1.06 / 0.614 (profiles/r02/restrict_ab.txt).
+// level 0 / level 1): 8 x 4 1.30 / 0.634, 8 x 2 1.13 / 0.601, 4 x 8 1.41 /
+// 0.644, 4 x 4 1.06 / 0.614 (profiles/r02/restrict_ab.txt; round 1: 16 x 2
+// 225 us/cycle against 8 x 4 191 at level 0).
 #ifndef MG_RESTRICT_G
 #define MG_RESTRICT_G 4
 #endif
