@@ -262,7 +262,11 @@ class Workload:
         self.hB = torch.from_numpy(np.ascontiguousarray(p.rhs)).pin_memory() if p.rhs_kind == "direct" else \
             torch.zeros((self.n, self.k), dtype=torch.float64).pin_memory()
         self.hX = torch.zeros((self.n, self.k), dtype=torch.float64).pin_memory()
-        self.hXcur = self.hV.clone().pin_memory() if p.rhs_kind == "mcf" else None
+        self.dV = torch.empty_like(self.V)
+        self.dF = torch.empty_like(self.Fr) if self.Fr is not None else None
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        self.evV = torch.cuda.Event()
+        self.evF = torch.cuda.Event()
         self.max_cycles = p.max_cycles
         self.rel_tol = p.rel_tol
         self.levels = None
@@ -309,42 +313,51 @@ class Workload:
         return cyc
 
     def step_host(self, status=None):
-        """The same step through the C ABI with the step's inputs and result
-        in HOST (pinned) buffers: positions, the data f (or X_t) and X0 go in,
-        X comes out; the library stages the host<->device copies inside the
-        calls.  B = M f is a device buffer (mg_apply_mass takes host and
-        device pointers independently), as a user keeps it.  Config 5: every
-        time step of the loop goes through host buffers (positions in, X_{t+1}
-        out), as an application displaying each frame would."""
+        """The same step end to end from HOST (pinned) buffers: the step's
+        inputs go up and its result comes back inside the timed region, and
+        every call is the C ABI.  C1-C4: positions V and the data f (C1: B)
+        are copied on a copy stream, V first; the library's assembly waits
+        for V only, so the copy of f overlaps assembly + Galerkin + factor;
+        X comes back through mg_solve's host-pointer path.  C5: the bench
+        step is the 20-time-step loop from V0, so its input is V0 and its
+        result X_20 (the intermediate positions stay on the device, as in the
+        device-resident leg)."""
+        import torch
         S, p = self.S, self.p
         status = [] if status is None else status
+        cs = self.copy_stream
+        cs.wait_stream(self.stream)
+        with torch.cuda.stream(cs):
+            self.dV.copy_(self.hV, non_blocking=True)
+            self.evV.record(cs)
+            if self.hF is not None:
+                self.dF.copy_(self.hF, non_blocking=True)
+            elif p.rhs_kind == "direct":
+                self.B.copy_(self.hB, non_blocking=True)
+            self.evF.record(cs)
+        self.stream.wait_event(self.evV)
         cyc = 0
         if p.rhs_kind == "mcf":
-            self.hXcur.copy_(self.hV)
-        for t in range(self.n_substeps()):
-            if p.rhs_kind == "mcf":
-                S.set_matrix_cotan(self.hXcur, p.mass_coeff, p.lap_coeff)
-                S.apply_mass(self.hXcur, self.B)
-                cyc += self._solve(self.B, self.hXcur, status)
-            else:
-                S.set_matrix_cotan(self.hV, p.mass_coeff, p.lap_coeff)
-                if self.hF is not None:
-                    S.apply_mass(self.hF, self.B)
-                    B = self.B
-                else:
-                    B = self.hB
-                cyc += self._solve(B, self.hX, status)
+            self.Xcur.copy_(self.dV)
+            for t in range(self.n_substeps()):
+                S.set_matrix_cotan(self.Xcur, p.mass_coeff, p.lap_coeff)
+                S.apply_mass(self.Xcur, self.B)
+                cyc += self._solve(self.B, self.Xcur, status)
+            self.hX.copy_(self.Xcur)          # X_20 back to the host (synchronous)
+            return cyc
+        S.set_matrix_cotan(self.dV, p.mass_coeff, p.lap_coeff)
+        self.stream.wait_event(self.evF)
+        if self.hF is not None:
+            S.apply_mass(self.dF, self.B)
+        cyc += self._solve(self.B, self.hX, status)
         return cyc
 
     def host_bytes(self):
-        """Host<->device bytes per bench step, counted from the host buffers the
-        step passes to the C ABI."""
+        """Host<->device bytes per bench step, counted from the host buffers
+        copied in step_host."""
         n, k = self.n, self.k
-        if self.p.rhs_kind == "mcf":
-            # per time step: positions (cotan), X_t (mass), X0 = X_t (solve) in; X_{t+1} out
-            return self.MCF_STEPS * (24 * n + 8 * n * k + 8 * n * k), self.MCF_STEPS * 8 * n * k
-        h2d = 24 * n + 8 * n * k         # positions into mg_set_matrix_cotan; f into mg_apply_mass or B into mg_solve
-        d2h = 8 * n * k                  # X out of mg_solve
+        h2d = 24 * n + (8 * n * k if self.p.rhs_kind != "mcf" else 0)   # positions (V or V0) + f / B
+        d2h = 8 * n * k                                                   # X (C5: X_20)
         return h2d, d2h
 
     def level_sizes(self):

@@ -349,7 +349,7 @@ constexpr int kGalStage2 = (kGalConCapK * 2 + 16) + ((kGalEntCapK + 1) * 2 + 32)
 
 template <int TCAP>
 constexpr size_t galt_smem() {
-    return (size_t)TCAP * (galt_ucap<TCAP>() + 1) * 8 + 3 * (size_t)galt_ucap<TCAP>() * 8 + 256 * 4 +
+    return (size_t)TCAP * galt_ucap<TCAP>() * 8 + 3 * (size_t)galt_ucap<TCAP>() * 8 + 256 * 4 +
            (size_t)kGalStage2 + 64;
 }
 
@@ -395,7 +395,13 @@ __global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_gale
     const uint16_t* __restrict__ gcodes, double* __restrict__ cval, const int* __restrict__ col,
     const double* __restrict__ val, const uint16_t* __restrict__ tp, const double4* __restrict__ prow_w) {
     constexpr int UCAP = galt_ucap<TCAP>();
-    constexpr int TSTR = UCAP + 1;   // odd stride: spreads the T reads of phase 2 over banks
+    // T stride = UCAP (a multiple of 16 doubles): in phase 1 lane l of a warp
+    // always hits bank pair l mod 16 whatever T-position it updates
+    // (conflict-free); phase 2 reads random (position, child) pairs with any
+    // stride.  The odd stride UCAP + 1 had 54% of the kernel's shared
+    // wavefronts as bank conflicts: C4 all levels 0.95 -> 0.86 ms
+    // (profiles/r02/galerkin_ab2.txt).
+    constexpr int TSTR = UCAP;
     constexpr int GB = GalTCfg<TCAP>::kBatch;
     extern __shared__ __align__(16) unsigned char galt_sm[];
     double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][TSTR]
@@ -428,9 +434,10 @@ __global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_gale
         const int4 m = __ldg(umeta + u0 + tid);   // {first nonzero, fine row, length, T length}
         const int e0 = m.x, len = m.z, L = m.w;
         const double4 wi = ldg_d4(prow_w + m.y);
+        double* Tu = Ts + tid;
 #pragma unroll
         for (int k = 0; k < TCAP; ++k)
-            if (k < L) Ts[k * TSTR + tid] = 0.0;
+            if (k < L) Tu[k * TSTR] = 0.0;
         for (int x = 0; x < len; x += GB) {
             int c[GB];
             double a[GB];
@@ -448,9 +455,9 @@ __global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_gale
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
                 const unsigned p0 = t[u] & 31u, p1 = (t[u] >> 5) & 31u, p2 = (t[u] >> 10) & 31u;
-                if (p0 != 31u) Ts[p0 * TSTR + tid] += a[u] * w[u].x;
-                if (p1 != 31u) Ts[p1 * TSTR + tid] += a[u] * w[u].y;
-                if (p2 != 31u) Ts[p2 * TSTR + tid] += a[u] * w[u].z;
+                if (p0 != 31u) Tu[p0 * TSTR] += a[u] * w[u].x;
+                if (p1 != 31u) Tu[p1 * TSTR] += a[u] * w[u].y;
+                if (p2 != 31u) Tu[p2 * TSTR] += a[u] * w[u].z;
             }
         }
         Ws[tid] = wi.x;
