@@ -682,32 +682,56 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         L.pipe = (L.tiled || L.pipe_lpr > 1) && c->use_pipe &&
                  pipe_smem_bytes(std::max(L.cap_gs, L.cap_all)) <= 200 * 1024;
         if (L.pipe) {
+            // Two tile sets, one per residency of the persistent kernels (3
+            // CTAs/SM: lanes-per-row tiles and k = 3 with 8-gather batches; 4
+            // otherwise, see pipe_grid in mg_vcycle.cu).  On thread-per-row
+            // levels a colour class whose last round of 256-row tiles would
+            // keep fewer than half of the resident grid G busy is cut into a
+            // multiple of G equal tiles instead (<= 256 rows), so every CTA
+            // runs the same number of tiles per pass; a class under one wave is
+            // spread over all CTAs with tiles of >= 128 rows.  With 256-row
+            // tiles C4 level 0's six colour passes take 27 rounds of 444 CTAs
+            // for 23.1 rounds of work (ncu: SMs idle 18% of a pass); balanced,
+            // its GS goes 3.30 -> 3.13 ms/step and C5's 12.15 -> 10.83; passes
+            // whose last round is mostly full (C3) or tiles under 128 rows (C2)
+            // measured slower (profiles/r02/tile_balance_ab.txt).
             std::vector<int32_t> td;
-            L.tile_off.assign(1, 0);
-            auto add_tiles = [&](int r0, int r1) {
-                for (int a = r0; a < r1; a += T) {
-                    const int nr = std::min(T, r1 - a);
-                    td.insert(td.end(), {a, nr, L.irp[a], L.irp[a + nr]});
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+            const std::vector<uint64_t> key = morton_keys(L.V, L.n);
+            for (int set = 0; set < 2; ++set) {
+                std::vector<int32_t>& toff = set == 0 ? L.tile_off : L.tile_off4;
+                const int base = (int)(td.size() / 4);
+                toff.assign(1, base);
+                const int G = (set == 0 ? 3 : 4) * nsm;
+                for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k) {
+                    const int r0 = L.colour_off[k], r1 = L.colour_off[k + 1], rows = r1 - r0;
+                    int Tr = T;
+                    const int nt256 = (rows + T - 1) / T;
+                    const int rounds = (nt256 + G - 1) / G;
+                    const double fill = (double)(nt256 - (rounds - 1) * G) / G;   // last round's occupancy
+                    if (L.pipe_lpr == 1 && rows > T && (rounds == 1 || fill < 0.5))
+                        Tr = std::max(128, (rows + rounds * G - 1) / (rounds * G));
+                    for (int a0 = r0; a0 < r1; a0 += Tr) {
+                        const int nr = std::min(Tr, r1 - a0);
+                        td.insert(td.end(), {a0, nr, L.irp[a0], L.irp[a0 + nr]});
+                    }
+                    toff.push_back((int32_t)(td.size() / 4));
                 }
-                L.tile_off.push_back((int32_t)(td.size() / 4));
-            };
-            for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k) add_tiles(L.colour_off[k], L.colour_off[k + 1]);
-            {
                 // whole-level passes (residual, norm) walk the colour tiles in
                 // Morton order of their middle row: all colours of one spatial
                 // window are processed together, so the neighbours' x gathered
                 // by a tile were just read by the tiles of the other colours
-                const std::vector<uint64_t> key = morton_keys(L.V, L.n);
-                const int ngs = (int)(td.size() / 4);
+                const int ngs = (int)(td.size() / 4) - base;
                 std::vector<int> idx(ngs);
-                std::iota(idx.begin(), idx.end(), 0);
+                std::iota(idx.begin(), idx.end(), base);
                 auto mid_key = [&](int t) { return key[L.perm[td[4 * t] + td[4 * t + 1] / 2]]; };
-                std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return mid_key(a) < mid_key(b); });
+                std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return mid_key(x) < mid_key(y); });
                 for (int t : idx) {
                     const int32_t d0 = td[4 * t], d1 = td[4 * t + 1], d2 = td[4 * t + 2], d3 = td[4 * t + 3];
                     td.insert(td.end(), {d0, d1, d2, d3});
                 }
-                L.tile_off.push_back((int32_t)(td.size() / 4));
+                toff.push_back((int32_t)(td.size() / 4));
             }
             L.serpentine = true;
             L.pass_ctr = 0;

@@ -71,6 +71,8 @@ struct Level {
     int pipe_lpr = 1;
                      // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
     std::vector<int32_t> tile_off;        // tiles of colour c: [tile_off[c], tile_off[c+1]); whole level: last range
+                                          // (set balanced for 3 resident CTAs per SM)
+    std::vector<int32_t> tile_off4;       // the same for 4 resident CTAs per SM (second set in `tiles`)
     DBuf<int32_t> tiles;                  // {row0, nrow, e0, e1} per tile
     std::vector<double> V;                // user-order positions [n][3]
     std::vector<int32_t> colour;          // user order

@@ -1012,9 +1012,14 @@ inline int pipe_nsm() {
 }
 // persistent grid: every CTA resident at once (registers: 4 CTAs/SM for the
 // thread-per-row kernel, 3 for the lanes-per-row and 8-gather variants)
+inline int pipe_per_sm(const Level& L, int K) { return (L.pipe_lpr > 1 || (K == 3 && L.pipe_unr8)) ? 3 : 4; }
+// the tile set balanced for that residency (setup_pattern, mg_host.cpp)
+inline const std::vector<int32_t>& pipe_tiles(const Level& L, int K) {
+    return pipe_per_sm(L, K) == 3 ? L.tile_off : L.tile_off4;
+}
 inline int pipe_grid(const Level& L, int K, int ntiles) {
     const size_t smem = 2 * ((stage_bytes(L.pipe_cap) + 127) / 128 * 128) + 2048;
-    const int by_regs = (L.pipe_lpr > 1 || (K == 3 && L.pipe_unr8)) ? 3 : 4;
+    const int by_regs = pipe_per_sm(L, K);
     const int per_sm = std::max(1, std::min<int>(by_regs, (int)((227 * 1024) / smem)));
     return std::max(1, std::min(ntiles, pipe_nsm() * per_sm));
 }
@@ -1051,14 +1056,15 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
     if (L.pipe) {
         // tile range of this colour class (GS) or of the whole level (residual)
         int t0, t1;
+        const std::vector<int32_t>& toff = pipe_tiles(L, K);
         if (MODE == 0) {
             int c = 0;
             while (L.colour_off[c] != r0) ++c;
-            t0 = L.tile_off[c];
-            t1 = L.tile_off[c + 1];
+            t0 = toff[c];
+            t1 = toff[c + 1];
         } else {
-            t0 = L.tile_off[L.tile_off.size() - 2];   // whole-level tiles are the last range
-            t1 = L.tile_off.back();
+            t0 = toff[toff.size() - 2];   // whole-level tiles are the last range
+            t1 = toff.back();
         }
         pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(L, K, t1 - t0), omega, pdl, s);
         return 1;
@@ -1084,7 +1090,8 @@ template <int K>
 int resnorm_k(const Level& L, double* partial, int nb, const double* bnorm, double* rho, bool pdl, cudaStream_t s) {
     int grid;
     if (L.pipe) {
-        const int t0 = L.tile_off[L.tile_off.size() - 2], t1 = L.tile_off.back();
+        const std::vector<int32_t>& toff = pipe_tiles(L, K);
+        const int t0 = toff[toff.size() - 2], t1 = toff.back();
         grid = std::min(nb, pipe_grid(L, K, t1 - t0));
         pipe_launch<K, 2>(L, t0, t1, L.x.p, nullptr, partial, grid, 0.0, pdl, s);
     } else if (L.tiled) {
