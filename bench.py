@@ -638,6 +638,22 @@ def run_mg(args):
                          f"in {tot['step_s']:.2f} s; value = V-cycles / host seconds, nothing projected",
                "phases_s": {k: round(tot[k], 4) for k in PHASE_KEYS}, "cycles": tot["cycles"], "cpu": hc}
 
+    # by time the largest class can be a latency-bound one (the small-level
+    # GS passes: L2-resident, one dependent launch per colour); reported next
+    # to the HBM roofline of the level-0 GS so the ranking is explicit
+    gs_b = breakdown.get("gs_sweep", {})
+    items = [(f"gs_sweep level {l}", v["ms"], v["launches"]) for l, v in gs_b.items()]
+    for cls_name in ("residual_restrict", "prolong", "resnorm", "galerkin", "assembly", "factor"):
+        for l, v in breakdown.get(cls_name, {}).items():
+            items.append((f"{cls_name} level {l}", v["ms"], v["launches"]))
+    small = [(l, v) for l, v in gs_b.items() if int(l) >= 3]
+    if small:
+        items.append(("gs_sweep levels 3+ (k_lpr_sweep, small colour classes)", sum(v["ms"] for _, v in small),
+                      sum(v["launches"] for _, v in small)))
+    tot_ms = sum(sum(v["ms"] for v in d.values()) for d in breakdown.values())
+    top = sorted(items, key=lambda t: -t[1])[:4]
+    dominant_by_time = [{"what": w, "ms_per_step": round(ms, 4), "share": round(ms / tot_ms, 3) if tot_ms else None,
+                         "launches": n, "us_per_launch": round(ms * 1e3 / n, 2) if n else None} for w, ms, n in top]
     vc_bytes = vcycle_bytes(levels_nnz, k)
     mean_solve = float(np.mean(solve_ms))
     mean_cyc = float(np.mean(cycles))
@@ -670,6 +686,7 @@ def run_mg(args):
                             "frac": (vc_bytes / (mean_solve / mean_cyc / 1e3) / 1e9) / peak if mean_cyc else None},
         "galerkin_bytes": galerkin_bytes(levels_nnz),
         "level_rooflines": level_rooflines(breakdown, levels_nnz, k, mean_cyc, peak, rebuilds=nsub),
+        "dominant_by_time": dominant_by_time,
         "breakdown_ms": breakdown,
         "setup_s_first_call": t_setup,
     }

@@ -602,6 +602,12 @@ __device__ __forceinline__ void cg_fetch(const double* G, int ld, double (&v)[4]
 // fp64 sqrt + division on the pivot chain cost ~250 cycles per step.
 __device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, double* rdg, int* err,
                                                volatile int* ready) {
+    // Warp 0, right-looking, lane i holds row i of the block in registers.
+    // Per pivot p: the pivot comes by shuffle, column p is scaled, every lane
+    // stores its element of column p of L into S[i][p] (one parallel store;
+    // the inverse warp reads columns) and into colb for the rank-1 update of
+    // the trailing rows; the column is published after the update (off the
+    // pivot chain).
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     double a[32];
@@ -610,22 +616,14 @@ __device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, do
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 32; ++p) {
-        if (lane == p) colb[32] = a[p];
-        __syncwarp();
-        double piv = colb[32];
+        double piv = __shfl_sync(0xffffffffu, a[p], p);
         bad |= !(piv > 0.0);
         piv = piv > 0.0 ? piv : 1.0;
         const double r = rsqrt_nr(piv);
         a[p] = lane == p ? piv * r : (lane > p ? a[p] * r : a[p]);
         colb[lane] = a[p];
-        if (lane == p) {   // row p of L is final: publish it for the inverse (warp 1)
-            rdg[p] = r;
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (c <= p) S[p][c] = a[c];
-            __threadfence_block();
-            ready[p] = 1;
-        }
+        S[lane][p] = a[p];   // rows < p hold the (unused) upper triangle
+        if (lane == p) rdg[p] = r;
         __syncwarp();
         const double lp = a[p];
 #pragma unroll
@@ -633,38 +631,35 @@ __device__ __forceinline__ void cg_chol32_warp(double (*S)[33], double* colb, do
             const double upd = fma(-lp, colb[c], a[c]);
             a[c] = lane >= c ? upd : a[c];
         }
+        if (lane == 0) {   // column p of L and 1/L_pp visible to warp 1
+            __threadfence_block();
+            ready[p] = 1;
+        }
         __syncwarp();
     }
-#pragma unroll
-    for (int c = 0; c < 32; ++c) S[lane][c] = a[c];
     if (bad && lane == 0) atomicExch(err, 1);
     __syncwarp();
 }
 
-// Warp 1: column `lane` of L^{-1} (L lower in S, 1/L_ii in rdg) into Li,
-// forward substitution with four independent partial sums per row; row i is
-// computed as soon as warp 0 has published row i of L, so the inverse runs
-// one pivot behind the factor instead of after it.
+// Warp 1: column `lane` of L^{-1} (L lower in S, 1/L_ii in rdg) into Li by
+// column-oriented forward substitution: x = e_lane; for p = 0..31: x_p *=
+// 1/L_pp, x_i -= L_ip x_p (i > p).  Step p needs only column p of L, so the
+// inverse runs one pivot behind the factor.
 __device__ __forceinline__ void cg_trinv32_warp(const double (*S)[33], const double* rdg, double (*Li)[33],
                                                 const volatile int* ready) {
     if (threadIdx.x < 32 || threadIdx.x >= 64) return;
     const int lane = threadIdx.x - 32;
     double xv[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        while (ready[i] == 0) {
+    for (int i = 0; i < 32; ++i) xv[i] = i == lane ? 1.0 : 0.0;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+        while (ready[p] == 0) {
         }
         __threadfence_block();
-        double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        xv[p] *= rdg[p];
 #pragma unroll
-        for (int q = 0; q < i; ++q) {
-            const double t = S[i][q] * xv[q];
-            if ((q & 3) == 0) s0 -= t;
-            else if ((q & 3) == 1) s1 -= t;
-            else if ((q & 3) == 2) s2 -= t;
-            else s3 -= t;
-        }
-        xv[i] = ((s0 + s1) + (s2 + s3)) * rdg[i];
+        for (int i = p + 1; i < 32; ++i) xv[i] = fma(-S[i][p], xv[p], xv[i]);
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i) Li[i][lane] = xv[i];
@@ -836,11 +831,28 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
         while (I * (I + 1) / 2 > t) --I;
         const int J = t - I * (I + 1) / 2;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        // the tiles of step k + 1 are fetched into registers while step k's
+        // product runs (each step would otherwise wait a full L2 round trip)
+        double pa[4], pb[4];
+        auto fetch = [&](int k) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = threadIdx.x + u * kCgThreads, r = q >> 5, c = q & 31;
+                pa[u] = __ldcg(W + (size_t)(k * 32 + r) * npad + I * 32 + c);
+                pb[u] = __ldcg(W + (size_t)(k * 32 + r) * npad + J * 32 + c);
+            }
+        };
+        fetch(I);
         for (int k = I; k < nb; ++k) {
             __syncthreads();
-            cg_load<true>(As, W + (size_t)(k * 32) * npad + I * 32, npad);    // As[r][p] = W_kI[p][r]
-            cg_load<false>(Bs, W + (size_t)(k * 32) * npad + J * 32, npad);   // Bs[p][c] = W_kJ[p][c]
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = threadIdx.x + u * kCgThreads, r = q >> 5, c = q & 31;
+                As[c][r] = pa[u];   // As[r][p] = W_kI[p][r]
+                Bs[r][c] = pb[u];   // Bs[p][c] = W_kJ[p][c]
+            }
             __syncthreads();
+            if (k + 1 < nb) fetch(k + 1);
             cg_mma(acc, As, Bs);
         }
         const int r0 = (threadIdx.x >> 4) * 2, c0 = (threadIdx.x & 15) * 2;
@@ -852,6 +864,7 @@ __global__ void __launch_bounds__(kCgThreads) k_chol_grid(double* __restrict__ D
         Zm[(size_t)c0 * npad + r0 + 1] = acc[2];
         Zm[(size_t)(c0 + 1) * npad + r0 + 1] = acc[3];
     }
+    cg_trace(tr, 102);
 }
 
 template <int K>
@@ -985,10 +998,30 @@ int launch_chol_grid(double* D, double* Linv, double* W, double* Z, int npad, in
     const int grid = std::max(2, std::min(grid_max, nb * (nb + 1) / 2 + 1));   // CTA 0 + >= 1 worker
     if (grid_max < 2) return -1;
     if (cudaMemsetAsync(ctr, 0, sizeof(unsigned), s) != cudaSuccess) return -1;
-    unsigned long long* trp = nullptr;   // phase timestamps of CTA 0 (debug builds pass a buffer)
+    unsigned long long* trp = nullptr;   // phase timestamps of CTA 0 (experiment builds pass a buffer)
+#ifdef MG_CHOL_TRACE
+    static unsigned long long* trbuf = nullptr;
+    if (!trbuf) cudaMalloc(&trbuf, 256 * sizeof(unsigned long long));
+    cudaMemsetAsync(trbuf, 0, 256 * sizeof(unsigned long long), s);
+    trp = trbuf;
+#endif
     void* args[] = {&D, &Linv, &W, &Z, &npad, &err, &ctr, &trp};
     const bool ok = cudaLaunchCooperativeKernel((const void*)k_chol_grid, dim3(grid), dim3(kCgThreads), args, 0, s) ==
                     cudaSuccess;
+#ifdef MG_CHOL_TRACE
+    {
+        unsigned long long h[256];
+        cudaMemcpyAsync(h, trbuf, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        auto us = [&](int a, int b) { return (h[b] && h[a]) ? (double)(h[b] - h[a]) * 1e-3 : -1.0; };
+        fprintf(stderr, "chol trace (us): zeroW %.1f prelude %.1f bar %.1f\n", us(0, 200) < 0 ? -1 : us(0, 200),
+                us(200, 201), us(1, 2));
+        for (int k = 0; k < nb; ++k)
+            fprintf(stderr, "  panel %2d: P1 %.1f bar %.1f P2 %.1f bar %.1f\n", k, us(k ? 6 + 4 * (k - 1) : 2, 3 + 4 * k),
+                    us(3 + 4 * k, 4 + 4 * k), us(4 + 4 * k, 5 + 4 * k), us(5 + 4 * k, 6 + 4 * k));
+        fprintf(stderr, "  factor total %.1f  tail (Z) %.1f\n", us(0, 100), us(101, 102));
+    }
+#endif
     return ok ? 1 : -1;
 }
 
