@@ -46,7 +46,8 @@ __device__ __forceinline__ void chol32_fast(double (*S)[33]) {
         a[p] = lane == p ? d : (lane > p ? a[p] * r : a[p]);
         const double lp = a[p];
 #pragma unroll
-        for (int c = p + 1; c < 32; ++c) {
+        for (int c = 1; c < 32; ++c) {
+            if (c <= p) continue;
             const double lcp = __shfl_sync(0xffffffffu, lp, c);
             const double upd = fma(-lp, lcp, a[c]);
             a[c] = lane >= c ? upd : a[c];
@@ -132,6 +133,52 @@ __device__ __forceinline__ void trinv32(const double (*S)[33], double (*Li)[33])
     for (int i = 0; i < 32; ++i) Li[i][lane] = xv[i];
 }
 
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double r = (double)rsqrtf((float)x);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    return r;
+}
+// factor AND inverse on one warp, registers only: lane i holds row i of A
+// (a[]) and column i of L^{-1} (xv[]); step p broadcasts column p of L by
+// shuffles (c = p+1 first: the next pivot's update), which serves both the
+// rank-1 update of the factor and the forward-substitution step p of the
+// inverse (xv_c -= L_cp * xv_p).
+__device__ __forceinline__ void chol32_fused(double (*S)[33], double (*Li)[33]) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        double a[32], xv[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            a[c] = S[lane][c];
+            xv[c] = c == lane ? 1.0 : 0.0;
+        }
+#pragma unroll
+        for (int p = 0; p < 32; ++p) {
+            double piv = __shfl_sync(0xffffffffu, a[p], p);
+            piv = piv > 0.0 ? piv : 1.0;
+            const double r = rsqrt_nr(piv);
+            const double l = lane == p ? piv * r : a[p] * r;   // column p of L (rows > p valid)
+            a[p] = lane >= p ? l : a[p];
+            xv[p] *= r;
+#pragma unroll
+            for (int c = 1; c < 32; ++c) {
+                if (c <= p) continue;
+                const double lcp = __shfl_sync(0xffffffffu, l, c);   // L_cp
+                const double upd = fma(-l, lcp, a[c]);
+                a[c] = lane >= c ? upd : a[c];
+                xv[c] = fma(-lcp, xv[p], xv[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            S[lane][c] = a[c];
+            Li[c][lane] = xv[c];
+        }
+    }
+    __syncthreads();
+}
+
 template <int V>
 __global__ void kbench(const double* A, double* out, long long* cyc, int reps) {
     __shared__ double S[32][33], Li[32][33], colb[40];
@@ -145,6 +192,7 @@ __global__ void kbench(const double* A, double* out, long long* cyc, int reps) {
         if (V == 3) chol32_smem(S, colb);
         if (V == 4) { trinv32_ilp(S, Li); __syncthreads(); }
         if (V == 5) { trinv32(S, Li); __syncthreads(); }
+        if (V == 6) chol32_fused(S, Li);
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) cyc[V] = (t1 - t0) / reps;
@@ -166,10 +214,11 @@ int main() {
         kbench<3><<<1, threads>>>(A, o, c, 20);
         kbench<4><<<1, threads>>>(A, o, c, 20);
         kbench<5><<<1, threads>>>(A, o, c, 20);
-        long long hc[6];
-        cudaMemcpy(hc, c, 48, cudaMemcpyDeviceToHost);
-        printf("threads %d: chol32 shfl %lld cyc, rsqrt %lld, shfl+trinv32 %lld, chol32 smem %lld, trinv32 ilp %lld, trinv32 %lld\n",
-               threads, hc[0], hc[1], hc[2], hc[3], hc[4], hc[5]);
+        kbench<6><<<1, threads>>>(A, o, c, 20);
+        long long hc[7];
+        cudaMemcpy(hc, c, 56, cudaMemcpyDeviceToHost);
+        printf("threads %d: chol32 shfl %lld cyc, rsqrt %lld, shfl+trinv32 %lld, chol32 smem %lld, trinv32 ilp %lld, trinv32 %lld, fused factor+inverse %lld\n",
+               threads, hc[0], hc[1], hc[2], hc[3], hc[4], hc[5], hc[6]);
     }
     return 0;
 }

@@ -18,4 +18,6 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tile_pipe|k_lpr_sweep|k_restrict|k_galerkin_t|k_chol_grid|k_cotan' -c 14 \
   -o $O/full_c4 python tools/ncu_target.py --config 4 --cycles 1 > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_tile_pipe|k_lpr_sweep|k_restrict|k_galerkin_t|k_chol_grid|k_cotan' -c 14 \
+  -o $O/full_c3 python tools/ncu_target.py --config 3 --cycles 1 > $O/ncu_full_c3.log 2>&1
 echo done > $O/DONE
