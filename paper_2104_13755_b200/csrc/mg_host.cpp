@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -24,6 +25,22 @@
 using namespace mg;
 
 namespace {
+
+// Experiment builds only (MG_NVCC_DEFINES=-DMG_SETUP_TRACE): wall time of
+// each host phase of the once-per-pattern setup on stderr.
+struct SetupClock {
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void stamp(const char* what, int l) {
+#ifdef MG_SETUP_TRACE
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "setup %-22s l=%d %8.3f s\n", what, l, std::chrono::duration<double>(n - t).count());
+        t = n;
+#else
+        (void)what;
+        (void)l;
+#endif
+    }
+};
 
 // ---------------------------------------------------------------------------
 // Alg. 3 (App. A) with readings A6-A8: degree = distinct
@@ -78,6 +95,27 @@ int32_t greedy_colouring(int32_t n, const int32_t* rp, const int32_t* col, int32
 
 // Symbolic Galerkin pattern (reading A9): coarse (I, J) is stored iff some
 // fine i with P[i,I] != 0 has a stored A[i,j] with P[j,J] != 0.
+// Host worker threads for the once-per-pattern integer setup: [0, n) cut
+// into contiguous chunks, fn(lo, hi, chunk) run concurrently; callers
+// concatenate per-chunk results in chunk order, so the output does not depend
+// on the thread count.
+template <class Fn>
+void parallel_chunks(int64_t n, int nchunks, Fn fn) {
+    nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, n / 4096 + 1));
+    if (nchunks == 1) {
+        fn((int64_t)0, n, 0);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nchunks; ++t)
+        th.emplace_back([=] { fn(n * t / nchunks, n * (t + 1) / nchunks, t); });
+    for (auto& x : th) x.join();
+}
+int host_threads() {
+    static const int n = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    return n;
+}
+
 void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t nc, const int32_t* Pc,
                       const double* Pw, std::vector<int32_t>& crp, std::vector<int32_t>& ccol) {
     std::vector<int32_t> cstart(nc + 1, 0);
@@ -90,29 +128,44 @@ void galerkin_pattern(int32_t nf, const int32_t* rp, const int32_t* col, int32_t
     for (int32_t i = 0; i < nf; ++i)
         for (int q = 0; q < 3; ++q)
             if (Pw[3 * i + q] != 0.0) child[fill[Pc[3 * i + q]]++] = i;
-    std::vector<int32_t> stamp(nc, -1);
-    std::vector<int32_t> row;
-    crp.assign(nc + 1, 0);
-    ccol.clear();
-    for (int32_t I = 0; I < nc; ++I) {
-        row.clear();
-        for (int32_t t = cstart[I]; t < cstart[I + 1]; ++t) {
-            const int32_t i = child[t];
-            for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
-                const int32_t j = col[e];
-                for (int q = 0; q < 3; ++q) {
-                    if (Pw[3 * j + q] == 0.0) continue;
-                    const int32_t J = Pc[3 * j + q];
-                    if (stamp[J] != I) {
-                        stamp[J] = I;
-                        row.push_back(J);
+    // coarse rows in contiguous chunks (independent; concatenated in order)
+    const int nch = host_threads();
+    std::vector<std::vector<int32_t>> part(nch), plen(nch);
+    parallel_chunks(nc, nch, [&](int64_t I0, int64_t I1, int t) {
+        std::vector<int32_t> stamp(nc, -1);
+        std::vector<int32_t> row;
+        std::vector<int32_t>& out = part[t];
+        std::vector<int32_t>& len = plen[t];
+        for (int32_t I = (int32_t)I0; I < (int32_t)I1; ++I) {
+            row.clear();
+            for (int32_t u = cstart[I]; u < cstart[I + 1]; ++u) {
+                const int32_t i = child[u];
+                for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+                    const int32_t j = col[e];
+                    for (int q = 0; q < 3; ++q) {
+                        if (Pw[3 * j + q] == 0.0) continue;
+                        const int32_t J = Pc[3 * j + q];
+                        if (stamp[J] != I) {
+                            stamp[J] = I;
+                            row.push_back(J);
+                        }
                     }
                 }
             }
+            std::sort(row.begin(), row.end());
+            out.insert(out.end(), row.begin(), row.end());
+            len.push_back((int32_t)row.size());
         }
-        std::sort(row.begin(), row.end());
-        ccol.insert(ccol.end(), row.begin(), row.end());
-        crp[I + 1] = (int32_t)ccol.size();
+    });
+    crp.assign(nc + 1, 0);
+    ccol.clear();
+    int32_t I = 0;
+    for (int t = 0; t < nch; ++t) {
+        ccol.insert(ccol.end(), part[t].begin(), part[t].end());
+        for (int32_t L : plen[t]) {
+            crp[I + 1] = crp[I] + L;
+            ++I;
+        }
     }
 }
 
@@ -580,6 +633,7 @@ namespace {
 int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<int32_t>& ucol) {
     const int H = c->H;
     c->drop_graphs();
+    SetupClock clk;
     for (int l = 0; l <= H; ++l) {
         Level& L = *c->lv[l];
         if (l == 0) {
@@ -591,8 +645,10 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                              L.ucol);
         }
         L.nnz = (int64_t)L.ucol.size();
+        clk.stamp("symbolic PtAP", l);
         L.colour.resize(L.n);
         L.ncolours = greedy_colouring(L.n, L.urp.data(), L.ucol.data(), L.colour.data());
+        clk.stamp("colouring", l);
         // internal order: colour-grouped with Morton locality inside a colour
         // (coarsest level: user order, it is only factorised)
         L.perm.resize(L.n);
@@ -628,6 +684,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             }
             L.irp[i + 1] = base + (int32_t)row.size();
         }
+        clk.stamp("order + internal CSR", l);
         const double avg = L.n ? (double)L.nnz / L.n : 1.0;
         L.lpr = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
         // tile-staged kernels for short rows (a thread per row, few gather
@@ -750,6 +807,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             // colour pass: a few entries per lane instead of one wave
             L.lpr_all = avg <= 24.0 ? 4 : 8;
         }
+        clk.stamp("tiles", l);
     }
     cudaStream_t s = c->stream;
     for (int l = 0; l <= H; ++l) {
@@ -758,8 +816,8 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         // row pointers / columns / values padded by 16 B: the bulk copies round sizes up
         std::vector<int32_t> rpad(L.irp), cpad(L.icol);
         rpad.resize(rpad.size() + 8, L.irp.back());
-        cpad.resize(cpad.size() + 8, 0);
-        if ((e = L.rp.upload(rpad, s)) || (e = L.col.upload(cpad, s)) || (e = L.val.alloc(std::max<int64_t>(L.nnz, 1) + 8)) ||
+        cpad.resize(cpad.size() + 16, 0);   // + Galerkin phase-1 vector windows (load8_shifted)
+        if ((e = L.rp.upload(rpad, s)) || (e = L.col.upload(cpad, s)) || (e = L.val.alloc(std::max<int64_t>(L.nnz, 1) + 16)) ||
             (e = L.dperm.upload(L.perm, s)) || (e = L.diperm.upload(L.iperm, s)) || (e = L.x.alloc((size_t)L.n * kMaxK)) ||
             (e = L.b.alloc((size_t)L.n * kMaxK)) || (e = L.r.alloc((size_t)L.n * kMaxK)))
             return c->cuda_fail(e, "pattern upload");
@@ -810,6 +868,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             {
                 GalT G;
                 if (build_galerkin_t(L, C, pc, pw, cnt, cidx, order, G)) {
+                    G.tp.resize(G.tp.size() + 16, 0);        // phase-1 16-byte windows read past the end
                     G.con.resize(G.con.size() + 8, 0);       // 16-byte staging loads may read past the ends
                     G.eoff.resize(G.eoff.size() + 8, 0);
                     G.rowidx.resize(G.rowidx.size() + 16, 0);
@@ -857,6 +916,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 cudaStreamSynchronize(s);
             }
         }
+        clk.stamp("P, Galerkin structure", l);
     }
     // coarsest dense factor storage
     const int nH = c->lv[H]->n;
@@ -915,7 +975,7 @@ int split_hierarchy(mg_ctx* c) {
     for (int l = 0; l <= c->H; ++l) {
         Level& L = *c->lv[l];
         cudaError_t e;
-        if ((e = L.qv.alloc(std::max<int64_t>(L.nnz, 1) + 8)) || (e = L.mv.alloc(std::max<int64_t>(L.nnz, 1) + 8)))
+        if ((e = L.qv.alloc(std::max<int64_t>(L.nnz, 1) + 16)) || (e = L.mv.alloc(std::max<int64_t>(L.nnz, 1) + 16)))
             return c->cuda_fail(e, "split operator alloc");
     }
     for (int l = 0; l < c->H; ++l)
@@ -1604,7 +1664,9 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
     const bool full_mode = c->dir || c->dir_all;
     if (!c->have_pattern || c->pattern_kind != 1 || c->pattern_hash != c->dir_version) {
         std::vector<int32_t> rp, cl, opp;
+        SetupClock clk;
         if ((rc = build_one_ring(c, rp, cl, opp))) return rc;
+        clk.stamp("one-ring + opposites", 0);
         c->have_pattern = false;
         if (full_mode) {
             // Dirichlet mode: assemble on the full mesh in user order, then
@@ -1615,8 +1677,10 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
             c->pattern_kind = 1;
             c->pattern_hash = c->dir_version;
         } else {
+        clk.stamp("(start)", 0);
         rc = setup_pattern(c, rp, cl);
         if (rc) return rc;
+        clk.stamp("setup_pattern total", 0);
         c->pattern_kind = 1;
         c->pattern_hash = c->dir_version;
         // opposite vertices in internal order
@@ -1749,7 +1813,7 @@ int mg_set_matrix_split(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_pt
     if ((rc = load_csr_pattern(c, n, nnz, row_ptr, col))) return rc;
     Level& L0 = *c->lv[0];
     cudaError_t e;
-    if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)))
+    if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 16)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 16)))
         return c->cuda_fail(e, "split operator alloc");
     const double* dq = nullptr;
     if ((rc = to_device(c, q_val, c->stageVal, (size_t)nnz, &dq))) return rc;
@@ -1768,7 +1832,7 @@ int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
     if ((rc = load_cotan_pattern(c, V))) return rc;
     Level& L0 = *c->lv[0];
     cudaError_t e;
-    if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 8)))
+    if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 16)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 16)))
         return c->cuda_fail(e, "split operator alloc");
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
         return launch_cotan(L0, c->opp.p, c->Vint.p, 0.0, 1.0, L0.qv.p, c->Mint.p, c->stream) +

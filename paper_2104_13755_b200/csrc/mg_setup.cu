@@ -381,6 +381,57 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef MG_GALT_GB
 #define MG_GALT_GB 8
 #endif
+#ifndef MG_GALT_VEC
+#define MG_GALT_VEC 1
+#endif
+// Eight consecutive CSR entries [e, e + 8) of a row: columns, values and
+// Galerkin T-codes.  Loads cover the 16-byte-aligned window that contains
+// them (arrays padded by >= 16 elements at the end, mg_host.cpp); the
+// misalignment is removed with selects on the (uniform-latency) registers.
+__device__ __forceinline__ void load8_shifted(const int* __restrict__ col, const double* __restrict__ val,
+                                              const uint16_t* __restrict__ tp, int e, int (&c)[8], double (&a)[8],
+                                              unsigned (&t)[8]) {
+    {   // columns: 12 ints from e & ~3
+        const int4* p = reinterpret_cast<const int4*>(col + (e & ~3));
+        const int4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
+        const int w[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+        const int h = e & 3;
+        int s1[11];
+#pragma unroll
+        for (int i = 0; i < 11; ++i) s1[i] = (h & 1) ? w[i + 1] : w[i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = (h & 2) ? s1[u + 2] : s1[u];
+    }
+    {   // values: 10 doubles from e & ~1
+        const double* b = val + (e & ~1);
+        double d[10];
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+            asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(d[2 * i]), "=d"(d[2 * i + 1]) : "l"(b + 2 * i));
+        const bool odd = e & 1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = odd ? d[u + 1] : d[u];
+    }
+    {   // T-codes: 16 halves from e & ~7
+        const uint4* p = reinterpret_cast<const uint4*>(tp + (e & ~7));
+        const uint4 q0 = __ldg(p), q1 = __ldg(p + 1);
+        const unsigned w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const int hh = e & 7, hw = hh >> 1;
+        unsigned t1[7], t2[5];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) t1[i] = (hw & 1) ? w[i + 1] : w[i];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) t2[i] = (hw & 2) ? t1[i + 2] : t1[i];
+        const unsigned sh = (hh & 1) * 16u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned pr = __funnelshift_r(t2[j], t2[j + 1], sh);
+            t[2 * j] = pr & 0xffffu;
+            t[2 * j + 1] = pr >> 16;
+        }
+    }
+}
+
 template <int TCAP>
 struct GalTCfg {
     static constexpr int kMinBlocks = MG_GALT_MINB;   // CTAs per SM
@@ -403,6 +454,7 @@ __global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_gale
     // (profiles/r02/galerkin_ab2.txt).
     constexpr int TSTR = UCAP;
     constexpr int GB = GalTCfg<TCAP>::kBatch;
+    static_assert(!MG_GALT_VEC || GB == 8, "vector phase-1 loads take 8 entries");
     extern __shared__ __align__(16) unsigned char galt_sm[];
     double* Ts = reinterpret_cast<double*>(galt_sm);                       // [TCAP][TSTR]
     double* Ws = Ts + (size_t)TCAP * TSTR;                                 // [3][UCAP]
@@ -442,6 +494,21 @@ __global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_gale
             int c[GB];
             double a[GB];
             unsigned t[GB];
+#if MG_GALT_VEC
+            // the chunk's columns, values and T-codes by aligned 16-byte loads
+            // from the aligned-down address, then shifted into place by the
+            // runtime misalignment (selects): 3 + 5 + 2 vector loads per 8
+            // nonzeros instead of 24 scalar ones (each lane streams its own
+            // row, so every load instruction is one L1 wavefront per lane)
+            load8_shifted(col, val, tp, e0 + x, c, a, t);
+#pragma unroll
+            for (int u = 0; u < GB; ++u) {
+                const bool ok = x + u < len;
+                c[u] = ok ? c[u] : m.y;
+                a[u] = ok ? a[u] : 0.0;
+                t[u] = ok ? t[u] : 0x7fffu;
+            }
+#else
 #pragma unroll
             for (int u = 0; u < GB; ++u) {
                 const bool ok = x + u < len;
@@ -449,6 +516,7 @@ __global__ void __launch_bounds__(kGalThreads, GalTCfg<TCAP>::kMinBlocks) k_gale
                 a[u] = ok ? __ldg(val + e0 + x + u) : 0.0;
                 t[u] = ok ? (unsigned)__ldg(tp + e0 + x + u) : 0x7fffu;
             }
+#endif
             double4 w[GB];
 #pragma unroll
             for (int u = 0; u < GB; ++u) w[u] = ldg_d4(prow_w + c[u]);
