@@ -467,12 +467,14 @@ struct mg_ctx {
     DBuf<int64_t> uk_src;
     DBuf<double> uk_val, full_val, full_V;
     DBuf<int32_t> full_opp;
+    DBuf<uint8_t> full_opp8;         // packed row-local slots of the opposite vertices (k_cotan_slots)
     Level full0;                     // full 1-ring pattern (user order) for cotan assembly in Dirichlet mode
     DBuf<int32_t> bl_rp, bl_col;     // 2-ring pattern (user order) of the bilaplacian (row f3)
     DBuf<double> bl_val;
 
     std::vector<int32_t> opp_user;   // cotan: 2 opposite vertices per user nnz (-1 none)
-    DBuf<int32_t> opp;               // internal
+    DBuf<int32_t> opp;               // internal (only when a row is too long for the packed slots)
+    DBuf<uint8_t> opp8;              // internal, packed row-local slots
     DBuf<double> Vstage, Vint, Mint, Muser;
 
     int npad = 0;
@@ -1012,7 +1014,10 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
     for (int it = 0; it < mu; ++it)
         for (int q = 0; q < L.ncolours; ++q) {
             const int k = reverse ? L.ncolours - 1 - q : q;
-            n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
+            // the class the next pass of this relaxation takes (its first tiles are prefetched into L2)
+            const int qn = q + 1 < L.ncolours ? q + 1 : (it + 1 < mu ? 0 : -1);
+            const int kn = qn < 0 ? -1 : (reverse ? L.ncolours - 1 - qn : qn);
+            n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s, kn < 0 ? -1 : L.colour_off[kn]);
         }
     return n;
 }
@@ -1574,6 +1579,49 @@ int mg_set_matrix(mg_ctx* c, int32_t n, int64_t nnz, const int32_t* row_ptr, con
     return rebuild_hierarchy(c);
 }
 
+// Opposite vertices as positions inside the row: every opposite vertex o of a
+// stored edge (i, j) closes a face (i, j, o), so o is itself a column of row
+// i.  One byte per stored entry: low nibble = position of the first opposite
+// vertex among row i's entries, high nibble = the second (15: none).  Rows
+// with more than 15 entries do not fit: `false` keeps the index table.
+static bool pack_opp_slots(int32_t n, const std::vector<int32_t>& rp, const std::vector<int32_t>& col,
+                           const std::vector<int32_t>& opp, std::vector<uint8_t>& out) {
+    out.assign((size_t)rp[n] + 16, 0xff);
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t e0 = rp[i], e1 = rp[i + 1];
+        if (e1 - e0 > 15) return false;
+        for (int32_t e = e0; e < e1; ++e) {
+            unsigned code = 0;
+            for (int s = 0; s < 2; ++s) {
+                const int32_t o = opp[2 * (size_t)e + s];
+                unsigned slot = 15;
+                if (o >= 0) {
+                    int32_t t = e0;
+                    while (t < e1 && col[t] != o) ++t;
+                    if (t == e1) return false;
+                    slot = (unsigned)(t - e0);
+                }
+                code |= slot << (4 * s);
+            }
+            out[e] = (uint8_t)code;
+        }
+    }
+    return true;
+}
+
+// Uploads the packed slots when every row fits, else the index table.
+static cudaError_t upload_opp(int32_t n, const std::vector<int32_t>& rp, const std::vector<int32_t>& col,
+                              const std::vector<int32_t>& opp, DBuf<int32_t>& d_idx, DBuf<uint8_t>& d_slot,
+                              cudaStream_t s) {
+    std::vector<uint8_t> packed;
+    if (pack_opp_slots(n, rp, col, opp, packed)) {
+        d_idx.release();
+        return d_slot.upload(packed, s);
+    }
+    d_slot.release();
+    return d_idx.upload(opp, s);
+}
+
 // Full-mesh 1-ring structures in user order (Dirichlet-mode cotan assembly and
 // the bilaplacian): pattern, opposite vertices, identity map, positions / L /
 // M buffers.
@@ -1588,7 +1636,7 @@ static int upload_full_one_ring(mg_ctx* c, const std::vector<int32_t>& rp, const
     c->full0.nnz = (int64_t)cl.size();
     cudaError_t e;
     if ((e = c->full0.rp.upload(rpad, c->stream)) || (e = c->full0.col.upload(cpad, c->stream)) ||
-        (e = c->full_opp.upload(opp, c->stream)) || (e = c->d_ident.upload(ident, c->stream)) ||
+        (e = upload_opp(n, rp, cl, opp, c->full_opp, c->full_opp8, c->stream)) || (e = c->d_ident.upload(ident, c->stream)) ||
         (e = c->full_V.alloc(4 * (size_t)n)) || (e = c->full_val.alloc(cl.size() + 8)) || (e = c->Muser.alloc(n)))
         return c->cuda_fail(e, "full 1-ring setup");
     return MG_OK;
@@ -1693,7 +1741,7 @@ static int load_cotan_pattern(mg_ctx* c, const double* V) {
             }
         }
         cudaError_t e;
-        if ((e = c->opp.upload(oi, c->stream)) || (e = c->Vint.alloc(4 * (size_t)n)) || (e = c->Mint.alloc(n)) ||
+        if ((e = upload_opp(n, L0.irp, L0.icol, oi, c->opp, c->opp8, c->stream)) || (e = c->Vint.alloc(4 * (size_t)n)) || (e = c->Mint.alloc(n)) ||
             (e = c->Muser.alloc(n)))
             return c->cuda_fail(e, "cotan setup");
         }
@@ -1719,7 +1767,7 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
     if (c->dir || c->dir_all) {
         // full mesh, user order: M lands directly in Muser
         c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
-            return launch_cotan(c->full0, c->full_opp.p, c->full_V.p, mass_coeff, lap_coeff, c->full_val.p, c->Muser.p,
+            return launch_cotan(c->full0, c->full_opp.p, c->full_opp8.p, c->full_V.p, mass_coeff, lap_coeff, c->full_val.p, c->Muser.p,
                                 c->stream);
         });
         if (c->dir_all) {
@@ -1732,7 +1780,7 @@ int mg_set_matrix_cotan(mg_ctx* c, const double* V, double mass_coeff, double la
         return rebuild_hierarchy(c);
     }
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
-        return launch_cotan(L0, c->opp.p, c->Vint.p, mass_coeff, lap_coeff, L0.val.p, c->Mint.p, c->stream) +
+        return launch_cotan(L0, c->opp.p, c->opp8.p, c->Vint.p, mass_coeff, lap_coeff, L0.val.p, c->Mint.p, c->stream) +
                launch_scatter_vec(L0.diperm.p, c->Mint.p, c->Muser.p, n, c->stream);
     });
     return rebuild_hierarchy(c);
@@ -1783,7 +1831,7 @@ int mg_set_matrix_bilaplacian(mg_ctx* c, const double* V, double mass_coeff, dou
     if ((rc = to_device(c, V, c->Vstage, 3 * (size_t)n, &dV))) return rc;
     c->timed(PC_ASSEMBLY, 0, s, [&] {
         return launch_gather_rows(3, c->d_ident.p, dV, c->full_V.p, n, s) +
-               launch_cotan(c->full0, c->full_opp.p, c->full_V.p, 0.0, 1.0, c->full_val.p, c->Muser.p, s) +
+               launch_cotan(c->full0, c->full_opp.p, c->full_opp8.p, c->full_V.p, 0.0, 1.0, c->full_val.p, c->Muser.p, s) +
                launch_bilaplacian(c->bl_rp.p, c->bl_col.p, c->full0.rp.p, c->full0.col.p, c->full_val.p, c->Muser.p,
                                   mass_coeff, bilap_coeff, c->bl_val.p, n, s);
     });
@@ -1835,8 +1883,8 @@ int mg_set_matrix_split_cotan(mg_ctx* c, const double* V) {
     if ((e = L0.qv.alloc(std::max<int64_t>(L0.nnz, 1) + 16)) || (e = L0.mv.alloc(std::max<int64_t>(L0.nnz, 1) + 16)))
         return c->cuda_fail(e, "split operator alloc");
     c->timed(PC_ASSEMBLY, 0, c->stream, [&] {
-        return launch_cotan(L0, c->opp.p, c->Vint.p, 0.0, 1.0, L0.qv.p, c->Mint.p, c->stream) +
-               launch_cotan(L0, c->opp.p, c->Vint.p, 1.0, 0.0, L0.mv.p, c->Mint.p, c->stream) +
+        return launch_cotan(L0, c->opp.p, c->opp8.p, c->Vint.p, 0.0, 1.0, L0.qv.p, c->Mint.p, c->stream) +
+               launch_cotan(L0, c->opp.p, c->opp8.p, c->Vint.p, 1.0, 0.0, L0.mv.p, c->Mint.p, c->stream) +
                launch_scatter_vec(L0.diperm.p, c->Mint.p, c->Muser.p, L0.n, c->stream);
     });
     c->have_mass = true;

@@ -128,7 +128,8 @@ constexpr int kLoopHistCycles = 4096;   // device history capacity (cycles)
 // launches issued.  `pdl`: launch with programmatic stream serialisation
 // (V-cycle graph).
 // mg_vcycle.cu
-int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
+int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s,
+          int next_r0 = -1);   // one colour class; next_r0: first row of the class the level's next GS pass takes (-1: none)
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
 int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGraphConditionalHandle h, cudaStream_t s);
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x
@@ -163,7 +164,7 @@ int launch_scatter_rows(int K, const int32_t* iperm, const double* src_int, doub
 int launch_dirichlet_rhs(int K, const int32_t* krp, const int32_t* kcol, const double* kval, const double* X,
                          double* b, int n, cudaStream_t s);
 int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64_t nnz, cudaStream_t s);
-int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
+int launch_cotan(const Level& L0, const int32_t* opp, const uint8_t* opp8, const double* Vint, double mass_coeff, double lap_coeff,
                  double* val, double* M_int, cudaStream_t s);
 int launch_bilaplacian(const int32_t* rp2, const int32_t* col2, const int32_t* rp1, const int32_t* col1,
                        const double* Lv, const double* M, double mass_coeff, double bilap_coeff, double* out, int n,

@@ -166,6 +166,121 @@ __global__ void __launch_bounds__(kBlock) k_cotan_assemble(const int* __restrict
     if (ediag >= 0) val[ediag] = mass_coeff * m + lap_coeff * (-lsum);
 }
 
+// K1, packed form (the default): the <= 2 opposite vertices of an edge (i, j)
+// are themselves columns of row i, so the table holds their positions inside
+// the row (one byte per stored entry, 15 = none; pack_opp_slots in
+// mg_host.cpp) instead of two vertex indices: 1 B instead of 8 B per entry
+// streamed, and for rows of <= kCotG entries each lane gathers only its own
+// column's position and takes the opposite vertices' positions from the
+// lanes holding them (7 position gathers per row instead of 19).  Longer rows
+// (up to 15 entries) look the opposite vertex up through the row's columns.
+// The arithmetic and the summation order are those of k_cotan_assemble:
+// bitwise the same values.
+__device__ __forceinline__ void cot_term(const double (&pi)[3], const double (&pj)[3], double xo, double yo, double zo,
+                                         double& cot_sum, double& area2) {
+    const double ax = pi[0] - xo, ay = pi[1] - yo, az = pi[2] - zo;
+    const double bx = pj[0] - xo, by = pj[1] - yo, bz = pj[2] - zo;
+    const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+    const double c2 = cx * cx + cy * cy + cz * cz;
+    const double ic = rsqrt_nr(c2);   // 1 / |cross| without fp64 sqrt + division
+    cot_sum += (ax * bx + ay * by + az * bz) * ic;
+    area2 += c2 * ic;
+}
+#ifndef MG_COT_R
+#define MG_COT_R 2
+#endif
+constexpr int kCotR = MG_COT_R;   // rows per 8-lane group, their loads batched (latency-bound kernel)
+__global__ void __launch_bounds__(kBlock) k_cotan_slots(const int* __restrict__ rp, const int* __restrict__ col,
+                                                        const uint8_t* __restrict__ opp8, const double* __restrict__ V,
+                                                        double mass_coeff, double lap_coeff,
+                                                        double* __restrict__ val, double* __restrict__ M, int n) {
+    const int g = (blockIdx.x * kBlock + threadIdx.x) / kCotG;
+    const int lane = threadIdx.x & (kCotG - 1);
+    const int ibase = g * kCotR;
+    if (ibase >= n) return;   // whole groups leave together
+    const unsigned mask = group_mask(kCotG);
+    // every load level of the kCotR rows goes out together: row pointers,
+    // then columns + slot codes, then positions
+    int e0[kCotR], e1[kCotR], j[kCotR];
+    unsigned code[kCotR];
+    double pi[kCotR][3], pj[kCotR][3];
+#pragma unroll
+    for (int r = 0; r < kCotR; ++r) {
+        const int i = ibase + r;
+        e0[r] = i < n ? rp[i] : 0;
+        e1[r] = i < n ? rp[i + 1] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kCotR; ++r) {
+        const int i = min(ibase + r, n - 1);
+        const int e = e0[r] + lane;
+        const bool have = e < e1[r] && e1[r] - e0[r] <= kCotG;
+        j[r] = have ? __ldcs(col + e) : i;
+        code[r] = have ? (unsigned)__ldcs(opp8 + e) : 0xffu;
+    }
+#pragma unroll
+    for (int r = 0; r < kCotR; ++r) {
+        const int i = min(ibase + r, n - 1);
+        ldrow<3>(V + 4 * (size_t)i, pi[r]);
+        ldrow<3>(V + 4 * (size_t)j[r], pj[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kCotR; ++r) {
+        const int i = ibase + r;
+        if (i >= n) break;   // uniform over the group
+        double lsum = 0.0, area2 = 0.0;
+        int ediag = -1;
+        if (e1[r] - e0[r] <= kCotG) {
+            const int e = e0[r] + lane;
+            const bool have = e < e1[r];
+            const bool edge = have && j[r] != i;
+            if (have && j[r] == i) ediag = e;
+            double cot_sum = 0.0;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                const unsigned slot = (code[r] >> (4 * s)) & 15u;
+                const double xo = __shfl_sync(mask, pj[r][0], (int)(slot & (kCotG - 1)), kCotG);
+                const double yo = __shfl_sync(mask, pj[r][1], (int)(slot & (kCotG - 1)), kCotG);
+                const double zo = __shfl_sync(mask, pj[r][2], (int)(slot & (kCotG - 1)), kCotG);
+                if (edge && slot != 15u) cot_term(pi[r], pj[r], xo, yo, zo, cot_sum, area2);
+            }
+            if (edge) {
+                const double lij = -0.5 * cot_sum;
+                lsum += lij;
+                __stcs(val + e, lap_coeff * lij);
+            }
+        } else {
+            for (int e = e0[r] + lane; e < e1[r]; e += kCotG) {
+                const int jj = __ldcs(col + e);
+                if (jj == i) {
+                    ediag = e;
+                    continue;
+                }
+                const unsigned cd = __ldcs(opp8 + e);
+                double pjj[3];
+                ldrow<3>(V + 4 * (size_t)jj, pjj);
+                double cot_sum = 0.0;
+#pragma unroll
+                for (int s = 0; s < 2; ++s) {
+                    const unsigned slot = (cd >> (4 * s)) & 15u;
+                    if (slot == 15u) continue;
+                    double po[3];
+                    ldrow<3>(V + 4 * (size_t)col[e0[r] + (int)slot], po);
+                    cot_term(pi[r], pjj, po[0], po[1], po[2], cot_sum, area2);
+                }
+                const double lij = -0.5 * cot_sum;
+                lsum += lij;
+                __stcs(val + e, lap_coeff * lij);
+            }
+        }
+        lsum = group_sum<kCotG>(lsum, mask);
+        area2 = group_sum<kCotG>(area2, mask);
+        const double m = area2 / 12.0;   // (1/6) * sum (|cross| / 2)
+        if (lane == 0) M[i] = m;
+        if (ediag >= 0) val[ediag] = mass_coeff * m + lap_coeff * (-lsum);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // App. D: A_h(alpha) = alpha Q_h + (1 - alpha) M_h on one level's
 // value array (identical patterns), a scaled sparse addition with 16-byte
@@ -987,8 +1102,13 @@ int launch_gather_vals(const int64_t* i2u, const double* src, double* dst, int64
     k_gather_vals<<<nblk(nnz, kBlock), kBlock, 0, s>>>(i2u, src, dst, nnz);
     return 1;
 }
-int launch_cotan(const Level& L0, const int32_t* opp, const double* Vint, double mass_coeff, double lap_coeff,
-                 double* val, double* M_int, cudaStream_t s) {
+int launch_cotan(const Level& L0, const int32_t* opp, const uint8_t* opp8, const double* Vint, double mass_coeff,
+                 double lap_coeff, double* val, double* M_int, cudaStream_t s) {
+    if (opp8) {
+        k_cotan_slots<<<nblk((int64_t)((L0.n + kCotR - 1) / kCotR) * kCotG, kBlock), kBlock, 0, s>>>(L0.rp.p, L0.col.p, opp8, Vint, mass_coeff,
+                                                                             lap_coeff, val, M_int, L0.n);
+        return 1;
+    }
     k_cotan_assemble<<<nblk((int64_t)L0.n * kCotG, kBlock), kBlock, 0, s>>>(L0.rp.p, L0.col.p, opp, Vint, mass_coeff, lap_coeff,
                                                             val, M_int, L0.n);
     return 1;

@@ -22,6 +22,44 @@
 namespace mg {
 namespace {
 
+// Experiment builds (MG_NVCC_DEFINES=-DMG_GS_TRACE, tools/gs_trace.py): thread
+// 0 of every CTA of a GS colour pass stamps %globaltimer at kernel entry,
+// after griddepcontrol.wait and at its end.  Compiled out of the product.
+#ifdef MG_GS_TRACE
+constexpr unsigned kGsTraceCap = 1u << 20;
+__device__ unsigned long long g_gs_trace[4 * kGsTraceCap];
+__device__ unsigned g_gs_trace_n;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct GsTrace {
+    unsigned long long t0, t1;
+    __device__ __forceinline__ void start() { if (threadIdx.x == 0) t0 = gtime(); }
+    __device__ __forceinline__ void waited() { if (threadIdx.x == 0) t1 = gtime(); }
+    __device__ __forceinline__ void end(int kid, int key) {
+        if (threadIdx.x == 0) {
+            const unsigned long long t2 = gtime();
+            const unsigned k = atomicAdd(&g_gs_trace_n, 1u);
+            if (k < kGsTraceCap) {
+                g_gs_trace[4 * k] = t0;
+                g_gs_trace[4 * k + 1] = t1;
+                g_gs_trace[4 * k + 2] = t2;
+                g_gs_trace[4 * k + 3] = ((unsigned long long)kid << 56) | ((unsigned long long)(unsigned)key << 24) |
+                                        (unsigned long long)(blockIdx.x & 0xffffff);
+            }
+        }
+    }
+};
+#else
+struct GsTrace {
+    __device__ __forceinline__ void start() {}
+    __device__ __forceinline__ void waited() {}
+    __device__ __forceinline__ void end(int, int) {}
+};
+#endif
+
 // ---------------------------------------------------------------------------
 // Tile-staged CSR rows (levels with short rows): a CTA owns kTile consecutive
 // rows; row pointers and the tile's contiguous run of (col, val) are staged
@@ -220,6 +258,22 @@ __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* sta
     if (vcnt > 0) bulk_g2s(vs, val + va, vcnt * 8, bar, pol);
 }
 
+// The same three ranges as issue_tile, as L2 prefetches (fire and forget):
+// the last refills of a colour pass fetch the first tiles of the NEXT pass of
+// the level, so that pass's first bulk copies find their data in L2 instead
+// of starting cold from DRAM.
+__device__ __forceinline__ void prefetch_tile(const TileDesc& d, const int* rp, const int* col, const double* val) {
+    const int ra = d.row0 & ~3;
+    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
+    const int ca = d.e0 & ~3;
+    const int ccnt = (d.e1 - ca + 3) & ~3;
+    const int va = d.e0 & ~1;
+    const int vcnt = (d.e1 - va + 1) & ~1;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp + ra), "r"(rcnt * 4) : "memory");
+    if (ccnt > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col + ca), "r"(ccnt * 4) : "memory");
+    if (vcnt > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(val + va), "r"(vcnt * 8) : "memory");
+}
+
 __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned char* stage, int cap) {
     const int* rps = reinterpret_cast<const int*>(stage);
     const int* cs = rps + (kTile + 8);
@@ -282,12 +336,15 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
                                                      const int* __restrict__ rp, const int* __restrict__ col,
                                                      const double* __restrict__ val, const double* __restrict__ b,
                                                      double* __restrict__ x, double* __restrict__ r,
-                                                     double* __restrict__ partial, int cap, double omega, int rev) {
+                                                     double* __restrict__ partial, int cap, double omega, int rev,
+                                                     int nx_begin, int nx_end, int nx_rev) {
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
     const int tid = threadIdx.x;
     const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
     unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
+    GsTrace trc;
+    trc.start();
     pdl_launch_dependents();
     const int nt = t_end - t_begin;
     const int mine = nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
@@ -304,8 +361,13 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
             const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
             issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
         }
+        for (int i = mine; i < 2; ++i) {   // a pass of < 2 tiles per CTA: the next pass's tiles right away
+            const int t = (int)blockIdx.x + (i - mine) * (int)gridDim.x;
+            if (t < nx_end - nx_begin) prefetch_tile(tiles[tile_ix(nx_begin, nx_end, t, nx_rev)], rp, col, val);
+        }
     }
     pdl_wait();
+    trc.waited();
     const uint64_t xpol = evict_last_policy();
     const uint64_t spol = evict_first_policy();
     double acc[K];
@@ -349,11 +411,17 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
             }
         }
         __syncthreads();   // stage sidx fully consumed
-        if (tid == 0 && i + 2 < mine) {
-            const TileDesc dn = tiles[tile_ix(t_begin, t_end, blockIdx.x + (i + 2) * gridDim.x, rev)];
-            issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
+        if (tid == 0) {
+            if (i + 2 < mine) {
+                const TileDesc dn = tiles[tile_ix(t_begin, t_end, blockIdx.x + (i + 2) * gridDim.x, rev)];
+                issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
+            } else {
+                const int t = (int)blockIdx.x + (i + 2 - mine) * (int)gridDim.x;
+                if (t < nx_end - nx_begin) prefetch_tile(tiles[tile_ix(nx_begin, nx_end, t, nx_rev)], rp, col, val);
+            }
         }
     }
+    if (MODE == 0) trc.end(1, t_begin);
     if (MODE == 2) {
         __shared__ double red[kTile / 32][K];
 #pragma unroll
@@ -389,6 +457,8 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
     const int lane = tid & (LPR - 1);
     const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
     unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
+    GsTrace trc;
+    trc.start();
     pdl_launch_dependents();
     const int nt = t_end - t_begin;
     const int mine = nt > (int)blockIdx.x ? (nt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
@@ -407,6 +477,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
         }
     }
     pdl_wait();
+    trc.waited();
     const uint64_t xpol = evict_last_policy();
     const uint64_t spol = evict_first_policy();
     double acc[K];
@@ -480,6 +551,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
             issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
         }
     }
+    if (MODE == 0) trc.end(2, t_begin);
     if (MODE == 2) {
         __shared__ double red[kTile / 32][K];
 #pragma unroll
@@ -494,6 +566,93 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
             partial[blockIdx.x * K + tid] = vsum;
         }
     }
+}
+
+// One-tile form of the k_tile_pipe_lpr GS pass, for colour classes whose
+// tiles all fit the resident grid (one tile per CTA: levels 1-2 of the large
+// configs).  One stage of shared memory and <= 64 registers, so 4 CTAs fit an
+// SM and the CTAs of the NEXT colour pass (launched programmatically as soon
+// as this pass's CTAs have started) are resident beside this pass's: their
+// prologue - tile descriptor, TMA bulk copies of the row pointers / columns /
+// values - runs under this pass, and after griddepcontrol.wait only the x
+// gathers remain on the critical path.  With the two-stage kernel (3 CTAs of
+// 80 registers and two stages per SM) most of the next pass's CTAs could not
+// become resident before this pass's left.  Same lane assignment and
+// summation order as k_tile_pipe_lpr: bitwise the same iterate.
+template <int K, int LPR>
+__global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __restrict__ tiles, int t_begin,
+                                                           const int* __restrict__ rp, const int* __restrict__ col,
+                                                           const double* __restrict__ val, const double* __restrict__ b,
+                                                           double* __restrict__ x, int cap) {
+    extern __shared__ __align__(128) unsigned char smem_pipe[];
+    __shared__ __align__(8) uint64_t bar;
+    constexpr int GB = 4;
+    const int tid = threadIdx.x;
+    const int tr = tid / LPR;
+    const int lane = tid & (LPR - 1);
+    GsTrace trc;
+    trc.start();
+    pdl_launch_dependents();
+    const TileDesc d = tiles[t_begin + (int)blockIdx.x];
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue_tile(d, smem_pipe, cap, &bar, rp, col, val, evict_first_policy());
+    }
+    __syncthreads();
+    const uint64_t xpol = evict_last_policy();
+    const uint64_t spol = evict_first_policy();
+    const StageView v = view_tile(d, smem_pipe, cap);
+    const bool valid = tr < d.nrow;
+    const int row = d.row0 + tr;
+    // the tile lands under the previous pass; the diagonal's group sum and
+    // reciprocal are formed before the wait (one nonzero term: exact)
+    mbar_wait(&bar, 0u);
+    const int qb = valid ? v.rps[tr] : 0, qe = valid ? v.rps[tr + 1] : 0;
+    double dg = 0.0;
+    for (int q = qb + lane; q < qe; q += LPR)
+        if (v.cs[q] == row) dg = v.vs[q];
+    dg = group_sum<LPR>(dg, 0xffffffffu);
+    const double inv = 1.0 / dg;
+    pdl_wait();
+    trc.waited();
+    double bv[K];
+    if (valid && lane == 0) ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
+    double s[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = 0.0;
+    for (int q0 = qb + lane; q0 < qe; q0 += GB * LPR) {
+        int j[GB];
+        double a[GB];
+        double xv[GB][K];
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+            const int q = q0 + u * LPR;
+            j[u] = q < qe ? v.cs[q] : -1;
+            a[u] = q < qe ? v.vs[q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < GB; ++u)
+            if (j[u] >= 0 && j[u] != row) ldrow_pol<K>(x + (size_t)j[u] * VS<K>::S, xv[u], xpol);
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+            if (j[u] < 0) continue;
+            if (j[u] != row) {
+#pragma unroll
+                for (int c = 0; c < K; ++c) s[c] = fma(a[u], xv[u][c], s[c]);
+            }
+        }
+    }
+    // groups never straddle a warp; every lane of the warp takes part
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], 0xffffffffu);
+    if (valid && lane == 0) {
+        double out[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) out[c] = div_by(bv[c] - s[c], dg, inv);
+        strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
+    }
+    trc.end(3, t_begin);
 }
 
 // ---------------------------------------------------------------------------
@@ -514,6 +673,8 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
     const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
     const int lane = threadIdx.x & (LPR - 1);
     const int row = r0 + g;
+    GsTrace trc;
+    trc.start();
     pdl_launch_dependents();
     const bool active = row < r1;
     const uint64_t pol = evict_first_policy();
@@ -531,9 +692,23 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
         j[u] = ok ? ld_stream(col + e, pol) : -1;
         a[u] = ok ? ld_stream(val + e, pol) : 0.0;
     }
-    pdl_wait();
-    if (!active) return;   // whole groups leave together
+    // the diagonal entry is among the lane's prefetched (or tail) entries:
+    // its group sum and reciprocal are formed before the wait, off the
+    // critical path of the colour pass (one nonzero term: exact)
     const unsigned mask = group_mask(LPR);
+    double d = 0.0, inv = 0.0;
+    if (MODE == 0 || MODE == 3) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (j[u] == row) d = a[u];
+        for (int e = e0 + lane + U * LPR; e < e1; e += LPR)
+            if (ld_stream(col + e, pol) == row) d = ld_stream(val + e, pol);
+        d = group_sum<LPR>(d, mask);
+        inv = 1.0 / d;
+    }
+    pdl_wait();
+    trc.waited();
+    if (!active) return;   // whole groups leave together
     const uint64_t xpol = evict_last_policy();
     // the row's right-hand side goes out with the gathers (one round trip)
     double bv[K];
@@ -541,7 +716,6 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
     double s[K], xi[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = xi[c] = 0.0;
-    double d = 0.0;
 #pragma unroll
     for (int u0 = 0; u0 < U; u0 += GB) {
         double xv[GB][K];
@@ -555,10 +729,8 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
             const int jj = j[u0 + u];
             if (jj < 0) continue;
             if (MODE == 0 && jj == row) {
-                d += a[u0 + u];
             } else {
                 if (MODE == 3 && jj == row) {
-                    d += a[u0 + u];
 #pragma unroll
                     for (int c = 0; c < K; ++c) xi[c] = xv[u][c];
                 }
@@ -571,12 +743,10 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
         const int jj = ld_stream(col + e, pol);
         const double av = ld_stream(val + e, pol);
         if (MODE == 0 && jj == row) {
-            d += av;
         } else {
             double xv[K];
             ldrow_pol<K>(x + (size_t)jj * VS<K>::S, xv, xpol);
             if (MODE == 3 && jj == row) {
-                d += av;
 #pragma unroll
                 for (int c = 0; c < K; ++c) xi[c] = xv[c];
             }
@@ -586,13 +756,11 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
     }
 #pragma unroll
     for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], mask);
-    if (MODE == 0 || MODE == 3) d = group_sum<LPR>(d, mask);
     if (MODE == 3)
 #pragma unroll
         for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], mask);   // only the diagonal's lane holds x_i
     if (lane == 0) {
         double out[K];
-        const double inv = (MODE == 0 || MODE == 3) ? 1.0 / d : 0.0;
 #pragma unroll
         for (int c = 0; c < K; ++c)
             out[c] = MODE == 0 ? div_by(bv[c] - s[c], d, inv)
@@ -600,6 +768,7 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
         if (MODE == 0) strow_pol<K>(x + (size_t)row * VS<K>::S, out, xpol);
         else strow<K>(r + (size_t)row * VS<K>::S, out);
     }
+    if (MODE == 0) trc.end(4, r0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1024,20 +1193,47 @@ inline int pipe_grid(const Level& L, int K, int ntiles) {
     return std::max(1, std::min(ntiles, pipe_nsm() * per_sm));
 }
 inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
+// k_tile_one_lpr: every tile of the pass on its own resident CTA (4 per SM by
+// registers, one stage of shared memory each)
+#ifndef MG_NEXT_PREFETCH
+#define MG_NEXT_PREFETCH 0
+#endif
+#ifndef MG_ONE_TILE
+#define MG_ONE_TILE 1
+#endif
+#ifndef MG_ONE_TILE_MIN_LPR
+#define MG_ONE_TILE_MIN_LPR 4
+#endif
+inline bool one_tile_ok(const Level& L, int ntiles) {
+    const size_t smem = pipe_smem(L.pipe_cap) / 2 + 1280;
+    const int per_sm = std::min<int>(4, (int)((227 * 1024) / smem));
+    return MG_ONE_TILE && ntiles <= pipe_nsm() * per_sm;
+}
 
 // MODE 0..3 over tiles [t0, t1) of level L (iterate read from xin)
 template <int K, int MODE>
 void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double* partial, int grid, double omega,
-                 bool pdl, cudaStream_t s) {
+                 bool pdl, cudaStream_t s, int nx0 = 0, int nx1 = 0) {
     const TileDesc* td = reinterpret_cast<const TileDesc*>(L.tiles.p);
     const size_t sm = pipe_smem(L.pipe_cap);
     const int rev = (MODE != 2 && L.serpentine) ? (L.pass_ctr++ & 1) : 0;   // norm partials keep one order
+    const int nxrev = L.serpentine ? (L.pass_ctr & 1) : 0;                  // direction of the level's next pass
+    if (MODE == 0 && L.pipe_lpr >= MG_ONE_TILE_MIN_LPR && one_tile_ok(L, t1 - t0)) {
+        const size_t sm1 = sm / 2;
+        const int g1 = t1 - t0;
+        switch (L.pipe_lpr) {
+            case 2: launch_k(pdl, k_tile_one_lpr<K, 2>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
+            case 4: launch_k(pdl, k_tile_one_lpr<K, 4>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
+            default: launch_k(pdl, k_tile_one_lpr<K, 8>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
+        }
+        return;
+    }
     switch (L.pipe_lpr) {
         case 1:
             if (K == 3 && L.pipe_unr8)
-                launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+                launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
             else
-                launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+                launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
             break;
         case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
         case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
@@ -1049,7 +1245,7 @@ void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double*
 // MODE 3: Jacobi out = x + omega D^{-1}(b - A x).  xin: iterate read (L.x if null).
 template <int K, int MODE>
 int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s, double* xin = nullptr,
-            double omega = 0.0) {
+            double omega = 0.0, int next_r0 = -1) {
     double* xp = xin ? xin : L.x.p;
     const int rows = r1 - r0;
     if (rows <= 0) return 0;
@@ -1066,7 +1262,14 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
             t0 = toff[toff.size() - 2];   // whole-level tiles are the last range
             t1 = toff.back();
         }
-        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(L, K, t1 - t0), omega, pdl, s);
+        int nx0 = 0, nx1 = 0;   // tiles of the colour class the next GS pass of this level takes
+        if (MODE == 0 && MG_NEXT_PREFETCH && next_r0 >= 0) {
+            int c = 0;
+            while (L.colour_off[c] != next_r0) ++c;
+            nx0 = toff[c];
+            nx1 = toff[c + 1];
+        }
+        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(L, K, t1 - t0), omega, pdl, s, nx0, nx1);
         return 1;
     }
     if (L.tiled) {
@@ -1126,6 +1329,9 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_pipe<K, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1163,8 +1369,8 @@ void init_vcycle_attributes() {
     set_attrs_k<4>();
 }
 
-int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
-    MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
+int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s, int next_r0) {
+    MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s, nullptr, 0.0, next_r0)))
 }
 // Device-side V-cycle loop (conditional WHILE graph node): after each cycle's
 // residual norm this kernel records rho into the history, applies mg_solve's
@@ -1247,3 +1453,20 @@ int vc_sumsq(int K, const double* v, int n, double* partial, int nb, double* out
 }
 
 }  // namespace mg
+
+#ifdef MG_GS_TRACE
+// experiment builds only: copy out / reset the GS pass trace
+extern "C" int mg_debug_gs_trace(unsigned long long* out, int max_entries, int reset) {
+    unsigned n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, mg::g_gs_trace_n, sizeof(n));
+    n = std::min(n, mg::kGsTraceCap);
+    const int m = std::min<int>((int)n, max_entries);
+    if (out && m > 0) cudaMemcpyFromSymbol(out, mg::g_gs_trace, (size_t)m * 4 * sizeof(unsigned long long));
+    if (reset) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(mg::g_gs_trace_n, &z, sizeof(z));
+    }
+    return m;
+}
+#endif

@@ -173,6 +173,45 @@ def test_single_level_is_direct_solve(ora):
     assert np.linalg.norm(X - xs) <= 1e-12 * np.linalg.norm(xs)
 
 
+def _fan_mesh(n_ring, closed, seed):
+    """Apex (valence n_ring) over a jittered ring; closed: a second apex below
+    (bipyramid), else an open disk whose ring edges are boundary edges."""
+    rng = np.random.default_rng(seed)
+    t = 2 * np.pi * (np.arange(n_ring) + 0.2 * rng.uniform(-1, 1, n_ring)) / n_ring
+    ring = np.stack([np.cos(t), np.sin(t), 0.1 * rng.standard_normal(n_ring)], axis=1)
+    V = [np.array([[0.05, -0.03, 0.8]]), ring]
+    F = [(0, 1 + k, 1 + (k + 1) % n_ring) for k in range(n_ring)]
+    if closed:
+        V.append(np.array([[-0.02, 0.04, -0.9]]))
+        b = n_ring + 1
+        F += [(b, 1 + (k + 1) % n_ring, 1 + k) for k in range(n_ring)]
+    return np.ascontiguousarray(np.concatenate(V), np.float64), np.asarray(F, np.int32)
+
+
+@pytest.mark.parametrize("n_ring,closed", [(6, True), (7, True), (9, True), (14, True), (20, True), (9, False),
+                                           (18, False)])
+def test_cotan_long_rows(ora, n_ring, closed):
+    """Rows of the 1-ring pattern longer than the 8 lanes of the assembly
+    kernel (row-local opposite-vertex slots looked up through the columns),
+    longer than 15 entries (index-table kernel), and boundary edges with a
+    single opposite vertex: mass and the single-level direct solve against
+    the oracle's assembly."""
+    from paper_2104_13755_b200 import mg
+    V, F = _fan_mesh(n_ring, closed, 5 + n_ring)
+    S = mg.Solver([(V, F)], [])
+    S.set_matrix_cotan(V, 1.0, 0.3)
+    A, M = ora.assemble(V, F, 1.0, 0.3)
+    Mg = mg.mg_get_mass(S.ctx, V.shape[0])
+    assert np.abs(Mg - M).max() <= 1e-12 * np.abs(M).max()
+    b = np.random.default_rng(3).standard_normal((V.shape[0], 2))
+    X = np.zeros_like(b)
+    rc, cyc, h = S.solve(b, X, rel_tol=1e-12, max_cycles=3)
+    xs = np.linalg.solve(A.to_scipy().toarray(), b)
+    assert rc == 0
+    assert np.linalg.norm(X - xs) <= 1e-11 * np.linalg.norm(xs)
+    S.close()
+
+
 def test_zero_rhs_and_loose_tolerance(ora):
     p = meshgen.make_config(1)
     S = gpu_solver(p)
