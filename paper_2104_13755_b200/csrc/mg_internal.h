@@ -67,6 +67,8 @@ struct Level {
     bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
     DBuf<int32_t> rcptr, rcidx;           // children lists in gal_order (ordered restriction)
     DBuf<double> rcw;
+    bool pipe_mixed = false;              // lanes-per-row tiles of mixed width (rows ordered by length bucket inside a colour)
+    std::vector<uint8_t> row_lpr;         // pipe_mixed: lanes per row, user order
     bool pipe_unr8 = false;               // k_tile_pipe with 8 gathers per batch (K = 3, 3 CTAs/SM)
     int pipe_lpr = 1;
                      // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)

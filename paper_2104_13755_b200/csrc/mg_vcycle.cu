@@ -243,7 +243,7 @@ struct StageView {
 __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* stage, int cap, uint64_t* bar,
                                            const int* rp, const int* col, const double* val, uint64_t pol) {
     const int ra = d.row0 & ~3;
-    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
+    const int rcnt = (d.row0 + (d.nrow & 0xffff) + 1 - ra + 3) & ~3;
     const int ca = d.e0 & ~3;
     const int ccnt = (d.e1 - ca + 3) & ~3;
     const int va = d.e0 & ~1;
@@ -264,7 +264,7 @@ __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* sta
 // of starting cold from DRAM.
 __device__ __forceinline__ void prefetch_tile(const TileDesc& d, const int* rp, const int* col, const double* val) {
     const int ra = d.row0 & ~3;
-    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
+    const int rcnt = (d.row0 + (d.nrow & 0xffff) + 1 - ra + 3) & ~3;
     const int ca = d.e0 & ~3;
     const int ccnt = (d.e1 - ca + 3) & ~3;
     const int va = d.e0 & ~1;
@@ -292,6 +292,17 @@ __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned
 __device__ __forceinline__ int tile_ix(int t_begin, int t_end, int t, int rev) {
     return rev ? t_end - 1 - t : t_begin + t;
 }
+
+// Lanes-per-row tiles carry their group width in the descriptor (nrow =
+// rows | lpr << 16): a colour class is ordered by row-length bucket and each
+// bucket gets its own width (setup_pattern, mg_host.cpp), so one launch mixes
+// tiles of 2, 4 and 8 lanes per row.  Same xor tree as group_sum<LPR>.
+__device__ __forceinline__ double group_sum_rt(double v, int lpr) {
+    for (int off = lpr >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+__device__ __forceinline__ int tile_lpr(const TileDesc& d) { return d.nrow >> 16; }
+__device__ __forceinline__ int tile_rows_of(const TileDesc& d) { return d.nrow & 0xffff; }
 
 template <int K, int UNR>
 __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, const double* __restrict__ x,
@@ -443,7 +454,7 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
 // k_tile_pipe, tiles of kTile / LPR rows; lane l of a row takes the staged
 // entries qb + l + u * LPR (the assignment and summation order of
 // k_lpr_sweep), so nothing but x and b is loaded after the PDL wait.
-template <int K, int LPR, int MODE>
+template <int K, int MODE>
 __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
                                                          const int* __restrict__ rp, const int* __restrict__ col,
                                                          const double* __restrict__ val, const double* __restrict__ b,
@@ -453,8 +464,6 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
     __shared__ __align__(8) uint64_t bar[2];
     constexpr int GB = 4;   // gathers in flight per lane (8 with 2 CTAs/SM measured slower)
     const int tid = threadIdx.x;
-    const int tr = tid / LPR;
-    const int lane = tid & (LPR - 1);
     const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
     unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
     GsTrace trc;
@@ -488,7 +497,10 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
         const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
         mbar_wait(&bar[sidx], (unsigned)((i >> 1) & 1));
         const StageView v = view_tile(d, stage[sidx], cap);
-        const bool valid = tr < d.nrow;
+        const int LPR = tile_lpr(d);
+        const int tr = tid / LPR;
+        const int lane = tid & (LPR - 1);
+        const bool valid = tr < tile_rows_of(d);
         const int row = d.row0 + tr;
         double bv[K];
         if (valid && lane == 0) ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
@@ -527,11 +539,11 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
         }
         // groups never straddle a warp; every lane of the warp takes part
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], 0xffffffffu);
-        if (MODE == 0 || MODE == 3) dg = group_sum<LPR>(dg, 0xffffffffu);
+        for (int c = 0; c < K; ++c) s[c] = group_sum_rt(s[c], LPR);
+        if (MODE == 0 || MODE == 3) dg = group_sum_rt(dg, LPR);
         if (MODE == 3)
 #pragma unroll
-            for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], 0xffffffffu);
+            for (int c = 0; c < K; ++c) xi[c] = group_sum_rt(xi[c], LPR);
         if (valid && lane == 0) {
             double out[K];
             const double inv = (MODE == 0 || MODE == 3) ? 1.0 / dg : 0.0;
@@ -579,7 +591,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
 // 80 registers and two stages per SM) most of the next pass's CTAs could not
 // become resident before this pass's left.  Same lane assignment and
 // summation order as k_tile_pipe_lpr: bitwise the same iterate.
-template <int K, int LPR>
+template <int K>
 __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __restrict__ tiles, int t_begin,
                                                            const int* __restrict__ rp, const int* __restrict__ col,
                                                            const double* __restrict__ val, const double* __restrict__ b,
@@ -588,12 +600,13 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     __shared__ __align__(8) uint64_t bar;
     constexpr int GB = 4;
     const int tid = threadIdx.x;
-    const int tr = tid / LPR;
-    const int lane = tid & (LPR - 1);
     GsTrace trc;
     trc.start();
     pdl_launch_dependents();
     const TileDesc d = tiles[t_begin + (int)blockIdx.x];
+    const int LPR = tile_lpr(d);
+    const int tr = tid / LPR;
+    const int lane = tid & (LPR - 1);
     if (tid == 0) {
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -603,7 +616,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     const uint64_t xpol = evict_last_policy();
     const uint64_t spol = evict_first_policy();
     const StageView v = view_tile(d, smem_pipe, cap);
-    const bool valid = tr < d.nrow;
+    const bool valid = tr < tile_rows_of(d);
     const int row = d.row0 + tr;
     // the tile lands under the previous pass; the diagonal's group sum and
     // reciprocal are formed before the wait (one nonzero term: exact)
@@ -612,7 +625,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     double dg = 0.0;
     for (int q = qb + lane; q < qe; q += LPR)
         if (v.cs[q] == row) dg = v.vs[q];
-    dg = group_sum<LPR>(dg, 0xffffffffu);
+    dg = group_sum_rt(dg, LPR);
     const double inv = 1.0 / dg;
     pdl_wait();
     trc.waited();
@@ -645,7 +658,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     }
     // groups never straddle a warp; every lane of the warp takes part
 #pragma unroll
-    for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], 0xffffffffu);
+    for (int c = 0; c < K; ++c) s[c] = group_sum_rt(s[c], LPR);
     if (valid && lane == 0) {
         double out[K];
 #pragma unroll
@@ -661,12 +674,20 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
 // after the wait its x gathers go out in batches of GB independent loads.
 // The group width is chosen per level so that one colour pass is about one
 // wave of the GPU (see choose_lpr in mg_host.cpp).
+#ifndef MG_LPR_PREFETCH64
+#define MG_LPR_PREFETCH64 1
+#endif
 template <int K, int LPR, int MODE>
 __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
                                                       const double* __restrict__ val, const double* __restrict__ b,
                                                       double* __restrict__ x, double* __restrict__ r, int r0, int r1,
                                                       double omega) {
-    constexpr int U = 32 / LPR;
+    // entries prefetched per lane: 64 per row for the wide groups (Galerkin
+    // rows reach ~40 entries; an entry left to the tail loop costs two more
+    // dependent round trips after the wait - tools/gs_trace.py: the CTAs
+    // holding such rows ended 1.1-1.3 us after the release against a median
+    // of 0.7), 32 per row otherwise
+    constexpr int U = MG_LPR_PREFETCH64 && LPR >= 16 ? 64 / LPR : 32 / LPR;
     // gathers in flight per lane: the whole prefetch for LPR >= 8, batches of
     // 4 for LPR = 4 (8 entries per lane) to keep registers / occupancy
     constexpr int GB = U <= 4 ? U : 4;
@@ -1219,25 +1240,16 @@ void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double*
     const int rev = (MODE != 2 && L.serpentine) ? (L.pass_ctr++ & 1) : 0;   // norm partials keep one order
     const int nxrev = L.serpentine ? (L.pass_ctr & 1) : 0;                  // direction of the level's next pass
     if (MODE == 0 && L.pipe_lpr >= MG_ONE_TILE_MIN_LPR && one_tile_ok(L, t1 - t0)) {
-        const size_t sm1 = sm / 2;
-        const int g1 = t1 - t0;
-        switch (L.pipe_lpr) {
-            case 2: launch_k(pdl, k_tile_one_lpr<K, 2>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
-            case 4: launch_k(pdl, k_tile_one_lpr<K, 4>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
-            default: launch_k(pdl, k_tile_one_lpr<K, 8>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
-        }
+        launch_k(pdl, k_tile_one_lpr<K>, t1 - t0, kTile, sm / 2, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap);
         return;
     }
-    switch (L.pipe_lpr) {
-        case 1:
-            if (K == 3 && L.pipe_unr8)
-                launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
-            else
-                launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
-            break;
-        case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
-        case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
-        default: launch_k(pdl, k_tile_pipe_lpr<K, 8, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+    if (L.pipe_lpr == 1) {
+        if (K == 3 && L.pipe_unr8)
+            launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
+        else
+            launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
+    } else {
+        launch_k(pdl, k_tile_pipe_lpr<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
     }
 }
 
@@ -1321,6 +1333,11 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_sweep<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_resnorm_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_chol_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1329,21 +1346,6 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_pipe<K, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_one_lpr<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_one_lpr<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_one_lpr<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_sweep<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 }
 
