@@ -629,10 +629,6 @@ struct mg_ctx {
 
 namespace {
 
-#ifndef MG_MIXED_LPR
-#define MG_MIXED_LPR 1
-#endif
-
 // ---------------------------------------------------------------------------
 // Pattern setup (per new level-0 pattern): colouring and internal ordering of
 // every level, coarse patterns, transposes of P, device upload.
@@ -659,49 +655,10 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         // (coarsest level: user order, it is only factorised)
         L.perm.resize(L.n);
         std::iota(L.perm.begin(), L.perm.end(), 0);
-        L.pipe_mixed = false;
-        L.row_lpr.clear();
         if (l < H) {
             const std::vector<uint64_t> key = morton_keys(L.V, L.n);
-            // Galerkin-fill levels with large colour classes (the pipelined
-            // lanes-per-row levels below): a pass costs one dependent x-gather
-            // round trip per 4 entries a lane holds (tools/gs_trace.py: C4
-            // level 1 at 2 lanes per row waits 5 rounds for its 33..40-entry
-            // rows), so every row gets the lanes that finish it in R rounds
-            // (2, 4 or 8 lanes: up to 8R, 16R, 32R entries), rows of one
-            // width are made contiguous inside the colour class (bucket, then
-            // Morton), and each class takes the smallest R whose tiles still
-            // fit the one-tile kernel's resident grid (4 CTAs per SM).
-            {
-                const double avg0 = L.n ? (double)L.nnz / L.n : 1.0;
-                const double crow = (double)L.n / std::max(1, L.ncolours);
-                if (MG_MIXED_LPR && c->use_pipe && avg0 > 12.0 && avg0 <= 40.0 && crow >= 6000.0) {
-                    int nsm = 148;
-                    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-                    const int slots = 4 * nsm;
-                    L.pipe_mixed = true;
-                    L.row_lpr.assign(L.n, 2);
-                    std::vector<std::vector<int32_t>> cls(L.ncolours);
-                    for (int32_t u = 0; u < L.n; ++u) cls[L.colour[u]].push_back(u);
-                    auto width = [](int len, int R) { return len <= 8 * R ? 2 : len <= 16 * R ? 4 : 8; };
-                    for (const auto& rows : cls) {
-                        int R = 1;
-                        for (; R < 4; ++R) {
-                            int64_t cnt[3] = {0, 0, 0};
-                            for (int32_t u : rows) {
-                                const int w = width(L.urp[u + 1] - L.urp[u], R);
-                                cnt[w == 2 ? 0 : w == 4 ? 1 : 2]++;
-                            }
-                            const int64_t ctas = (cnt[0] + 127) / 128 + (cnt[1] + 63) / 64 + (cnt[2] + 31) / 32;
-                            if (ctas <= slots) break;
-                        }
-                        for (int32_t u : rows) L.row_lpr[u] = (uint8_t)width(L.urp[u + 1] - L.urp[u], R);
-                    }
-                }
-            }
             std::sort(L.perm.begin(), L.perm.end(), [&](int32_t a, int32_t b) {
                 if (L.colour[a] != L.colour[b]) return L.colour[a] < L.colour[b];
-                if (L.pipe_mixed && L.row_lpr[a] != L.row_lpr[b]) return L.row_lpr[a] < L.row_lpr[b];
                 if (key[a] != key[b]) return key[a] < key[b];
                 return a < b;
             });
@@ -760,7 +717,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     break;
                 }
         }
-        L.pipe_lpr = avg <= tile_avg ? 1 : L.pipe_mixed ? 8 : auto_lpr;
+        L.pipe_lpr = avg <= tile_avg ? 1 : auto_lpr;
         if (L.pipe_lpr != 0 && L.pipe_lpr != 1 && L.pipe_lpr != 2 && L.pipe_lpr != 4 && L.pipe_lpr != 8) L.pipe_lpr = 0;
         // k = 3: all ~6 off-diagonal gathers of a row in one batch (80 registers,
         // 3 CTAs/SM) beat two batches at 4 CTAs/SM (C4: 366 -> 372 V-cycles/s,
@@ -777,16 +734,6 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
         L.cap_gs = 0;
         for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k)
             L.cap_gs = std::max(L.cap_gs, tile_max(L.colour_off[k], L.colour_off[k + 1]));
-        if (L.pipe_mixed) {
-            // mixed tiles start at bucket boundaries: bound every tile by the
-            // largest run of its own row count (128 / 64 / 32 rows of 2 / 4 / 8 lanes)
-            int m = 1;
-            for (int32_t a = 0; a < L.n; ++a) {
-                const int w = L.row_lpr[L.perm[a]];
-                m = std::max(m, L.irp[std::min<int32_t>(a + tile_rows() / w, L.n)] - L.irp[a]);
-            }
-            L.cap_gs = L.cap_all = m;
-        }
         L.cap_gs = std::max(L.cap_gs, 1);
         L.cap_all = std::max(L.cap_all, 1);
         L.tiled = L.pipe_lpr == 1 && (size_t)std::max(L.cap_gs, L.cap_all) * 12 <= tile_smem_limit();
@@ -824,25 +771,9 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     const double fill = (double)(nt256 - (rounds - 1) * G) / G;   // last round's occupancy
                     if (L.pipe_lpr == 1 && rows > T && (rounds == 1 || fill < 0.5))
                         Tr = std::max(128, (rows + rounds * G - 1) / (rounds * G));
-                    if (L.pipe_mixed) {
-                        // one run of tiles per width bucket; the width rides in the descriptor
-                        for (int b0 = r0; b0 < r1;) {
-                            const int w = L.row_lpr[L.perm[b0]];
-                            int b1 = b0;
-                            while (b1 < r1 && L.row_lpr[L.perm[b1]] == w) ++b1;
-                            const int Tw = tile_rows() / w;
-                            for (int a0 = b0; a0 < b1; a0 += Tw) {
-                                const int nr = std::min(Tw, b1 - a0);
-                                td.insert(td.end(), {a0, nr | (w << 16), L.irp[a0], L.irp[a0 + nr]});
-                            }
-                            b0 = b1;
-                        }
-                    } else {
-                        const int wenc = L.pipe_lpr > 1 ? (L.pipe_lpr << 16) : 0;   // lanes-per-row kernels read the width here
-                        for (int a0 = r0; a0 < r1; a0 += Tr) {
-                            const int nr = std::min(Tr, r1 - a0);
-                            td.insert(td.end(), {a0, nr | wenc, L.irp[a0], L.irp[a0 + nr]});
-                        }
+                    for (int a0 = r0; a0 < r1; a0 += Tr) {
+                        const int nr = std::min(Tr, r1 - a0);
+                        td.insert(td.end(), {a0, nr, L.irp[a0], L.irp[a0 + nr]});
                     }
                     toff.push_back((int32_t)(td.size() / 4));
                 }
@@ -853,7 +784,7 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 const int ngs = (int)(td.size() / 4) - base;
                 std::vector<int> idx(ngs);
                 std::iota(idx.begin(), idx.end(), base);
-                auto mid_key = [&](int t) { return key[L.perm[td[4 * t] + (td[4 * t + 1] & 0xffff) / 2]]; };
+                auto mid_key = [&](int t) { return key[L.perm[td[4 * t] + td[4 * t + 1] / 2]]; };
                 std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return mid_key(x) < mid_key(y); });
                 for (int t : idx) {
                     const int32_t d0 = td[4 * t], d1 = td[4 * t + 1], d2 = td[4 * t + 2], d3 = td[4 * t + 3];
@@ -1083,10 +1014,7 @@ int relax(mg_ctx* c, int K, Level& L, int mu, bool reverse, bool pdl, cudaStream
     for (int it = 0; it < mu; ++it)
         for (int q = 0; q < L.ncolours; ++q) {
             const int k = reverse ? L.ncolours - 1 - q : q;
-            // the class the next pass of this relaxation takes (its first tiles are prefetched into L2)
-            const int qn = q + 1 < L.ncolours ? q + 1 : (it + 1 < mu ? 0 : -1);
-            const int kn = qn < 0 ? -1 : (reverse ? L.ncolours - 1 - qn : qn);
-            n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s, kn < 0 ? -1 : L.colour_off[kn]);
+            n += vc_gs(K, L, L.colour_off[k], L.colour_off[k + 1], pdl, s);
         }
     return n;
 }

@@ -67,8 +67,6 @@ struct Level {
     bool restrict_ordered = true;         // (this level coarse) restriction visits rows in gal_order
     DBuf<int32_t> rcptr, rcidx;           // children lists in gal_order (ordered restriction)
     DBuf<double> rcw;
-    bool pipe_mixed = false;              // lanes-per-row tiles of mixed width (rows ordered by length bucket inside a colour)
-    std::vector<uint8_t> row_lpr;         // pipe_mixed: lanes per row, user order
     bool pipe_unr8 = false;               // k_tile_pipe with 8 gathers per batch (K = 3, 3 CTAs/SM)
     int pipe_lpr = 1;
                      // lanes per row of the pipelined tiles (tiles of kTile / pipe_lpr rows)
@@ -130,8 +128,7 @@ constexpr int kLoopHistCycles = 4096;   // device history capacity (cycles)
 // launches issued.  `pdl`: launch with programmatic stream serialisation
 // (V-cycle graph).
 // mg_vcycle.cu
-int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s,
-          int next_r0 = -1);   // one colour class; next_r0: first row of the class the level's next GS pass takes (-1: none)
+int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s);          // one colour class
 int vc_residual(int K, const Level& L, bool pdl, cudaStream_t s);
 int vc_loop_check(int K, const double* rho, LoopState* st, double* hist, cudaGraphConditionalHandle h, cudaStream_t s);
 int vc_jacobi(int K, const Level& L, double* xin, double* xout, double omega, bool pdl, cudaStream_t s);  // xout = xin + omega D^-1 (b - A xin)                    // L.r = L.b - A L.x

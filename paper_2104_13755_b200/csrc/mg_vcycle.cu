@@ -243,7 +243,7 @@ struct StageView {
 __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* stage, int cap, uint64_t* bar,
                                            const int* rp, const int* col, const double* val, uint64_t pol) {
     const int ra = d.row0 & ~3;
-    const int rcnt = (d.row0 + (d.nrow & 0xffff) + 1 - ra + 3) & ~3;
+    const int rcnt = (d.row0 + d.nrow + 1 - ra + 3) & ~3;
     const int ca = d.e0 & ~3;
     const int ccnt = (d.e1 - ca + 3) & ~3;
     const int va = d.e0 & ~1;
@@ -256,22 +256,6 @@ __device__ __forceinline__ void issue_tile(const TileDesc& d, unsigned char* sta
     bulk_g2s(rps, rp + ra, rcnt * 4, bar, pol);
     if (ccnt > 0) bulk_g2s(cs, col + ca, ccnt * 4, bar, pol);
     if (vcnt > 0) bulk_g2s(vs, val + va, vcnt * 8, bar, pol);
-}
-
-// The same three ranges as issue_tile, as L2 prefetches (fire and forget):
-// the last refills of a colour pass fetch the first tiles of the NEXT pass of
-// the level, so that pass's first bulk copies find their data in L2 instead
-// of starting cold from DRAM.
-__device__ __forceinline__ void prefetch_tile(const TileDesc& d, const int* rp, const int* col, const double* val) {
-    const int ra = d.row0 & ~3;
-    const int rcnt = (d.row0 + (d.nrow & 0xffff) + 1 - ra + 3) & ~3;
-    const int ca = d.e0 & ~3;
-    const int ccnt = (d.e1 - ca + 3) & ~3;
-    const int va = d.e0 & ~1;
-    const int vcnt = (d.e1 - va + 1) & ~1;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rp + ra), "r"(rcnt * 4) : "memory");
-    if (ccnt > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(col + ca), "r"(ccnt * 4) : "memory");
-    if (vcnt > 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(val + va), "r"(vcnt * 8) : "memory");
 }
 
 __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned char* stage, int cap) {
@@ -292,17 +276,6 @@ __device__ __forceinline__ StageView view_tile(const TileDesc& d, const unsigned
 __device__ __forceinline__ int tile_ix(int t_begin, int t_end, int t, int rev) {
     return rev ? t_end - 1 - t : t_begin + t;
 }
-
-// Lanes-per-row tiles carry their group width in the descriptor (nrow =
-// rows | lpr << 16): a colour class is ordered by row-length bucket and each
-// bucket gets its own width (setup_pattern, mg_host.cpp), so one launch mixes
-// tiles of 2, 4 and 8 lanes per row.  Same xor tree as group_sum<LPR>.
-__device__ __forceinline__ double group_sum_rt(double v, int lpr) {
-    for (int off = lpr >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-}
-__device__ __forceinline__ int tile_lpr(const TileDesc& d) { return d.nrow >> 16; }
-__device__ __forceinline__ int tile_rows_of(const TileDesc& d) { return d.nrow & 0xffff; }
 
 template <int K, int UNR>
 __device__ __forceinline__ void stage_row(const StageView& v, int t, int row, const double* __restrict__ x,
@@ -347,8 +320,7 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
                                                      const int* __restrict__ rp, const int* __restrict__ col,
                                                      const double* __restrict__ val, const double* __restrict__ b,
                                                      double* __restrict__ x, double* __restrict__ r,
-                                                     double* __restrict__ partial, int cap, double omega, int rev,
-                                                     int nx_begin, int nx_end, int nx_rev) {
+                                                     double* __restrict__ partial, int cap, double omega, int rev) {
     extern __shared__ __align__(128) unsigned char smem_pipe[];
     __shared__ __align__(8) uint64_t bar[2];
     const int tid = threadIdx.x;
@@ -371,10 +343,6 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
         for (int i = 0; i < 2 && i < mine; ++i) {
             const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
             issue_tile(d, stage[i], cap, &bar[i], rp, col, val, pol);
-        }
-        for (int i = mine; i < 2; ++i) {   // a pass of < 2 tiles per CTA: the next pass's tiles right away
-            const int t = (int)blockIdx.x + (i - mine) * (int)gridDim.x;
-            if (t < nx_end - nx_begin) prefetch_tile(tiles[tile_ix(nx_begin, nx_end, t, nx_rev)], rp, col, val);
         }
     }
     pdl_wait();
@@ -422,14 +390,9 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
             }
         }
         __syncthreads();   // stage sidx fully consumed
-        if (tid == 0) {
-            if (i + 2 < mine) {
-                const TileDesc dn = tiles[tile_ix(t_begin, t_end, blockIdx.x + (i + 2) * gridDim.x, rev)];
-                issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
-            } else {
-                const int t = (int)blockIdx.x + (i + 2 - mine) * (int)gridDim.x;
-                if (t < nx_end - nx_begin) prefetch_tile(tiles[tile_ix(nx_begin, nx_end, t, nx_rev)], rp, col, val);
-            }
+        if (tid == 0 && i + 2 < mine) {
+            const TileDesc dn = tiles[tile_ix(t_begin, t_end, blockIdx.x + (i + 2) * gridDim.x, rev)];
+            issue_tile(dn, stage[sidx], cap, &bar[sidx], rp, col, val, pol);
         }
     }
     if (MODE == 0) trc.end(1, t_begin);
@@ -454,7 +417,7 @@ __global__ void __launch_bounds__(kTile, UNR >= 8 && K >= 3 ? 3 : 4) k_tile_pipe
 // k_tile_pipe, tiles of kTile / LPR rows; lane l of a row takes the staged
 // entries qb + l + u * LPR (the assignment and summation order of
 // k_lpr_sweep), so nothing but x and b is loaded after the PDL wait.
-template <int K, int MODE>
+template <int K, int LPR, int MODE>
 __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __restrict__ tiles, int t_begin, int t_end,
                                                          const int* __restrict__ rp, const int* __restrict__ col,
                                                          const double* __restrict__ val, const double* __restrict__ b,
@@ -464,6 +427,8 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
     __shared__ __align__(8) uint64_t bar[2];
     constexpr int GB = 4;   // gathers in flight per lane (8 with 2 CTAs/SM measured slower)
     const int tid = threadIdx.x;
+    const int tr = tid / LPR;
+    const int lane = tid & (LPR - 1);
     const size_t sb = (stage_bytes(cap) + 127) / 128 * 128;
     unsigned char* stage[2] = {smem_pipe, smem_pipe + sb};
     GsTrace trc;
@@ -497,10 +462,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
         const TileDesc d = tiles[tile_ix(t_begin, t_end, blockIdx.x + i * gridDim.x, rev)];
         mbar_wait(&bar[sidx], (unsigned)((i >> 1) & 1));
         const StageView v = view_tile(d, stage[sidx], cap);
-        const int LPR = tile_lpr(d);
-        const int tr = tid / LPR;
-        const int lane = tid & (LPR - 1);
-        const bool valid = tr < tile_rows_of(d);
+        const bool valid = tr < d.nrow;
         const int row = d.row0 + tr;
         double bv[K];
         if (valid && lane == 0) ldrow_pol<K>(b + (size_t)row * VS<K>::S, bv, spol);
@@ -539,11 +501,11 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
         }
         // groups never straddle a warp; every lane of the warp takes part
 #pragma unroll
-        for (int c = 0; c < K; ++c) s[c] = group_sum_rt(s[c], LPR);
-        if (MODE == 0 || MODE == 3) dg = group_sum_rt(dg, LPR);
+        for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], 0xffffffffu);
+        if (MODE == 0 || MODE == 3) dg = group_sum<LPR>(dg, 0xffffffffu);
         if (MODE == 3)
 #pragma unroll
-            for (int c = 0; c < K; ++c) xi[c] = group_sum_rt(xi[c], LPR);
+            for (int c = 0; c < K; ++c) xi[c] = group_sum<LPR>(xi[c], 0xffffffffu);
         if (valid && lane == 0) {
             double out[K];
             const double inv = (MODE == 0 || MODE == 3) ? 1.0 / dg : 0.0;
@@ -591,7 +553,7 @@ __global__ void __launch_bounds__(kTile, 3) k_tile_pipe_lpr(const TileDesc* __re
 // 80 registers and two stages per SM) most of the next pass's CTAs could not
 // become resident before this pass's left.  Same lane assignment and
 // summation order as k_tile_pipe_lpr: bitwise the same iterate.
-template <int K>
+template <int K, int LPR>
 __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __restrict__ tiles, int t_begin,
                                                            const int* __restrict__ rp, const int* __restrict__ col,
                                                            const double* __restrict__ val, const double* __restrict__ b,
@@ -600,13 +562,12 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     __shared__ __align__(8) uint64_t bar;
     constexpr int GB = 4;
     const int tid = threadIdx.x;
+    const int tr = tid / LPR;
+    const int lane = tid & (LPR - 1);
     GsTrace trc;
     trc.start();
     pdl_launch_dependents();
     const TileDesc d = tiles[t_begin + (int)blockIdx.x];
-    const int LPR = tile_lpr(d);
-    const int tr = tid / LPR;
-    const int lane = tid & (LPR - 1);
     if (tid == 0) {
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -616,7 +577,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     const uint64_t xpol = evict_last_policy();
     const uint64_t spol = evict_first_policy();
     const StageView v = view_tile(d, smem_pipe, cap);
-    const bool valid = tr < tile_rows_of(d);
+    const bool valid = tr < d.nrow;
     const int row = d.row0 + tr;
     // the tile lands under the previous pass; the diagonal's group sum and
     // reciprocal are formed before the wait (one nonzero term: exact)
@@ -625,7 +586,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     double dg = 0.0;
     for (int q = qb + lane; q < qe; q += LPR)
         if (v.cs[q] == row) dg = v.vs[q];
-    dg = group_sum_rt(dg, LPR);
+    dg = group_sum<LPR>(dg, 0xffffffffu);
     const double inv = 1.0 / dg;
     pdl_wait();
     trc.waited();
@@ -658,7 +619,7 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
     }
     // groups never straddle a warp; every lane of the warp takes part
 #pragma unroll
-    for (int c = 0; c < K; ++c) s[c] = group_sum_rt(s[c], LPR);
+    for (int c = 0; c < K; ++c) s[c] = group_sum<LPR>(s[c], 0xffffffffu);
     if (valid && lane == 0) {
         double out[K];
 #pragma unroll
@@ -1216,9 +1177,6 @@ inline int pipe_grid(const Level& L, int K, int ntiles) {
 inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
 // k_tile_one_lpr: every tile of the pass on its own resident CTA (4 per SM by
 // registers, one stage of shared memory each)
-#ifndef MG_NEXT_PREFETCH
-#define MG_NEXT_PREFETCH 0
-#endif
 #ifndef MG_ONE_TILE
 #define MG_ONE_TILE 1
 #endif
@@ -1234,22 +1192,30 @@ inline bool one_tile_ok(const Level& L, int ntiles) {
 // MODE 0..3 over tiles [t0, t1) of level L (iterate read from xin)
 template <int K, int MODE>
 void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double* partial, int grid, double omega,
-                 bool pdl, cudaStream_t s, int nx0 = 0, int nx1 = 0) {
+                 bool pdl, cudaStream_t s) {
     const TileDesc* td = reinterpret_cast<const TileDesc*>(L.tiles.p);
     const size_t sm = pipe_smem(L.pipe_cap);
     const int rev = (MODE != 2 && L.serpentine) ? (L.pass_ctr++ & 1) : 0;   // norm partials keep one order
-    const int nxrev = L.serpentine ? (L.pass_ctr & 1) : 0;                  // direction of the level's next pass
     if (MODE == 0 && L.pipe_lpr >= MG_ONE_TILE_MIN_LPR && one_tile_ok(L, t1 - t0)) {
-        launch_k(pdl, k_tile_one_lpr<K>, t1 - t0, kTile, sm / 2, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap);
+        const size_t sm1 = sm / 2;
+        const int g1 = t1 - t0;
+        switch (L.pipe_lpr) {
+            case 2: launch_k(pdl, k_tile_one_lpr<K, 2>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
+            case 4: launch_k(pdl, k_tile_one_lpr<K, 4>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
+            default: launch_k(pdl, k_tile_one_lpr<K, 8>, g1, kTile, sm1, s, td, t0, L.rp.p, L.col.p, L.val.p, L.b.p, xin, L.pipe_cap); break;
+        }
         return;
     }
-    if (L.pipe_lpr == 1) {
-        if (K == 3 && L.pipe_unr8)
-            launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
-        else
-            launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev, nx0, nx1, nxrev);
-    } else {
-        launch_k(pdl, k_tile_pipe_lpr<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+    switch (L.pipe_lpr) {
+        case 1:
+            if (K == 3 && L.pipe_unr8)
+                launch_k(pdl, k_tile_pipe<K, MODE, 8>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+            else
+                launch_k(pdl, k_tile_pipe<K, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev);
+            break;
+        case 2: launch_k(pdl, k_tile_pipe_lpr<K, 2, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+        case 4: launch_k(pdl, k_tile_pipe_lpr<K, 4, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
+        default: launch_k(pdl, k_tile_pipe_lpr<K, 8, MODE>, grid, kTile, sm, s, td, t0, t1, L.rp.p, L.col.p, L.val.p, L.b.p, xin, r, partial, L.pipe_cap, omega, rev); break;
     }
 }
 
@@ -1257,7 +1223,7 @@ void pipe_launch(const Level& L, int t0, int t1, double* xin, double* r, double*
 // MODE 3: Jacobi out = x + omega D^{-1}(b - A x).  xin: iterate read (L.x if null).
 template <int K, int MODE>
 int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s, double* xin = nullptr,
-            double omega = 0.0, int next_r0 = -1) {
+            double omega = 0.0) {
     double* xp = xin ? xin : L.x.p;
     const int rows = r1 - r0;
     if (rows <= 0) return 0;
@@ -1274,14 +1240,7 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
             t0 = toff[toff.size() - 2];   // whole-level tiles are the last range
             t1 = toff.back();
         }
-        int nx0 = 0, nx1 = 0;   // tiles of the colour class the next GS pass of this level takes
-        if (MODE == 0 && MG_NEXT_PREFETCH && next_r0 >= 0) {
-            int c = 0;
-            while (L.colour_off[c] != next_r0) ++c;
-            nx0 = toff[c];
-            nx1 = toff[c + 1];
-        }
-        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(L, K, t1 - t0), omega, pdl, s, nx0, nx1);
+        pipe_launch<K, MODE>(L, t0, t1, xp, r, nullptr, pipe_grid(L, K, t1 - t0), omega, pdl, s);
         return 1;
     }
     if (L.tiled) {
@@ -1333,11 +1292,6 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_sweep<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_resnorm_tiled<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_chol_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_one_lpr<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1346,6 +1300,21 @@ void set_attrs_k() {
     cudaFuncSetAttribute(k_tile_pipe<K, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_pipe<K, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_one_lpr<K, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_tile_pipe_lpr<K, 8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_tile_sweep<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
 }
 
@@ -1371,8 +1340,8 @@ void init_vcycle_attributes() {
     set_attrs_k<4>();
 }
 
-int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s, int next_r0) {
-    MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s, nullptr, 0.0, next_r0)))
+int vc_gs(int K, const Level& L, int r0, int r1, bool pdl, cudaStream_t s) {
+    MG_K_SWITCH(K, (sweep_k<KK, 0>(L, r0, r1, nullptr, pdl, s)))
 }
 // Device-side V-cycle loop (conditional WHILE graph node): after each cycle's
 // residual norm this kernel records rho into the history, applies mg_solve's
