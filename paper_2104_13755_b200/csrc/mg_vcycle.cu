@@ -635,8 +635,8 @@ __global__ void __launch_bounds__(kTile, 4) k_tile_one_lpr(const TileDesc* __res
 // after the wait its x gathers go out in batches of GB independent loads.
 // The group width is chosen per level so that one colour pass is about one
 // wave of the GPU (see choose_lpr in mg_host.cpp).
-#ifndef MG_LPR_PREFETCH64
-#define MG_LPR_PREFETCH64 1
+#ifndef MG_LPR_WIDE_ENTRIES
+#define MG_LPR_WIDE_ENTRIES 64   // entries per row prefetched by the 16- and 32-lane groups
 #endif
 template <int K, int LPR, int MODE>
 __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const int* __restrict__ rp, const int* __restrict__ col,
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
     // dependent round trips after the wait - tools/gs_trace.py: the CTAs
     // holding such rows ended 1.1-1.3 us after the release against a median
     // of 0.7), 32 per row otherwise
-    constexpr int U = MG_LPR_PREFETCH64 && LPR >= 16 ? 64 / LPR : 32 / LPR;
+    constexpr int U = LPR >= 16 ? MG_LPR_WIDE_ENTRIES / LPR : 32 / LPR;
     // gathers in flight per lane: the whole prefetch for LPR >= 8, batches of
     // 4 for LPR = 4 (8 entries per lane) to keep registers / occupancy
     constexpr int GB = U <= 4 ? U : 4;
