@@ -253,6 +253,19 @@ int mg_util_galerkin_pattern(int32_t n_fine, const int32_t* row_ptr, const int32
                              const int32_t* P_cols, const double* P_w, int32_t* c_row_ptr, int64_t* c_nnz,
                              int32_t* c_col);
 
+/* 1-ring CSR pattern of a triangle mesh (sorted columns, diagonal included:
+ * the fixed pattern of the cotan assembly) and, per stored entry, the
+ * row-local positions of the <= 2 vertices opposite the edge (i, col): low
+ * nibble = position among row i's entries of the first, high nibble = of the
+ * second, 15 = none (diagonal, boundary edge: natural BC) - the
+ * table k_cotan_slots reads.  F: [n_faces][3] host.  Two-call protocol: call
+ * with col == NULL to get *nnz and row_ptr[n+1]; then with col[*nnz] and
+ * slots[*nnz] (slots may be NULL).  Errors: MG_ERR_INVALID_ARG, MG_ERR_INPUT
+ * (index out of range, a vertex in no face), MG_ERR_SHAPE (slots requested
+ * and a row has more than 15 entries: the library then keeps vertex indices). */
+int mg_util_one_ring(int32_t n, int32_t n_faces, const int32_t* F, int32_t* row_ptr, int64_t* nnz, int32_t* col,
+                     uint8_t* slots);
+
 /* ---- execution options ----------------------------------------------------- */
 
 /* How the same arithmetic is scheduled (results are bitwise identical except

@@ -629,6 +629,10 @@ struct mg_ctx {
 
 namespace {
 
+#ifndef MG_LPR_BALANCE
+#define MG_LPR_BALANCE 1
+#endif
+
 // ---------------------------------------------------------------------------
 // Pattern setup (per new level-0 pattern): colouring and internal ordering of
 // every level, coarse patterns, transposes of P, device upload.
@@ -771,6 +775,12 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                     const double fill = (double)(nt256 - (rounds - 1) * G) / G;   // last round's occupancy
                     if (L.pipe_lpr == 1 && rows > T && (rounds == 1 || fill < 0.5))
                         Tr = std::max(128, (rows + rounds * G - 1) / (rounds * G));
+                    // lanes-per-row levels: a class under one wave is spread over
+                    // the whole resident grid (tiles of >= T / 2 rows), so every SM
+                    // holds the same number of CTAs of the pass instead of 3 on some
+                    // SMs and 2 on the others
+                    if (MG_LPR_BALANCE && L.pipe_lpr > 1 && rounds == 1 && rows > T)
+                        Tr = std::min(T, std::max(T / 2, (rows + G - 1) / G));
                     for (int a0 = r0; a0 < r1; a0 += Tr) {
                         const int nr = std::min(Tr, r1 - a0);
                         td.insert(td.end(), {a0, nr, L.irp[a0], L.irp[a0 + nr]});
@@ -795,8 +805,14 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
             L.serpentine = true;
             L.pass_ctr = 0;
             L.pipe_cap = std::max(L.cap_gs, L.cap_all);
-            cudaError_t e = L.tiles.upload(td, c->stream);
-            if (e) return c->cuda_fail(e, "tile upload");
+            // balanced tiles do not start on multiples of T: size the stages by the tiles as built
+            for (size_t t = 0; t + 3 < td.size(); t += 4) L.pipe_cap = std::max(L.pipe_cap, td[t + 3] - td[t + 2]);
+            if (pipe_smem_bytes(L.pipe_cap) > 200 * 1024) {
+                L.pipe = false;
+            } else {
+                cudaError_t e = L.tiles.upload(td, c->stream);
+                if (e) return c->cuda_fail(e, "tile upload");
+            }
         }
         if (!L.tiled) {
             // lanes per row of a colour pass (each lane prefetches 32 / LPR entries
@@ -1641,8 +1657,9 @@ static int upload_full_one_ring(mg_ctx* c, const std::vector<int32_t>& rp, const
 
 // 1-ring CSR pattern of F[0] (sorted, diagonal included) and the two opposite
 // vertices of every stored edge (-1: none / diagonal), user order.
-static int build_one_ring(mg_ctx* c, std::vector<int32_t>& rp, std::vector<int32_t>& cl, std::vector<int32_t>& opp) {
-    const int32_t n = c->n_full;
+// Returns -1, or the first vertex that is in no face.
+static int32_t one_ring_core(int32_t n, int32_t nF0, const int32_t* F0, std::vector<int32_t>& rp,
+                             std::vector<int32_t>& cl, std::vector<int32_t>& opp) {
     rp.assign(n + 1, 0);
     cl.clear();
     opp.clear();
@@ -1651,12 +1668,12 @@ static int build_one_ring(mg_ctx* c, std::vector<int32_t>& rp, std::vector<int32
         int32_t i, j, o;
     };
     std::vector<HalfEdge> he;
-    he.reserve(6 * (size_t)c->nF0);
-    for (int32_t f = 0; f < c->nF0; ++f)
+    he.reserve(6 * (size_t)nF0);
+    for (int32_t f = 0; f < nF0; ++f)
         for (int k = 0; k < 3; ++k) {
-            const int32_t o = c->F0[3 * (size_t)f + k];
-            const int32_t i = c->F0[3 * (size_t)f + (k + 1) % 3];
-            const int32_t j = c->F0[3 * (size_t)f + (k + 2) % 3];
+            const int32_t o = F0[3 * (size_t)f + k];
+            const int32_t i = F0[3 * (size_t)f + (k + 1) % 3];
+            const int32_t j = F0[3 * (size_t)f + (k + 2) % 3];
             he.push_back({i, j, o});
             he.push_back({j, i, o});
         }
@@ -1686,7 +1703,7 @@ static int build_one_ring(mg_ctx* c, std::vector<int32_t>& rp, std::vector<int32
             }
             any = true;
         }
-        if (!any) return c->fail(MG_ERR_INPUT, "vertex %d is in no face of F[0]", i);
+        if (!any) return i;
         if (!diag_done) {
             cl.push_back(i);
             opp.push_back(-1);
@@ -1694,6 +1711,11 @@ static int build_one_ring(mg_ctx* c, std::vector<int32_t>& rp, std::vector<int32
         }
         rp[i + 1] = (int32_t)cl.size();
     }
+    return -1;
+}
+static int build_one_ring(mg_ctx* c, std::vector<int32_t>& rp, std::vector<int32_t>& cl, std::vector<int32_t>& opp) {
+    const int32_t bad = one_ring_core(c->n_full, c->nF0, c->F0.data(), rp, cl, opp);
+    if (bad >= 0) return c->fail(MG_ERR_INPUT, "vertex %d is in no face of F[0]", bad);
     return MG_OK;
 }
 
@@ -2239,6 +2261,24 @@ int mg_util_greedy_colouring(int32_t n, const int32_t* row_ptr, const int32_t* c
     if (n < 0 || (n > 0 && (!row_ptr || !col || !colour))) return MG_ERR_INVALID_ARG;
     const int32_t k = greedy_colouring(n, row_ptr, col, colour);
     if (n_colours) *n_colours = k;
+    return MG_OK;
+}
+
+int mg_util_one_ring(int32_t n, int32_t n_faces, const int32_t* F, int32_t* row_ptr, int64_t* nnz, int32_t* col,
+                     uint8_t* slots) {
+    if (n < 0 || n_faces < 0 || !F || !row_ptr || !nnz) return MG_ERR_INVALID_ARG;
+    for (int64_t t = 0; t < 3 * (int64_t)n_faces; ++t)
+        if (F[t] < 0 || F[t] >= n) return MG_ERR_INPUT;
+    std::vector<int32_t> rp, cl, opp;
+    if (one_ring_core(n, n_faces, F, rp, cl, opp) >= 0) return MG_ERR_INPUT;
+    std::memcpy(row_ptr, rp.data(), sizeof(int32_t) * ((size_t)n + 1));
+    *nnz = (int64_t)cl.size();
+    if (col) std::memcpy(col, cl.data(), sizeof(int32_t) * cl.size());
+    if (slots) {
+        std::vector<uint8_t> packed;
+        if (!pack_opp_slots(n, rp, cl, opp, packed)) return MG_ERR_SHAPE;   // a row over 15 entries: index table instead
+        std::memcpy(slots, packed.data(), cl.size());
+    }
     return MG_OK;
 }
 

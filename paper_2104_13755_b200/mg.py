@@ -68,6 +68,7 @@ def lib():
             "mg_get_coarse_factor": (C.c_int, [_vp, _vp]),
             "mg_util_greedy_colouring": (C.c_int, [i32, _vp, _vp, _vp, _vp]),
             "mg_util_galerkin_pattern": (C.c_int, [i32, _vp, _vp, i32, _vp, _vp, _vp, _vp, _vp]),
+            "mg_util_one_ring": (C.c_int, [i32, i32, _vp, _vp, _vp, _vp, _vp]),
             "mg_set_profiling": (C.c_int, [_vp, C.c_int]),
             "mg_get_profile": (C.c_int, [_vp, _vp, _vp]),
             "mg_launch_count": (i64, [_vp]),
@@ -311,6 +312,23 @@ def mg_util_greedy_colouring(row_ptr, col):
     if rc:
         raise MGError(rc, "mg_util_greedy_colouring")
     return out, k.value
+
+
+def mg_util_one_ring(n, F, slots=True):
+    """(row_ptr, col, slots) of the 1-ring pattern of faces F [nF][3]."""
+    F = np.ascontiguousarray(F, np.int32)
+    rp = np.zeros(n + 1, np.int32)
+    nnz = C.c_int64(0)
+    rc = lib().mg_util_one_ring(int(n), F.shape[0], F.ctypes.data, rp.ctypes.data, C.byref(nnz), None, None)
+    if rc != MG_OK:
+        raise MGError(rc, "mg_util_one_ring")
+    col = np.zeros(nnz.value, np.int32)
+    sl = np.zeros(nnz.value, np.uint8) if slots else None
+    rc = lib().mg_util_one_ring(int(n), F.shape[0], F.ctypes.data, rp.ctypes.data, C.byref(nnz), col.ctypes.data,
+                                sl.ctypes.data if slots else None)
+    if rc != MG_OK:
+        raise MGError(rc, "mg_util_one_ring")
+    return rp, col, sl
 
 
 def mg_util_galerkin_pattern(row_ptr, col, n_coarse, P_cols, P_w):

@@ -115,3 +115,66 @@ def test_profile_classes_match_library():
     n = int(re.search(r"constexpr int kProfClasses = (\d+);", src).group(1))
     enum = re.findall(r"PC_\w+ = (\d+)", src)
     assert len(mg.PROF_CLASSES) == n == len(enum) == max(map(int, enum)) + 1
+
+
+def _brute_opposites(F, i, j):
+    """Vertices o with a face {i, j, o} (brute force over the face list)."""
+    out = []
+    for f in F:
+        s = set(int(v) for v in f)
+        if i in s and j in s:
+            out.extend(s - {i, j})
+    return sorted(out)
+
+
+def _fan(n_ring, closed):
+    F = [(0, 1 + k, 1 + (k + 1) % n_ring) for k in range(n_ring)]
+    n = n_ring + 1
+    if closed:
+        F += [(n, 1 + (k + 1) % n_ring, 1 + k) for k in range(n_ring)]
+        n += 1
+    return n, np.asarray(F, np.int32)
+
+
+@pytest.mark.parametrize("mesh", ["ico2", "cyl", "fan9", "disk7", "fan14"])
+def test_one_ring_pattern_and_opposite_slots(ora, mglib, mesh):
+    """Host pattern setup of the cotan assembly: the 1-ring CSR pattern equals
+    the oracle's assembled pattern, and the packed row-local slots decode to
+    exactly the vertices opposite each stored edge (brute force over the face
+    list); diagonal entries and missing opposites (boundary edges) decode to
+    'none'."""
+    if mesh == "ico2":
+        V, F = meshgen.icosphere(2)
+        n = V.shape[0]
+    elif mesh == "cyl":
+        p = meshgen.make_config(3, grid=(12, 9))
+        V, F = p.levels[0]
+        n = V.shape[0]
+    else:
+        n, F = _fan(int(mesh[3:] if mesh.startswith("fan") else mesh[4:]), mesh.startswith("fan"))
+        V = None
+    rp, col, sl = mglib.mg_util_one_ring(n, F)
+    if V is not None:
+        A, _ = ora.assemble(np.ascontiguousarray(V, np.float64), np.asarray(F, np.int32), 1.0, 1.0)
+        orp, ocol, _ = A.arrays()
+        assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+    for i in range(n):
+        row = col[rp[i]:rp[i + 1]]
+        assert np.all(np.diff(row) > 0) and i in row
+        for e in range(rp[i], rp[i + 1]):
+            j = int(col[e])
+            got = sorted(int(row[s]) for s in (int(sl[e]) & 15, int(sl[e]) >> 4) if s != 15)
+            want = [] if j == i else _brute_opposites(F, i, j)
+            assert got == want, (i, j)
+
+
+def test_one_ring_errors(mglib):
+    n, F = _fan(20, True)                      # apex rows of 21 entries: no packed form
+    rp, col, _ = mglib.mg_util_one_ring(n, F, slots=False)
+    assert rp[1] - rp[0] == 21
+    with pytest.raises(mglib.MGError):
+        mglib.mg_util_one_ring(n, F)
+    with pytest.raises(mglib.MGError):
+        mglib.mg_util_one_ring(n + 1, F)       # a vertex in no face
+    with pytest.raises(mglib.MGError):
+        mglib.mg_util_one_ring(3, np.array([[0, 1, 5]], np.int32))   # index out of range
