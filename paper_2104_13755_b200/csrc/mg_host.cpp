@@ -791,15 +791,24 @@ int setup_pattern(mg_ctx* c, const std::vector<int32_t>& urp, const std::vector<
                 // Morton order of their middle row: all colours of one spatial
                 // window are processed together, so the neighbours' x gathered
                 // by a tile were just read by the tiles of the other colours
-                const int ngs = (int)(td.size() / 4) - base;
-                std::vector<int> idx(ngs);
-                std::iota(idx.begin(), idx.end(), base);
-                auto mid_key = [&](int t) { return key[L.perm[td[4 * t] + td[4 * t + 1] / 2]]; };
-                std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return mid_key(x) < mid_key(y); });
-                for (int t : idx) {
-                    const int32_t d0 = td[4 * t], d1 = td[4 * t + 1], d2 = td[4 * t + 2], d3 = td[4 * t + 3];
-                    td.insert(td.end(), {d0, d1, d2, d3});
+                std::vector<int32_t> wl;   // the whole-level tile set before ordering
+                if (L.pipe_lpr > 1) {
+                    // lanes-per-row levels: the whole-level passes are not bound to one
+                    // wave, so they take full tiles of T rows per colour class (the
+                    // balanced GS tiles would leave a quarter of their lanes idle)
+                    for (int k = 0; k + 1 < (int)L.colour_off.size(); ++k)
+                        for (int a0 = L.colour_off[k]; a0 < L.colour_off[k + 1]; a0 += T) {
+                            const int nr = std::min(T, L.colour_off[k + 1] - a0);
+                            wl.insert(wl.end(), {a0, nr, L.irp[a0], L.irp[a0 + nr]});
+                        }
+                } else {
+                    wl.assign(td.begin() + 4 * (size_t)base, td.end());
                 }
+                std::vector<int> idx(wl.size() / 4);
+                std::iota(idx.begin(), idx.end(), 0);
+                auto mid_key = [&](int t) { return key[L.perm[wl[4 * t] + wl[4 * t + 1] / 2]]; };
+                std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return mid_key(x) < mid_key(y); });
+                for (int t : idx) td.insert(td.end(), {wl[4 * t], wl[4 * t + 1], wl[4 * t + 2], wl[4 * t + 3]});
                 toff.push_back((int32_t)(td.size() / 4));
             }
             L.serpentine = true;

@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kBlock, LPR == 4 ? 4 : 1) k_lpr_sweep(const in
     // gathers in flight per lane: the whole prefetch for LPR >= 8, batches of
     // 4 for LPR = 4 (8 entries per lane) to keep registers / occupancy
     constexpr int GB = U <= 4 ? U : 4;
-    const int g = (blockIdx.x * kBlock + threadIdx.x) / LPR;
+    const int g = (int)(blockIdx.x * blockDim.x + threadIdx.x) / LPR;
     const int lane = threadIdx.x & (LPR - 1);
     const int row = r0 + g;
     GsTrace trc;
@@ -1177,6 +1177,9 @@ inline int pipe_grid(const Level& L, int K, int ntiles) {
 inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
 // k_tile_one_lpr: every tile of the pass on its own resident CTA (4 per SM by
 // registers, one stage of shared memory each)
+#ifndef MG_LPR_GS_BLOCK
+#define MG_LPR_GS_BLOCK 256
+#endif
 #ifndef MG_ONE_TILE
 #define MG_ONE_TILE 1
 #endif
@@ -1250,12 +1253,15 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
         return 1;
     }
     const int lpr = MODE == 0 ? L.lpr : L.lpr_all;
-    const int grid = nblk((int64_t)rows * lpr, kBlock);
+    // a GS colour pass of a small level is a few hundred CTAs at most: smaller
+    // CTAs spread its rows evenly over the SMs
+    const int blk = (MODE == 0 && lpr >= 16) ? MG_LPR_GS_BLOCK : kBlock;
+    const int grid = nblk((int64_t)rows * lpr, blk);
     switch (lpr) {
-        case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
-        case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
-        case 16: launch_k(pdl, k_lpr_sweep<K, 16, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
-        default: launch_k(pdl, k_lpr_sweep<K, 32, MODE>, grid, kBlock, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, blk, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        case 8: launch_k(pdl, k_lpr_sweep<K, 8, MODE>, grid, blk, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        case 16: launch_k(pdl, k_lpr_sweep<K, 16, MODE>, grid, blk, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
+        default: launch_k(pdl, k_lpr_sweep<K, 32, MODE>, grid, blk, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
     }
     return 1;
 }
