@@ -1177,9 +1177,6 @@ inline int pipe_grid(const Level& L, int K, int ntiles) {
 inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 128); }
 // k_tile_one_lpr: every tile of the pass on its own resident CTA (4 per SM by
 // registers, one stage of shared memory each)
-#ifndef MG_LPR_GS_BLOCK
-#define MG_LPR_GS_BLOCK 256
-#endif
 #ifndef MG_ONE_TILE
 #define MG_ONE_TILE 1
 #endif
@@ -1253,9 +1250,11 @@ int sweep_k(const Level& L, int r0, int r1, double* r, bool pdl, cudaStream_t s,
         return 1;
     }
     const int lpr = MODE == 0 ? L.lpr : L.lpr_all;
-    // a GS colour pass of a small level is a few hundred CTAs at most: smaller
-    // CTAs spread its rows evenly over the SMs
-    const int blk = (MODE == 0 && lpr >= 16) ? MG_LPR_GS_BLOCK : kBlock;
+    // a GS colour pass that would not put a 256-thread CTA on every SM runs
+    // 128-thread CTAs (its rows spread over twice the SMs: C4 levels 4 / 5
+    // 1.08 / 0.96 -> 1.00 / 0.93 ms/step; passes of more CTAs than SMs measured
+    // slower that way, C4 level 3 1.35 -> 1.42; profiles/r02/lpr_block_ab.txt)
+    const int blk = (MODE == 0 && lpr >= 16 && nblk((int64_t)rows * lpr, kBlock) < pipe_nsm()) ? kBlock / 2 : kBlock;
     const int grid = nblk((int64_t)rows * lpr, blk);
     switch (lpr) {
         case 4: launch_k(pdl, k_lpr_sweep<K, 4, MODE>, grid, blk, 0, s, L.rp.p, L.col.p, L.val.p, L.b.p, xp, r, r0, r1, omega); break;
