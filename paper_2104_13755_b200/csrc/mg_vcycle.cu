@@ -1181,7 +1181,7 @@ inline size_t pipe_smem(int cap) { return 2 * ((stage_bytes(cap) + 127) / 128 * 
 #define MG_ONE_TILE 1
 #endif
 #ifndef MG_ONE_TILE_MIN_LPR
-#define MG_ONE_TILE_MIN_LPR 4
+#define MG_ONE_TILE_MIN_LPR 2
 #endif
 inline bool one_tile_ok(const Level& L, int ntiles) {
     const size_t smem = pipe_smem(L.pipe_cap) / 2 + 1280;
